@@ -1,0 +1,207 @@
+"""Problem containers and the synthetic instance families of BASELINE.json.
+
+The solver consumes any object exposing ``C f g m n cost_fro_norm
+marginal_norm`` (the accessors of the reference ``OTProblem``,
+instance.py:109-150), so a reference ``otsolve.OTProblem`` can be passed in
+unchanged.  This module provides a minimal equivalent for callers that do not
+have the reference installed, plus the generators for the benchmark configs
+(SURVEY.md §8(d)):
+
+* ``sqeuclid_grid_cost(r)`` — squared Euclidean grid cost as EXACT integers
+  ``di^2 + dj^2`` (``grid_cost('l2')**2`` rounds through sqrt).
+* ``whitenoise_marginals(r, seed)`` — the reference ``synth_instance(
+  "whitenoise", r, seed)`` + ``marginal_from_image`` (instance.py:350-351,
+  369-376, 300-305, 78-82), restated.
+* ``rect_l1_cost`` / ``sparse_marginals`` — the builder-defined rectangular
+  C4 family.
+
+The on-device twins of the cost generators live in the CUDA library
+(``pdot_gen_cost``); both produce integers, so they agree bit for bit.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+class InstanceError(ValueError):
+    """Invalid instance data (mirrors instance.py:28-29)."""
+
+
+def _finite(values, name):
+    arr = np.array(values, dtype=np.float64)
+    if not np.all(np.isfinite(arr)):
+        raise InstanceError(f"non-finite {name} entry")
+    return arr
+
+
+class Marginal:
+    """Probability vector normalised to unit sum (instance.py:66-85)."""
+
+    def __init__(self, weights):
+        w = _finite(weights, "marginal")
+        if w.ndim != 1 or w.size < 1:
+            raise InstanceError("marginal must be a non-empty vector")
+        if np.any(w < 0):
+            raise InstanceError("negative marginal entry")
+        total = float(w.sum())
+        if total <= 0.0:
+            raise InstanceError("marginal has zero mass")
+        self.weights = w / total
+
+    def __len__(self):
+        return self.weights.size
+
+
+class CostMatrix:
+    """Non-negative cost matrix (instance.py:88-106)."""
+
+    def __init__(self, entries, norm_kind="explicit"):
+        e = _finite(entries, "cost")
+        if e.ndim != 2:
+            raise InstanceError("cost must be a 2-D matrix")
+        if np.any(e < 0):
+            raise InstanceError("negative cost entry")
+        self.entries = e
+        self.norm_kind = norm_kind
+
+    @property
+    def shape(self):
+        return self.entries.shape
+
+
+class OTProblem:
+    """Cost + marginals with the accessors the solver reads (instance.py:109-150)."""
+
+    def __init__(self, cost, row_marginal, col_marginal):
+        if not isinstance(cost, CostMatrix):
+            cost = CostMatrix(cost)
+        if not isinstance(row_marginal, Marginal):
+            row_marginal = Marginal(row_marginal)
+        if not isinstance(col_marginal, Marginal):
+            col_marginal = Marginal(col_marginal)
+        m, n = cost.shape
+        if len(row_marginal) != m or len(col_marginal) != n:
+            raise InstanceError("dimension mismatch between cost and marginals")
+        self.cost, self.row_marginal, self.col_marginal = cost, row_marginal, col_marginal
+        self._fro = None
+        self._marg = None
+
+    @property
+    def m(self):
+        return self.cost.shape[0]
+
+    @property
+    def n(self):
+        return self.cost.shape[1]
+
+    @property
+    def C(self):
+        return self.cost.entries
+
+    @property
+    def f(self):
+        return self.row_marginal.weights
+
+    @property
+    def g(self):
+        return self.col_marginal.weights
+
+    @property
+    def cost_fro_norm(self):
+        if self._fro is None:
+            self._fro = float(np.linalg.norm(self.C))
+        return self._fro
+
+    @property
+    def marginal_norm(self):
+        if self._marg is None:
+            self._marg = float(np.linalg.norm(self.f) + np.linalg.norm(self.g))
+        return self._marg
+
+
+def make_problem(C, f, g):
+    return OTProblem(CostMatrix(C), Marginal(f), Marginal(g))
+
+
+# ---------------------------------------------------------------------------
+# benchmark families
+# ---------------------------------------------------------------------------
+def grid_coords(r):
+    """Row-major integer coordinates (k // r, k % r) (instance.py:161-164)."""
+    k = np.arange(r * r, dtype=np.int64)
+    return k // r, k % r
+
+
+def sqeuclid_grid_cost(r):
+    """Exact squared-Euclidean cost between the cells of an r x r grid."""
+    a, b = grid_coords(r)
+    da = a[:, None] - a[None, :]
+    db = b[:, None] - b[None, :]
+    return (da * da + db * db).astype(np.float64)
+
+
+def l1_grid_cost(r):
+    a, b = grid_coords(r)
+    return (np.abs(a[:, None] - a[None, :]) + np.abs(b[:, None] - b[None, :])).astype(np.float64)
+
+
+def whitenoise_images(r, seed):
+    """synth_instance("whitenoise", r, seed), instance.py:350-351, 369-376."""
+    if r < 2:
+        raise InstanceError("synthetic images need resolution >= 2")
+    rng = np.random.default_rng(seed)
+    return rng.random((r, r)), rng.random((r, r))
+
+
+def whitenoise_marginals(r, seed):
+    src, dst = whitenoise_images(r, seed)
+    return Marginal(src.ravel()).weights, Marginal(dst.ravel()).weights
+
+
+def sqeuclid_problem(r, seed):
+    """C1/C2/C3/C5 family: whitenoise marginals, exact sq-Euclidean cost."""
+    f, g = whitenoise_marginals(r, seed)
+    return OTProblem(CostMatrix(sqeuclid_grid_cost(r)), Marginal(f), Marginal(g))
+
+
+RECT_SRC = (64, 128)   # C4 source grid (rows, cols)  -> m = 8192
+RECT_DST = (128, 256)  # C4 target grid               -> n = 32768
+
+
+def rect_l1_cost(src_shape=RECT_SRC, dst_shape=RECT_DST):
+    """C4: L1 cost from a source grid scaled by 2 onto the target lattice."""
+    sr, sc = src_shape
+    tr, tc = dst_shape
+    k = np.arange(sr * sc, dtype=np.int64)
+    a, b = 2 * (k // sc), 2 * (k % sc)
+    l = np.arange(tr * tc, dtype=np.int64)
+    c, d = l // tc, l % tc
+    return (np.abs(a[:, None] - c[None, :]) + np.abs(b[:, None] - d[None, :])).astype(np.float64)
+
+
+def sparse_marginals(size, seed, density=0.1):
+    """C4 marginals: `density` of the cells carry U(0.1, 1.1) mass, the rest 0."""
+    rng = np.random.default_rng(seed)
+    k = max(1, int(round(density * size)))
+    support = rng.choice(size, size=k, replace=False)
+    w = np.zeros(size)
+    w[support] = 0.1 + rng.random(k)
+    return Marginal(w).weights
+
+
+def rect_problem(seed, src_shape=RECT_SRC, dst_shape=RECT_DST):
+    m = src_shape[0] * src_shape[1]
+    n = dst_shape[0] * dst_shape[1]
+    f = sparse_marginals(m, 2 * seed)
+    g = sparse_marginals(n, 2 * seed + 1)
+    return OTProblem(CostMatrix(rect_l1_cost(src_shape, dst_shape)), Marginal(f), Marginal(g))
+
+
+def grid_side(mn):
+    r = math.isqrt(mn)
+    if r * r != mn:
+        raise InstanceError("not a square grid size")
+    return r
