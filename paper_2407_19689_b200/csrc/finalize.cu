@@ -1,0 +1,626 @@
+// Finalize kernel (K2 of every pass) and the device-side controller.
+//
+// Blocks [0, CB) reduce the column partials of 64 columns each; blocks
+// [CB, CB+T) reduce the row partials of one row tile each.  Both then apply
+// the O(m+n) vector updates of the pass (p+ / q+, the dual running average,
+// the KKT primal residuals, ...) and write per-block scalar partials.  The
+// last block to finish (ticket counter) reduces those in a fixed order and
+// runs the controller: the restart / termination / line-search logic of
+// pdhg.py:298-378 on the device, so the host never waits on an iteration.
+//
+// Reduction order is fixed: the T row tiles are cut into kGroups=8 contiguous
+// groups, summed sequentially inside a group and pairwise across groups.  A
+// row-sharded multi-GPU run owning whole groups reproduces the same tree.
+#include <math.h>
+
+#include "pdot_internal.cuh"
+
+namespace pdot {
+namespace {
+
+constexpr int kColsPerBlock = 64;
+
+// fixed-order block sum of K per-thread values; result valid in thread 0
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double* red /* [kWarps][K] */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int msk = 16; msk >= 1; msk >>= 1) x += __shfl_xor_sync(0xffffffffu, x, msk);
+    v[k] = x;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) red[warp * K + k] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double acc = red[k];
+      for (int w = 1; w < kWarps; ++w) acc += red[w * K + k];
+      v[k] = acc;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double pair8(const double* g) {
+  return ((g[0] + g[1]) + (g[2] + g[3])) + ((g[4] + g[5]) + (g[6] + g[7]));
+}
+
+__device__ __forceinline__ int nq_of(int op) {
+  return op == OP_STEP ? 4 : 1;
+}
+
+// ---------------------------------------------------------------------------
+// column blocks
+// ---------------------------------------------------------------------------
+template <int NQ>
+__device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_out, double* smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
+  const int64_t GS = (c.T + kGroups - 1) / kGroups;
+  const int64_t t0 = warp * GS, t1 = imin64(c.T, t0 + GS);
+  double2 acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = make_double2(0.0, 0.0);
+  if (j < c.n) {
+    for (int64_t t = t0; t < t1; ++t) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(c.colpart + (t * NQ + q) * c.ldx + j));
+        acc[q].x += v.x;
+        acc[q].y += v.y;
+      }
+    }
+  }
+  // smem [group][q][64]
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    smem[(warp * NQ + q) * kColsPerBlock + lane * 2] = acc[q].x;
+    smem[(warp * NQ + q) * kColsPerBlock + lane * 2 + 1] = acc[q].y;
+  }
+  __syncthreads();
+  const int jj = threadIdx.x;
+  j_out = (int64_t)b * kColsPerBlock + jj;
+  if (jj < kColsPerBlock) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double g8[kGroups];
+#pragma unroll
+      for (int gi = 0; gi < kGroups; ++gi) g8[gi] = smem[(gi * NQ + q) * kColsPerBlock + jj];
+      col[q] = pair8(g8);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) col[q] = 0.0;
+  }
+  __syncthreads();
+}
+
+template <int NQ>
+__device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ]) {
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) row[q] = 0.0;
+  if (i >= c.m) return;
+  for (int64_t u = 0; u < c.U; ++u) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) row[q] += __ldcg(c.rowpart + (u * NQ + q) * c.m + i);
+  }
+}
+
+__device__ void column_block(Ctl& c, int op, int b, double* smem) {
+  double vals[kMaxColScal];
+#pragma unroll
+  for (int s = 0; s < kMaxColScal; ++s) vals[s] = 0.0;
+  int64_t j;
+  if (op == OP_STEP) {
+    double col[4];
+    column_sums<4>(c, b, col, j, smem);
+    if (threadIdx.x < kColsPerBlock && j < c.n) {
+      const Slot& sx = c.slot[c.sX];
+      const Slot& sa = c.slot[c.sA];
+      const double qj = sx.q[j], gj = c.g[j];
+      const double qn = qj + c.sigma * (gj - col[0]);        // pdhg.py:128
+      const double dq = qn - qj;                              // pdhg.py:141
+      c.slot[c.sXn].q[j] = qn;
+      vals[0] = dq * dq;
+      vals[1] = dq * col[1];
+      const double pcx = col[2] - gj;                         // kkt.py:69
+      vals[2] = pcx * pcx;
+      vals[4] = gj * qn;
+      vals[6] = qn * qn;
+      if (!c.unit) {
+        const double qaj = sa.q[j];
+        const double qan = qaj + (qn - qaj) / c.kd;           // pdhg.py:317
+        c.slot[c.sAn].q[j] = qan;
+        const double pca = col[3] - gj;
+        vals[3] = pca * pca;
+        vals[5] = gj * qan;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c.cols_out[q * c.ldx + j] = col[q];
+    }
+  } else if (op == OP_KKT) {
+    double col[1];
+    column_sums<1>(c, b, col, j, smem);
+    if (threadIdx.x < kColsPerBlock && j < c.n) {
+      c.cols_out[j] = col[0];
+      if (c.C) {
+        const Slot& sx = c.slot[c.sX];
+        const double qj = sx.q[j], gj = c.g[j];
+        const double pc = col[0] - gj;
+        vals[0] = pc * pc;
+        vals[1] = gj * qj;
+        vals[2] = qj * qj;
+      }
+    }
+  } else if (op == OP_DIFF || op == OP_DIST) {
+    double col[1];
+    column_sums<1>(c, b, col, j, smem);
+    if (threadIdx.x < kColsPerBlock && j < c.n) {
+      c.cols_out[j] = col[0];
+      const double* qa = (op == OP_DIFF) ? c.slot[c.sX].q : c.slot[c.sZ].q;
+      const double* qb = (op == OP_DIFF) ? c.slot[c.sXn].q : c.slot[c.sCand].q;
+      const double dq = qb[j] - qa[j];
+      vals[0] = dq * dq;
+      vals[1] = dq * col[0];
+    }
+  } else if (op == OP_ROUND) {
+    double col[1];
+    column_sums<1>(c, b, col, j, smem);
+    if (threadIdx.x < kColsPerBlock && j < c.n) {
+      c.cols_out[j] = col[0];
+      const double gj = c.g[j];
+      if (c.round_stage == 1) {                       // rounding.py:26-28
+        c.vec_b[j] = col[0] > 0.0 ? fmin(gj / col[0], 1.0) : 1.0;
+      } else if (c.round_stage == 2) {                // rounding.py:34
+        const double e = gj - col[0];
+        c.vec_b[c.ldx + j] = e < 0.0 ? 0.0 : e;
+      } else if (c.round_stage == 3) {
+        vals[0] = gj * c.slot[c.sX].q[j];             // dual objective, pdhg.py:384
+        const double pc = col[0] - gj;
+        vals[1] = fabs(pc);
+      }
+    }
+  }
+  block_sum<kMaxColScal>(vals, smem);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < kMaxColScal; ++s) c.colblk[(int64_t)b * kMaxColScal + s] = vals[s];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// row blocks (one per row tile)
+// ---------------------------------------------------------------------------
+__device__ void row_block(Ctl& c, int op, int t, double* smem) {
+  double vals[kMaxRowScal];
+#pragma unroll
+  for (int s = 0; s < kMaxRowScal; ++s) vals[s] = 0.0;
+  const int64_t i0 = (int64_t)t * c.TM;
+  const int rows = (int)imin64(c.TM, c.m - i0);
+  // row-side scalars / tile scalars of this op
+  const int nr = op == OP_STEP ? 7 : op == OP_KKT ? 3 : op == OP_ROUND ? 3 : 2;
+  const int ns = op == OP_STEP ? 6 : op == OP_KKT ? 3 : 1;
+  for (int r = threadIdx.x; r < c.TM; r += kRedThreads) {
+    const int64_t i = i0 + r;
+    const bool ok = r < rows;
+    if (op == OP_STEP) {
+      double row[4];
+      row_sums<4>(c, ok ? i : c.m, row);
+      if (ok) {
+        const Slot& sx = c.slot[c.sX];
+        const Slot& sa = c.slot[c.sA];
+        const double pi = sx.p[i], fi = c.f[i];
+        const double pn = pi + c.sigma * (fi - row[0]);       // pdhg.py:127
+        const double dp = pn - pi;                             // pdhg.py:140
+        c.slot[c.sXn].p[i] = pn;
+        vals[0] += dp * dp;
+        vals[1] += dp * row[1];
+        const double prx = row[2] - fi;                        // kkt.py:68
+        vals[2] += prx * prx;
+        vals[4] += fi * pn;
+        vals[6] += pn * pn;
+        if (!c.unit) {
+          const double pai = sa.p[i];
+          const double pan = pai + (pn - pai) / c.kd;          // pdhg.py:316
+          c.slot[c.sAn].p[i] = pan;
+          const double pra = row[3] - fi;
+          vals[3] += pra * pra;
+          vals[5] += fi * pan;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c.rows_out[q * c.m + i] = row[q];
+      }
+    } else if (op == OP_KKT) {
+      double row[1];
+      row_sums<1>(c, ok ? i : c.m, row);
+      if (ok) {
+        c.rows_out[i] = row[0];
+        if (c.C) {
+          const double pi = c.slot[c.sX].p[i], fi = c.f[i];
+          const double pr = row[0] - fi;
+          vals[0] += pr * pr;
+          vals[1] += fi * pi;
+          vals[2] += pi * pi;
+        }
+      }
+    } else if (op == OP_DIFF || op == OP_DIST) {
+      double row[1];
+      row_sums<1>(c, ok ? i : c.m, row);
+      if (ok) {
+        c.rows_out[i] = row[0];
+        const double* pa = (op == OP_DIFF) ? c.slot[c.sX].p : c.slot[c.sZ].p;
+        const double* pb = (op == OP_DIFF) ? c.slot[c.sXn].p : c.slot[c.sCand].p;
+        const double dp = pb[i] - pa[i];
+        vals[0] += dp * dp;
+        vals[1] += dp * row[0];
+      }
+    } else if (op == OP_ROUND) {
+      double row[1];
+      row_sums<1>(c, ok ? i : c.m, row);
+      if (ok) {
+        c.rows_out[i] = row[0];
+        const double fi = c.f[i];
+        if (c.round_stage == 0) {                                  // rounding.py:21-24
+          c.vec_a[i] = row[0] > 0.0 ? fmin(fi / row[0], 1.0) : 1.0;
+        } else if (c.round_stage == 2) {                           // rounding.py:33-35
+          const double e = fi - row[0];
+          const double er = e < 0.0 ? 0.0 : e;
+          c.vec_a[c.m + i] = er;
+          vals[0] += er;
+        } else if (c.round_stage == 3) {
+          vals[1] += fi * c.slot[c.sX].p[i];
+          vals[2] += fabs(row[0] - fi);
+        }
+      }
+    }
+  }
+  block_sum<kMaxRowScal>(vals, smem);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nr; ++s) c.rowblk[(int64_t)t * kMaxRowScal + s] = vals[s];
+  }
+  // tile scalars of this row tile (sum over column tiles, in order)
+  if (threadIdx.x < ns) {
+    double acc = 0.0;
+    for (int64_t u = 0; u < c.U; ++u) acc += __ldcg(c.tilescal + ((int64_t)t * c.U + u) * kMaxNS + threadIdx.x);
+    c.rowblk[(int64_t)t * kMaxRowScal + nr + threadIdx.x] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// controller
+// ---------------------------------------------------------------------------
+struct Sums {
+  double R[kMaxRowScal];  // row side (+ tile scalars), hierarchical over row tiles
+  double K[kMaxColScal];  // column side, over column blocks
+};
+
+__device__ void reduce_blocks(const Ctl& c, Sums* S, double* smem) {
+  // row side: (scalar s, group g, half h) -> 16 * 8 * 2 = 256 threads
+  {
+    const int tid = threadIdx.x;
+    const int s = tid >> 4, g = (tid >> 1) & 7, h = tid & 1;
+    const int64_t GS = (c.T + kGroups - 1) / kGroups;
+    const int64_t t0 = g * GS, t1 = imin64(c.T, t0 + GS);
+    const int64_t mid = t0 + (imax64(t1 - t0, 0) + 1) / 2;
+    const int64_t a = h ? mid : t0, e = h ? t1 : mid;
+    double acc = 0.0;
+    for (int64_t t = a; t < e; ++t) acc += __ldcg(c.rowblk + t * kMaxRowScal + s);
+    smem[tid] = acc;
+  }
+  // column side: (scalar s, part w) -> 8 * 32
+  {
+    const int tid = threadIdx.x;
+    const int s = tid >> 5, w = tid & 31;
+    const int64_t per = (c.CB + 31) / 32;
+    const int64_t b0 = w * per, b1 = imin64(c.CB, b0 + per);
+    double acc = 0.0;
+    for (int64_t b = b0; b < b1; ++b) acc += __ldcg(c.colblk + b * kMaxColScal + s);
+    smem[256 + tid] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x < kMaxRowScal) {
+    const int s = threadIdx.x;
+    double g8[kGroups];
+    for (int g = 0; g < kGroups; ++g) g8[g] = smem[s * 16 + g * 2] + smem[s * 16 + g * 2 + 1];
+    S->R[s] = pair8(g8);
+  } else if (threadIdx.x >= 32 && threadIdx.x < 32 + kMaxColScal) {
+    const int s = threadIdx.x - 32;
+    double acc = 0.0;
+    for (int w = 0; w < 32; ++w) acc += smem[256 + s * 32 + w];
+    S->K[s] = acc;
+  }
+  __syncthreads();
+}
+
+__device__ void ring_push(Ctl& c, int type, int ia, double x, double y, double z) {
+  if (!c.ring) return;
+  Event* e = c.ring + (c.ring_head & (kRingCap - 1));
+  e->type = type;
+  e->ia = ia;
+  e->x = x;
+  e->y = y;
+  e->z = z;
+  c.ring_head += 1;
+}
+
+// kkt.py:79-85: returns the configured metric, *rel = relative composite
+__device__ double kkt_metric(const Ctl& c, double psq, double dsq, double pobj, double dobj, double* rel) {
+  const double gap = pobj - dobj;
+  const double gr = gap / c.scale_R;
+  const double comp = sqrt(psq + dsq + gr * gr);
+  const double r = sqrt(psq) / (1.0 + c.marg_norm) + sqrt(dsq) / (1.0 + c.cost_fro) +
+                   fabs(gap) / (1.0 + fabs(pobj) + fabs(dobj));
+  *rel = r;
+  return c.relative ? r : comp;
+}
+
+__device__ int pick_free(const Ctl& c, int avoid) {
+  for (int s = 0; s < kNSlot; ++s)
+    if (s != c.sX && s != c.sA && s != c.sZ && s != c.sB && s != avoid) return s;
+  return -1;  // unreachable with kNSlot = 6
+}
+
+__device__ void prepare_step(Ctl& c) {
+  c.sXn = pick_free(c, -1);
+  c.sAn = pick_free(c, c.sXn);
+  c.tau = c.eta / c.omega;     // pdhg.py:86-87
+  c.sigma = c.eta * c.omega;   // pdhg.py:90-91
+  c.kd = (double)(c.inner + 1);
+  c.op = OP_STEP;
+}
+
+__device__ void finish(Ctl& c, int reason, int final_slot, double final_rel) {
+  c.done = 1;
+  c.reason = reason;
+  c.sFinal = final_slot;
+  c.final_rel = final_rel;
+  c.op = OP_NONE;
+}
+
+__device__ void fail(Ctl& c, int err) {
+  c.done = 1;
+  c.error = err;
+  c.op = OP_NONE;
+}
+
+// pdhg.py:363-376
+__device__ void do_restart(Ctl& c, int cand_slot, double cand_kkt) {
+  ring_push(c, EV_RESTART, (int)c.inner, cand_kkt, c.omega, 0.0);
+  c.outer += 1;
+  c.inner = 0;
+  c.sX = c.sA = c.sZ = cand_slot;
+  c.epoch_kkt = cand_kkt;
+  c.prev_cand = cand_kkt;
+  c.pending = 0;
+}
+
+// pdhg.py:198-222
+__device__ bool should_restart(const Ctl& c, double cand) {
+  if (!c.adaptive) return cand <= c.beta * c.epoch_kkt;
+  if (cand <= c.beta_suff * c.epoch_kkt) return true;
+  if (cand <= c.beta_nec * c.epoch_kkt && cand > c.prev_cand) return true;
+  return (double)c.inner >= c.beta_art * (double)c.total;
+}
+
+// loop-top limit checks, pdhg.py:299-306
+__device__ bool limits_hit(Ctl& c) {
+  if (c.total >= c.max_iters) {
+    finish(c, R_ITER, c.sB, c.best_rel);
+    return true;
+  }
+  if (c.stop_request || (c.deadline_ns != 0 && globaltimer_ns() > c.deadline_ns)) {
+    finish(c, R_TIME, c.sB, c.best_rel);
+    return true;
+  }
+  return false;
+}
+
+__device__ void control_step(Ctl& c, const Sums& S) {
+  // ---- 1. resolve the KKT of the input iterate (evaluated at pdhg.py:331-378)
+  if (c.pending) {
+    c.pending = 0;
+    double rel_cur, rel_avg;
+    const double kc = kkt_metric(c, c.pend_psq_cur, S.R[11], c.pend_pobj_cur, c.pend_dobj_cur, &rel_cur);
+    const double ka = kkt_metric(c, c.pend_psq_avg, S.R[12], c.pend_pobj_avg, c.pend_dobj_avg, &rel_avg);
+    const bool take_cur = kc < ka;  // tie -> average (pdhg.py:335-338)
+    const int cand_slot = take_cur ? c.sX : c.sA;
+    const double cand = take_cur ? kc : ka;
+    const double cand_rel = take_cur ? rel_cur : rel_avg;
+    if (c.trace_level > 0) ring_push(c, EV_CAND, 0, cand, 0.0, 0.0);
+    if (cand < c.best_kkt) {  // pdhg.py:342-344 (role alias instead of a copy)
+      c.sB = cand_slot;
+      c.best_kkt = cand;
+      c.best_rel = cand_rel;
+    }
+    if (cand <= c.tol) {  // pdhg.py:345-348
+      finish(c, R_TOL, cand_slot, cand_rel);
+      return;
+    }
+    if (should_restart(c, cand)) {
+      if (c.adaptive) {  // need |cand - anchor| first: one distance pass
+        c.sCand = cand_slot;
+        c.cand_kkt = cand;
+        c.cand_rel = cand_rel;
+        c.op = OP_DIST;
+        return;
+      }
+      do_restart(c, cand_slot, cand);
+      prepare_step(c);  // the speculative trial started from the old iterate: rerun
+      return;
+    }
+    c.prev_cand = cand;
+  }
+  // ---- 2. loop top
+  if (limits_hit(c)) return;
+  // ---- 3. the trial step of this pass (pdhg.py:230-251)
+  const double dd = S.R[7], dpp = S.R[0], dqq = S.K[0];
+  double bound = INFINITY;
+  if (c.adaptive) {
+    const double numer = c.omega * dd + (dpp + dqq) / c.omega;
+    const double denom = 2.0 * fabs(S.R[1] + S.K[1]);
+    bound = denom <= c.eps_zero ? INFINITY : numer / denom;
+    if (!(c.eta <= bound)) {
+      c.halvings += 1;
+      c.rejected += 1;
+      if (c.trace_level > 1) ring_push(c, EV_REJECT, 0, c.eta, bound, 0.0);
+      if (c.halvings >= 80) {
+        fail(c, E_LINESEARCH);
+        return;
+      }
+      c.eta *= 0.5;
+      prepare_step(c);
+      return;
+    }
+  }
+  if (c.trace_level > 0) ring_push(c, EV_ACCEPT, c.adaptive, c.eta, bound, 0.0);
+  if (c.adaptive && isfinite(bound)) {
+    const double grown = 1.05 * c.eta;
+    c.eta = bound < grown ? bound : grown;  // min(1.05 eta, bound)
+  }
+  c.halvings = 0;
+  c.total += 1;
+  c.inner += 1;
+  c.sX = c.sXn;
+  c.sA = c.sAn;
+  // pdhg.py:319-322
+  const double nrm = sqrt((S.R[10] + S.R[6]) + S.K[6]);
+  if (!isfinite(nrm)) {
+    fail(c, E_NONFINITE);
+    return;
+  }
+  if (nrm > c.scale_R) c.scale_R = nrm;
+  if (c.inner % c.kkt_stride == 0) {
+    c.pending = 1;
+    c.pend_psq_cur = S.R[2] + S.K[2];
+    c.pend_pobj_cur = S.R[8];
+    c.pend_dobj_cur = S.R[4] + S.K[4];
+    c.pend_psq_avg = S.R[3] + S.K[3];
+    c.pend_pobj_avg = S.R[9];
+    c.pend_dobj_avg = S.R[5] + S.K[5];
+  }
+  prepare_step(c);
+}
+
+__device__ void control_dist(Ctl& c, const Sums& S) {
+  // pdhg.py:353-362 + primal_weight_update pdhg.py:174-186
+  const double dX = sqrt(S.R[2]);
+  const double dpq = sqrt(S.R[0] + S.K[0]);
+  if (dX > c.eps_zero && dpq > c.eps_zero)
+    c.omega = exp(c.theta * log(dpq / dX) + (1.0 - c.theta) * log(c.omega));
+  do_restart(c, c.sCand, c.cand_kkt);
+  prepare_step(c);
+}
+
+__device__ void control_start(Ctl& c, const Sums& S) {
+  // pdhg.py:278-296
+  const double nrm = sqrt((S.R[5] + S.R[2]) + S.K[2]);
+  c.scale_R = nrm > 1.0 ? nrm : 1.0;
+  const double psq = S.R[0] + S.K[0];
+  const double pobj = S.R[3], dsq = S.R[4];
+  const double dobj = S.R[1] + S.K[1];
+  double rel;
+  const double k0 = kkt_metric(c, psq, dsq, pobj, dobj, &rel);
+  c.epoch_kkt = c.prev_cand = c.best_kkt = k0;
+  c.best_rel = rel;
+  c.sA = c.sZ = c.sB = c.sX;
+  c.pending = 0;
+  ring_push(c, EV_START, 0, k0, rel, 0.0);
+  if (k0 <= c.tol) {
+    finish(c, R_TOL, c.sX, rel);
+    return;
+  }
+  prepare_step(c);
+}
+
+__device__ void control_unit(Ctl& c, int op, const Sums& S) {
+  if (op == OP_KKT) {
+    const double psq = S.R[0] + S.K[0];
+    const double pobj = S.R[3], dsq = S.R[4];
+    const double dobj = S.R[1] + S.K[1];
+    double rel;
+    const double gap = pobj - dobj;
+    const int32_t saved = c.relative;
+    c.relative = 0;
+    const double comp = kkt_metric(c, psq, dsq, pobj, dobj, &rel);
+    c.relative = saved;
+    c.out[0] = gap; c.out[1] = comp; c.out[2] = rel; c.out[3] = pobj; c.out[4] = dobj;
+    c.out[5] = psq; c.out[6] = dsq; c.out[7] = S.R[5]; c.out[8] = S.R[2]; c.out[9] = S.K[2];
+  } else if (op == OP_DIFF) {
+    const double dd = S.R[2], dpp = S.R[0], dqq = S.K[0];
+    const double numer = c.omega * dd + (dpp + dqq) / c.omega;
+    const double denom = 2.0 * fabs(S.R[1] + S.K[1]);
+    c.out[0] = denom <= c.eps_zero ? INFINITY : numer / denom;
+    c.out[1] = dd; c.out[2] = dpp; c.out[3] = dqq; c.out[4] = S.R[1] + S.K[1];
+  } else if (op == OP_STEP) {
+    c.out[0] = S.R[7];  // |dX|^2
+    c.out[1] = S.R[10]; // |X+|^2
+  } else if (op == OP_ROUND) {
+    if (c.round_stage == 2) {
+      c.out[20] = S.R[0];                       // total deficit
+      c.out[21] = S.R[0] <= 1e-14 ? 0.0 : 1.0;  // rounding.py:36
+    } else if (c.round_stage == 3) {
+      c.out[22] = S.R[3];            // <C, X_feas>
+      c.out[23] = S.R[1] + S.K[0];   // f.p + g.q
+      c.out[19] = S.R[2] + S.K[1];   // l1 marginal violation of X_feas
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__ ctlp, int force_op) {
+  __shared__ double smem[kWarps * 4 * kColsPerBlock + 64];
+  __shared__ Sums S;
+  __shared__ int is_last;
+  Ctl& c = *ctlp;
+  if (c.done) return;
+  const int op = force_op >= 0 ? force_op : c.op;
+  if (op == OP_NONE) return;
+  if ((int64_t)blockIdx.x < c.CB) column_block(c, op, blockIdx.x, smem);
+  else row_block(c, op, (int)(blockIdx.x - c.CB), smem);
+
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(c.counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  reduce_blocks(c, &S, smem);
+  if (threadIdx.x == 0) {
+    if (c.unit) {
+      control_unit(c, op, S);
+    } else {
+      c.passes += 1;
+      if (op == OP_STEP) control_step(c, S);
+      else if (op == OP_DIST) control_dist(c, S);
+      else if (op == OP_KKT) control_start(c, S);
+      // publish to the host mirror
+      if (c.status) {
+        __threadfence_system();
+        c.status->total = c.total;
+        c.status->outer = c.outer;
+        c.status->passes = c.passes;
+        c.status->ring_head = c.ring_head;
+        c.status->final_slot = c.sFinal;
+        c.status->reason = c.reason;
+        c.status->error = c.error;
+        __threadfence_system();
+        c.status->done = c.done;
+      }
+    }
+    *c.counter = 0u;
+  }
+}
+
+}  // namespace
+
+void launch_finalize_pass(Ctl* ctl_dev, const Ctl& h, int force_op, cudaStream_t s) {
+  const unsigned blocks = (unsigned)(h.CB + h.T);
+  finalize_kernel<<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op);
+}
+
+}  // namespace pdot

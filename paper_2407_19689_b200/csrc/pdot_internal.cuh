@@ -1,0 +1,195 @@
+// Internal definitions shared by the PDOT CUDA translation units.
+//
+// Layout: every m x n matrix is row-major fp64 with an even
+// leading dimension, so a thread can own an aligned column pair and move it with
+// one 128-bit load/store.  A "slot" is one primal-dual point (X, p, q); the
+// solver keeps NSLOT slots and moves ROLES (current, average, anchor, best, the
+// two outputs of the in-flight pass) between them instead of copying matrices.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pdot {
+
+constexpr int kWarps = 8;                 // warps per streaming CTA
+constexpr int kThreads = kWarps * 32;     // 256
+constexpr int kTileN = kWarps * 64;       // 512 columns per tile (each lane: 2 columns)
+constexpr int kMaxNQ = 4;                 // row/col quantities per pass (STEP: e, d, X+, A')
+constexpr int kMaxNS = 8;                 // per-tile scalar partials
+constexpr int kGroups = 8;                // row-tile groups of the hierarchical reduction
+constexpr int kNSlot = 6;
+constexpr int kRedThreads = 256;          // finalize-kernel block size
+constexpr int kMaxRowScal = 16;           // per-row-tile scalar partials (finalize)
+constexpr int kMaxColScal = 8;            // per-column-block scalar partials (finalize)
+constexpr int kRingCap = 1 << 16;         // trace/event ring entries (host mapped)
+
+enum Op : int {
+  OP_STEP = 0,   // trial step + running average + dual-violation of the input iterate
+  OP_DIST = 1,   // ||cand - anchor||^2 at an adaptive restart
+  OP_KKT = 2,    // KKT blocks of one slot (start of solve / unit kkt_error / apply_A)
+  OP_DIFF = 3,   // rows/cols/norm of (slot b - slot a)   (unit stepsize_bound)
+  OP_ROUND = 4,  // one of the rounding passes (stage in ctl->round_stage)
+  OP_NONE = 5,
+};
+
+enum Reason : int { R_NONE = 0, R_TOL = 1, R_ITER = 2, R_TIME = 3 };
+enum Err : int { E_OK = 0, E_NONFINITE = 1, E_LINESEARCH = 2 };
+
+enum EvType : int { EV_START = 1, EV_ACCEPT = 2, EV_CAND = 3, EV_RESTART = 4, EV_REJECT = 5 };
+
+struct Event {
+  int32_t type;
+  int32_t ia;      // restart length (EV_RESTART)
+  double x, y, z;  // ACCEPT: eta, bound ; CAND: cand_kkt ; RESTART: kkt, omega ; START: kkt
+};
+
+// Host-mapped status mirror: written by the controller every pass, read by the
+// host poll loop without any copy or synchronisation.
+struct Status {
+  volatile int32_t done;
+  volatile int32_t reason;
+  volatile int32_t error;
+  volatile int32_t final_slot;
+  volatile int64_t total;
+  volatile int64_t outer;
+  volatile int64_t passes;
+  volatile int64_t ring_head;
+};
+
+struct Slot {
+  double* X;
+  double* p;
+  double* q;
+};
+
+// Device control block.  Written only by the controller thread (last block of
+// the finalize kernel) and read by every kernel of the next pass.
+struct Ctl {
+  // ---- problem / config (set once) ----
+  int64_t m, n, ldc, ldx;
+  int64_t T, U;            // row tiles, column tiles
+  int64_t TM;              // rows per tile
+  int64_t CB;              // finalize column blocks
+  double cost_fro, marg_norm;
+  double tol, beta, beta_suff, beta_nec, beta_art, theta, eps_zero;
+  int64_t max_iters, kkt_stride;
+  int32_t adaptive, relative, unit, trace_level;
+  uint64_t deadline_ns;    // %globaltimer deadline (0 = none)
+  int32_t stop_request;    // host may set to force a time-limit stop
+  // ---- step state ----
+  double eta, omega, tau, sigma, kd;
+  // ---- counters ----
+  int64_t total, inner, outer, passes, halvings, rejected, restarts_pending;
+  // ---- KKT bookkeeping ----
+  double epoch_kkt, prev_cand, best_kkt, best_rel, scale_R;
+  int32_t pending;          // KKT of the current iterate awaits this pass's dual violation
+  double pend_psq_cur, pend_pobj_cur, pend_dobj_cur;
+  double pend_psq_avg, pend_pobj_avg, pend_dobj_avg;
+  double cand_kkt, cand_rel;   // candidate that triggered the pending restart
+  double final_rel;
+  // ---- roles ----
+  int32_t sX, sA, sZ, sB, sXn, sAn, sCand, sFinal;
+  int32_t op, done, reason, error;
+  int32_t round_stage;
+  int32_t kkt_write_viol;   // unit kkt_error: also write the dual-violation matrix
+  // ---- unit-call outputs ----
+  double out[24];
+  // ---- ring ----
+  int64_t ring_head;
+  // ---- pointers ----
+  const double* C;
+  const double* f;
+  const double* g;
+  Slot slot[kNSlot];
+  double* colpart;    // [T][NQ][ldx]
+  double* rowpart;    // [U][NQ][m]
+  double* tilescal;   // [T][U][kMaxNS]
+  double* rowblk;     // [T][kMaxRowScal]
+  double* colblk;     // [CB][kMaxColScal]
+  double* rows_out;   // [NQ][m] full row sums of the last pass (finalize writes)
+  double* cols_out;   // [NQ][ldx] full column sums of the last pass
+  double* vec_a;      // scratch m (rounding row scale / error)
+  double* vec_b;      // scratch n (rounding col scale / error)
+  double* viol_out;   // unit kkt: dual-violation matrix (ldx) or null
+  unsigned int* counter;   // last-block-done counter for the finalize kernel
+  Status* status;          // host mapped
+  Event* ring;             // host mapped, kRingCap entries
+};
+
+// ---------------------------------------------------------------------------
+// small device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+  double2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_stream2(double* p, double2 v) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+// Transposed butterfly: V independent per-lane values (V a power of two, <= 32)
+// are summed across the warp.  Afterwards lane L holds the total of value
+// index (L >> s) & (V-1) with s = log2(32 / V)... computed by owner_index().
+// Every sum follows the same fixed tree, so results are deterministic.
+template <int V>
+__device__ __forceinline__ void warp_transpose_sum(double (&v)[V]) {
+  const int lane = threadIdx.x & 31;
+  int mask = 16;
+#pragma unroll
+  for (int w = V / 2; w >= 1; w /= 2) {
+    const bool upper = (lane & mask) != 0;
+#pragma unroll
+    for (int t = 0; t < w; ++t) {
+      const double send = upper ? v[t] : v[t + w];
+      const double keep = upper ? v[t + w] : v[t];
+      v[t] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+    }
+    mask >>= 1;
+  }
+#pragma unroll
+  for (; mask >= 1; mask >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], mask);
+}
+
+// value index held by `lane` after warp_transpose_sum<V>; valid for every lane
+template <int V>
+__device__ __forceinline__ int transpose_owner_index(int lane) {
+  // bits consumed: 16 -> V/2 ... ; index = lane >> (5 - log2 V)
+  constexpr int lg = (V >= 32) ? 5 : (V >= 16) ? 4 : (V >= 8) ? 3 : (V >= 4) ? 2 : (V >= 2) ? 1 : 0;
+  return lane >> (5 - lg);
+}
+
+// lane that writes value idx (the lowest lane holding it)
+template <int V>
+__device__ __forceinline__ bool transpose_is_writer(int lane) {
+  constexpr int lg = (V >= 32) ? 5 : (V >= 16) ? 4 : (V >= 8) ? 3 : (V >= 4) ? 2 : (V >= 2) ? 1 : 0;
+  return (lane & ((1 << (5 - lg)) - 1)) == 0;
+}
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+__device__ __forceinline__ double sqr_acc(double acc, double x) { return __fma_rn(x, x, acc); }
+__device__ __forceinline__ double mul_acc(double acc, double x, double y) { return __fma_rn(x, y, acc); }
+
+// numpy np.maximum(x, 0.0) for a scalar: NaN propagates, -0.0 stays -0.0
+__device__ __forceinline__ double relu_np(double x) { return x < 0.0 ? 0.0 : x; }
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// host-side launchers (defined in the .cu files)
+// ---------------------------------------------------------------------------
+void launch_stream_pass(const Ctl* ctl_dev, const Ctl& ctl_host, int force_op, cudaStream_t s);
+void launch_finalize_pass(Ctl* ctl_dev, const Ctl& ctl_host, int force_op, cudaStream_t s);
+size_t stream_smem_bytes(int64_t TM);
+
+}  // namespace pdot

@@ -1,0 +1,814 @@
+// Host runtime and C ABI of libpdot.so (include/pdot.h).
+//
+// One handle = one m x n problem shape on one GPU: it owns the NSLOT primal-dual
+// slots, the reduction partials, the device control block, a host-mapped status
+// mirror and trace ring, and one CUDA graph of `L` (stream pass, finalize pass)
+// pairs.  pdot_solve() replays that graph until the device controller reports
+// done; the host only polls the mapped status between graph launches (two
+// batches in flight), so no iteration waits on the host.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <chrono>
+#include <string>
+#include <vector>
+
+#include "../../include/pdot.h"
+#include "pdot_internal.cuh"
+
+using pdot::Ctl;
+
+struct pdot_solver {
+  int device = 0;
+  int64_t m = 0, n = 0, ldx = 0, TM = 0, T = 0, U = 0, CB = 0;
+  cudaStream_t stream = nullptr;
+  Ctl host{};
+  Ctl* dev = nullptr;
+  double* slot_mem = nullptr;
+  double* work = nullptr;
+  unsigned* counter = nullptr;
+  pdot::Status* status_h = nullptr;
+  pdot::Status* status_d = nullptr;
+  pdot::Event* ring_h = nullptr;
+  pdot::Event* ring_d = nullptr;
+  int64_t ring_tail = 0;
+  std::vector<pdot_event> events;
+  cudaGraphExec_t graph = nullptr;
+  int graph_L = 0;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  int64_t launches = 0;
+  bool problem_set = false;
+  std::chrono::steady_clock::time_point wall0;
+  double elapsed_before = 0.0;
+  int poll_L = 8;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what, int line) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "CUDA error %s (%s) at solver.cu:%d in %s", cudaGetErrorName(e),
+           cudaGetErrorString(e), line, what);
+  return set_err(PDOT_ECUDA, buf);
+}
+
+#define CK(x)                                                  \
+  do {                                                         \
+    cudaError_t e_ = (x);                                      \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #x, __LINE__); \
+  } while (0)
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+__global__ void stamp_deadline_kernel(Ctl* c, uint64_t remaining_ns) {
+  c->deadline_ns = pdot::globaltimer_ns() + remaining_ns;
+}
+
+__global__ void set_int_kernel(int32_t* p, int32_t v) { *p = v; }
+
+__global__ void apply_at_kernel(const double* __restrict__ p, const double* __restrict__ q, int64_t m,
+                                int64_t n, double* __restrict__ out, int64_t ldo) {
+  const int64_t total = m * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    out[i * ldo + j] = p[i] + q[j];  // operator.py:43
+  }
+}
+
+__global__ void gen_cost_kernel(double* __restrict__ C, int64_t m, int64_t n, int64_t ldc, int kind,
+                                int64_t a0, int64_t a1, int64_t a2, int64_t a3) {
+  const int64_t total = m * ldc;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / ldc, j = e - i * ldc;
+    int64_t v = 0;
+    if (j < n) {
+      if (kind == PDOT_COST_SQEUCLID_GRID || kind == PDOT_COST_L1_GRID) {
+        const int64_t r = a0;
+        const int64_t di = i / r - j / r, dj = i % r - j % r;
+        v = (kind == PDOT_COST_SQEUCLID_GRID) ? di * di + dj * dj : (di < 0 ? -di : di) + (dj < 0 ? -dj : dj);
+      } else {
+        const int64_t sc = a1, tc = a3;
+        const int64_t ai = 2 * (i / sc), bi = 2 * (i % sc);
+        const int64_t cj = j / tc, dj = j % tc;
+        const int64_t x = ai - cj, y = bi - dj;
+        v = (x < 0 ? -x : x) + (y < 0 ? -y : y);
+      }
+    }
+    C[e] = (double)v;
+  }
+}
+
+// deterministic sum of squares: per-block fixed tree, then one block in order
+__global__ void sumsq_partial_kernel(const double* __restrict__ C, int64_t m, int64_t n, int64_t ldc,
+                                     double* __restrict__ part) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  const int64_t total = m * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    const double v = C[i * ldc + j];
+    acc = __fma_rn(v, v, acc);
+  }
+  for (int msk = 16; msk >= 1; msk >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, msk);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+__global__ void sum_final_kernel(const double* __restrict__ part, int nb, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[b];
+    *out = sqrt(s);
+  }
+}
+
+int check_ld(int64_t ld, int64_t n, const char* what) {
+  if (ld < n || (ld & 1)) {
+    return set_err(PDOT_EINVAL, std::string(what) + ": leading dimension must be >= n and even");
+  }
+  return PDOT_OK;
+}
+
+int upload_ctl(pdot_solver* h) {
+  CK(cudaMemcpyAsync(h->dev, &h->host, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
+  return PDOT_OK;
+}
+
+int download_ctl(pdot_solver* h) {
+  CK(cudaMemcpyAsync(&h->host, h->dev, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return PDOT_OK;
+}
+
+// one (stream, finalize) pass with an explicit op, outside any graph
+int run_pass(pdot_solver* h, int op) {
+  pdot::launch_stream_pass(h->dev, h->host, op, h->stream);
+  pdot::launch_finalize_pass(h->dev, h->host, op, h->stream);
+  h->launches += 2;
+  CK(cudaGetLastError());
+  return PDOT_OK;
+}
+
+void unit_ctl(pdot_solver* h) {
+  Ctl& c = h->host;
+  c.unit = 1;
+  c.done = 0;
+  c.status = nullptr;
+  c.ring = nullptr;
+  c.kkt_write_viol = 0;
+  c.viol_out = nullptr;
+}
+
+int copy_matrix(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t m, int64_t n,
+                cudaStream_t s) {
+  CK(cudaMemcpy2DAsync(dst, ldd * sizeof(double), src, lds * sizeof(double), n * sizeof(double), m,
+                       cudaMemcpyDefault, s));
+  return PDOT_OK;
+}
+
+int copy_vec(double* dst, const double* src, int64_t n, cudaStream_t s) {
+  CK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDefault, s));
+  return PDOT_OK;
+}
+
+void drain_ring(pdot_solver* h) {
+  const int64_t head = h->status_h->ring_head;
+  for (int64_t t = h->ring_tail; t < head; ++t) {
+    const pdot::Event& e = h->ring_h[t & (pdot::kRingCap - 1)];
+    pdot_event o;
+    o.type = e.type;
+    o.ia = e.ia;
+    o.x = e.x;
+    o.y = e.y;
+    o.z = e.z;
+    h->events.push_back(o);
+  }
+  h->ring_tail = head;
+}
+
+int build_graph(pdot_solver* h, int L) {
+  if (h->graph && h->graph_L == L) return PDOT_OK;
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  for (int i = 0; i < L; ++i) {
+    pdot::launch_stream_pass(h->dev, h->host, -1, h->stream);
+    pdot::launch_finalize_pass(h->dev, h->host, -1, h->stream);
+  }
+  CK(cudaStreamEndCapture(h->stream, &g));
+  CK(cudaGraphInstantiate(&h->graph, g, 0));
+  cudaGraphDestroy(g);
+  h->graph_L = L;
+  return PDOT_OK;
+}
+
+int auto_batch(const pdot_solver* h) {
+  // aim for ~10 ms of work per graph launch, 4..64 passes
+  const double est_us = 40.0 * (double)h->m * (double)h->n / 6.0e6 + 8.0;
+  int L = (int)(10000.0 / est_us);
+  if (L < 4) L = 4;
+  if (L > 64) L = 64;
+  return L;
+}
+
+// replay the graph until the controller reports done
+int drive(pdot_solver* h, int L) {
+  int rc = build_graph(h, L);
+  if (rc) return rc;
+  int64_t i = 0;
+  for (;;) {
+    CK(cudaGraphLaunch(h->graph, h->stream));
+    h->launches += 2 * L;
+    CK(cudaEventRecord(h->ev[i & 1], h->stream));
+    if (i > 0) {
+      CK(cudaEventSynchronize(h->ev[(i - 1) & 1]));
+      drain_ring(h);
+      if (h->status_h->done) break;
+    }
+    ++i;
+  }
+  CK(cudaEventRecord(h->t1, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  drain_ring(h);
+  return PDOT_OK;
+}
+
+int result_from_ctl(pdot_solver* h, pdot_result* res, double wall_s) {
+  int rc = download_ctl(h);
+  if (rc) return rc;
+  const Ctl& c = h->host;
+  if (res) {
+    res->reason = c.reason;
+    res->final_slot = c.sFinal;
+    res->iterations = c.total;
+    res->restarts = c.outer;
+    res->passes = c.passes;
+    res->rejected = c.rejected;
+    res->final_relative_kkt = c.final_rel;
+    res->eta = c.eta;
+    res->omega = c.omega;
+    res->scale_R = c.scale_R;
+    res->elapsed_s = wall_s;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->t0, h->t1);
+    res->device_s = ms * 1e-3;
+  }
+  if (c.error == pdot::E_NONFINITE)
+    return set_err(PDOT_ENONFINITE, "numerical failure: non-finite iterate");
+  if (c.error == pdot::E_LINESEARCH)
+    return set_err(PDOT_ELINESEARCH, "step-size line search failed to find an admissible eta");
+  return PDOT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pdot_last_error(void) { return g_err.c_str(); }
+
+int pdot_version(void) { return 1; }
+
+int pdot_create(int64_t m, int64_t n, int device, pdot_solver** out) {
+  if (!out) return set_err(PDOT_EINVAL, "null output handle");
+  *out = nullptr;
+  if (m < 1 || n < 1) return set_err(PDOT_EINVAL, "plan dimensions must be positive");
+  DeviceGuard dg(device);
+  CK(cudaSetDevice(device));
+  pdot_solver* h = new pdot_solver();
+  h->device = device;
+  h->m = m;
+  h->n = n;
+  h->ldx = round_up(n, 2);
+  int64_t TM = 128;
+  if (const char* e = getenv("PDOT_TM")) TM = atoll(e);
+  if (TM != 64 && TM != 128 && TM != 256) TM = 128;
+  h->TM = TM;
+  h->T = (m + TM - 1) / TM;
+  h->U = (n + pdot::kTileN - 1) / pdot::kTileN;
+  h->CB = (n + 63) / 64;
+
+  const int64_t mat = m * h->ldx;
+  const int64_t per_slot = mat + round_up(m, 2) + h->ldx;
+  size_t bytes_slots = (size_t)per_slot * pdot::kNSlot * sizeof(double);
+  // work: colpart T*4*ldx, rowpart U*4*m, tilescal T*U*kMaxNS, rowblk T*16, colblk CB*8,
+  //       rows_out 4*m, cols_out 4*ldx, vec_a 2*m, vec_b 2*ldx, scratch 64
+  const int64_t w_colpart = h->T * 4 * h->ldx;
+  const int64_t w_rowpart = h->U * 4 * round_up(m, 2);
+  const int64_t w_tiles = h->T * h->U * pdot::kMaxNS;
+  const int64_t w_rowblk = h->T * pdot::kMaxRowScal;
+  const int64_t w_colblk = h->CB * pdot::kMaxColScal;
+  const int64_t w_rows = 4 * round_up(m, 2), w_cols = 4 * h->ldx;
+  const int64_t w_va = 2 * round_up(m, 2), w_vb = 2 * h->ldx;
+  const int64_t w_total = w_colpart + w_rowpart + w_tiles + w_rowblk + w_colblk + w_rows + w_cols + w_va +
+                          w_vb + 4096;
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaMalloc(&h->dev, sizeof(Ctl))) != cudaSuccess ||
+      (e = cudaMalloc(&h->slot_mem, bytes_slots)) != cudaSuccess ||
+      (e = cudaMalloc(&h->work, (size_t)w_total * sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&h->counter, sizeof(unsigned) * 4)) != cudaSuccess ||
+      (e = cudaHostAlloc(&h->status_h, sizeof(pdot::Status), cudaHostAllocMapped)) != cudaSuccess ||
+      (e = cudaHostAlloc(&h->ring_h, sizeof(pdot::Event) * pdot::kRingCap, cudaHostAllocMapped)) !=
+          cudaSuccess ||
+      (e = cudaHostGetDevicePointer(&h->status_d, h->status_h, 0)) != cudaSuccess ||
+      (e = cudaHostGetDevicePointer(&h->ring_d, h->ring_h, 0)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&h->ev[0], cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&h->ev[1], cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreate(&h->t0)) != cudaSuccess || (e = cudaEventCreate(&h->t1)) != cudaSuccess) {
+    int rc = cuda_fail(e, "pdot_create allocation", __LINE__);
+    pdot_destroy(h);
+    return rc;
+  }
+  memset((void*)h->status_h, 0, sizeof(pdot::Status));
+  if ((e = cudaMemsetAsync(h->slot_mem, 0, bytes_slots, h->stream)) != cudaSuccess ||
+      (e = cudaMemsetAsync(h->work, 0, (size_t)w_total * sizeof(double), h->stream)) != cudaSuccess ||
+      (e = cudaMemsetAsync(h->counter, 0, sizeof(unsigned) * 4, h->stream)) != cudaSuccess) {
+    int rc = cuda_fail(e, "pdot_create memset", __LINE__);
+    pdot_destroy(h);
+    return rc;
+  }
+  Ctl& c = h->host;
+  memset(&c, 0, sizeof(Ctl));
+  c.m = m;
+  c.n = n;
+  c.ldx = h->ldx;
+  c.ldc = h->ldx;
+  c.T = h->T;
+  c.U = h->U;
+  c.TM = TM;
+  c.CB = h->CB;
+  for (int s = 0; s < pdot::kNSlot; ++s) {
+    double* base = h->slot_mem + (size_t)s * per_slot;
+    c.slot[s].X = base;
+    c.slot[s].p = base + mat;
+    c.slot[s].q = base + mat + round_up(m, 2);
+  }
+  double* w = h->work;
+  c.colpart = w; w += w_colpart;
+  c.rowpart = w; w += w_rowpart;
+  c.tilescal = w; w += w_tiles;
+  c.rowblk = w; w += w_rowblk;
+  c.colblk = w; w += w_colblk;
+  c.rows_out = w; w += w_rows;
+  c.cols_out = w; w += w_cols;
+  c.vec_a = w; w += w_va;
+  c.vec_b = w; w += w_vb;
+  c.counter = h->counter;
+  c.status = h->status_d;
+  c.ring = h->ring_d;
+  c.op = pdot::OP_NONE;
+  c.done = 1;
+  c.sX = 0;
+  c.sA = c.sZ = c.sB = 0;
+  if (upload_ctl(h) != PDOT_OK || cudaStreamSynchronize(h->stream) != cudaSuccess) {
+    int rc = set_err(PDOT_ECUDA, "pdot_create: control block upload failed");
+    pdot_destroy(h);
+    return rc;
+  }
+  // kernel attributes once, outside any capture
+  pdot::launch_stream_pass(h->dev, h->host, pdot::OP_NONE, h->stream);
+  if ((e = cudaStreamSynchronize(h->stream)) != cudaSuccess) {
+    int rc = cuda_fail(e, "pdot_create warmup", __LINE__);
+    pdot_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return PDOT_OK;
+}
+
+int pdot_destroy(pdot_solver* h) {
+  if (!h) return PDOT_OK;
+  DeviceGuard dg(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  if (h->dev) cudaFree(h->dev);
+  if (h->slot_mem) cudaFree(h->slot_mem);
+  if (h->work) cudaFree(h->work);
+  if (h->counter) cudaFree(h->counter);
+  if (h->status_h) cudaFreeHost(h->status_h);
+  if (h->ring_h) cudaFreeHost(h->ring_h);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->t0) cudaEventDestroy(h->t0);
+  if (h->t1) cudaEventDestroy(h->t1);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return PDOT_OK;
+}
+
+int pdot_geometry(const pdot_solver* h, int64_t* ldx, int64_t* row_tile, int64_t* n_row_tiles,
+                  int64_t* n_col_tiles) {
+  if (!h) return set_err(PDOT_EINVAL, "null handle");
+  if (ldx) *ldx = h->ldx;
+  if (row_tile) *row_tile = h->TM;
+  if (n_row_tiles) *n_row_tiles = h->T;
+  if (n_col_tiles) *n_col_tiles = h->U;
+  return PDOT_OK;
+}
+
+int pdot_set_problem(pdot_solver* h, const double* C_dev, int64_t ldc, const double* f_dev,
+                     const double* g_dev, double cost_fro_norm, double marginal_norm) {
+  if (!h || !C_dev || !f_dev || !g_dev) return set_err(PDOT_EINVAL, "null argument");
+  if (int rc = check_ld(ldc, h->n, "C")) return rc;
+  if (((uintptr_t)C_dev & 15) != 0) return set_err(PDOT_EINVAL, "C must be 16-byte aligned");
+  h->host.C = C_dev;
+  h->host.ldc = ldc;
+  h->host.f = f_dev;
+  h->host.g = g_dev;
+  h->host.cost_fro = cost_fro_norm;
+  h->host.marg_norm = marginal_norm;
+  h->problem_set = true;
+  return PDOT_OK;
+}
+
+int pdot_set_slot(pdot_solver* h, int slot, const double* X_any, int64_t ldX, const double* p_any,
+                  const double* q_any) {
+  if (!h || slot < 0 || slot >= pdot::kNSlot) return set_err(PDOT_EINVAL, "bad handle or slot");
+  DeviceGuard dg(h->device);
+  const pdot::Slot& s = h->host.slot[slot];
+  if (X_any) {
+    if (ldX < h->n) return set_err(PDOT_EINVAL, "X: leading dimension must be >= n");
+    if (int rc = copy_matrix(s.X, h->ldx, X_any, ldX, h->m, h->n, h->stream)) return rc;
+  } else {
+    CK(cudaMemsetAsync(s.X, 0, (size_t)h->m * h->ldx * sizeof(double), h->stream));
+  }
+  if (p_any) {
+    if (int rc = copy_vec(s.p, p_any, h->m, h->stream)) return rc;
+  } else {
+    CK(cudaMemsetAsync(s.p, 0, h->m * sizeof(double), h->stream));
+  }
+  if (q_any) {
+    if (int rc = copy_vec(s.q, q_any, h->n, h->stream)) return rc;
+  } else {
+    CK(cudaMemsetAsync(s.q, 0, h->n * sizeof(double), h->stream));
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  return PDOT_OK;
+}
+
+int pdot_get_slot(pdot_solver* h, int slot, double* X_any, int64_t ldX, double* p_any, double* q_any) {
+  if (!h || slot < 0 || slot >= pdot::kNSlot) return set_err(PDOT_EINVAL, "bad handle or slot");
+  DeviceGuard dg(h->device);
+  const pdot::Slot& s = h->host.slot[slot];
+  if (X_any) {
+    if (ldX < h->n) return set_err(PDOT_EINVAL, "X: leading dimension must be >= n");
+    if (int rc = copy_matrix(X_any, ldX, s.X, h->ldx, h->m, h->n, h->stream)) return rc;
+  }
+  if (p_any)
+    if (int rc = copy_vec(p_any, s.p, h->m, h->stream)) return rc;
+  if (q_any)
+    if (int rc = copy_vec(q_any, s.q, h->n, h->stream)) return rc;
+  CK(cudaStreamSynchronize(h->stream));
+  return PDOT_OK;
+}
+
+int pdot_slot_ptrs(pdot_solver* h, int slot, double** X, double** p, double** q) {
+  if (!h || slot < 0 || slot >= pdot::kNSlot) return set_err(PDOT_EINVAL, "bad handle or slot");
+  if (X) *X = h->host.slot[slot].X;
+  if (p) *p = h->host.slot[slot].p;
+  if (q) *q = h->host.slot[slot].q;
+  return PDOT_OK;
+}
+
+int pdot_begin(pdot_solver* h, const pdot_config* cfg, double elapsed_before_s) {
+  if (!h || !cfg) return set_err(PDOT_EINVAL, "null argument");
+  if (!h->problem_set) return set_err(PDOT_ESTATE, "pdot_set_problem was not called");
+  // pdhg.py:61-75
+  if (!(cfg->tol > 0) || !(cfg->time_limit_s > 0) || cfg->max_iters < 1)
+    return set_err(PDOT_EINVAL, "tol, time_limit_s and max_iters must be positive");
+  if (!(cfg->beta > 0.0 && cfg->beta < 1.0)) return set_err(PDOT_EINVAL, "beta must lie in (0, 1)");
+  if (!(0.0 < cfg->beta_sufficient && cfg->beta_sufficient < cfg->beta_necessary && cfg->beta_necessary < 1.0))
+    return set_err(PDOT_EINVAL, "need 0 < beta_sufficient < beta_necessary < 1");
+  if (cfg->kkt_stride < 1) return set_err(PDOT_EINVAL, "kkt_stride must be >= 1");
+  if (!(cfg->omega0 > 0)) return set_err(PDOT_EINVAL, "step parameters must be positive");
+  DeviceGuard dg(h->device);
+  h->wall0 = std::chrono::steady_clock::now();
+  h->elapsed_before = elapsed_before_s;
+  h->poll_L = cfg->poll_passes > 0 ? cfg->poll_passes : auto_batch(h);
+  Ctl& c = h->host;
+  c.unit = 0;
+  c.tol = cfg->tol;
+  c.beta = cfg->beta;
+  c.beta_suff = cfg->beta_sufficient;
+  c.beta_nec = cfg->beta_necessary;
+  c.beta_art = cfg->beta_artificial;
+  c.theta = cfg->theta;
+  c.eps_zero = cfg->eps_zero;
+  c.max_iters = cfg->max_iters;
+  c.kkt_stride = cfg->kkt_stride;
+  c.adaptive = cfg->adaptive;
+  c.relative = cfg->relative;
+  c.trace_level = cfg->trace_level;
+  c.eta = cfg->eta0 > 0 ? cfg->eta0 : 1.0 / (2.0 * sqrt((double)(h->m + h->n)));
+  c.omega = cfg->omega0;
+  c.tau = c.sigma = c.kd = 0.0;
+  c.total = c.inner = c.outer = c.passes = c.halvings = c.rejected = 0;
+  c.pending = 0;
+  c.sX = c.sA = c.sZ = c.sB = c.sFinal = 0;
+  c.sXn = 1;
+  c.sAn = 2;
+  c.op = pdot::OP_KKT;
+  c.done = 0;
+  c.reason = c.error = 0;
+  c.ring_head = 0;
+  c.status = h->status_d;
+  c.ring = h->ring_d;
+  c.kkt_write_viol = 0;
+  c.viol_out = nullptr;
+  const double remaining = cfg->time_limit_s - elapsed_before_s;
+  c.stop_request = remaining <= 0.0 ? 1 : 0;
+  c.deadline_ns = 0;
+  memset((void*)h->status_h, 0, sizeof(pdot::Status));
+  h->ring_tail = 0;
+  h->events.clear();
+  if (int rc = upload_ctl(h)) return rc;
+  if (remaining > 0.0 && remaining < 1e9) {
+    stamp_deadline_kernel<<<1, 1, 0, h->stream>>>(h->dev, (uint64_t)(remaining * 1e9));
+    h->launches += 1;
+    CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(h->t0, h->stream));
+  return PDOT_OK;
+}
+
+int pdot_advance(pdot_solver* h, int64_t max_passes, pdot_progress* prog) {
+  if (!h) return set_err(PDOT_EINVAL, "null handle");
+  DeviceGuard dg(h->device);
+  if (max_passes < 0) {
+    if (int rc = drive(h, h->poll_L)) return rc;
+  } else {
+    for (int64_t i = 0; i < max_passes; ++i)
+      if (int rc = run_pass(h, -1)) return rc;
+    CK(cudaEventRecord(h->t1, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    drain_ring(h);
+  }
+  if (prog) {
+    if (int rc = download_ctl(h)) return rc;
+    const Ctl& c = h->host;
+    prog->done = c.done;
+    prog->roles[0] = c.sX;
+    prog->roles[1] = c.sA;
+    prog->roles[2] = c.sZ;
+    prog->roles[3] = c.sB;
+    prog->op = c.op;
+    prog->iterations = c.total;
+    prog->restarts = c.outer;
+    prog->passes = c.passes;
+  }
+  return PDOT_OK;
+}
+
+int pdot_finish(pdot_solver* h, pdot_result* res) {
+  if (!h) return set_err(PDOT_EINVAL, "null handle");
+  DeviceGuard dg(h->device);
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - h->wall0).count();
+  return result_from_ctl(h, res, wall + h->elapsed_before);
+}
+
+int pdot_solve(pdot_solver* h, const pdot_config* cfg, double elapsed_before_s, pdot_result* res) {
+  if (int rc = pdot_begin(h, cfg, elapsed_before_s)) return rc;
+  if (int rc = pdot_advance(h, -1, nullptr)) return rc;
+  return pdot_finish(h, res);
+}
+
+int pdot_resume(pdot_solver* h, int64_t max_iters, pdot_result* res) {
+  if (!h) return set_err(PDOT_EINVAL, "null handle");
+  DeviceGuard dg(h->device);
+  if (int rc = download_ctl(h)) return rc;
+  Ctl& c = h->host;
+  if (c.unit || c.error || c.reason == pdot::R_TOL || c.reason == pdot::R_NONE)
+    return set_err(PDOT_ESTATE, "pdot_resume: no limited run to resume");
+  c.max_iters = max_iters;
+  c.done = 0;
+  c.reason = 0;
+  c.op = pdot::OP_STEP;  // re-run the trial that the limit discarded
+  c.deadline_ns = 0;
+  c.stop_request = 0;
+  memset((void*)h->status_h, 0, sizeof(pdot::Status));
+  h->status_h->ring_head = c.ring_head;
+  if (int rc = upload_ctl(h)) return rc;
+  CK(cudaEventRecord(h->t0, h->stream));
+  const auto wall0 = std::chrono::steady_clock::now();
+  if (int rc = drive(h, h->poll_L)) return rc;
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+  return result_from_ctl(h, res, wall);
+}
+
+int64_t pdot_get_events(pdot_solver* h, pdot_event* out, int64_t cap) {
+  if (!h) return 0;
+  const int64_t k = std::min<int64_t>(cap, (int64_t)h->events.size());
+  if (out && k > 0) memcpy(out, h->events.data(), k * sizeof(pdot_event));
+  h->events.erase(h->events.begin(), h->events.begin() + k);
+  return k;
+}
+
+int pdot_round(pdot_solver* h, int slot, double* Xf_any, int64_t ldX, double* out3) {
+  if (!h || slot < 0 || slot >= pdot::kNSlot) return set_err(PDOT_EINVAL, "bad handle or slot");
+  if (!h->problem_set) return set_err(PDOT_ESTATE, "pdot_set_problem was not called");
+  DeviceGuard dg(h->device);
+  Ctl& c = h->host;
+  unit_ctl(h);
+  c.sX = slot;
+  const int scratch = (slot + 1) % pdot::kNSlot;
+  c.viol_out = Xf_any ? c.slot[scratch].X : nullptr;
+  c.round_stage = 0;
+  c.op = pdot::OP_ROUND;
+  if (int rc = upload_ctl(h)) return rc;
+  for (int stage = 0; stage < 4; ++stage) {
+    set_int_kernel<<<1, 1, 0, h->stream>>>(&h->dev->round_stage, stage);
+    h->launches += 1;
+    if (int rc = run_pass(h, pdot::OP_ROUND)) return rc;
+  }
+  double outv[5];
+  CK(cudaMemcpyAsync(outv, &h->dev->out[19], 5 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (out3) {
+    out3[0] = outv[3];  // <C, X_feas>
+    out3[1] = outv[4];  // f.p + g.q
+    out3[2] = outv[0];  // l1 marginal violation
+  }
+  if (Xf_any) {
+    if (ldX < h->n) return set_err(PDOT_EINVAL, "X_feas: leading dimension must be >= n");
+    if (int rc = copy_matrix(Xf_any, ldX, c.slot[scratch].X, h->ldx, h->m, h->n, h->stream)) return rc;
+    CK(cudaStreamSynchronize(h->stream));
+  }
+  return PDOT_OK;
+}
+
+int pdot_unit_step(pdot_solver* h, double tau, double sigma) {
+  if (!h || !h->problem_set) return set_err(PDOT_ESTATE, "problem not set");
+  DeviceGuard dg(h->device);
+  Ctl& c = h->host;
+  unit_ctl(h);
+  c.sX = 0; c.sA = 0; c.sXn = 1; c.sAn = 2;
+  c.tau = tau; c.sigma = sigma; c.kd = 1.0;
+  c.op = pdot::OP_STEP;
+  if (int rc = upload_ctl(h)) return rc;
+  if (int rc = run_pass(h, pdot::OP_STEP)) return rc;
+  CK(cudaStreamSynchronize(h->stream));
+  return PDOT_OK;
+}
+
+int pdot_unit_bound(pdot_solver* h, double omega, double eps_zero, double* out5) {
+  if (!h) return set_err(PDOT_EINVAL, "null handle");
+  DeviceGuard dg(h->device);
+  Ctl& c = h->host;
+  unit_ctl(h);
+  c.sX = 0; c.sXn = 1;
+  c.omega = omega; c.eps_zero = eps_zero;
+  c.op = pdot::OP_DIFF;
+  if (int rc = upload_ctl(h)) return rc;
+  if (int rc = run_pass(h, pdot::OP_DIFF)) return rc;
+  double o[5];
+  CK(cudaMemcpyAsync(o, &h->dev->out[0], 5 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (out5) memcpy(out5, o, sizeof(o));
+  return PDOT_OK;
+}
+
+static int unit_kkt_impl(pdot_solver* h, bool with_cost, double scale_R, double* viol_any, int64_t ldV,
+                         double* rows_any, double* cols_any, double* out10) {
+  DeviceGuard dg(h->device);
+  Ctl& c = h->host;
+  unit_ctl(h);
+  const double* Csave = c.C;
+  if (!with_cost) c.C = nullptr;
+  c.sX = 0;
+  c.scale_R = scale_R;
+  c.kkt_write_viol = (viol_any && with_cost) ? 1 : 0;
+  c.viol_out = c.kkt_write_viol ? c.slot[1].X : nullptr;
+  c.op = pdot::OP_KKT;
+  int rc = upload_ctl(h);
+  c.C = Csave;
+  if (rc) return rc;
+  if ((rc = run_pass(h, pdot::OP_KKT))) return rc;
+  double o[10];
+  CK(cudaMemcpyAsync(o, &h->dev->out[0], 10 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if (rows_any && (rc = copy_vec(rows_any, c.rows_out, h->m, h->stream))) return rc;
+  if (cols_any && (rc = copy_vec(cols_any, c.cols_out, h->n, h->stream))) return rc;
+  if (c.kkt_write_viol && (rc = copy_matrix(viol_any, ldV, c.slot[1].X, h->ldx, h->m, h->n, h->stream)))
+    return rc;
+  CK(cudaStreamSynchronize(h->stream));
+  if (out10) memcpy(out10, o, sizeof(o));
+  return PDOT_OK;
+}
+
+int pdot_unit_kkt(pdot_solver* h, double scale_R, double* viol_any, int64_t ldV, double* rows_any,
+                  double* cols_any, double* out10) {
+  if (!h || !h->problem_set) return set_err(PDOT_ESTATE, "problem not set");
+  if (!(scale_R > 0)) return set_err(PDOT_EINVAL, "scale_R must be positive");
+  if (viol_any && ldV < h->n) return set_err(PDOT_EINVAL, "viol: leading dimension must be >= n");
+  return unit_kkt_impl(h, true, scale_R, viol_any, ldV, rows_any, cols_any, out10);
+}
+
+int pdot_unit_apply_A(pdot_solver* h, double* rows_any, double* cols_any) {
+  if (!h) return set_err(PDOT_EINVAL, "null handle");
+  return unit_kkt_impl(h, false, 1.0, nullptr, 0, rows_any, cols_any, nullptr);
+}
+
+int pdot_apply_At(const double* p_dev, const double* q_dev, int64_t m, int64_t n, double* out_dev,
+                  int64_t ldo) {
+  if (!p_dev || !q_dev || !out_dev || m < 1 || n < 1 || ldo < n) return set_err(PDOT_EINVAL, "bad argument");
+  const int64_t total = m * n;
+  const int threads = 256;
+  const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 32);
+  apply_at_kernel<<<blocks, threads>>>(p_dev, q_dev, m, n, out_dev, ldo);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return PDOT_OK;
+}
+
+int pdot_gen_cost(double* C_dev, int64_t m, int64_t n, int64_t ldc, int kind, const int64_t* a) {
+  if (!C_dev || !a || m < 1 || n < 1 || ldc < n) return set_err(PDOT_EINVAL, "bad argument");
+  if (kind == PDOT_COST_SQEUCLID_GRID || kind == PDOT_COST_L1_GRID) {
+    if (a[0] * a[1] != m || m != n || a[0] != a[1]) return set_err(PDOT_EINVAL, "grid cost needs m = n = r*r");
+  } else if (kind == PDOT_COST_L1_RECT) {
+    if (a[0] * a[1] != m || a[2] * a[3] != n) return set_err(PDOT_EINVAL, "rect cost shape mismatch");
+  } else {
+    return set_err(PDOT_EINVAL, "unknown cost kind");
+  }
+  gen_cost_kernel<<<148 * 16, 256>>>(C_dev, m, n, ldc, kind, a[0], a[1], a[2], a[3]);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return PDOT_OK;
+}
+
+int pdot_fro_norm(const double* C_dev, int64_t m, int64_t n, int64_t ldc, double* out) {
+  if (!C_dev || !out || m < 1 || n < 1 || ldc < n) return set_err(PDOT_EINVAL, "bad argument");
+  const int nb = 148 * 8;
+  double* part = nullptr;
+  CK(cudaMalloc(&part, (nb + 1) * sizeof(double)));
+  sumsq_partial_kernel<<<nb, 256>>>(C_dev, m, n, ldc, part);
+  sum_final_kernel<<<1, 32>>>(part, nb, part + nb);
+  cudaError_t e = cudaMemcpy(out, part + nb, sizeof(double), cudaMemcpyDeviceToHost);
+  cudaFree(part);
+  if (e != cudaSuccess) return cuda_fail(e, "pdot_fro_norm", __LINE__);
+  return PDOT_OK;
+}
+
+int pdot_time_stream_kernel(pdot_solver* h, int iters, double* ms_per_launch) {
+  if (!h || iters < 1 || !h->problem_set) return set_err(PDOT_EINVAL, "bad argument");
+  DeviceGuard dg(h->device);
+  Ctl& c = h->host;
+  c.unit = 0;
+  c.done = 0;
+  c.status = nullptr;
+  c.ring = nullptr;
+  c.sX = 0; c.sA = 1; c.sXn = 2; c.sAn = 3;
+  c.tau = 1e-3; c.sigma = 1e-3; c.kd = 3.0;
+  c.op = pdot::OP_STEP;
+  if (int rc = upload_ctl(h)) return rc;
+  for (int i = 0; i < 2; ++i) pdot::launch_stream_pass(h->dev, h->host, pdot::OP_STEP, h->stream);
+  CK(cudaEventRecord(h->t0, h->stream));
+  for (int i = 0; i < iters; ++i) pdot::launch_stream_pass(h->dev, h->host, pdot::OP_STEP, h->stream);
+  CK(cudaEventRecord(h->t1, h->stream));
+  h->launches += iters + 2;
+  CK(cudaEventSynchronize(h->t1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->t0, h->t1));
+  if (ms_per_launch) *ms_per_launch = ms / iters;
+  c.status = h->status_d;
+  c.ring = h->ring_d;
+  c.done = 1;
+  c.op = pdot::OP_NONE;
+  return upload_ctl(h);
+}
+
+int64_t pdot_kernel_launches(const pdot_solver* h) { return h ? h->launches : 0; }
+
+}  // extern "C"

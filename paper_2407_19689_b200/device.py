@@ -1,0 +1,204 @@
+"""Device residency: problems on the GPU and cached solver handles.
+
+PyTorch is used only as the device allocator and for host<->device copies;
+all arithmetic on the path runs in libpdot.so's kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+
+def require_cuda(device: int = 0) -> None:
+    if torch is None or not torch.cuda.is_available():
+        raise RuntimeError("PDOT needs a CUDA device: there is no CPU fallback")
+    if device >= torch.cuda.device_count():
+        raise RuntimeError(f"CUDA device {device} not present")
+
+
+def even(n: int) -> int:
+    return n + (n & 1)
+
+
+def _h2d_matrix(A: np.ndarray, device: int):
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    m, n = A.shape
+    t = torch.zeros((m, even(n)), dtype=torch.float64, device=f"cuda:{device}")
+    t[:, :n].copy_(torch.from_numpy(A))
+    return t
+
+
+def _h2d_vector(v: np.ndarray, device: int):
+    return torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(f"cuda:{device}")
+
+
+class DeviceProblem:
+    """An OT problem resident in HBM: C (m x ldc, ldc even), f (m), g (n).
+
+    Exposes the OTProblem accessors the solver needs (m, n, cost_fro_norm,
+    marginal_norm; instance.py:122-150).  ``host`` keeps the originating host
+    problem when there is one.
+    """
+
+    def __init__(self, C_t, f_t, g_t, m, n, cost_fro_norm, marginal_norm, device=0, host=None):
+        self.C_t, self.f_t, self.g_t = C_t, f_t, g_t
+        self.m, self.n = int(m), int(n)
+        self.cost_fro_norm = float(cost_fro_norm)
+        self.marginal_norm = float(marginal_norm)
+        self.device = device
+        self.host = host
+
+    @property
+    def ldc(self) -> int:
+        return int(self.C_t.stride(0))
+
+    @classmethod
+    def from_host(cls, prob, device: int = 0) -> "DeviceProblem":
+        require_cuda(device)
+        C = np.asarray(prob.C, dtype=np.float64)
+        return cls(_h2d_matrix(C, device), _h2d_vector(prob.f, device), _h2d_vector(prob.g, device),
+                   C.shape[0], C.shape[1], prob.cost_fro_norm, prob.marginal_norm, device, host=prob)
+
+    @classmethod
+    def generated(cls, kind: int, m: int, n: int, shape_args, f: np.ndarray, g: np.ndarray,
+                  device: int = 0) -> "DeviceProblem":
+        """Cost built on the device (pdot_gen_cost), marginals from the host."""
+        require_cuda(device)
+        lib = _lib.load()
+        C_t = torch.empty((m, even(n)), dtype=torch.float64, device=f"cuda:{device}")
+        args = (ctypes.c_int64 * 4)(*shape_args)
+        torch.cuda.synchronize(device)
+        _lib.check(lib.pdot_gen_cost(C_t.data_ptr(), m, n, C_t.stride(0), kind, args))
+        fro = ctypes.c_double()
+        _lib.check(lib.pdot_fro_norm(C_t.data_ptr(), m, n, C_t.stride(0), ctypes.byref(fro)))
+        marg = float(np.linalg.norm(f) + np.linalg.norm(g))
+        return cls(C_t, _h2d_vector(f, device), _h2d_vector(g, device), m, n, fro.value, marg, device)
+
+    @classmethod
+    def sqeuclid_grid(cls, r: int, seed: int, device: int = 0) -> "DeviceProblem":
+        """Configs C1/C2/C3/C5: whitenoise marginals, exact squared-Euclidean grid cost."""
+        from .instances import whitenoise_marginals
+        f, g = whitenoise_marginals(r, seed)
+        return cls.generated(_lib.COST_SQEUCLID_GRID, r * r, r * r, (r, r, 0, 0), f, g, device)
+
+    @classmethod
+    def rect_l1(cls, seed: int, src=(64, 128), dst=(128, 256), device: int = 0) -> "DeviceProblem":
+        """Config C4: rectangular L1 cost with sparse-support marginals."""
+        from .instances import sparse_marginals
+        m, n = src[0] * src[1], dst[0] * dst[1]
+        f = sparse_marginals(m, 2 * seed)
+        g = sparse_marginals(n, 2 * seed + 1)
+        return cls.generated(_lib.COST_L1_RECT, m, n, (src[0], src[1], dst[0], dst[1]), f, g, device)
+
+
+def as_device_problem(prob, device: int = 0) -> DeviceProblem:
+    if isinstance(prob, DeviceProblem):
+        return prob
+    return DeviceProblem.from_host(prob, device)
+
+
+class Handle:
+    """Owns one pdot_solver* (one problem shape on one GPU)."""
+
+    def __init__(self, m: int, n: int, device: int = 0):
+        require_cuda(device)
+        torch.cuda.init()
+        self.lib = _lib.load()
+        ptr = ctypes.c_void_p()
+        _lib.check(self.lib.pdot_create(m, n, device, ctypes.byref(ptr)))
+        self.ptr = ptr
+        self.m, self.n, self.device = m, n, device
+        ldx = ctypes.c_int64()
+        _lib.check(self.lib.pdot_geometry(ptr, ctypes.byref(ldx), None, None, None))
+        self.ldx = ldx.value
+        self.bytes = 6 * 8 * m * self.ldx
+        self.bound_problem = None
+
+    def close(self):
+        if self.ptr:
+            self.lib.pdot_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def bind(self, dp: DeviceProblem) -> None:
+        torch.cuda.synchronize(dp.device)
+        _lib.check(self.lib.pdot_set_problem(self.ptr, dp.C_t.data_ptr(), dp.ldc, dp.f_t.data_ptr(),
+                                             dp.g_t.data_ptr(), dp.cost_fro_norm, dp.marginal_norm))
+        self.bound_problem = dp  # keep the borrowed buffers alive
+
+    def set_slot(self, slot: int, X=None, p=None, q=None) -> None:
+        keep = []
+
+        def ptr(a, shape):
+            if a is None:
+                return None, 0
+            if torch is not None and isinstance(a, torch.Tensor):
+                if tuple(a.shape) != shape:
+                    raise ValueError("shape mismatch")
+                t = a.to(dtype=torch.float64)
+                if t.dim() == 2 and t.stride(1) != 1:
+                    t = t.contiguous()
+                keep.append(t)
+                return t.data_ptr(), (t.stride(0) if t.dim() == 2 else 0)
+            arr = np.ascontiguousarray(a, dtype=np.float64)
+            if arr.shape != shape:
+                raise ValueError(f"shape mismatch: expected {shape}, got {arr.shape}")
+            keep.append(arr)
+            return arr.ctypes.data, (arr.shape[1] if arr.ndim == 2 else 0)
+
+        Xp, ld = ptr(X, (self.m, self.n))
+        pp, _ = ptr(p, (self.m,))
+        qp, _ = ptr(q, (self.n,))
+        if keep and torch is not None:
+            torch.cuda.synchronize(self.device)
+        _lib.check(self.lib.pdot_set_slot(self.ptr, slot, Xp, ld if Xp else self.n, pp, qp))
+
+    def get_slot(self, slot: int, want_X=True):
+        X = np.empty((self.m, self.n)) if want_X else None
+        p = np.empty(self.m)
+        q = np.empty(self.n)
+        _lib.check(self.lib.pdot_get_slot(self.ptr, slot, X.ctypes.data if want_X else None, self.n,
+                                          p.ctypes.data, q.ctypes.data))
+        return X, p, q
+
+    def launches(self) -> int:
+        return int(self.lib.pdot_kernel_launches(self.ptr))
+
+
+_HANDLES: dict = {}
+_BIG = 1 << 30
+
+
+def get_handle(m: int, n: int, device: int = 0) -> Handle:
+    key = (m, n, device)
+    h = _HANDLES.get(key)
+    if h is not None:
+        return h
+    need = 6 * 8 * m * even(n)
+    if need > _BIG or sum(x.bytes for x in _HANDLES.values()) > 4 * _BIG or len(_HANDLES) > 32:
+        release_handles()
+    h = Handle(m, n, device)
+    _HANDLES[key] = h
+    return h
+
+
+def release_handles() -> None:
+    for h in list(_HANDLES.values()):
+        h.close()
+    _HANDLES.clear()
+    if torch is not None and torch.cuda.is_available():
+        torch.cuda.empty_cache()

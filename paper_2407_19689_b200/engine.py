@@ -1,0 +1,164 @@
+"""``solve``: the restarted-PDHG loop of pdhg.py:254-399 on the device.
+
+The Python side only (1) moves the problem and the start point into HBM,
+(2) hands the configuration to ``pdot_solve`` (C ABI), which replays CUDA
+graphs of fused passes while the device controller makes every restart /
+termination / step-size decision, and (3) turns the device result and the
+trace-event ring into the reference's ``(Iterate, SolveReport)``.
+
+With a ``SolveTrace`` that needs iterate snapshots (``restart_points`` are
+always recorded by the reference; ``record_inner`` adds every iterate) the
+loop advances one pass at a time so the snapshots can be copied out.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import asdict
+
+import numpy as np
+
+from . import _lib
+from .config import ADAPTIVE, RELATIVE, SolverConfig, SolveTrace
+from .device import DeviceProblem, as_device_problem, get_handle
+from .records import Iterate, SolveReport
+
+
+def _config_struct(config: SolverConfig, trace_level: int, poll_passes: int = 0) -> _lib.Config:
+    c = _lib.Config()
+    c.tol = config.tol
+    c.time_limit_s = config.time_limit_s
+    c.beta = config.beta
+    c.beta_sufficient = config.beta_sufficient
+    c.beta_necessary = config.beta_necessary
+    c.beta_artificial = config.beta_artificial
+    c.theta = config.theta
+    c.eps_zero = config.eps_zero
+    c.max_iters = int(config.max_iters)
+    c.kkt_stride = int(config.kkt_stride)
+    c.adaptive = 1 if config.restart_mode == ADAPTIVE else 0
+    c.relative = 1 if config.kkt_mode == RELATIVE else 0
+    c.eta0 = -1.0 if config.eta0 is None else float(config.eta0)
+    c.omega0 = config.omega0
+    c.trace_level = trace_level
+    c.poll_passes = poll_passes
+    return c
+
+
+def _events(h) -> list:
+    out = []
+    buf = (_lib.Event * 4096)()
+    while True:
+        k = h.lib.pdot_get_events(h.ptr, buf, 4096)
+        out.extend((buf[i].type, buf[i].ia, buf[i].x, buf[i].y) for i in range(k))
+        if k < 4096:
+            return out
+
+
+def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = None,
+          trace: SolveTrace | None = None, *, device: int = 0, return_device: bool = False,
+          poll_passes: int = 0):
+    """Run restarted PDHG until the KKT tolerance, iteration or time limit.
+
+    Same contract as the reference ``otsolve.solve`` (pdhg.py:254-265):
+    returns the final pre-rounding iterate and a report whose objective and
+    duality gap are evaluated on the rounded feasible plan; on a limit the
+    best evaluated candidate is returned.  ``prob`` may be a host problem
+    (numpy ``C f g``) or a ``DeviceProblem`` already in HBM.  With
+    ``return_device=True`` the iterate stays on the device (a ``(slot, handle)``
+    pair is returned in place of numpy arrays; see ``solve_device``).
+    """
+    t_start = time.perf_counter()
+    if config is None:
+        config = SolverConfig()
+    dp = as_device_problem(prob, device)
+    h = get_handle(dp.m, dp.n, dp.device)
+    h.bind(dp)
+    if initial is not None:
+        h.set_slot(0, initial.X, initial.p, initial.q)
+    else:
+        h.set_slot(0, None, None, None)
+    stepwise = trace is not None
+    cfg = _config_struct(config, trace_level=1 if trace is not None else 0, poll_passes=poll_passes)
+    res = _lib.Result()
+    lib = h.lib
+    if not stepwise:
+        _lib.check(lib.pdot_solve(h.ptr, ctypes.byref(cfg), time.perf_counter() - t_start, ctypes.byref(res)))
+    else:
+        _lib.check(lib.pdot_begin(h.ptr, ctypes.byref(cfg), time.perf_counter() - t_start))
+        prog = _lib.Progress()
+        seen_iter = seen_outer = 0
+        while True:
+            _lib.check(lib.pdot_advance(h.ptr, 1, ctypes.byref(prog)))
+            if prog.done:
+                break
+            if prog.restarts > seen_outer:
+                seen_outer = prog.restarts
+                X, p, q = h.get_slot(prog.roles[0])
+                trace.restart_points.append(Iterate(X, p, q))
+            if prog.iterations > seen_iter:
+                seen_iter = prog.iterations
+                if trace.record_inner:
+                    X, p, q = h.get_slot(prog.roles[0])
+                    trace.inner_iterates.append(Iterate(X, p, q))
+                    X, p, q = h.get_slot(prog.roles[1])
+                    trace.inner_averages.append(Iterate(X, p, q))
+        _lib.check(lib.pdot_finish(h.ptr, ctypes.byref(res)))
+        if prog.restarts > seen_outer:  # a restart on the very last pass
+            X, p, q = h.get_slot(prog.roles[0])
+            trace.restart_points.append(Iterate(X, p, q))
+    elapsed = time.perf_counter() - t_start
+
+    restart_lengths, restart_kkts = [], []
+    for typ, ia, x, y in _events(h):
+        if typ == _lib.EV_START:
+            restart_kkts.append(x)
+        elif typ == _lib.EV_RESTART:
+            restart_lengths.append(int(ia))
+            restart_kkts.append(x)
+            if trace is not None:
+                trace.restart_kkts.append(x)
+                trace.omegas.append(y)
+        elif trace is not None and typ == _lib.EV_ACCEPT:
+            trace.etas.append(x)
+            if ia:
+                trace.step_bounds.append(y)
+        elif trace is not None and typ == _lib.EV_CAND:
+            trace.candidate_kkts.append(x)
+
+    # rounding + rounded objective on the device (pdhg.py:382-384)
+    out = (ctypes.c_double * 3)()
+    _lib.check(lib.pdot_round(h.ptr, res.final_slot, None, 0, out))
+    rounded_obj, dual_obj = float(out[0]), float(out[1])
+    reason = _lib.REASONS.get(res.reason, "unknown")
+    report = SolveReport(
+        method="pdot",
+        solved=reason == "tolerance",
+        wall_time_s=0.0 if config.deterministic else float(res.elapsed_s),
+        iterations=int(res.iterations),
+        restarts=int(res.restarts),
+        final_relative_kkt=float(res.final_relative_kkt),
+        rounded_objective=rounded_obj,
+        duality_gap=abs(rounded_obj - dual_obj),
+        termination_reason=reason,
+        config_echo=asdict(config),
+        restart_lengths=restart_lengths,
+        restart_kkts=[float(v) for v in restart_kkts],
+    )
+    report._passes = int(res.passes)  # noqa: SLF001 - diagnostics for bench/tests
+    report._e2e_s = elapsed  # noqa: SLF001
+    if return_device:
+        return (int(res.final_slot), h), report
+    X, p, q = h.get_slot(res.final_slot)
+    return Iterate(X, p, q), report
+
+
+def solve_device(prob: DeviceProblem, config: SolverConfig | None = None, **kw):
+    """solve() that leaves the iterate in HBM: returns ((slot, handle), report)."""
+    return solve(prob, config, return_device=True, **kw)
+
+
+def pre_rounding_objective(prob, it: Iterate) -> float:
+    """<C, X> of a returned iterate (host helper for reports)."""
+    return float(np.vdot(np.asarray(prob.C), it.X))
