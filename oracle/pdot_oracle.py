@@ -163,7 +163,7 @@ class _Point:
         return stacked_norm(self.X, self.p, self.q)
 
 
-def oracle_solve(prob, cfg, initial=None, record=None, clock=time.perf_counter):
+def oracle_solve(prob, cfg, initial=None, record=None, clock=time.perf_counter, on_iteration=None):
     """Restarted PDHG exactly as pdhg.py:254-399.
 
     ``prob`` is anything with ``C f g m n cost_fro_norm marginal_norm``;
@@ -229,6 +229,8 @@ def oracle_solve(prob, cfg, initial=None, record=None, clock=time.perf_counter):
         cur = nxt
         total += 1
         inner += 1
+        if on_iteration is not None:
+            on_iteration(total)
         # running mean, pdhg.py:314-317
         avg.X += (cur.X - avg.X) / inner
         avg.p += (cur.p - avg.p) / inner

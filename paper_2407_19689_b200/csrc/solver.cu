@@ -44,6 +44,8 @@ struct pdot_solver {
   std::chrono::steady_clock::time_point wall0;
   double elapsed_before = 0.0;
   int poll_L = 8;
+  Ctl saved{};          // control block of the last solve (unit calls reuse the device block)
+  bool has_saved = false;
 };
 
 namespace {
@@ -271,6 +273,8 @@ int result_from_ctl(pdot_solver* h, pdot_result* res, double wall_s) {
   int rc = download_ctl(h);
   if (rc) return rc;
   const Ctl& c = h->host;
+  h->saved = c;
+  h->has_saved = true;
   if (res) {
     res->reason = c.reason;
     res->final_slot = c.sFinal;
@@ -609,7 +613,8 @@ int pdot_solve(pdot_solver* h, const pdot_config* cfg, double elapsed_before_s, 
 int pdot_resume(pdot_solver* h, int64_t max_iters, pdot_result* res) {
   if (!h) return set_err(PDOT_EINVAL, "null handle");
   DeviceGuard dg(h->device);
-  if (int rc = download_ctl(h)) return rc;
+  if (!h->has_saved) return set_err(PDOT_ESTATE, "pdot_resume: no finished solve on this handle");
+  h->host = h->saved;
   Ctl& c = h->host;
   if (c.unit || c.error || c.reason == pdot::R_TOL || c.reason == pdot::R_NONE)
     return set_err(PDOT_ESTATE, "pdot_resume: no limited run to resume");

@@ -1,0 +1,25 @@
+"""Short driver for ncu: C3 instance, a few solve iterations, then STEP kernels.
+
+    python scripts/prof_step.py [--r 128] [--iters 30] [--kernel-launches 3]
+"""
+import argparse
+import ctypes
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import paper_2407_19689_b200 as pd  # noqa: E402
+from paper_2407_19689_b200 import _lib  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--r", type=int, default=128)
+ap.add_argument("--iters", type=int, default=30)
+ap.add_argument("--kernel-launches", type=int, default=3)
+a = ap.parse_args()
+dp = pd.DeviceProblem.sqeuclid_grid(a.r, 0)
+(slot, h), rep = pd.solve_device(dp, pd.SolverConfig(tol=1e-12, max_iters=a.iters))
+ms = ctypes.c_double()
+_lib.check(h.lib.pdot_time_stream_kernel(h.ptr, a.kernel_launches, ctypes.byref(ms)))
+print(f"iters {rep.iterations} passes {rep._passes} step-kernel {ms.value:.3f} ms "
+      f"-> {40 * a.r**4 / ms.value / 1e6:.0f} GB/s")
