@@ -139,8 +139,10 @@ int64_t pdot_get_events(pdot_solver* h, pdot_event* out, int64_t cap);
 int pdot_round(pdot_solver* h, int slot, double* Xf_any, int64_t ldX, double* out3);
 
 /* ---- unit entry points on slot 0 (input) / slot 1 (second input or output) ---- */
-/* pdhg_step (pdhg.py:121-129): slot0 -> slot1 */
-int pdot_unit_step(pdot_solver* h, double tau, double sigma);
+/* pdhg_step (pdhg.py:121-129): slot0 -> slot1.  With k > 0 the running-average
+ * update of pdhg.py:314-317 is applied too: slot2 (average) -> slot3 with
+ * A' = A + (X+ - A)/k (and the same for p, q). */
+int pdot_unit_step(pdot_solver* h, double tau, double sigma, double k);
 /* stepsize_bound (pdhg.py:132-149) for (slot0 -> slot1); out5 = {bound, |dX|^2, |dp|^2, |dq|^2, coupling} */
 int pdot_unit_bound(pdot_solver* h, double omega, double eps_zero, double* out5);
 /* kkt_error (kkt.py:56-94) of slot0; viol_any (ld ldV) receives the dual-violation matrix unless NULL;

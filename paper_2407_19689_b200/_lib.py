@@ -93,7 +93,7 @@ _SIGS = {
     "pdot_resume": ([_P, _I64, ctypes.POINTER(Result)], ctypes.c_int),
     "pdot_get_events": ([_P, ctypes.POINTER(Event), _I64], _I64),
     "pdot_round": ([_P, ctypes.c_int, _P, _I64, _DP], ctypes.c_int),
-    "pdot_unit_step": ([_P, _D, _D], ctypes.c_int),
+    "pdot_unit_step": ([_P, _D, _D, _D], ctypes.c_int),
     "pdot_unit_bound": ([_P, _D, _D, _DP], ctypes.c_int),
     "pdot_unit_kkt": ([_P, _D, _P, _I64, _P, _P, _DP], ctypes.c_int),
     "pdot_unit_apply_A": ([_P, _P, _P], ctypes.c_int),

@@ -51,10 +51,6 @@ __device__ __forceinline__ double pair8(const double* g) {
   return ((g[0] + g[1]) + (g[2] + g[3])) + ((g[4] + g[5]) + (g[6] + g[7]));
 }
 
-__device__ __forceinline__ int nq_of(int op) {
-  return op == OP_STEP ? 4 : 1;
-}
-
 // ---------------------------------------------------------------------------
 // column blocks
 // ---------------------------------------------------------------------------
@@ -133,9 +129,9 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem) {
       vals[2] = pcx * pcx;
       vals[4] = gj * qn;
       vals[6] = qn * qn;
-      if (!c.unit) {
+      if (!c.unit || c.unit_avg) {
         const double qaj = sa.q[j];
-        const double qan = qaj + (qn - qaj) / c.kd;           // pdhg.py:317
+        const double qan = qaj + div_by_count(qn - qaj, c.kd, c.rkd);  // pdhg.py:317
         c.slot[c.sAn].q[j] = qan;
         const double pca = col[3] - gj;
         vals[3] = pca * pca;
@@ -225,9 +221,9 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
         vals[2] += prx * prx;
         vals[4] += fi * pn;
         vals[6] += pn * pn;
-        if (!c.unit) {
+        if (!c.unit || c.unit_avg) {
           const double pai = sa.p[i];
-          const double pan = pai + (pn - pai) / c.kd;          // pdhg.py:316
+          const double pan = pai + div_by_count(pn - pai, c.kd, c.rkd);  // pdhg.py:316
           c.slot[c.sAn].p[i] = pan;
           const double pra = row[3] - fi;
           vals[3] += pra * pra;
@@ -372,6 +368,7 @@ __device__ void prepare_step(Ctl& c) {
   c.tau = c.eta / c.omega;     // pdhg.py:86-87
   c.sigma = c.eta * c.omega;   // pdhg.py:90-91
   c.kd = (double)(c.inner + 1);
+  c.rkd = 1.0 / c.kd;
   c.op = OP_STEP;
 }
 

@@ -13,7 +13,8 @@
 namespace pdot {
 
 constexpr int kWarps = 8;                 // warps per streaming CTA
-constexpr int kThreads = kWarps * 32;     // 256
+constexpr int kThreads = kWarps * 32;     // 256 worker threads
+constexpr int kBlockThreads = kThreads + 32;  // + one producer warp (TMA walker)
 constexpr int kTileN = kWarps * 64;       // 512 columns per tile (each lane: 2 columns)
 constexpr int kMaxNQ = 4;                 // row/col quantities per pass (STEP: e, d, X+, A')
 constexpr int kMaxNS = 8;                 // per-tile scalar partials
@@ -75,10 +76,11 @@ struct Ctl {
   double tol, beta, beta_suff, beta_nec, beta_art, theta, eps_zero;
   int64_t max_iters, kkt_stride;
   int32_t adaptive, relative, unit, trace_level;
+  int32_t unit_avg;        // unit STEP call that also updates a running average
   uint64_t deadline_ns;    // %globaltimer deadline (0 = none)
   int32_t stop_request;    // host may set to force a time-limit stop
   // ---- step state ----
-  double eta, omega, tau, sigma, kd;
+  double eta, omega, tau, sigma, kd, rkd;   // rkd = RN(1/kd)
   // ---- counters ----
   int64_t total, inner, outer, passes, halvings, rejected, restarts_pending;
   // ---- KKT bookkeeping ----
@@ -178,6 +180,18 @@ __device__ __forceinline__ double mul_acc(double acc, double x, double y) { retu
 
 // numpy np.maximum(x, 0.0) for a scalar: NaN propagates, -0.0 stays -0.0
 __device__ __forceinline__ double relu_np(double x) { return x < 0.0 ? 0.0 : x; }
+
+// x / k, correctly rounded (bit-identical to IEEE division), for a positive
+// integer-valued k with rk = RN(1/k).  Markstein: q0 = RN(x*rk) is faithful,
+// r = x - k*q0 is exact under FMA, and RN(q0 + r*rk) = RN(x/k) whenever no
+// intermediate underflows; |x| < 2^-900 (never seen on the path) takes the
+// library division.  Replaces a ~70-instruction IEEE division per element.
+__device__ __forceinline__ double div_by_count(double x, double k, double rk) {
+  if (fabs(x) < 0x1p-900 && x != 0.0) return __ddiv_rn(x, k);
+  const double q0 = __dmul_rn(x, rk);
+  const double r = __fma_rn(-q0, k, x);
+  return __fma_rn(r, rk, q0);
+}
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;

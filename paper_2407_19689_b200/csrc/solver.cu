@@ -185,6 +185,7 @@ int run_pass(pdot_solver* h, int op) {
 void unit_ctl(pdot_solver* h) {
   Ctl& c = h->host;
   c.unit = 1;
+  c.unit_avg = 0;
   c.done = 0;
   c.status = nullptr;
   c.ring = nullptr;
@@ -525,6 +526,7 @@ int pdot_begin(pdot_solver* h, const pdot_config* cfg, double elapsed_before_s) 
   h->poll_L = cfg->poll_passes > 0 ? cfg->poll_passes : auto_batch(h);
   Ctl& c = h->host;
   c.unit = 0;
+  c.unit_avg = 0;
   c.tol = cfg->tol;
   c.beta = cfg->beta;
   c.beta_suff = cfg->beta_sufficient;
@@ -539,7 +541,7 @@ int pdot_begin(pdot_solver* h, const pdot_config* cfg, double elapsed_before_s) 
   c.trace_level = cfg->trace_level;
   c.eta = cfg->eta0 > 0 ? cfg->eta0 : 1.0 / (2.0 * sqrt((double)(h->m + h->n)));
   c.omega = cfg->omega0;
-  c.tau = c.sigma = c.kd = 0.0;
+  c.tau = c.sigma = c.kd = c.rkd = 0.0;
   c.total = c.inner = c.outer = c.passes = c.halvings = c.rejected = 0;
   c.pending = 0;
   c.sX = c.sA = c.sZ = c.sB = c.sFinal = 0;
@@ -675,13 +677,15 @@ int pdot_round(pdot_solver* h, int slot, double* Xf_any, int64_t ldX, double* ou
   return PDOT_OK;
 }
 
-int pdot_unit_step(pdot_solver* h, double tau, double sigma) {
+int pdot_unit_step(pdot_solver* h, double tau, double sigma, double k) {
   if (!h || !h->problem_set) return set_err(PDOT_ESTATE, "problem not set");
   DeviceGuard dg(h->device);
   Ctl& c = h->host;
   unit_ctl(h);
-  c.sX = 0; c.sA = 0; c.sXn = 1; c.sAn = 2;
-  c.tau = tau; c.sigma = sigma; c.kd = 1.0;
+  const bool avg = k > 0;
+  c.unit_avg = avg ? 1 : 0;
+  c.sX = 0; c.sA = avg ? 2 : 0; c.sXn = 1; c.sAn = avg ? 3 : 2;
+  c.tau = tau; c.sigma = sigma; c.kd = avg ? k : 1.0; c.rkd = 1.0 / c.kd;
   c.op = pdot::OP_STEP;
   if (int rc = upload_ctl(h)) return rc;
   if (int rc = run_pass(h, pdot::OP_STEP)) return rc;
@@ -795,7 +799,7 @@ int pdot_time_stream_kernel(pdot_solver* h, int iters, double* ms_per_launch) {
   c.status = nullptr;
   c.ring = nullptr;
   c.sX = 0; c.sA = 1; c.sXn = 2; c.sAn = 3;
-  c.tau = 1e-3; c.sigma = 1e-3; c.kd = 3.0;
+  c.tau = 1e-3; c.sigma = 1e-3; c.kd = 3.0; c.rkd = 1.0 / 3.0;
   c.op = pdot::OP_STEP;
   if (int rc = upload_ctl(h)) return rc;
   for (int i = 0; i < 2; ++i) pdot::launch_stream_pass(h->dev, h->host, pdot::OP_STEP, h->stream);

@@ -52,7 +52,7 @@ struct StepOp {
   const double* q;
   const double* pa;
   const double* qa;
-  double tau, kd;
+  double tau, kd, rkd;
   bool with_avg;
 
   struct Col { double q0, q1, qa0, qa1; };
@@ -64,46 +64,35 @@ struct StepOp {
     cl.qa0 = g.v0 ? qa[g.j] : 0.0;
     cl.qa1 = g.v1 ? qa[g.j + 1] : 0.0;
   }
-  __device__ __forceinline__ void load(Frag& fr, const Geo& g, int64_t i) const {
-    fr.c = ld_stream2(C + i * g.ldc + g.j);
-    fr.x = ld_stream2(X + i * g.ldx + g.j);
-    fr.a = with_avg ? ld_stream2(A + i * g.ldx + g.j) : make_double2(0.0, 0.0);
-    fr.p = __ldg(p + i);
-    fr.pa = __ldg(pa + i);
+  // One plan entry.  o = {e, d, X+, A'}; s = the six scalar sums.
+  __device__ __forceinline__ void elem(double c, double x, double a, double pi, double qj, double pai,
+                                       double qaj, double (&o)[NQ], double (&s)[NS]) const {
+    const double pq = pi + qj;                  // apply_At
+    const double sres = c - pq;                 // C - A^T(p,q)
+    const double xn = relu_np(x - tau * sres);  // projected primal step
+    const double d = xn - x;                    // displacement
+    const double e = (xn + xn) - x;             // 2 X+ - X  (xn + xn == 2.0*xn exactly)
+    const double an = a + div_by_count(xn - a, kd, rkd);  // running mean
+    const double vc = relu_np(pq - c);          // dual violation, current (p,q)
+    const double va = relu_np((pai + qaj) - c); // dual violation, average (pa,qa)
+    o[0] = e; o[1] = d; o[2] = xn; o[3] = an;
+    s[0] = sqr_acc(s[0], d);
+    s[1] = mul_acc(s[1], c, xn);
+    s[2] = mul_acc(s[2], c, an);
+    s[3] = sqr_acc(s[3], xn);
+    s[4] = sqr_acc(s[4], vc);
+    s[5] = sqr_acc(s[5], va);
   }
-  __device__ __forceinline__ void elem(double c, double x, double a, double pi, double qj,
-                                       double pai, double qaj, bool valid, double (&o)[NQ],
-                                       double (&s)[NS], double& xn_out, double& an_out) const {
-    const double pq = pi + qj;                 // apply_At
-    const double sres = c - pq;                // C - A^T(p,q)
-    const double xn = relu_np(x - tau * sres); // projected primal step
-    const double e = 2.0 * xn - x;             // extrapolation
-    const double d = xn - x;                   // displacement
-    const double an = a + (xn - a) / kd;       // running mean (IEEE division)
-    const double vc = relu_np(pq - c);         // dual violation, current (p,q)
-    const double va = relu_np((pai + qaj) - c);// dual violation, average (pa,qa)
-    if (valid) {
-      o[0] = e; o[1] = d; o[2] = xn; o[3] = an;
-      s[0] = sqr_acc(s[0], d);
-      s[1] = mul_acc(s[1], c, xn);
-      s[2] = mul_acc(s[2], c, an);
-      s[3] = sqr_acc(s[3], xn);
-      s[4] = sqr_acc(s[4], vc);
-      s[5] = sqr_acc(s[5], va);
-      xn_out = xn; an_out = an;
-    } else {
-      o[0] = o[1] = o[2] = o[3] = 0.0;
-      xn_out = 0.0; an_out = 0.0;
-    }
-  }
+  // masked variant for edge tiles and the unit (no running average) call
   __device__ __forceinline__ void compute(const Frag& fr, const Geo& g, int64_t i, const Col& cl,
                                           double (&o0)[NQ], double (&o1)[NQ], double (&s)[NS]) const {
-    double xa, xb, aa, ab;
-    elem(fr.c.x, fr.x.x, fr.a.x, fr.p, cl.q0, fr.pa, cl.qa0, g.v0, o0, s, xa, aa);
-    elem(fr.c.y, fr.x.y, fr.a.y, fr.p, cl.q1, fr.pa, cl.qa1, g.v1, o1, s, xb, ab);
+    const double2 a = with_avg ? fr.a : make_double2(0.0, 0.0);
+    if (g.v0) elem(fr.c.x, fr.x.x, a.x, fr.p, cl.q0, fr.pa, cl.qa0, o0, s);
+    if (g.v1) elem(fr.c.y, fr.x.y, a.y, fr.p, cl.q1, fr.pa, cl.qa1, o1, s);
+    if (!with_avg) { o0[3] = 0.0; o1[3] = 0.0; }
     if (g.v0) {
-      st_stream2(Xn + i * g.ldx + g.j, make_double2(xa, xb));
-      if (with_avg) st_stream2(An + i * g.ldx + g.j, make_double2(aa, ab));
+      st_stream2(Xn + i * g.ldx + g.j, make_double2(o0[2], g.v1 ? o1[2] : 0.0));
+      if (with_avg) st_stream2(An + i * g.ldx + g.j, make_double2(o0[3], g.v1 ? o1[3] : 0.0));
     }
   }
 };
@@ -233,85 +222,31 @@ struct RoundOp {
 };
 
 // ---------------------------------------------------------------------------
-// generic tile walker
+// per-tile flush shared by both walkers: column partials (registers -> global),
+// scalars (warp butterfly -> fixed-order sum over warps), row partials
+// (per-warp smem entries -> fixed-order sum over warps).
 // ---------------------------------------------------------------------------
-template <class Op>
-__device__ __forceinline__ void tile_pass(const Op& op, const Ctl& c, double* smem) {
-  constexpr int NQ = Op::NQ, NS = Op::NS, RB = Op::RB;
-  constexpr int V = RB * NQ;  // values per butterfly (power of two)
-  static_assert((V & (V - 1)) == 0 && V <= 32, "RB*NQ must be a power of two <= 32");
+template <int NQ, int NS>
+__device__ __forceinline__ void tile_flush(const Ctl& c, const Geo& g, bool worker, double (&cacc)[NQ][2],
+                                           const double (&sacc)[NS], double* rowbuf, double* sbuf) {
   constexpr int NSP = (NS <= 1) ? 1 : (NS <= 2) ? 2 : (NS <= 4) ? 4 : 8;
-
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Geo g;
-  g.m = c.m; g.n = c.n; g.ldc = c.ldc; g.ldx = c.ldx; g.TM = c.TM;
-  g.i0 = (int64_t)blockIdx.y * c.TM;
-  g.rows = (int)imin64(c.TM, c.m - g.i0);
-  g.j = (int64_t)blockIdx.x * kTileN + warp * 64 + lane * 2;
-  g.v0 = g.j < c.n;
-  g.v1 = g.j + 1 < c.n;
-  const bool warp_live = ((int64_t)blockIdx.x * kTileN + warp * 64) < c.n;
-
-  double* rowbuf = smem;  // [TM][NQ][kWarps]
-  double cacc[NQ][2];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = 0.0;
-  double sacc[NS];
-#pragma unroll
-  for (int s = 0; s < NS; ++s) sacc[s] = 0.0;
-
-  typename Op::Col cl;
-  op.load_col(cl, g);
-
-  for (int r0 = 0; r0 < g.rows; r0 += RB) {
-    typename Op::Frag fr[RB];
-    if (warp_live) {
-#pragma unroll
-      for (int rr = 0; rr < RB; ++rr)
-        if (r0 + rr < g.rows && g.v0) op.load(fr[rr], g, g.i0 + r0 + rr);
-    }
-    double rv[V];
-#pragma unroll
-    for (int rr = 0; rr < RB; ++rr) {
-      double o0[NQ], o1[NQ];
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) o0[q] = o1[q] = 0.0;
-      if (warp_live && r0 + rr < g.rows && g.v0) op.compute(fr[rr], g, g.i0 + r0 + rr, cl, o0, o1, sacc);
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        cacc[q][0] += o0[q];
-        cacc[q][1] += o1[q];
-        rv[rr * NQ + q] = o0[q] + o1[q];
-      }
-    }
-    warp_transpose_sum<V>(rv);
-    if (transpose_is_writer<V>(lane)) {
-      const int idx = transpose_owner_index<V>(lane);
-      const int rr = idx / NQ, q = idx % NQ;
-      rowbuf[((r0 + rr) * NQ + q) * kWarps + warp] = rv[0];
-    }
-  }
-
-  // column partials: one 128-bit store per quantity
-  if (g.v0) {
+  if (worker && g.v0) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
       *reinterpret_cast<double2*>(c.colpart + ((int64_t)blockIdx.y * NQ + q) * c.ldx + g.j) =
           make_double2(cacc[q][0], cacc[q][1]);
   }
-
-  // scalars: warp butterfly, then fixed-order sum over warps
-  double sv[NSP];
+  if (worker) {
+    double sv[NSP];
 #pragma unroll
-  for (int s = 0; s < NSP; ++s) sv[s] = (s < NS) ? sacc[s] : 0.0;
-  warp_transpose_sum<NSP>(sv);
-  double* sbuf = smem + (size_t)c.TM * NQ * kWarps;  // [kWarps][NSP]
-  if (transpose_is_writer<NSP>(lane)) sbuf[warp * NSP + transpose_owner_index<NSP>(lane)] = sv[0];
+    for (int s = 0; s < NSP; ++s) sv[s] = (s < NS) ? sacc[s] : 0.0;
+    warp_transpose_sum<NSP>(sv);
+    if (transpose_is_writer<NSP>(lane)) sbuf[warp * NSP + transpose_owner_index<NSP>(lane)] = sv[0];
+  }
   __syncthreads();
-
-  // row partials: combine the 8 warps in order
   const int nrow_vals = g.rows * NQ;
-  for (int e = threadIdx.x; e < nrow_vals; e += kThreads) {
+  for (int e = threadIdx.x; e < nrow_vals; e += blockDim.x) {
     const double* b = rowbuf + (size_t)e * kWarps;
     double acc = b[0];
 #pragma unroll
@@ -327,8 +262,274 @@ __device__ __forceinline__ void tile_pass(const Op& op, const Ctl& c, double* sm
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 2) stream_kernel(const Ctl* __restrict__ ctlp, int force_op) {
-  extern __shared__ double smem[];
+__device__ __forceinline__ Geo make_geo(const Ctl& c, bool worker) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Geo g;
+  g.m = c.m; g.n = c.n; g.ldc = c.ldc; g.ldx = c.ldx; g.TM = c.TM;
+  g.i0 = (int64_t)blockIdx.y * c.TM;
+  g.rows = (int)imin64(c.TM, c.m - g.i0);
+  g.j = (int64_t)blockIdx.x * kTileN + warp * 64 + lane * 2;
+  g.v0 = worker && g.j < c.n;
+  g.v1 = worker && g.j + 1 < c.n;
+  return g;
+}
+
+// row values of one batch -> warp butterfly -> this warp's smem row partials
+template <int NQ, int RB>
+__device__ __forceinline__ void push_rows(double (&rv)[RB * NQ], double* rowbuf, int r0, bool worker) {
+  constexpr int V = RB * NQ;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  warp_transpose_sum<V>(rv);
+  if (worker && transpose_is_writer<V>(lane)) {
+    const int idx = transpose_owner_index<V>(lane);
+    const int rr = idx / NQ, q = idx % NQ;
+    rowbuf[((r0 + rr) * NQ + q) * kWarps + warp] = rv[0];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic walker: direct 128-bit loads (all ops; the rare ones use it)
+// ---------------------------------------------------------------------------
+template <class Op>
+__device__ __forceinline__ void tile_pass(const Op& op, const Ctl& c, double* smem) {
+  constexpr int NQ = Op::NQ, NS = Op::NS, RB = Op::RB;
+  constexpr int V = RB * NQ;
+  static_assert((V & (V - 1)) == 0 && V <= 32, "RB*NQ must be a power of two <= 32");
+  const int warp = threadIdx.x >> 5;
+  const bool worker = warp < kWarps;
+  const Geo g = make_geo(c, worker);
+  double* rowbuf = smem;                              // [TM][NQ][kWarps]
+  double* sbuf = smem + (size_t)c.TM * NQ * kWarps;   // [kWarps][8]
+  double cacc[NQ][2];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = 0.0;
+  double sacc[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) sacc[s] = 0.0;
+  typename Op::Col cl;
+  if (worker) op.load_col(cl, g);
+
+  for (int r0 = 0; r0 < g.rows; r0 += RB) {
+    typename Op::Frag fr[RB];
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr)
+      if (r0 + rr < g.rows && g.v0) op.load(fr[rr], g, g.i0 + r0 + rr);
+    double rv[V];
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+      double o0[NQ], o1[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) o0[q] = o1[q] = 0.0;
+      if (r0 + rr < g.rows && g.v0) op.compute(fr[rr], g, g.i0 + r0 + rr, cl, o0, o1, sacc);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        cacc[q][0] += o0[q];
+        cacc[q][1] += o1[q];
+        rv[rr * NQ + q] = o0[q] + o1[q];
+      }
+    }
+    push_rows<NQ, RB>(rv, rowbuf, r0, worker);
+  }
+  tile_flush<NQ, NS>(c, g, worker, cacc, sacc, rowbuf, sbuf);
+}
+
+// ---------------------------------------------------------------------------
+// TMA walker for the hot STEP op.  Warp kWarps is the producer: one elected
+// lane streams each stage (kStageRows rows of C, X and A for the tile's 512
+// columns, 4 KB per row per matrix) into a kStages-deep shared-memory ring with
+// cp.async.bulk + mbarrier transaction counts, evict-first in L2.  The 8
+// consumer warps read their 128-bit column pair from shared memory, run the
+// fused update, store X+ / A' straight to HBM and release the slot.  Loads are
+// thereby always kStages-1 stages ahead of the math, independent of registers.
+// ---------------------------------------------------------------------------
+#ifndef PDOT_STAGES
+#define PDOT_STAGES 6
+#endif
+#ifndef PDOT_MINB
+#define PDOT_MINB 1
+#endif
+constexpr int kStages = PDOT_STAGES;
+constexpr int kStageRows = 2;
+constexpr int kRowBytes = kTileN * 8;                  // 4096
+constexpr int kStageBytes = kStageRows * 3 * kRowBytes;  // 24576
+constexpr int kBarBytes = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigned char* smem) {
+  constexpr int NQ = StepOp::NQ, NS = StepOp::NS, R = kStageRows;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool worker = warp < kWarps;
+  const Geo g = make_geo(c, worker);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kStages;
+  unsigned char* stages = smem + kBarBytes;
+  double* pbuf = reinterpret_cast<double*>(stages + kStages * kStageBytes);  // p, pa of the tile rows
+  double* pabuf = pbuf + c.TM;
+  double* rowbuf = pabuf + c.TM;
+  double* sbuf = rowbuf + (size_t)c.TM * NQ * kWarps;
+  const int nst = (g.rows + R - 1) / R;
+  const int64_t col0 = (int64_t)blockIdx.x * kTileN;
+  const int64_t vcols = imin64(kTileN, c.n - col0);
+  const uint32_t rowbytes = (uint32_t)(((vcols + 1) & ~1LL) * 8);
+  const uint32_t pbytes = (uint32_t)(((g.rows + 1) & ~1) * 8);
+  const int nmat = op.with_avg ? 3 : 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  double cacc[NQ][2];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = 0.0;
+  double sacc[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) sacc[s] = 0.0;
+
+  if (!worker) {
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      const double* src[3] = {op.C + g.i0 * c.ldc + col0, op.X + g.i0 * c.ldx + col0, op.A + g.i0 * c.ldx + col0};
+      const int64_t ld[3] = {c.ldc, c.ldx, c.ldx};
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % kStages;
+        if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) + 1) & 1);
+        const int nr = min(R, g.rows - it * R);
+        uint32_t tx = (uint32_t)(nr * nmat) * rowbytes;
+        if (it == 0) tx += 2 * pbytes;
+        mbar_expect_tx(&full[s], tx);
+        if (it == 0) {
+          bulk_g2s(pbuf, op.p + g.i0, pbytes, &full[0], pol);
+          bulk_g2s(pabuf, op.pa + g.i0, pbytes, &full[0], pol);
+        }
+        unsigned char* dst = stages + s * kStageBytes;
+        for (int r = 0; r < nr; ++r) {
+          const int64_t row = (int64_t)it * R + r;
+          for (int k = 0; k < nmat; ++k)
+            bulk_g2s(dst + (r * 3 + k) * kRowBytes, src[k] + row * ld[k], rowbytes, &full[s], pol);
+        }
+      }
+    }
+  } else {
+    StepOp::Col cl;
+    op.load_col(cl, g);
+    const int off = (warp * 64 + lane * 2) * 8;  // byte offset of the column pair in a staged row
+    const bool fast = op.with_avg && g.rows == c.TM && vcols == kTileN;
+    if (fast) {
+      // full tile: no masks, running output pointers
+      double* xo = op.Xn + g.i0 * c.ldx + g.j;
+      double* ao = op.An + g.i0 * c.ldx + g.j;
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % kStages;
+        mbar_wait(&full[s], (it / kStages) & 1);
+        const unsigned char* st = stages + s * kStageBytes;
+        double rv[R * NQ];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const double2 cc = *reinterpret_cast<const double2*>(st + (rr * 3 + 0) * kRowBytes + off);
+          const double2 xx = *reinterpret_cast<const double2*>(st + (rr * 3 + 1) * kRowBytes + off);
+          const double2 aa = *reinterpret_cast<const double2*>(st + (rr * 3 + 2) * kRowBytes + off);
+          const double pi = pbuf[it * R + rr], pai = pabuf[it * R + rr];
+          double o0[NQ], o1[NQ];
+          op.elem(cc.x, xx.x, aa.x, pi, cl.q0, pai, cl.qa0, o0, sacc);
+          op.elem(cc.y, xx.y, aa.y, pi, cl.q1, pai, cl.qa1, o1, sacc);
+          st_stream2(xo, make_double2(o0[2], o1[2]));
+          st_stream2(ao, make_double2(o0[3], o1[3]));
+          xo += c.ldx;
+          ao += c.ldx;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            cacc[q][0] += o0[q];
+            cacc[q][1] += o1[q];
+            rv[rr * NQ + q] = o0[q] + o1[q];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        push_rows<NQ, R>(rv, rowbuf, it * R, true);
+      }
+    } else {
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % kStages;
+        mbar_wait(&full[s], (it / kStages) & 1);
+        const unsigned char* st = stages + s * kStageBytes;
+        double rv[R * NQ];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const int r = it * R + rr;
+          double o0[NQ], o1[NQ];
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) o0[q] = o1[q] = 0.0;
+          if (r < g.rows && g.v0) {
+            StepOp::Frag fr;
+            fr.c = *reinterpret_cast<const double2*>(st + (rr * 3 + 0) * kRowBytes + off);
+            fr.x = *reinterpret_cast<const double2*>(st + (rr * 3 + 1) * kRowBytes + off);
+            fr.a = op.with_avg ? *reinterpret_cast<const double2*>(st + (rr * 3 + 2) * kRowBytes + off)
+                               : make_double2(0.0, 0.0);
+            fr.p = pbuf[r];
+            fr.pa = pabuf[r];
+            op.compute(fr, g, g.i0 + r, cl, o0, o1, sacc);
+          }
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            cacc[q][0] += o0[q];
+            cacc[q][1] += o1[q];
+            rv[rr * NQ + q] = o0[q] + o1[q];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        push_rows<NQ, R>(rv, rowbuf, it * R, true);
+      }
+    }
+  }
+  tile_flush<NQ, NS>(c, g, worker, cacc, sacc, rowbuf, sbuf);
+}
+
+__global__ void __launch_bounds__(kBlockThreads, PDOT_MINB) stream_kernel(const Ctl* __restrict__ ctlp, int force_op) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* smem = reinterpret_cast<double*>(smem_raw);
   const Ctl& c = *ctlp;
   if (c.done) return;
   const int op = force_op >= 0 ? force_op : c.op;
@@ -340,8 +541,8 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const Ctl* __restri
       o.C = c.C; o.X = sx.X; o.A = sa.X;
       o.Xn = c.slot[c.sXn].X; o.An = c.slot[c.sAn].X;
       o.p = sx.p; o.q = sx.q; o.pa = sa.p; o.qa = sa.q;
-      o.tau = c.tau; o.kd = c.kd; o.with_avg = !c.unit;
-      tile_pass(o, c, smem);
+      o.tau = c.tau; o.kd = c.kd; o.rkd = c.rkd; o.with_avg = !c.unit || c.unit_avg;
+      step_tma(o, c, smem_raw);
       break;
     }
     case OP_KKT: {
@@ -381,18 +582,19 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const Ctl* __restri
 }  // namespace
 
 size_t stream_smem_bytes(int64_t TM) {
-  return (size_t)TM * kMaxNQ * kWarps * sizeof(double) + kWarps * 8 * sizeof(double);
+  const size_t rowbuf = (size_t)TM * kMaxNQ * kWarps * sizeof(double) + kWarps * 8 * sizeof(double);
+  return kBarBytes + (size_t)kStages * kStageBytes + 2 * TM * sizeof(double) + rowbuf;
 }
 
 void launch_stream_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaStream_t s) {
   static bool attr_set = false;
   const size_t smem = stream_smem_bytes(h.TM);
   if (!attr_set) {
-    cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     attr_set = true;
   }
   dim3 grid((unsigned)h.U, (unsigned)h.T);
-  stream_kernel<<<grid, kThreads, smem, s>>>(ctl_dev, force_op);
+  stream_kernel<<<grid, kBlockThreads, smem, s>>>(ctl_dev, force_op);
 }
 
 }  // namespace pdot

@@ -62,9 +62,23 @@ def pdhg_step(prob, it: Iterate, tau: float, sigma: float) -> Iterate:
     """One primal-dual step (pdhg.py:121-129) on the GPU."""
     dp, h = _bound_handle(prob)
     h.set_slot(0, it.X, it.p, it.q)
-    _lib.check(h.lib.pdot_unit_step(h.ptr, float(tau), float(sigma)))
+    _lib.check(h.lib.pdot_unit_step(h.ptr, float(tau), float(sigma), 0.0))
     X, p, q = h.get_slot(1)
     return Iterate(X, p, q)
+
+
+def step_and_average(prob, it: Iterate, avg: Iterate, tau: float, sigma: float, k: int):
+    """pdhg_step plus the running-mean update avg + (next - avg)/k of pdhg.py:314-317,
+    in the fused kernel the solve loop runs.  Returns (next, new_average)."""
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    dp, h = _bound_handle(prob)
+    h.set_slot(0, it.X, it.p, it.q)
+    h.set_slot(2, avg.X, avg.p, avg.q)
+    _lib.check(h.lib.pdot_unit_step(h.ptr, float(tau), float(sigma), float(k)))
+    X, p, q = h.get_slot(1)
+    A, pa, qa = h.get_slot(3)
+    return Iterate(X, p, q), Iterate(A, pa, qa)
 
 
 def stepsize_bound(it: Iterate, it_next: Iterate, omega: float, eps_zero: float = 1e-10) -> float:

@@ -20,6 +20,11 @@ a = ap.parse_args()
 dp = pd.DeviceProblem.sqeuclid_grid(a.r, 0)
 (slot, h), rep = pd.solve_device(dp, pd.SolverConfig(tol=1e-12, max_iters=a.iters))
 ms = ctypes.c_double()
+import torch  # noqa: E402
+
+torch.cuda.synchronize()
+torch.cuda.profiler.start()  # ncu --profile-from-start off captures only the STEP launches below
 _lib.check(h.lib.pdot_time_stream_kernel(h.ptr, a.kernel_launches, ctypes.byref(ms)))
+torch.cuda.profiler.stop()
 print(f"iters {rep.iterations} passes {rep._passes} step-kernel {ms.value:.3f} ms "
       f"-> {40 * a.r**4 / ms.value / 1e6:.0f} GB/s")

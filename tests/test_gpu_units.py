@@ -121,3 +121,32 @@ def test_step_matches_oracle_large(pd):
     assert np.array_equal(nxt.X, Xn)
     _close(nxt.p, pn)
     _close(nxt.q, qn)
+
+
+def test_running_average_bit_identical(pd):
+    """A' = A + (X+ - A)/k in the fused kernel (Markstein division with a
+    precomputed 1/k) is bit-identical to numpy's IEEE division, for many k."""
+    from oracle import pdot_oracle as O
+    from paper_2407_19689_b200 import instances as inst
+    from paper_2407_19689_b200.units import step_and_average
+    prob = inst.sqeuclid_problem(16, 5)  # 256 x 256: full and edge tiles
+    rng = np.random.default_rng(2)
+    X = rng.random((256, 256)) * 1e-2
+    X[rng.random(X.shape) < 0.5] = 0.0
+    # averages with a wide spread of exponents, including exact zeros
+    A = rng.random((256, 256)) * np.exp2(rng.integers(-60, 10, (256, 256)))
+    A[rng.random(A.shape) < 0.2] = 0.0
+    p, q = rng.standard_normal(256), rng.standard_normal(256)
+    pa, qa = rng.standard_normal(256), rng.standard_normal(256)
+    for k in (1, 2, 3, 7, 10, 49, 999, 123457):
+        nxt, av = step_and_average(prob, pd.Iterate(X, p, q), pd.Iterate(A, pa, qa), 0.02, 0.3, k)
+        Xn, _, _ = O.primal_dual_step(prob.C, prob.f, prob.g, X, p, q, 0.02, 0.3)
+        assert np.array_equal(nxt.X, Xn)
+        ref = A.copy()
+        ref += (Xn - ref) / k          # pdhg.py:315, numpy IEEE division
+        assert np.array_equal(av.X, ref), k
+        rp = pa.copy()
+        rp += (nxt.p - rp) / k         # pdhg.py:316 on the GPU's own p+
+        rq = qa.copy()
+        rq += (nxt.q - rq) / k
+        assert np.array_equal(av.p, rp) and np.array_equal(av.q, rq), k
