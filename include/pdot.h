@@ -156,11 +156,35 @@ int pdot_unit_apply_A(pdot_solver* h, double* rows_any, double* cols_any);
 int pdot_apply_At(const double* p_dev, const double* q_dev, int64_t m, int64_t n, double* out_dev,
                   int64_t ldo);
 
+/* ---- row sharding over GPUs ----
+ * Rows are split in whole groups of the 8-group reduction tree (1, 2, 4 or 8
+ * shards; the number of 128-row tiles must be a multiple of 8), so every GPU
+ * count reproduces the single-GPU reduction order bit for bit.  Per pass each
+ * shard reduces its groups' column partials and scalars, one all-gather
+ * (NCCL over NVLink) exchanges them, and every shard runs the identical
+ * combine + controller.  Shard handles bind their row slices of C and f (and
+ * the full g); everything else (p, the averages, ...) is local to the rows. */
+int pdot_shard_rows(int64_t m_total, int nranks, int rank, int64_t* row0, int64_t* row1);
+int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int device, pdot_solver** out);
+int pdot_shard_info(const pdot_solver* h, int64_t* m_total, int64_t* row0, int32_t* nranks, int32_t* rank);
+/* NCCL communicator: rank 0 creates the 128-byte id, the host broadcasts it. */
+int pdot_nccl_unique_id(void* out128);
+int pdot_comm_init(pdot_solver* h, const void* id128);
+/* Single-GPU emulation of a sharded run (tests): the host steps every shard
+ * through phase 0 (stream + group partials), pdot_exchange_local, phase 1
+ * (combine + controller). */
+int pdot_set_virtual(pdot_solver* h, int on);
+int pdot_shard_pass(pdot_solver* h, int phase, pdot_progress* prog);
+int pdot_exchange_local(pdot_solver** hs, int count);
+
 /* ---- instance generation on the device ---- */
 #define PDOT_COST_SQEUCLID_GRID 0 /* a = (r, r): (di^2 + dj^2) on an r x r grid   */
 #define PDOT_COST_L1_GRID 1       /* a = (r, r): |di| + |dj|                      */
 #define PDOT_COST_L1_RECT 2       /* a = (sr, sc, tr, tc): |2 a_i - c_j| + |2 b_i - d_j| */
 int pdot_gen_cost(double* C_dev, int64_t m, int64_t n, int64_t ldc, int kind, const int64_t* a);
+/* rows [row0, row0 + rows) of the same matrix (a row shard) */
+int pdot_gen_cost_rows(double* C_dev, int64_t row0, int64_t rows, int64_t n, int64_t ldc, int kind,
+                       const int64_t* a);
 /* ||C||_F on the device (deterministic): used for OTProblem.cost_fro_norm of device-built C */
 int pdot_fro_norm(const double* C_dev, int64_t m, int64_t n, int64_t ldc, double* out);
 

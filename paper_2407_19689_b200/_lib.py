@@ -33,7 +33,9 @@ EXPORTS = (
     "pdot_set_problem", "pdot_set_slot", "pdot_get_slot", "pdot_slot_ptrs", "pdot_solve",
     "pdot_begin", "pdot_advance", "pdot_finish", "pdot_resume", "pdot_get_events", "pdot_round",
     "pdot_unit_step", "pdot_unit_bound", "pdot_unit_kkt", "pdot_unit_apply_A", "pdot_apply_At",
-    "pdot_gen_cost", "pdot_fro_norm", "pdot_time_stream_kernel", "pdot_kernel_launches",
+    "pdot_gen_cost", "pdot_gen_cost_rows", "pdot_fro_norm", "pdot_time_stream_kernel",
+    "pdot_kernel_launches", "pdot_shard_rows", "pdot_create_shard", "pdot_shard_info",
+    "pdot_nccl_unique_id", "pdot_comm_init", "pdot_set_virtual", "pdot_shard_pass", "pdot_exchange_local",
 )
 
 
@@ -102,6 +104,18 @@ _SIGS = {
     "pdot_fro_norm": ([_P, _I64, _I64, _I64, _DP], ctypes.c_int),
     "pdot_time_stream_kernel": ([_P, ctypes.c_int, _DP], ctypes.c_int),
     "pdot_kernel_launches": ([_P], _I64),
+    "pdot_gen_cost_rows": ([_P, _I64, _I64, _I64, _I64, ctypes.c_int, ctypes.POINTER(_I64)], ctypes.c_int),
+    "pdot_shard_rows": ([_I64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_I64), ctypes.POINTER(_I64)],
+                        ctypes.c_int),
+    "pdot_create_shard": ([_I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)],
+                          ctypes.c_int),
+    "pdot_shard_info": ([_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_int32),
+                         ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
+    "pdot_nccl_unique_id": ([_P], ctypes.c_int),
+    "pdot_comm_init": ([_P, _P], ctypes.c_int),
+    "pdot_set_virtual": ([_P, ctypes.c_int], ctypes.c_int),
+    "pdot_shard_pass": ([_P, ctypes.c_int, ctypes.POINTER(Progress)], ctypes.c_int),
+    "pdot_exchange_local": ([ctypes.POINTER(_P), ctypes.c_int], ctypes.c_int),
 }
 
 _lib = None

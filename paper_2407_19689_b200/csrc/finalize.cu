@@ -54,25 +54,66 @@ __device__ __forceinline__ double pair8(const double* g) {
 // ---------------------------------------------------------------------------
 // column blocks
 // ---------------------------------------------------------------------------
+// Sum of the column partials of reduction group g over its row tiles, in tile
+// order: the within-group order that every GPU count reproduces.
 template <int NQ>
-__device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_out, double* smem) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
-  const int64_t GS = (c.T + kGroups - 1) / kGroups;
-  const int64_t t0 = warp * GS, t1 = imin64(c.T, t0 + GS);
-  double2 acc[NQ];
+__device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j, double2 (&acc)[NQ]) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = make_double2(0.0, 0.0);
-  if (j < c.n) {
-    for (int64_t t = t0; t < t1; ++t) {
+  const int64_t ta = imax64((int64_t)g * c.GS, c.t0);
+  const int64_t tb = imin64(imin64((int64_t)(g + 1) * c.GS, c.Tg), c.t0 + c.T);
+  if (j >= c.n) return;
+  for (int64_t t = ta; t < tb; ++t) {
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const double2 v = __ldcg(reinterpret_cast<const double2*>(c.colpart + (t * NQ + q) * c.ldx + j));
-        acc[q].x += v.x;
-        acc[q].y += v.y;
-      }
+    for (int q = 0; q < NQ; ++q) {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(c.colpart + ((t - c.t0) * NQ + q) * c.ldx + j));
+      acc[q].x += v.x;
+      acc[q].y += v.y;
     }
   }
+}
+
+// FIN_A: this shard's groups -> gbuf[g][q][j]
+template <int NQ>
+__device__ void column_group_partials(const Ctl& c, int b) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = c.g0 + warp;
+  if (g >= c.g1) return;
+  const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
+  double2 acc[NQ];
+  group_column_sum<NQ>(c, g, j, acc);
+  if (j < c.n) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      *reinterpret_cast<double2*>(c.gbuf + g * c.gstride + q * c.ldx + j) = acc[q];
+  }
+}
+
+// Full column sums = pairwise combination of the 8 group sums (FIN_FUSED: the
+// groups are computed here; FIN_B: they come from the exchange buffer).
+template <int NQ>
+__device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_out, double* smem, int mode) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int jj = threadIdx.x;
+  j_out = (int64_t)b * kColsPerBlock + jj;
+  if (mode == FIN_B) {
+    if (jj < kColsPerBlock && j_out < c.n) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        double g8[kGroups];
+#pragma unroll
+        for (int gi = 0; gi < kGroups; ++gi) g8[gi] = __ldcg(c.gbuf + gi * c.gstride + q * c.ldx + j_out);
+        col[q] = pair8(g8);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) col[q] = 0.0;
+    }
+    return;
+  }
+  const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
+  double2 acc[NQ];
+  group_column_sum<NQ>(c, warp, j, acc);
   // smem [group][q][64]
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
@@ -80,8 +121,6 @@ __device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_o
     smem[(warp * NQ + q) * kColsPerBlock + lane * 2 + 1] = acc[q].y;
   }
   __syncthreads();
-  const int jj = threadIdx.x;
-  j_out = (int64_t)b * kColsPerBlock + jj;
   if (jj < kColsPerBlock) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -108,14 +147,14 @@ __device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ]) {
   }
 }
 
-__device__ void column_block(Ctl& c, int op, int b, double* smem) {
+__device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
   double vals[kMaxColScal];
 #pragma unroll
   for (int s = 0; s < kMaxColScal; ++s) vals[s] = 0.0;
   int64_t j;
   if (op == OP_STEP) {
     double col[4];
-    column_sums<4>(c, b, col, j, smem);
+    column_sums<4>(c, b, col, j, smem, mode);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       const Slot& sx = c.slot[c.sX];
       const Slot& sa = c.slot[c.sA];
@@ -142,7 +181,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem) {
     }
   } else if (op == OP_KKT) {
     double col[1];
-    column_sums<1>(c, b, col, j, smem);
+    column_sums<1>(c, b, col, j, smem, mode);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       c.cols_out[j] = col[0];
       if (c.C) {
@@ -156,7 +195,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem) {
     }
   } else if (op == OP_DIFF || op == OP_DIST) {
     double col[1];
-    column_sums<1>(c, b, col, j, smem);
+    column_sums<1>(c, b, col, j, smem, mode);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       c.cols_out[j] = col[0];
       const double* qa = (op == OP_DIFF) ? c.slot[c.sX].q : c.slot[c.sZ].q;
@@ -167,7 +206,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem) {
     }
   } else if (op == OP_ROUND) {
     double col[1];
-    column_sums<1>(c, b, col, j, smem);
+    column_sums<1>(c, b, col, j, smem, mode);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       c.cols_out[j] = col[0];
       const double gj = c.g[j];
@@ -292,26 +331,46 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
 // controller
 // ---------------------------------------------------------------------------
 struct Sums {
-  double R[kMaxRowScal];  // row side (+ tile scalars), hierarchical over row tiles
+  double R[kMaxRowScal];  // row side (+ tile scalars): pairwise over the 8 groups
   double K[kMaxColScal];  // column side, over column blocks
+  int stop_any;           // a time-limit stop requested on any rank
 };
 
-__device__ void reduce_blocks(const Ctl& c, Sums* S, double* smem) {
-  // row side: (scalar s, group g, half h) -> 16 * 8 * 2 = 256 threads
-  {
-    const int tid = threadIdx.x;
-    const int s = tid >> 4, g = (tid >> 1) & 7, h = tid & 1;
-    const int64_t GS = (c.T + kGroups - 1) / kGroups;
-    const int64_t t0 = g * GS, t1 = imin64(c.T, t0 + GS);
-    const int64_t mid = t0 + (imax64(t1 - t0, 0) + 1) / 2;
-    const int64_t a = h ? mid : t0, e = h ? t1 : mid;
-    double acc = 0.0;
-    for (int64_t t = a; t < e; ++t) acc += __ldcg(c.rowblk + t * kMaxRowScal + s);
-    smem[tid] = acc;
+// Row-side scalar s of reduction group g: the group's row tiles split in two
+// halves, each summed in tile order, then added.  Shards compute this for
+// their own groups (FIN_A); the single-GPU path computes it for all 8.
+__device__ __forceinline__ double group_row_scalar(const Ctl& c, int s, int g, int half) {
+  const int64_t ga = (int64_t)g * c.GS, gb = imin64((int64_t)(g + 1) * c.GS, c.Tg);
+  const int64_t mid = ga + (imax64(gb - ga, 0) + 1) / 2;
+  const int64_t a = half ? mid : ga, e = half ? gb : mid;
+  double acc = 0.0;
+  for (int64_t t = a; t < e; ++t) acc += __ldcg(c.rowblk + (t - c.t0) * kMaxRowScal + s);
+  return acc;
+}
+
+__device__ __forceinline__ bool local_stop(const Ctl& c) {
+  return c.stop_request || (c.deadline_ns != 0 && globaltimer_ns() > c.deadline_ns);
+}
+
+// FIN_A last block: this shard's group scalars (+ its stop vote) -> gbuf
+__device__ void group_scalar_partials(Ctl& c) {
+  const int tid = threadIdx.x;
+  const int s = tid >> 3, gi = tid & 7;
+  const int g = c.g0 + gi;
+  if (s < kMaxRowScal && g < c.g1) {
+    double v = group_row_scalar(c, s, g, 0) + group_row_scalar(c, s, g, 1);
+    if (s == kMaxRowScal - 1) v = (g == c.g0 && local_stop(c)) ? 1.0 : 0.0;
+    c.gbuf[g * c.gstride + 4 * c.ldx + s] = v;
   }
-  // column side: (scalar s, part w) -> 8 * 32
-  {
-    const int tid = threadIdx.x;
+}
+
+__device__ void reduce_blocks(const Ctl& c, Sums* S, double* smem, int mode) {
+  const int tid = threadIdx.x;
+  if (mode == FIN_FUSED) {  // (scalar s, group g, half h) -> 16 * 8 * 2 = 256 threads
+    const int s = tid >> 4, g = (tid >> 1) & 7, h = tid & 1;
+    smem[tid] = group_row_scalar(c, s, g, h);
+  }
+  {  // column side: (scalar s, part w) -> 8 * 32
     const int s = tid >> 5, w = tid & 31;
     const int64_t per = (c.CB + 31) / 32;
     const int64_t b0 = w * per, b1 = imin64(c.CB, b0 + per);
@@ -320,16 +379,28 @@ __device__ void reduce_blocks(const Ctl& c, Sums* S, double* smem) {
     smem[256 + tid] = acc;
   }
   __syncthreads();
-  if (threadIdx.x < kMaxRowScal) {
-    const int s = threadIdx.x;
+  if (tid < kMaxRowScal) {
+    const int s = tid;
     double g8[kGroups];
-    for (int g = 0; g < kGroups; ++g) g8[g] = smem[s * 16 + g * 2] + smem[s * 16 + g * 2 + 1];
+    for (int g = 0; g < kGroups; ++g)
+      g8[g] = (mode == FIN_B) ? __ldcg(c.gbuf + g * c.gstride + 4 * c.ldx + s)
+                              : smem[s * 16 + g * 2] + smem[s * 16 + g * 2 + 1];
     S->R[s] = pair8(g8);
-  } else if (threadIdx.x >= 32 && threadIdx.x < 32 + kMaxColScal) {
-    const int s = threadIdx.x - 32;
+  } else if (tid >= 32 && tid < 32 + kMaxColScal) {
+    const int s = tid - 32;
     double acc = 0.0;
     for (int w = 0; w < 32; ++w) acc += smem[256 + s * 32 + w];
     S->K[s] = acc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (mode == FIN_B) {
+      double any = 0.0;
+      for (int g = 0; g < kGroups; ++g) any += __ldcg(c.gbuf + g * c.gstride + 4 * c.ldx + kMaxRowScal - 1);
+      S->stop_any = any > 0.0;
+    } else {
+      S->stop_any = local_stop(c);
+    }
   }
   __syncthreads();
 }
@@ -406,12 +477,12 @@ __device__ bool should_restart(const Ctl& c, double cand) {
 }
 
 // loop-top limit checks, pdhg.py:299-306
-__device__ bool limits_hit(Ctl& c) {
+__device__ bool limits_hit(Ctl& c, const Sums& S) {
   if (c.total >= c.max_iters) {
     finish(c, R_ITER, c.sB, c.best_rel);
     return true;
   }
-  if (c.stop_request || (c.deadline_ns != 0 && globaltimer_ns() > c.deadline_ns)) {
+  if (S.stop_any) {
     finish(c, R_TIME, c.sB, c.best_rel);
     return true;
   }
@@ -454,7 +525,7 @@ __device__ void control_step(Ctl& c, const Sums& S) {
     c.prev_cand = cand;
   }
   // ---- 2. loop top
-  if (limits_hit(c)) return;
+  if (limits_hit(c, S)) return;
   // ---- 3. the trial step of this pass (pdhg.py:230-251)
   const double dd = S.R[7], dpp = S.R[0], dqq = S.K[0];
   double bound = INFINITY;
@@ -569,7 +640,7 @@ __device__ void control_unit(Ctl& c, int op, const Sums& S) {
   }
 }
 
-__global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__ ctlp, int force_op) {
+__global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__ ctlp, int force_op, int mode) {
   __shared__ double smem[kWarps * 4 * kColsPerBlock + 64];
   __shared__ Sums S;
   __shared__ int is_last;
@@ -577,8 +648,16 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   if (c.done) return;
   const int op = force_op >= 0 ? force_op : c.op;
   if (op == OP_NONE) return;
-  if ((int64_t)blockIdx.x < c.CB) column_block(c, op, blockIdx.x, smem);
-  else row_block(c, op, (int)(blockIdx.x - c.CB), smem);
+  if ((int64_t)blockIdx.x < c.CB) {
+    if (mode == FIN_A) {
+      if (op == OP_STEP) column_group_partials<4>(c, blockIdx.x);
+      else column_group_partials<1>(c, blockIdx.x);
+    } else {
+      column_block(c, op, blockIdx.x, smem, mode);
+    }
+  } else {
+    row_block(c, op, (int)(blockIdx.x - c.CB), smem);
+  }
 
   __threadfence();
   __syncthreads();
@@ -586,7 +665,13 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  reduce_blocks(c, &S, smem);
+  if (mode == FIN_A) {
+    group_scalar_partials(c);
+    __syncthreads();
+    if (threadIdx.x == 0) *c.counter = 0u;
+    return;
+  }
+  reduce_blocks(c, &S, smem, mode);
   if (threadIdx.x == 0) {
     if (c.unit) {
       control_unit(c, op, S);
@@ -615,9 +700,9 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
 
 }  // namespace
 
-void launch_finalize_pass(Ctl* ctl_dev, const Ctl& h, int force_op, cudaStream_t s) {
-  const unsigned blocks = (unsigned)(h.CB + h.T);
-  finalize_kernel<<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op);
+void launch_finalize_pass(Ctl* ctl_dev, const Ctl& h, int force_op, int mode, cudaStream_t s) {
+  const unsigned blocks = (unsigned)(mode == FIN_B ? h.CB : h.CB + h.T);
+  finalize_kernel<<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op, mode);
 }
 
 }  // namespace pdot

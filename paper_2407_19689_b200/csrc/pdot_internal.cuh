@@ -69,9 +69,16 @@ struct Slot {
 struct Ctl {
   // ---- problem / config (set once) ----
   int64_t m, n, ldc, ldx;
-  int64_t T, U;            // row tiles, column tiles
+  int64_t T, U;            // row tiles (local), column tiles
   int64_t TM;              // rows per tile
   int64_t CB;              // finalize column blocks
+  // ---- row sharding; single GPU: m_total = m, Tg = T, t0 = 0, groups 0..8 ----
+  int64_t m_total, row0;   // global rows, first local row
+  int64_t Tg, t0, GS;      // global row tiles, first local tile, tiles per reduction group
+  int32_t g0, g1;          // local reduction groups [g0, g1)
+  int32_t nranks, rank;
+  double* gbuf;            // [kGroups][gstride]: per-group column sums (4 x ldx) + 16 scalars
+  int64_t gstride;
   double cost_fro, marg_norm;
   double tol, beta, beta_suff, beta_nec, beta_art, theta, eps_zero;
   int64_t max_iters, kkt_stride;
@@ -203,7 +210,8 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // host-side launchers (defined in the .cu files)
 // ---------------------------------------------------------------------------
 void launch_stream_pass(const Ctl* ctl_dev, const Ctl& ctl_host, int force_op, cudaStream_t s);
-void launch_finalize_pass(Ctl* ctl_dev, const Ctl& ctl_host, int force_op, cudaStream_t s);
+enum FinMode : int { FIN_FUSED = 0, FIN_A = 1, FIN_B = 2 };
+void launch_finalize_pass(Ctl* ctl_dev, const Ctl& ctl_host, int force_op, int mode, cudaStream_t s);
 size_t stream_smem_bytes(int64_t TM);
 
 }  // namespace pdot

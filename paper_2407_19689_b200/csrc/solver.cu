@@ -11,6 +11,9 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <dlfcn.h>
+
+#include <algorithm>
 #include <chrono>
 #include <string>
 #include <vector>
@@ -46,6 +49,13 @@ struct pdot_solver {
   int poll_L = 8;
   Ctl saved{};          // control block of the last solve (unit calls reuse the device block)
   bool has_saved = false;
+  // ---- row sharding ----
+  int nranks = 1, rank = 0;
+  int64_t m_total = 0, row0 = 0;
+  double* gbuf = nullptr;
+  int64_t gstride = 0;
+  void* nccl_comm = nullptr;  // ncclComm_t when nranks > 1 and a communicator was attached
+  bool virtual_shards = false;  // exchange driven by the host (single-GPU emulation)
 };
 
 namespace {
@@ -101,12 +111,13 @@ __global__ void apply_at_kernel(const double* __restrict__ p, const double* __re
   }
 }
 
-__global__ void gen_cost_kernel(double* __restrict__ C, int64_t m, int64_t n, int64_t ldc, int kind,
-                                int64_t a0, int64_t a1, int64_t a2, int64_t a3) {
+__global__ void gen_cost_kernel(double* __restrict__ C, int64_t row0, int64_t m, int64_t n, int64_t ldc,
+                                int kind, int64_t a0, int64_t a1, int64_t a2, int64_t a3) {
   const int64_t total = m * ldc;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / ldc, j = e - i * ldc;
+    const int64_t il = e / ldc, j = e - il * ldc;
+    const int64_t i = row0 + il;
     int64_t v = 0;
     if (j < n) {
       if (kind == PDOT_COST_SQEUCLID_GRID || kind == PDOT_COST_L1_GRID) {
@@ -174,10 +185,11 @@ int download_ctl(pdot_solver* h) {
 }
 
 // one (stream, finalize) pass with an explicit op, outside any graph
+int launch_pass(pdot_solver* h, int op);
+
 int run_pass(pdot_solver* h, int op) {
-  pdot::launch_stream_pass(h->dev, h->host, op, h->stream);
-  pdot::launch_finalize_pass(h->dev, h->host, op, h->stream);
-  h->launches += 2;
+  if (h->virtual_shards) return set_err(PDOT_ESTATE, "virtual shards are stepped with pdot_shard_pass");
+  if (int rc = launch_pass(h, op)) return rc;
   CK(cudaGetLastError());
   return PDOT_OK;
 }
@@ -205,6 +217,99 @@ int copy_vec(double* dst, const double* src, int64_t n, cudaStream_t s) {
   return PDOT_OK;
 }
 
+// ---------------------------------------------------------------------------
+// NCCL (torch's libnccl.so.2, loaded at run time only for multi-GPU handles)
+// ---------------------------------------------------------------------------
+struct NcclId {
+  char internal[128];
+};
+struct NcclApi {
+  bool ok = false;
+  int (*get_unique_id)(NcclId*) = nullptr;
+  int (*comm_init_rank)(void**, int, NcclId, int) = nullptr;
+  int (*all_gather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  const char* (*error_string)(int) = nullptr;
+};
+constexpr int kNcclFloat64 = 8;  // ncclDouble
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  void* lib = nullptr;
+  for (const char* nm : names) {
+    lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (lib) break;
+  }
+  if (!lib) return api;
+  api.get_unique_id = (int (*)(NcclId*))dlsym(lib, "ncclGetUniqueId");
+  api.comm_init_rank = (int (*)(void**, int, NcclId, int))dlsym(lib, "ncclCommInitRank");
+  api.all_gather = (int (*)(const void*, void*, size_t, int, void*, cudaStream_t))dlsym(lib, "ncclAllGather");
+  api.comm_destroy = (int (*)(void*))dlsym(lib, "ncclCommDestroy");
+  api.error_string = (const char* (*)(int))dlsym(lib, "ncclGetErrorString");
+  api.ok = api.get_unique_id && api.comm_init_rank && api.all_gather && api.comm_destroy && api.error_string;
+  return api;
+}
+
+int nccl_fail(int r, const char* what) {
+  std::string msg = std::string("NCCL error in ") + what + ": ";
+  msg += nccl().error_string ? nccl().error_string(r) : "unknown";
+  return set_err(PDOT_ENCCL, msg);
+}
+
+// Group-aligned row range of one shard (all ranks share the global tiling).
+int shard_geometry(int64_t m_total, int64_t TM, int nranks, int rank, int64_t* Tg, int64_t* GS, int* g0,
+                   int* g1, int64_t* row0, int64_t* row1) {
+  const int64_t T = (m_total + TM - 1) / TM;
+  if (nranks != 1 && nranks != 2 && nranks != 4 && nranks != 8)
+    return set_err(PDOT_EINVAL, "row sharding supports 1, 2, 4 or 8 shards");
+  if (rank < 0 || rank >= nranks) return set_err(PDOT_EINVAL, "rank out of range");
+  if (nranks > 1 && T % pdot::kGroups != 0)
+    return set_err(PDOT_EINVAL, "row sharding needs the number of 128-row tiles to be a multiple of 8");
+  const int64_t gs = (T + pdot::kGroups - 1) / pdot::kGroups;
+  const int per = pdot::kGroups / nranks;
+  *Tg = T;
+  *GS = gs;
+  *g0 = rank * per;
+  *g1 = (rank + 1) * per;
+  const int64_t t0 = std::min<int64_t>((int64_t)*g0 * gs, T), t1 = std::min<int64_t>((int64_t)*g1 * gs, T);
+  *row0 = std::min(t0 * TM, m_total);
+  *row1 = std::min(t1 * TM, m_total);
+  return PDOT_OK;
+}
+
+bool split_mode(const pdot_solver* h) { return h->nranks > 1; }
+
+// all-gather of the per-group partials (in place: every rank owns a contiguous chunk)
+int exchange(pdot_solver* h) {
+  if (h->virtual_shards) return PDOT_OK;  // the host copies between handles
+  if (!h->nccl_comm) return set_err(PDOT_ESTATE, "sharded handle without a communicator");
+  const int per = pdot::kGroups / h->nranks;
+  const size_t count = (size_t)per * h->gstride;
+  double* send = h->gbuf + (size_t)h->rank * count;
+  const int r = nccl().all_gather(send, h->gbuf, count, kNcclFloat64, h->nccl_comm, h->stream);
+  if (r != 0) return nccl_fail(r, "ncclAllGather");
+  return PDOT_OK;
+}
+
+// one pass: K1, then K2 (single GPU) or K2a -> exchange -> K2b (row shards)
+int launch_pass(pdot_solver* h, int op) {
+  pdot::launch_stream_pass(h->dev, h->host, op, h->stream);
+  if (!split_mode(h)) {
+    pdot::launch_finalize_pass(h->dev, h->host, op, pdot::FIN_FUSED, h->stream);
+    h->launches += 2;
+  } else {
+    pdot::launch_finalize_pass(h->dev, h->host, op, pdot::FIN_A, h->stream);
+    if (int rc = exchange(h)) return rc;
+    pdot::launch_finalize_pass(h->dev, h->host, op, pdot::FIN_B, h->stream);
+    h->launches += 3;
+  }
+  return PDOT_OK;
+}
+
 void drain_ring(pdot_solver* h) {
   const int64_t head = h->status_h->ring_head;
   for (int64_t t = h->ring_tail; t < head; ++t) {
@@ -228,11 +333,12 @@ int build_graph(pdot_solver* h, int L) {
   }
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-  for (int i = 0; i < L; ++i) {
-    pdot::launch_stream_pass(h->dev, h->host, -1, h->stream);
-    pdot::launch_finalize_pass(h->dev, h->host, -1, h->stream);
-  }
+  int rc = PDOT_OK;
+  const int64_t before = h->launches;
+  for (int i = 0; i < L && rc == PDOT_OK; ++i) rc = launch_pass(h, -1);
+  h->launches = before;
   CK(cudaStreamEndCapture(h->stream, &g));
+  if (rc) return rc;
   CK(cudaGraphInstantiate(&h->graph, g, 0));
   cudaGraphDestroy(g);
   h->graph_L = L;
@@ -255,7 +361,7 @@ int drive(pdot_solver* h, int L) {
   int64_t i = 0;
   for (;;) {
     CK(cudaGraphLaunch(h->graph, h->stream));
-    h->launches += 2 * L;
+    h->launches += (split_mode(h) ? 3 : 2) * L;
     CK(cudaEventRecord(h->ev[i & 1], h->stream));
     if (i > 0) {
       CK(cudaEventSynchronize(h->ev[(i - 1) & 1]));
@@ -307,10 +413,37 @@ const char* pdot_last_error(void) { return g_err.c_str(); }
 
 int pdot_version(void) { return 1; }
 
+static int64_t row_tile() {
+  int64_t TM = 128;
+  if (const char* e = getenv("PDOT_TM")) TM = atoll(e);
+  if (TM != 64 && TM != 128 && TM != 256) TM = 128;
+  return TM;
+}
+
+int pdot_shard_rows(int64_t m_total, int nranks, int rank, int64_t* row0, int64_t* row1) {
+  if (m_total < 1) return set_err(PDOT_EINVAL, "plan dimensions must be positive");
+  int64_t Tg, GS, r0, r1;
+  int g0, g1;
+  if (int rc = shard_geometry(m_total, row_tile(), nranks, rank, &Tg, &GS, &g0, &g1, &r0, &r1)) return rc;
+  if (row0) *row0 = r0;
+  if (row1) *row1 = r1;
+  return PDOT_OK;
+}
+
 int pdot_create(int64_t m, int64_t n, int device, pdot_solver** out) {
+  return pdot_create_shard(m, n, 1, 0, device, out);
+}
+
+int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int device, pdot_solver** out) {
   if (!out) return set_err(PDOT_EINVAL, "null output handle");
   *out = nullptr;
-  if (m < 1 || n < 1) return set_err(PDOT_EINVAL, "plan dimensions must be positive");
+  if (m_total < 1 || n < 1) return set_err(PDOT_EINVAL, "plan dimensions must be positive");
+  const int64_t TM = row_tile();
+  int64_t Tg, GS, row0, row1;
+  int g0, g1;
+  if (int rc = shard_geometry(m_total, TM, nranks, rank, &Tg, &GS, &g0, &g1, &row0, &row1)) return rc;
+  const int64_t m = row1 - row0;
+  if (m < 1) return set_err(PDOT_EINVAL, "empty row shard");
   DeviceGuard dg(device);
   CK(cudaSetDevice(device));
   pdot_solver* h = new pdot_solver();
@@ -318,11 +451,13 @@ int pdot_create(int64_t m, int64_t n, int device, pdot_solver** out) {
   h->m = m;
   h->n = n;
   h->ldx = round_up(n, 2);
-  int64_t TM = 128;
-  if (const char* e = getenv("PDOT_TM")) TM = atoll(e);
-  if (TM != 64 && TM != 128 && TM != 256) TM = 128;
   h->TM = TM;
   h->T = (m + TM - 1) / TM;
+  h->nranks = nranks;
+  h->rank = rank;
+  h->m_total = m_total;
+  h->row0 = row0;
+  h->gstride = round_up(4 * h->ldx + pdot::kMaxRowScal, 2);
   h->U = (n + pdot::kTileN - 1) / pdot::kTileN;
   h->CB = (n + 63) / 64;
 
@@ -338,8 +473,9 @@ int pdot_create(int64_t m, int64_t n, int device, pdot_solver** out) {
   const int64_t w_colblk = h->CB * pdot::kMaxColScal;
   const int64_t w_rows = 4 * round_up(m, 2), w_cols = 4 * h->ldx;
   const int64_t w_va = 2 * round_up(m, 2), w_vb = 2 * h->ldx;
+  const int64_t w_gbuf = pdot::kGroups * h->gstride;
   const int64_t w_total = w_colpart + w_rowpart + w_tiles + w_rowblk + w_colblk + w_rows + w_cols + w_va +
-                          w_vb + 4096;
+                          w_vb + w_gbuf + 4096;
   cudaError_t e;
   if ((e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaMalloc(&h->dev, sizeof(Ctl))) != cudaSuccess ||
@@ -392,6 +528,18 @@ int pdot_create(int64_t m, int64_t n, int device, pdot_solver** out) {
   c.cols_out = w; w += w_cols;
   c.vec_a = w; w += w_va;
   c.vec_b = w; w += w_vb;
+  c.gbuf = w; w += w_gbuf;
+  h->gbuf = c.gbuf;
+  c.gstride = h->gstride;
+  c.m_total = m_total;
+  c.row0 = row0;
+  c.Tg = Tg;
+  c.t0 = row0 / TM;
+  c.GS = GS;
+  c.g0 = g0;
+  c.g1 = g1;
+  c.nranks = nranks;
+  c.rank = rank;
   c.counter = h->counter;
   c.status = h->status_d;
   c.ring = h->ring_d;
@@ -420,6 +568,7 @@ int pdot_destroy(pdot_solver* h) {
   DeviceGuard dg(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->graph) cudaGraphExecDestroy(h->graph);
+  if (h->nccl_comm && nccl().ok) nccl().comm_destroy(h->nccl_comm);
   if (h->dev) cudaFree(h->dev);
   if (h->slot_mem) cudaFree(h->slot_mem);
   if (h->work) cudaFree(h->work);
@@ -539,7 +688,7 @@ int pdot_begin(pdot_solver* h, const pdot_config* cfg, double elapsed_before_s) 
   c.adaptive = cfg->adaptive;
   c.relative = cfg->relative;
   c.trace_level = cfg->trace_level;
-  c.eta = cfg->eta0 > 0 ? cfg->eta0 : 1.0 / (2.0 * sqrt((double)(h->m + h->n)));
+  c.eta = cfg->eta0 > 0 ? cfg->eta0 : 1.0 / (2.0 * sqrt((double)(h->m_total + h->n)));  // pdhg.py:225-227
   c.omega = cfg->omega0;
   c.tau = c.sigma = c.kd = c.rkd = 0.0;
   c.total = c.inner = c.outer = c.passes = c.halvings = c.rejected = 0;
@@ -573,6 +722,7 @@ int pdot_begin(pdot_solver* h, const pdot_config* cfg, double elapsed_before_s) 
 
 int pdot_advance(pdot_solver* h, int64_t max_passes, pdot_progress* prog) {
   if (!h) return set_err(PDOT_EINVAL, "null handle");
+  if (h->virtual_shards) return set_err(PDOT_ESTATE, "virtual shards are stepped with pdot_shard_pass");
   DeviceGuard dg(h->device);
   if (max_passes < 0) {
     if (int rc = drive(h, h->poll_L)) return rc;
@@ -763,15 +913,23 @@ int pdot_apply_At(const double* p_dev, const double* q_dev, int64_t m, int64_t n
 }
 
 int pdot_gen_cost(double* C_dev, int64_t m, int64_t n, int64_t ldc, int kind, const int64_t* a) {
-  if (!C_dev || !a || m < 1 || n < 1 || ldc < n) return set_err(PDOT_EINVAL, "bad argument");
+  if (!a) return set_err(PDOT_EINVAL, "bad argument");
+  const int64_t m_total = (kind == PDOT_COST_L1_RECT) ? a[0] * a[1] : a[0] * a[1];
+  if (m != m_total) return set_err(PDOT_EINVAL, "cost shape mismatch");
+  return pdot_gen_cost_rows(C_dev, 0, m, n, ldc, kind, a);
+}
+
+int pdot_gen_cost_rows(double* C_dev, int64_t row0, int64_t rows, int64_t n, int64_t ldc, int kind,
+                       const int64_t* a) {
+  if (!C_dev || !a || rows < 1 || n < 1 || ldc < n || row0 < 0) return set_err(PDOT_EINVAL, "bad argument");
   if (kind == PDOT_COST_SQEUCLID_GRID || kind == PDOT_COST_L1_GRID) {
-    if (a[0] * a[1] != m || m != n || a[0] != a[1]) return set_err(PDOT_EINVAL, "grid cost needs m = n = r*r");
+    if (a[0] != a[1] || a[0] * a[1] != n || row0 + rows > n) return set_err(PDOT_EINVAL, "grid cost needs m = n = r*r");
   } else if (kind == PDOT_COST_L1_RECT) {
-    if (a[0] * a[1] != m || a[2] * a[3] != n) return set_err(PDOT_EINVAL, "rect cost shape mismatch");
+    if (row0 + rows > a[0] * a[1] || a[2] * a[3] != n) return set_err(PDOT_EINVAL, "rect cost shape mismatch");
   } else {
     return set_err(PDOT_EINVAL, "unknown cost kind");
   }
-  gen_cost_kernel<<<148 * 16, 256>>>(C_dev, m, n, ldc, kind, a[0], a[1], a[2], a[3]);
+  gen_cost_kernel<<<148 * 16, 256>>>(C_dev, row0, rows, n, ldc, kind, a[0], a[1], a[2], a[3]);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   return PDOT_OK;
@@ -819,5 +977,97 @@ int pdot_time_stream_kernel(pdot_solver* h, int iters, double* ms_per_launch) {
 }
 
 int64_t pdot_kernel_launches(const pdot_solver* h) { return h ? h->launches : 0; }
+
+int pdot_nccl_unique_id(void* out128) {
+  if (!out128) return set_err(PDOT_EINVAL, "null output");
+  if (!nccl().ok) return set_err(PDOT_ENCCL, "libnccl.so.2 could not be loaded");
+  NcclId id;
+  const int r = nccl().get_unique_id(&id);
+  if (r != 0) return nccl_fail(r, "ncclGetUniqueId");
+  memcpy(out128, id.internal, sizeof(id.internal));
+  return PDOT_OK;
+}
+
+int pdot_comm_init(pdot_solver* h, const void* id128) {
+  if (!h || !id128) return set_err(PDOT_EINVAL, "null argument");
+  if (h->nranks == 1) return PDOT_OK;
+  if (!nccl().ok) return set_err(PDOT_ENCCL, "libnccl.so.2 could not be loaded");
+  DeviceGuard dg(h->device);
+  NcclId id;
+  memcpy(id.internal, id128, sizeof(id.internal));
+  void* comm = nullptr;
+  const int r = nccl().comm_init_rank(&comm, h->nranks, id, h->rank);
+  if (r != 0) return nccl_fail(r, "ncclCommInitRank");
+  h->nccl_comm = comm;
+  h->virtual_shards = false;
+  return PDOT_OK;
+}
+
+int pdot_shard_info(const pdot_solver* h, int64_t* m_total, int64_t* row0, int32_t* nranks, int32_t* rank) {
+  if (!h) return set_err(PDOT_EINVAL, "null handle");
+  if (m_total) *m_total = h->m_total;
+  if (row0) *row0 = h->row0;
+  if (nranks) *nranks = h->nranks;
+  if (rank) *rank = h->rank;
+  return PDOT_OK;
+}
+
+int pdot_set_virtual(pdot_solver* h, int on) {
+  if (!h) return set_err(PDOT_EINVAL, "null handle");
+  if (h->nranks == 1) return set_err(PDOT_EINVAL, "virtual exchange needs a sharded handle");
+  h->virtual_shards = on != 0;
+  return PDOT_OK;
+}
+
+int pdot_shard_pass(pdot_solver* h, int phase, pdot_progress* prog) {
+  if (!h || h->nranks == 1) return set_err(PDOT_EINVAL, "pdot_shard_pass needs a sharded handle");
+  DeviceGuard dg(h->device);
+  if (phase == 0) {
+    pdot::launch_stream_pass(h->dev, h->host, -1, h->stream);
+    pdot::launch_finalize_pass(h->dev, h->host, -1, pdot::FIN_A, h->stream);
+    h->launches += 2;
+  } else {
+    pdot::launch_finalize_pass(h->dev, h->host, -1, pdot::FIN_B, h->stream);
+    h->launches += 1;
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(h->t1, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  drain_ring(h);
+  if (prog) {
+    if (int rc = download_ctl(h)) return rc;
+    const Ctl& c = h->host;
+    prog->done = c.done;
+    prog->roles[0] = c.sX;
+    prog->roles[1] = c.sA;
+    prog->roles[2] = c.sZ;
+    prog->roles[3] = c.sB;
+    prog->op = c.op;
+    prog->iterations = c.total;
+    prog->restarts = c.outer;
+    prog->passes = c.passes;
+  }
+  return PDOT_OK;
+}
+
+int pdot_exchange_local(pdot_solver** hs, int count) {
+  if (!hs || count < 1) return set_err(PDOT_EINVAL, "bad argument");
+  for (int i = 0; i < count; ++i)
+    if (!hs[i] || hs[i]->nranks != count || hs[i]->rank != i || hs[i]->device != hs[0]->device)
+      return set_err(PDOT_EINVAL, "pdot_exchange_local: handles must be ranks 0..count-1 on one device");
+  DeviceGuard dg(hs[0]->device);
+  CK(cudaDeviceSynchronize());
+  const int per = pdot::kGroups / count;
+  for (int src = 0; src < count; ++src) {
+    const size_t chunk = (size_t)per * hs[src]->gstride;
+    for (int dst = 0; dst < count; ++dst) {
+      if (dst == src) continue;
+      CK(cudaMemcpy(hs[dst]->gbuf + (size_t)src * chunk, hs[src]->gbuf + (size_t)src * chunk,
+                    chunk * sizeof(double), cudaMemcpyDeviceToDevice));
+    }
+  }
+  CK(cudaDeviceSynchronize());
+  return PDOT_OK;
+}
 
 }  // extern "C"

@@ -56,6 +56,7 @@ class DeviceProblem:
         self.marginal_norm = float(marginal_norm)
         self.device = device
         self.host = host
+        self.m_total, self.row0 = self.m, 0
 
     @property
     def ldc(self) -> int:
@@ -70,34 +71,55 @@ class DeviceProblem:
 
     @classmethod
     def generated(cls, kind: int, m: int, n: int, shape_args, f: np.ndarray, g: np.ndarray,
-                  device: int = 0) -> "DeviceProblem":
-        """Cost built on the device (pdot_gen_cost), marginals from the host."""
+                  device: int = 0, fro: float | None = None, rows=None) -> "DeviceProblem":
+        """Cost built on the device (pdot_gen_cost_rows), marginals from the host.
+
+        ``rows = (row0, row1)`` builds only that row shard (C rows and f entries);
+        ``fro`` is the exact ||C||_F of the FULL matrix (instances.*_fro_norm),
+        so every shard and GPU count sees the same KKT normaliser."""
         require_cuda(device)
         lib = _lib.load()
-        C_t = torch.empty((m, even(n)), dtype=torch.float64, device=f"cuda:{device}")
+        row0, row1 = (0, m) if rows is None else rows
+        C_t = torch.empty((row1 - row0, even(n)), dtype=torch.float64, device=f"cuda:{device}")
         args = (ctypes.c_int64 * 4)(*shape_args)
         torch.cuda.synchronize(device)
-        _lib.check(lib.pdot_gen_cost(C_t.data_ptr(), m, n, C_t.stride(0), kind, args))
-        fro = ctypes.c_double()
-        _lib.check(lib.pdot_fro_norm(C_t.data_ptr(), m, n, C_t.stride(0), ctypes.byref(fro)))
+        _lib.check(lib.pdot_gen_cost_rows(C_t.data_ptr(), row0, row1 - row0, n, C_t.stride(0), kind, args))
+        if fro is None:
+            if rows is not None:
+                raise ValueError("a row shard needs the exact full-matrix Frobenius norm")
+            out = ctypes.c_double()
+            _lib.check(lib.pdot_fro_norm(C_t.data_ptr(), m, n, C_t.stride(0), ctypes.byref(out)))
+            fro = out.value
         marg = float(np.linalg.norm(f) + np.linalg.norm(g))
-        return cls(C_t, _h2d_vector(f, device), _h2d_vector(g, device), m, n, fro.value, marg, device)
+        dp = cls(C_t, _h2d_vector(f[row0:row1], device), _h2d_vector(g, device), row1 - row0, n, fro, marg,
+                 device)
+        dp.m_total, dp.row0 = m, row0
+        return dp
 
     @classmethod
-    def sqeuclid_grid(cls, r: int, seed: int, device: int = 0) -> "DeviceProblem":
+    def sqeuclid_grid(cls, r: int, seed: int, device: int = 0, rows=None) -> "DeviceProblem":
         """Configs C1/C2/C3/C5: whitenoise marginals, exact squared-Euclidean grid cost."""
-        from .instances import whitenoise_marginals
+        from .instances import sqeuclid_fro_norm, whitenoise_marginals
         f, g = whitenoise_marginals(r, seed)
-        return cls.generated(_lib.COST_SQEUCLID_GRID, r * r, r * r, (r, r, 0, 0), f, g, device)
+        return cls.generated(_lib.COST_SQEUCLID_GRID, r * r, r * r, (r, r, 0, 0), f, g, device,
+                             fro=sqeuclid_fro_norm(r), rows=rows)
 
     @classmethod
-    def rect_l1(cls, seed: int, src=(64, 128), dst=(128, 256), device: int = 0) -> "DeviceProblem":
+    def rect_l1(cls, seed: int, src=(64, 128), dst=(128, 256), device: int = 0, rows=None) -> "DeviceProblem":
         """Config C4: rectangular L1 cost with sparse-support marginals."""
-        from .instances import sparse_marginals
+        from .instances import rect_l1_fro_norm, sparse_marginals
         m, n = src[0] * src[1], dst[0] * dst[1]
         f = sparse_marginals(m, 2 * seed)
         g = sparse_marginals(n, 2 * seed + 1)
-        return cls.generated(_lib.COST_L1_RECT, m, n, (src[0], src[1], dst[0], dst[1]), f, g, device)
+        return cls.generated(_lib.COST_L1_RECT, m, n, (src[0], src[1], dst[0], dst[1]), f, g, device,
+                             fro=rect_l1_fro_norm(src, dst), rows=rows)
+
+    def row_shard(self, row0: int, row1: int) -> "DeviceProblem":
+        """View of rows [row0, row1) of this (full) problem: C rows and f entries."""
+        dp = DeviceProblem(self.C_t[row0:row1], self.f_t[row0:row1], self.g_t, row1 - row0, self.n,
+                           self.cost_fro_norm, self.marginal_norm, self.device)
+        dp.m_total, dp.row0 = self.m, row0
+        return dp
 
 
 def as_device_problem(prob, device: int = 0) -> DeviceProblem:
@@ -107,15 +129,22 @@ def as_device_problem(prob, device: int = 0) -> DeviceProblem:
 
 
 class Handle:
-    """Owns one pdot_solver* (one problem shape on one GPU)."""
+    """Owns one pdot_solver* (one problem shape, or one row shard, on one GPU)."""
 
-    def __init__(self, m: int, n: int, device: int = 0):
+    def __init__(self, m: int, n: int, device: int = 0, nranks: int = 1, rank: int = 0):
         require_cuda(device)
         torch.cuda.init()
         self.lib = _lib.load()
         ptr = ctypes.c_void_p()
-        _lib.check(self.lib.pdot_create(m, n, device, ctypes.byref(ptr)))
+        _lib.check(self.lib.pdot_create_shard(m, n, nranks, rank, device, ctypes.byref(ptr)))
         self.ptr = ptr
+        self.nranks, self.rank, self.m_total = nranks, rank, m
+        if nranks > 1:
+            r0, r1 = ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(self.lib.pdot_shard_rows(m, nranks, rank, ctypes.byref(r0), ctypes.byref(r1)))
+            self.row0, m = r0.value, r1.value - r0.value
+        else:
+            self.row0 = 0
         self.m, self.n, self.device = m, n, device
         ldx = ctypes.c_int64()
         _lib.check(self.lib.pdot_geometry(ptr, ctypes.byref(ldx), None, None, None))

@@ -25,7 +25,7 @@ from .device import DeviceProblem, as_device_problem, get_handle
 from .records import Iterate, SolveReport
 
 
-def _config_struct(config: SolverConfig, trace_level: int, poll_passes: int = 0) -> _lib.Config:
+def config_struct(config: SolverConfig, trace_level: int, poll_passes: int = 0) -> _lib.Config:
     c = _lib.Config()
     c.tol = config.tol
     c.time_limit_s = config.time_limit_s
@@ -56,6 +56,50 @@ def _events(h) -> list:
             return out
 
 
+def assemble_report(h, res, config: SolverConfig, trace: SolveTrace | None, round_slot: bool = True):
+    """Trace events + device result -> SolveReport (pdhg.py:380-399)."""
+    lib = h.lib
+    restart_lengths, restart_kkts = [], []
+    for typ, ia, x, y in _events(h):
+        if typ == _lib.EV_START:
+            restart_kkts.append(x)
+        elif typ == _lib.EV_RESTART:
+            restart_lengths.append(int(ia))
+            restart_kkts.append(x)
+            if trace is not None:
+                trace.restart_kkts.append(x)
+                trace.omegas.append(y)
+        elif trace is not None and typ == _lib.EV_ACCEPT:
+            trace.etas.append(x)
+            if ia:
+                trace.step_bounds.append(y)
+        elif trace is not None and typ == _lib.EV_CAND:
+            trace.candidate_kkts.append(x)
+    rounded_obj = dual_obj = float("nan")
+    if round_slot:
+        # rounding + rounded objective on the device (pdhg.py:382-384)
+        out = (ctypes.c_double * 3)()
+        _lib.check(lib.pdot_round(h.ptr, res.final_slot, None, 0, out))
+        rounded_obj, dual_obj = float(out[0]), float(out[1])
+    reason = _lib.REASONS.get(res.reason, "unknown")
+    report = SolveReport(
+        method="pdot",
+        solved=reason == "tolerance",
+        wall_time_s=0.0 if config.deterministic else float(res.elapsed_s),
+        iterations=int(res.iterations),
+        restarts=int(res.restarts),
+        final_relative_kkt=float(res.final_relative_kkt),
+        rounded_objective=rounded_obj,
+        duality_gap=abs(rounded_obj - dual_obj),
+        termination_reason=reason,
+        config_echo=asdict(config),
+        restart_lengths=restart_lengths,
+        restart_kkts=[float(v) for v in restart_kkts],
+    )
+    report._passes = int(res.passes)  # noqa: SLF001 - diagnostics for bench/tests
+    return report
+
+
 def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = None,
           trace: SolveTrace | None = None, *, device: int = 0, return_device: bool = False,
           poll_passes: int = 0):
@@ -80,7 +124,7 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
     else:
         h.set_slot(0, None, None, None)
     stepwise = trace is not None
-    cfg = _config_struct(config, trace_level=1 if trace is not None else 0, poll_passes=poll_passes)
+    cfg = config_struct(config, trace_level=1 if trace is not None else 0, poll_passes=poll_passes)
     res = _lib.Result()
     lib = h.lib
     if not stepwise:
@@ -110,43 +154,7 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
             trace.restart_points.append(Iterate(X, p, q))
     elapsed = time.perf_counter() - t_start
 
-    restart_lengths, restart_kkts = [], []
-    for typ, ia, x, y in _events(h):
-        if typ == _lib.EV_START:
-            restart_kkts.append(x)
-        elif typ == _lib.EV_RESTART:
-            restart_lengths.append(int(ia))
-            restart_kkts.append(x)
-            if trace is not None:
-                trace.restart_kkts.append(x)
-                trace.omegas.append(y)
-        elif trace is not None and typ == _lib.EV_ACCEPT:
-            trace.etas.append(x)
-            if ia:
-                trace.step_bounds.append(y)
-        elif trace is not None and typ == _lib.EV_CAND:
-            trace.candidate_kkts.append(x)
-
-    # rounding + rounded objective on the device (pdhg.py:382-384)
-    out = (ctypes.c_double * 3)()
-    _lib.check(lib.pdot_round(h.ptr, res.final_slot, None, 0, out))
-    rounded_obj, dual_obj = float(out[0]), float(out[1])
-    reason = _lib.REASONS.get(res.reason, "unknown")
-    report = SolveReport(
-        method="pdot",
-        solved=reason == "tolerance",
-        wall_time_s=0.0 if config.deterministic else float(res.elapsed_s),
-        iterations=int(res.iterations),
-        restarts=int(res.restarts),
-        final_relative_kkt=float(res.final_relative_kkt),
-        rounded_objective=rounded_obj,
-        duality_gap=abs(rounded_obj - dual_obj),
-        termination_reason=reason,
-        config_echo=asdict(config),
-        restart_lengths=restart_lengths,
-        restart_kkts=[float(v) for v in restart_kkts],
-    )
-    report._passes = int(res.passes)  # noqa: SLF001 - diagnostics for bench/tests
+    report = assemble_report(h, res, config, trace)
     report._e2e_s = elapsed  # noqa: SLF001
     if return_device:
         return (int(res.final_slot), h), report

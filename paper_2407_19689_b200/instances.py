@@ -205,3 +205,46 @@ def grid_side(mn):
     if r * r != mn:
         raise InstanceError("not a square grid size")
     return r
+
+
+# ---------------------------------------------------------------------------
+# exact Frobenius norms of the generated integer costs.  Every GPU count (and
+# the host) then sees the same cost_fro_norm, so the KKT normalisers -- and
+# with them the whole trajectory -- are independent of the sharding.
+# ---------------------------------------------------------------------------
+def _pair_power_sums(xs, ys, k):
+    """sum over (x in xs, y in ys) of |x - y|**k, exact (Python ints)."""
+    return sum(abs(x - y) ** k for x in xs for y in ys)
+
+
+def sqeuclid_fro_norm(r):
+    """||C||_F for C_ij = (a_i-a_j)^2 + (b_i-b_j)^2 on an r x r grid:
+    sum = 2 r^2 S4 + 2 S2^2 with S_k = sum_{a,a'} (a-a')^k."""
+    axis = range(r)
+    s2 = _pair_power_sums(axis, axis, 2)
+    s4 = _pair_power_sums(axis, axis, 4)
+    total = 2 * r * r * s4 + 2 * s2 * s2
+    return math.sqrt(float(total))
+
+
+def l1_grid_fro_norm(r):
+    axis = range(r)
+    s1 = _pair_power_sums(axis, axis, 1)
+    s2 = _pair_power_sums(axis, axis, 2)
+    total = 2 * r * r * s2 + 2 * s1 * s1
+    return math.sqrt(float(total))
+
+
+def rect_l1_fro_norm(src_shape=RECT_SRC, dst_shape=RECT_DST):
+    """||C||_F of rect_l1_cost: C = |2 r_s - r_t| + |2 c_s - c_t|."""
+    sr, sc = src_shape
+    tr, tc = dst_shape
+    rows_s = [2 * x for x in range(sr)]
+    cols_s = [2 * x for x in range(sc)]
+    rows_t, cols_t = range(tr), range(tc)
+    dx2 = _pair_power_sums(rows_s, rows_t, 2)
+    dy2 = _pair_power_sums(cols_s, cols_t, 2)
+    dx1 = _pair_power_sums(rows_s, rows_t, 1)
+    dy1 = _pair_power_sums(cols_s, cols_t, 1)
+    total = sc * tc * dx2 + sr * tr * dy2 + 2 * dx1 * dy1
+    return math.sqrt(float(total))
