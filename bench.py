@@ -19,9 +19,10 @@ same metric through the public API ``solve(host_problem, config)`` with the
 HBM copy peak; `cpu_baseline` = the oracle port (the reference's numpy
 algorithm) on this host.
 
-N > 1 (torchrun): every rank solves its own C3 instance on its own GPU
-("replicas", weak scaling) - the row-sharded single-instance path is not
-wired into the benchmark yet.
+N > 1 (torchrun): ONE C3 instance row-sharded over the N GPUs (strong
+scaling): each rank generates its rows of C on its GPU, and every pass does
+one NCCL all-gather of the per-group column partials.
+`value` is then iterations of that one instance per second.
 """
 
 from __future__ import annotations
@@ -35,18 +36,24 @@ import sys
 import time
 from pathlib import Path
 
+import numpy as np
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "PDOT iters/sec & time-to-1e-4 KKT at m=n=16384 fp64; HBM GB/s vs peak"
 
 CONFIGS = {
-    "c3": dict(r=128, seed=0, tol=1e-4,
+    "c3": dict(r=128, m=16384, n=16384, seed=0, tol=1e-4,
                workload="C3: m=n=16384 (128x128 grid), whitenoise marginals seed 0, exact squared-Euclidean cost, tol 1e-4"),
-    "c2": dict(r=64, seed=0, tol=1e-6,
+    "c2": dict(r=64, m=4096, n=4096, seed=0, tol=1e-6,
                workload="C2: m=n=4096 (64x64 grid), whitenoise marginals seed 0, exact squared-Euclidean cost, tol 1e-6"),
-    "c1": dict(r=32, seed=0, tol=1e-4,
+    "c1": dict(r=32, m=1024, n=1024, seed=0, tol=1e-4,
                workload="C1: m=n=1024 (32x32 grid), whitenoise marginals seed 0, exact squared-Euclidean cost, tol 1e-4"),
+    "c4": dict(kind="rect", m=8192, n=32768, seed=0, tol=1e-4,
+               workload="C4: m=8192 (64x128 grid) x n=32768 (128x256 grid), L1 cost, 10% sparse-support marginals seed 0, tol 1e-4"),
+    "c5": dict(r=256, m=65536, n=65536, seed=0, tol=1e-4,
+               workload="C5: m=n=65536 (256x256 grid), whitenoise marginals seed 0, exact squared-Euclidean cost, tol 1e-4 (needs >= 2 GPUs)"),
 }
 BYTES_PER_ELEM = 40  # read C, X, A; write X+, A' (fp64) - SURVEY §8(d)
 
@@ -136,7 +143,7 @@ def run_reference(args, cfgd):
         return 0
     from paper_2407_19689_b200 import instances as inst
     t0 = time.perf_counter()
-    prob = inst.sqeuclid_problem(cfgd["r"], cfgd["seed"])
+    prob = make_host_problem(inst, cfgd)
     _ = prob.cost_fro_norm, prob.marginal_norm
     build_s = time.perf_counter() - t0
     warm, steps = min(args.warmup, 1), max(1, min(args.steps, 2))
@@ -150,12 +157,38 @@ def run_reference(args, cfgd):
         "cpu_baseline": {"value": ips, "unit": "iter/s", "cores": cores, "kind": "port",
                          "sample": f"{steps} timed PDHG iterations (after {warm} warm-up) of oracle/pdot_oracle.py "
                                    f"(numpy restatement of the reference, bit-identical on golden fixtures) at "
-                                   f"the full {cfgd['r']**2}x{cfgd['r']**2} instance; OpenBLAS threads = host cores; "
+                                   f"the full {cfgd['m']}x{cfgd['n']} instance; OpenBLAS threads = host cores; "
                                    f"instance build {build_s:.1f}s excluded"},
         "e2e": {"value": ips, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def make_device_problem(pd, cfgd, local, rows=None):
+    if cfgd.get("kind") == "rect":
+        return pd.DeviceProblem.rect_l1(cfgd["seed"], device=local, rows=rows)
+    return pd.DeviceProblem.sqeuclid_grid(cfgd["r"], cfgd["seed"], device=local, rows=rows)
+
+
+def make_host_problem(inst, cfgd, rows=None):
+    """Host (numpy) instance, or just its row shard, for the end-to-end run."""
+    from types import SimpleNamespace
+    if rows is None:
+        if cfgd.get("kind") == "rect":
+            return inst.rect_problem(cfgd["seed"])
+        return inst.sqeuclid_problem(cfgd["r"], cfgd["seed"])
+    r0, r1 = rows
+    if cfgd.get("kind") == "rect":
+        m, n = cfgd["m"], cfgd["n"]
+        f, g = inst.sparse_marginals(m, 2 * cfgd["seed"]), inst.sparse_marginals(n, 2 * cfgd["seed"] + 1)
+        C, fro = inst.rect_l1_cost_rows(r0, r1), inst.rect_l1_fro_norm()
+    else:
+        f, g = inst.whitenoise_marginals(cfgd["r"], cfgd["seed"])
+        C, fro = inst.sqeuclid_grid_cost_rows(cfgd["r"], r0, r1), inst.sqeuclid_fro_norm(cfgd["r"])
+    marg = float(np.linalg.norm(f) + np.linalg.norm(g))
+    return SimpleNamespace(C=C, f=f[r0:r1], g=g, m=r1 - r0, n=C.shape[1], cost_fro_norm=fro,
+                           marginal_norm=marg, row0=r0, m_total=len(f))
 
 
 def main():
@@ -180,22 +213,44 @@ def main():
     import paper_2407_19689_b200 as pd
     from paper_2407_19689_b200 import _lib
     from paper_2407_19689_b200 import instances as inst
+    from paper_2407_19689_b200.shard import ShardedSolver, shard_rows
 
     rank, world, local = dist_info()
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
-    r, m = cfgd["r"], cfgd["r"] ** 2
-    n = m
+    m, n = cfgd["m"], cfgd["n"]
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    dp = pd.DeviceProblem.sqeuclid_grid(r, cfgd["seed"], device=local)
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        tt = torch.tensor([x], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    rows = shard_rows(m, world, rank) if world > 1 else None
+    dp = make_device_problem(pd, cfgd, local, rows)
+    if world > 1:
+        solver = ShardedSolver(dp, world, rank)
+        h = solver.h
+
+        def run(cfg):
+            return solver.solve(cfg)[1]
+    else:
+        solver = None
+        h = None
+
+        def run(cfg):
+            nonlocal h
+            (_, h), rep = pd.solve_device(dp, cfg, device=local)
+            return rep
     # warm-up: W iterations (graph build, caches, clocks)
-    (slot, h), warm_rep = pd.solve_device(dp, pd.SolverConfig(tol=1e-12, max_iters=args.warmup), device=local)
+    warm_rep = run(pd.SolverConfig(tol=1e-12, max_iters=args.warmup))
     lib = h.lib
     launches0 = h.launches()
     sampler = ClockSampler(local)
@@ -208,24 +263,20 @@ def main():
     clocks = sampler.stop()
     launches = h.launches() - launches0
     steps_done = int(res.iterations) - args.warmup
-    t = float(res.device_s)
-    if world > 1:
-        tt = torch.tensor([t], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt.item())
+    t = max_over_ranks(float(res.device_s))
     passes_timed = int(res.passes) - warm_rep._passes
     ms_per_step = 1e3 * t / steps_done
-    value = world * steps_done / t
+    value = steps_done / t  # iterations of the one instance per second, whole job
 
     # the dominant kernel alone: fused STEP streaming pass, CUDA events on its stream
     ms_k = ctypes.c_double()
     _lib.check(lib.pdot_time_stream_kernel(h.ptr, 20, ctypes.byref(ms_k)))
     peak, peak_src = peaks()
-    algo_bytes = BYTES_PER_ELEM * m * n
+    algo_bytes = BYTES_PER_ELEM * h.m * n
     achieved = algo_bytes / (ms_k.value * 1e-3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "step_kernel_traffic.json"
-    if tp.exists():
+    if tp.exists() and world == 1 and args.config == "c3":
         try:
             traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
         except (ValueError, OSError):
@@ -234,8 +285,8 @@ def main():
     extra = {}
     if not args.no_tol:
         # time-to-tolerance: a fresh device-resident solve at the configured tol
-        (_, _), rep_tol = pd.solve_device(dp, pd.SolverConfig(tol=cfgd["tol"]), device=local)
-        extra["time_to_tol"] = {"seconds": rep_tol.wall_time_s, "iterations": rep_tol.iterations,
+        rep_tol = run(pd.SolverConfig(tol=cfgd["tol"]))
+        extra["time_to_tol"] = {"seconds": max_over_ranks(rep_tol.wall_time_s), "iterations": rep_tol.iterations,
                                 "restarts": rep_tol.restarts, "passes": rep_tol._passes,
                                 "final_relative_kkt": rep_tol.final_relative_kkt,
                                 "rounded_objective": rep_tol.rounded_objective,
@@ -244,30 +295,40 @@ def main():
     e2e = None
     host_prob = None
     if not args.no_e2e:
-        host_prob = inst.sqeuclid_problem(r, cfgd["seed"])
-        _ = host_prob.cost_fro_norm, host_prob.marginal_norm
-        del dp
-        pd.release_handles()
+        host_prob = make_host_problem(inst, cfgd, rows)
+        if world == 1:
+            _ = host_prob.cost_fro_norm, host_prob.marginal_norm
+            del dp
+            pd.release_handles()
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        it, rep_e = pd.solve(host_prob, pd.SolverConfig(tol=cfgd["tol"]), device=local)
-        e2e_s = time.perf_counter() - t0
+        if world == 1:
+            it, rep_e = pd.solve(host_prob, pd.SolverConfig(tol=cfgd["tol"]), device=local)
+            api = "paper_2407_19689_b200.solve(OTProblem numpy, SolverConfig(tol))"
+        else:
+            dph = pd.DeviceProblem.from_host(host_prob, local)
+            dph.m_total, dph.row0 = host_prob.m_total, host_prob.row0
+            solver.h.bind(dph)
+            _, rep_e = solver.solve(pd.SolverConfig(tol=cfgd["tol"]))
+            it = solver.local_iterate()
+            api = "paper_2407_19689_b200.shard.ShardedSolver.solve (row shard from host numpy)"
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
         barrier()
         iters = max(1, rep_e.iterations)
-        h2d = 8 * (m * n + m + n)
-        d2h = 8 * (m * n + m + n)
-        e2e = {"value": world * iters / e2e_s, "unit": "iter/s",
+        h2d = 8 * (host_prob.m * n + host_prob.m + n)
+        d2h = 8 * (host_prob.m * n + host_prob.m + n)
+        e2e = {"value": iters / e2e_s, "unit": "iter/s",
                "h2d_bytes_per_step": h2d // iters, "d2h_bytes_per_step": d2h // iters,
                "seconds": e2e_s, "iterations": rep_e.iterations, "h2d_bytes_per_call": h2d,
-               "d2h_bytes_per_call": d2h, "api": "paper_2407_19689_b200.solve(OTProblem numpy, SolverConfig(tol))",
+               "d2h_bytes_per_call": d2h, "api": api,
                "rounded_objective": rep_e.rounded_objective, "termination_reason": rep_e.termination_reason}
         del it
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         if host_prob is None:
-            host_prob = inst.sqeuclid_problem(r, cfgd["seed"])
+            host_prob = make_host_problem(inst, cfgd)
         ips, timed_s, _ = oracle_iterations_per_s(host_prob, cfgd["tol"], 0, 1)
         cpu = {"value": ips, "unit": "iter/s", "cores": os.cpu_count(), "kind": "port",
                "sample": f"1 PDHG iteration (plus the start KKT) of oracle/pdot_oracle.py, the numpy restatement "
@@ -277,16 +338,17 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world, "steps": steps_done,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (on-device cost generator, seeded whitenoise marginals)",
-            "config": {"workload": cfgd["workload"], "m": m, "n": n, "global_batch": world, "seq_len": 0,
-                       "parallelism": "replicas" if world > 1 else "single",
-                       "l2_policy": "inputs larger than L2 (C, X, avg: 2.15 GB each per pass)",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (on-device cost generator, seeded marginals)",
+            "config": {"workload": cfgd["workload"], "m": m, "n": n, "global_batch": 1, "seq_len": 0,
+                       "parallelism": f"rows{world}" if world > 1 else "single",
+                       "l2_policy": "inputs larger than L2 (C, X, average streamed every pass)",
                        "timed_window": f"iterations {args.warmup + 1}..{args.warmup + steps_done} of the solve, tol test disabled"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "stream_kernel (OP_STEP)", "kernel_ms": ms_k.value,
-                         "algorithmic_bytes_per_launch": algo_bytes},
+                         "kernel": "stream_kernel (OP_STEP)" + (" per GPU" if world > 1 else ""),
+                         "kernel_ms": ms_k.value, "algorithmic_bytes_per_launch": algo_bytes},
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": int(launches),
@@ -295,6 +357,8 @@ def main():
         }
         line.update(extra)
         print(json.dumps(line), flush=True)
+    if solver is not None:
+        solver.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

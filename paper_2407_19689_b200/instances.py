@@ -143,6 +143,14 @@ def sqeuclid_grid_cost(r):
     return (da * da + db * db).astype(np.float64)
 
 
+def sqeuclid_grid_cost_rows(r, row0, row1):
+    """Rows [row0, row1) of sqeuclid_grid_cost(r) without building the rest."""
+    a, b = grid_coords(r)
+    da = a[row0:row1, None] - a[None, :]
+    db = b[row0:row1, None] - b[None, :]
+    return (da * da + db * db).astype(np.float64)
+
+
 def l1_grid_cost(r):
     a, b = grid_coords(r)
     return (np.abs(a[:, None] - a[None, :]) + np.abs(b[:, None] - b[None, :])).astype(np.float64)
@@ -176,6 +184,16 @@ def rect_l1_cost(src_shape=RECT_SRC, dst_shape=RECT_DST):
     sr, sc = src_shape
     tr, tc = dst_shape
     k = np.arange(sr * sc, dtype=np.int64)
+    a, b = 2 * (k // sc), 2 * (k % sc)
+    l = np.arange(tr * tc, dtype=np.int64)
+    c, d = l // tc, l % tc
+    return (np.abs(a[:, None] - c[None, :]) + np.abs(b[:, None] - d[None, :])).astype(np.float64)
+
+
+def rect_l1_cost_rows(row0, row1, src_shape=RECT_SRC, dst_shape=RECT_DST):
+    sr, sc = src_shape
+    tr, tc = dst_shape
+    k = np.arange(row0, row1, dtype=np.int64)
     a, b = 2 * (k // sc), 2 * (k % sc)
     l = np.arange(tr * tc, dtype=np.int64)
     c, d = l // tc, l % tc
