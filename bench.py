@@ -233,7 +233,7 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         return float(tt.item())
 
-    rows = shard_rows(m, world, rank) if world > 1 else None
+    rows = shard_rows(m, n, world, rank) if world > 1 else None
     dp = make_device_problem(pd, cfgd, local, rows)
     if world > 1:
         solver = ShardedSolver(dp, world, rank)

@@ -164,7 +164,7 @@ int pdot_apply_At(const double* p_dev, const double* q_dev, int64_t m, int64_t n
  * (NCCL over NVLink) exchanges them, and every shard runs the identical
  * combine + controller.  Shard handles bind their row slices of C and f (and
  * the full g); everything else (p, the averages, ...) is local to the rows. */
-int pdot_shard_rows(int64_t m_total, int nranks, int rank, int64_t* row0, int64_t* row1);
+int pdot_shard_rows(int64_t m_total, int64_t n, int nranks, int rank, int64_t* row0, int64_t* row1);
 int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int device, pdot_solver** out);
 int pdot_shard_info(const pdot_solver* h, int64_t* m_total, int64_t* row0, int32_t* nranks, int32_t* rank);
 /* NCCL communicator: rank 0 creates the 128-byte id, the host broadcasts it. */
@@ -192,6 +192,8 @@ int pdot_fro_norm(const double* C_dev, int64_t m, int64_t n, int64_t ldc, double
 /* Launch the streaming STEP kernel `iters` times on the current state (no
  * controller) and time it with CUDA events on the kernel's stream. */
 int pdot_time_stream_kernel(pdot_solver* h, int iters, double* ms_per_launch);
+/* Time the finalize kernel alone (OP_STEP reductions + vector updates, no controller decisions). */
+int pdot_time_finalize(pdot_solver* h, int iters, double* ms_per_launch);
 /* Number of kernels launched so far by this handle (graph nodes count individually). */
 int64_t pdot_kernel_launches(const pdot_solver* h);
 

@@ -34,7 +34,7 @@ EXPORTS = (
     "pdot_begin", "pdot_advance", "pdot_finish", "pdot_resume", "pdot_get_events", "pdot_round",
     "pdot_unit_step", "pdot_unit_bound", "pdot_unit_kkt", "pdot_unit_apply_A", "pdot_apply_At",
     "pdot_gen_cost", "pdot_gen_cost_rows", "pdot_fro_norm", "pdot_time_stream_kernel",
-    "pdot_kernel_launches", "pdot_shard_rows", "pdot_create_shard", "pdot_shard_info",
+    "pdot_kernel_launches", "pdot_time_finalize", "pdot_shard_rows", "pdot_create_shard", "pdot_shard_info",
     "pdot_nccl_unique_id", "pdot_comm_init", "pdot_set_virtual", "pdot_shard_pass", "pdot_exchange_local",
 )
 
@@ -104,8 +104,9 @@ _SIGS = {
     "pdot_fro_norm": ([_P, _I64, _I64, _I64, _DP], ctypes.c_int),
     "pdot_time_stream_kernel": ([_P, ctypes.c_int, _DP], ctypes.c_int),
     "pdot_kernel_launches": ([_P], _I64),
+    "pdot_time_finalize": ([_P, ctypes.c_int, _DP], ctypes.c_int),
     "pdot_gen_cost_rows": ([_P, _I64, _I64, _I64, _I64, ctypes.c_int, ctypes.POINTER(_I64)], ctypes.c_int),
-    "pdot_shard_rows": ([_I64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_I64), ctypes.POINTER(_I64)],
+    "pdot_shard_rows": ([_I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_I64), ctypes.POINTER(_I64)],
                         ctypes.c_int),
     "pdot_create_shard": ([_I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)],
                           ctypes.c_int),

@@ -36,13 +36,15 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* red /* [kWarps
     for (int k = 0; k < K; ++k) red[warp * K + k] = v[k];
   }
   __syncthreads();
+  if (threadIdx.x < K) {  // value k summed over the warps in order by thread k
+    double acc = red[threadIdx.x];
+    for (int w = 1; w < kWarps; ++w) acc += red[w * K + threadIdx.x];
+    red[kWarps * K + threadIdx.x] = acc;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double acc = red[k];
-      for (int w = 1; w < kWarps; ++w) acc += red[w * K + k];
-      v[k] = acc;
-    }
+    for (int k = 0; k < K; ++k) v[k] = red[kWarps * K + k];
   }
   __syncthreads();
 }
@@ -141,7 +143,20 @@ __device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ]) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) row[q] = 0.0;
   if (i >= c.m) return;
-  for (int64_t u = 0; u < c.U; ++u) {
+  constexpr int B = 4;
+  int64_t u = 0;
+  for (; u + B <= c.U; u += B) {
+    double v[B][NQ];
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) v[k][q] = __ldcg(c.rowpart + ((u + k) * NQ + q) * c.m + i);
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) row[q] += v[k][q];
+  }
+  for (; u < c.U; ++u) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) row[q] += __ldcg(c.rowpart + (u * NQ + q) * c.m + i);
   }
@@ -644,6 +659,7 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   __shared__ double smem[kWarps * 4 * kColsPerBlock + 64];
   __shared__ Sums S;
   __shared__ int is_last;
+  __shared__ Ctl cs;
   Ctl& c = *ctlp;
   if (c.done) return;
   const int op = force_op >= 0 ? force_op : c.op;
@@ -671,31 +687,39 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
     if (threadIdx.x == 0) *c.counter = 0u;
     return;
   }
-  reduce_blocks(c, &S, smem, mode);
+  // the controller works on a shared-memory copy of the control block
+  constexpr int kWords = (int)(sizeof(Ctl) / sizeof(unsigned long long));
+  unsigned long long* cw = reinterpret_cast<unsigned long long*>(&cs);
+  const unsigned long long* gw = reinterpret_cast<const unsigned long long*>(ctlp);
+  for (int i = threadIdx.x; i < kWords; i += blockDim.x) cw[i] = __ldcg(gw + i);
+  __syncthreads();
+  reduce_blocks(cs, &S, smem, mode);
   if (threadIdx.x == 0) {
-    if (c.unit) {
-      control_unit(c, op, S);
+    if (cs.unit) {
+      control_unit(cs, op, S);
     } else {
-      c.passes += 1;
-      if (op == OP_STEP) control_step(c, S);
-      else if (op == OP_DIST) control_dist(c, S);
-      else if (op == OP_KKT) control_start(c, S);
-      // publish to the host mirror
-      if (c.status) {
-        __threadfence_system();
-        c.status->total = c.total;
-        c.status->outer = c.outer;
-        c.status->passes = c.passes;
-        c.status->ring_head = c.ring_head;
-        c.status->final_slot = c.sFinal;
-        c.status->reason = c.reason;
-        c.status->error = c.error;
-        __threadfence_system();
-        c.status->done = c.done;
+      cs.passes += 1;
+      if (op == OP_STEP) control_step(cs, S);
+      else if (op == OP_DIST) control_dist(cs, S);
+      else if (op == OP_KKT) control_start(cs, S);
+      // publish to the host mirror (read by the host only after the pass's
+      // completion event, which orders these mapped-memory writes)
+      if (cs.status) {
+        cs.status->total = cs.total;
+        cs.status->outer = cs.outer;
+        cs.status->passes = cs.passes;
+        cs.status->ring_head = cs.ring_head;
+        cs.status->final_slot = cs.sFinal;
+        cs.status->reason = cs.reason;
+        cs.status->error = cs.error;
+        cs.status->done = cs.done;
       }
     }
-    *c.counter = 0u;
   }
+  __syncthreads();
+  unsigned long long* gwo = reinterpret_cast<unsigned long long*>(ctlp);
+  for (int i = threadIdx.x; i < kWords; i += blockDim.x) gwo[i] = cw[i];
+  if (threadIdx.x == 0) *cs.counter = 0u;
 }
 
 }  // namespace

@@ -125,6 +125,7 @@ struct Ctl {
   Status* status;          // host mapped
   Event* ring;             // host mapped, kRingCap entries
 };
+static_assert(sizeof(Ctl) % 8 == 0, "the controller copies Ctl as 8-byte words");
 
 // ---------------------------------------------------------------------------
 // small device helpers

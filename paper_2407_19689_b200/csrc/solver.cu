@@ -413,18 +413,24 @@ const char* pdot_last_error(void) { return g_err.c_str(); }
 
 int pdot_version(void) { return 1; }
 
-static int64_t row_tile() {
+// Rows per streaming tile: 128 (measured best from 4096^2 up), halved for
+// small plans until the grid has at least one tile per SM (1024^2: TM = 16,
+// 5x faster than 128).  Depends on the GLOBAL shape only, so every shard of a
+// row-sharded run uses the same tiling and reduction tree.
+static int64_t row_tile(int64_t m_total, int64_t n) {
   int64_t TM = 128;
+  const int64_t U = (n + pdot::kTileN - 1) / pdot::kTileN;
+  while (TM > 16 && ((m_total + TM - 1) / TM) * U < 148) TM /= 2;
   if (const char* e = getenv("PDOT_TM")) TM = atoll(e);
-  if (TM != 64 && TM != 128 && TM != 256) TM = 128;
+  if (TM != 8 && TM != 16 && TM != 32 && TM != 64 && TM != 128 && TM != 256) TM = 128;
   return TM;
 }
 
-int pdot_shard_rows(int64_t m_total, int nranks, int rank, int64_t* row0, int64_t* row1) {
-  if (m_total < 1) return set_err(PDOT_EINVAL, "plan dimensions must be positive");
+int pdot_shard_rows(int64_t m_total, int64_t n, int nranks, int rank, int64_t* row0, int64_t* row1) {
+  if (m_total < 1 || n < 1) return set_err(PDOT_EINVAL, "plan dimensions must be positive");
   int64_t Tg, GS, r0, r1;
   int g0, g1;
-  if (int rc = shard_geometry(m_total, row_tile(), nranks, rank, &Tg, &GS, &g0, &g1, &r0, &r1)) return rc;
+  if (int rc = shard_geometry(m_total, row_tile(m_total, n), nranks, rank, &Tg, &GS, &g0, &g1, &r0, &r1)) return rc;
   if (row0) *row0 = r0;
   if (row1) *row1 = r1;
   return PDOT_OK;
@@ -438,7 +444,7 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
   if (!out) return set_err(PDOT_EINVAL, "null output handle");
   *out = nullptr;
   if (m_total < 1 || n < 1) return set_err(PDOT_EINVAL, "plan dimensions must be positive");
-  const int64_t TM = row_tile();
+  const int64_t TM = row_tile(m_total, n);
   int64_t Tg, GS, row0, row1;
   int g0, g1;
   if (int rc = shard_geometry(m_total, TM, nranks, rank, &Tg, &GS, &g0, &g1, &row0, &row1)) return rc;
@@ -1067,6 +1073,29 @@ int pdot_exchange_local(pdot_solver** hs, int count) {
     }
   }
   CK(cudaDeviceSynchronize());
+  return PDOT_OK;
+}
+
+int pdot_time_finalize(pdot_solver* h, int iters, double* ms_per_launch) {
+  if (!h || iters < 1 || !h->problem_set) return set_err(PDOT_EINVAL, "bad argument");
+  DeviceGuard dg(h->device);
+  Ctl& c = h->host;
+  unit_ctl(h);
+  c.sX = 0; c.sA = 1; c.sXn = 2; c.sAn = 3;
+  c.unit_avg = 1;
+  c.tau = 1e-3; c.sigma = 1e-3; c.kd = 3.0; c.rkd = 1.0 / 3.0;
+  c.op = pdot::OP_STEP;
+  if (int rc = upload_ctl(h)) return rc;
+  pdot::launch_stream_pass(h->dev, h->host, pdot::OP_STEP, h->stream);
+  for (int i = 0; i < 2; ++i) pdot::launch_finalize_pass(h->dev, h->host, pdot::OP_STEP, pdot::FIN_FUSED, h->stream);
+  CK(cudaEventRecord(h->t0, h->stream));
+  for (int i = 0; i < iters; ++i) pdot::launch_finalize_pass(h->dev, h->host, pdot::OP_STEP, pdot::FIN_FUSED, h->stream);
+  CK(cudaEventRecord(h->t1, h->stream));
+  h->launches += iters + 3;
+  CK(cudaEventSynchronize(h->t1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->t0, h->t1));
+  if (ms_per_launch) *ms_per_launch = ms / iters;
   return PDOT_OK;
 }
 

@@ -141,7 +141,7 @@ class Handle:
         self.nranks, self.rank, self.m_total = nranks, rank, m
         if nranks > 1:
             r0, r1 = ctypes.c_int64(), ctypes.c_int64()
-            _lib.check(self.lib.pdot_shard_rows(m, nranks, rank, ctypes.byref(r0), ctypes.byref(r1)))
+            _lib.check(self.lib.pdot_shard_rows(m, n, nranks, rank, ctypes.byref(r0), ctypes.byref(r1)))
             self.row0, m = r0.value, r1.value - r0.value
         else:
             self.row0 = 0

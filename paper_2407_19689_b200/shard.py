@@ -32,19 +32,33 @@ from .records import Iterate
 GROUPS = 8
 
 
-def shard_rows(m_total: int, nranks: int, rank: int, row_tile: int = 128):
+def row_tile(m_total: int, n: int) -> int:
+    """Rows per streaming tile (mirror of row_tile() in csrc/solver.cu)."""
+    import os
+    tm = 128
+    u = -(-n // 512)
+    while tm > 16 and -(-m_total // tm) * u < 148:
+        tm //= 2
+    env = os.environ.get("PDOT_TM")
+    if env is not None:
+        tm = int(env) if int(env) in (8, 16, 32, 64, 128, 256) else 128
+    return tm
+
+
+def shard_rows(m_total: int, n: int, nranks: int, rank: int):
     """Group-aligned row range of a shard (pure-Python mirror of pdot_shard_rows)."""
-    T = -(-m_total // row_tile)
+    row_tile_ = row_tile(m_total, n)
+    T = -(-m_total // row_tile_)
     if nranks not in (1, 2, 4, 8):
         raise ValueError("row sharding supports 1, 2, 4 or 8 shards")
     if not 0 <= rank < nranks:
         raise ValueError("rank out of range")
     if nranks > 1 and T % GROUPS:
-        raise ValueError("row sharding needs the number of 128-row tiles to be a multiple of 8")
+        raise ValueError("row sharding needs the number of row tiles to be a multiple of 8")
     gs = -(-T // GROUPS)
     per = GROUPS // nranks
     t0, t1 = min(rank * per * gs, T), min((rank + 1) * per * gs, T)
-    return min(t0 * row_tile, m_total), min(t1 * row_tile, m_total)
+    return min(t0 * row_tile_, m_total), min(t1 * row_tile_, m_total)
 
 
 def _bind_shard(h: Handle, dp: DeviceProblem) -> None:

@@ -26,5 +26,12 @@ torch.cuda.synchronize()
 torch.cuda.profiler.start()  # ncu --profile-from-start off captures only the STEP launches below
 _lib.check(h.lib.pdot_time_stream_kernel(h.ptr, a.kernel_launches, ctypes.byref(ms)))
 torch.cuda.profiler.stop()
+res = _lib.Result()
+_lib.check(h.lib.pdot_resume(h.ptr, a.iters + 100, ctypes.byref(res)))
+per_pass = res.device_s / (res.passes - rep._passes)
+msf = ctypes.c_double()
+_lib.check(h.lib.pdot_time_finalize(h.ptr, 50, ctypes.byref(msf)))
+print(f"finalize {msf.value * 1e3:.1f} us; solve pass {per_pass * 1e3:.4f} ms, overhead/pass "
+      f"{(per_pass * 1e3 - ms.value) * 1e3:.1f} us")
 print(f"iters {rep.iterations} passes {rep._passes} step-kernel {ms.value:.3f} ms "
       f"-> {40 * a.r**4 / ms.value / 1e6:.0f} GB/s")

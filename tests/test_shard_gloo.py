@@ -62,9 +62,9 @@ def _worker(rank, world, port, out_q):
     lib = _lib.load()
     m_total = 2048
     r0, r1 = ctypes.c_int64(), ctypes.c_int64()
-    assert lib.pdot_shard_rows(m_total, world, rank, ctypes.byref(r0), ctypes.byref(r1)) == 0
+    assert lib.pdot_shard_rows(m_total, 4096, world, rank, ctypes.byref(r0), ctypes.byref(r1)) == 0
     res["rows"] = (r0.value, r1.value)
-    res["rows_py"] = shard_rows(m_total, world, rank)
+    res["rows_py"] = shard_rows(m_total, 4096, world, rank)
     # 2. NCCL id broadcast
     res["id"] = nccl_unique_id(None)
     # 3. exchange model: the "global" column partials are seeded identically
