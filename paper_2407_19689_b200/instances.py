@@ -156,6 +156,75 @@ def l1_grid_cost(r):
     return (np.abs(a[:, None] - a[None, :]) + np.abs(b[:, None] - b[None, :])).astype(np.float64)
 
 
+GRID_KINDS = ("l1", "l2", "linf")
+SYNTH_CLASSES = ("whitenoise", "shapes", "cauchy_like")
+
+
+def grid_cost(r, norm_kind, normalize=False):
+    """Pairwise l1 / l2 / linf distances between the cells of an r x r grid
+    (restates instance.py:167-191 with the same numpy operations, so the
+    entries are bit-identical; l2 goes through sqrt)."""
+    if r < 1:
+        raise InstanceError("grid resolution must be positive")
+    if norm_kind not in GRID_KINDS:
+        raise InstanceError(f"grid cost kind must be one of {GRID_KINDS}")
+    a, b = grid_coords(r)
+    coords = np.stack([a, b], axis=1).astype(np.float64)
+    diff = np.abs(coords[:, None, :] - coords[None, :, :])
+    if norm_kind == "l1":
+        entries = diff.sum(axis=2)
+    elif norm_kind == "l2":
+        entries = np.sqrt((diff ** 2).sum(axis=2))
+    else:
+        entries = diff.max(axis=2)
+    if normalize and entries.max() > 0:
+        entries = entries / entries.max()
+    return CostMatrix(entries, norm_kind)
+
+
+def _rect(rng, rows, cols):
+    r0 = int(rng.integers(rows.start, rows.stop))
+    r1 = int(rng.integers(r0, rows.stop))
+    c0 = int(rng.integers(cols.start, cols.stop))
+    c1 = int(rng.integers(c0, cols.stop))
+    return r0, r1, c0, c1
+
+
+def _synth_image(kind, r, rng):
+    """One synthetic image (instance.py:208-226), same RNG call sequence."""
+    if kind == "whitenoise":
+        return rng.random((r, r))
+    if kind == "shapes":
+        pixels = np.zeros((r, r))
+        split = int(rng.integers(1, r))
+        for rows in (range(0, split), range(split, r)):
+            r0, r1, c0, c1 = _rect(rng, rows, range(0, r))
+            pixels[r0:r1 + 1, c0:c1 + 1] = 1.0
+        return pixels
+    if kind == "cauchy_like":
+        center = rng.integers(0, r, size=2)
+        ii, jj = np.meshgrid(np.arange(r), np.arange(r), indexing="ij")
+        d2 = (ii - center[0]) ** 2 + (jj - center[1]) ** 2
+        return 1.0 / (1.0 + d2.astype(np.float64))
+    raise InstanceError(f"unknown synthetic class {kind!r}")
+
+
+def synth_images(kind, r, seed):
+    """Deterministic pair of synthetic images (instance.py:222-229)."""
+    if kind not in SYNTH_CLASSES:
+        raise InstanceError(f"unknown synthetic class {kind!r}")
+    if r < 2:
+        raise InstanceError("synthetic images need resolution >= 2")
+    rng = np.random.default_rng(seed)
+    return _synth_image(kind, r, rng), _synth_image(kind, r, rng)
+
+
+def grid_problem(kind, r, norm_kind, seed):
+    """Full grid instance: two synthetic images + grid cost (instance.py:232-239)."""
+    src, dst = synth_images(kind, r, seed)
+    return OTProblem(grid_cost(r, norm_kind), Marginal(src.ravel()), Marginal(dst.ravel()))
+
+
 def whitenoise_images(r, seed):
     """synth_instance("whitenoise", r, seed), instance.py:350-351, 369-376."""
     if r < 2:

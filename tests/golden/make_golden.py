@@ -111,7 +111,20 @@ def solve_cases():
     return cases
 
 
+def instance_cases():
+    """Reference instance generators on fixed seeds (pins instances.py)."""
+    out = {}
+    for kind in ("whitenoise", "shapes", "cauchy_like"):
+        for norm in ("l1", "l2", "linf"):
+            prob = ot.grid_problem(kind, 6, norm, seed=11)
+            out[f"{kind}_{norm}_C"] = prob.C
+            out[f"{kind}_{norm}_f"] = prob.f
+            out[f"{kind}_{norm}_g"] = prob.g
+    return out
+
+
 def main():
+    np.savez_compressed(HERE / "instances.npz", **instance_cases())
     np.savez_compressed(HERE / "elements.npz", **element_cases())
     arrays = {}
     meta = {}

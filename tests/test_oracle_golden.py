@@ -94,3 +94,15 @@ def test_c1_seed0_report():
                 "restart_lengths", "termination_reason"):
         assert rep[key] == gold["report"][key], key
     assert rep["pre_rounding_objective"] == gold["pre_rounding_objective"]
+
+
+def test_instance_generators_match_reference():
+    """grid_cost / synth images / grid_problem restated in instances.py are
+    bit-identical to the reference's (fixtures from the reference itself)."""
+    G = np.load(GOLD / "instances.npz")
+    for kind in ("whitenoise", "shapes", "cauchy_like"):
+        for norm in ("l1", "l2", "linf"):
+            prob = inst.grid_problem(kind, 6, norm, 11)
+            assert np.array_equal(prob.C, G[f"{kind}_{norm}_C"]), (kind, norm)
+            assert np.array_equal(prob.f, G[f"{kind}_{norm}_f"]), (kind, norm)
+            assert np.array_equal(prob.g, G[f"{kind}_{norm}_g"]), (kind, norm)
