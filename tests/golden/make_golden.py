@@ -166,6 +166,18 @@ def main():
         print("C1 seed", seed, rep.iterations, rep.restarts)
     (HERE / "c1.json").write_text(json.dumps(c1, indent=1, sort_keys=True))
 
+    # objective parity at tight tolerance: 256^2 sq-Euclidean, tol 1e-8,
+    # and C1 seeds 1-2 at tol 1e-4 (trajectory-sensitive; compared in the envelope)
+    p4 = {}
+    for r, seed, tol in ((16, 0, 1e-8), (16, 1, 1e-8), (16, 2, 1e-8), (32, 1, 1e-4), (32, 2, 1e-4)):
+        f, g = inst.whitenoise_marginals(r, seed)
+        prob = ref_problem(inst.sqeuclid_grid_cost(r), f, g)
+        it, rep = ot.solve(prob, ot.SolverConfig(tol=tol, deterministic=True))
+        p4[f"r{r}_s{seed}_tol{tol:g}"] = dict(r=r, seed=seed, tol=tol, report=json.loads(rep.to_json()),
+                                               pre_rounding_objective=float(np.vdot(prob.C, it.X)))
+        print("P4", r, seed, tol, rep.iterations, rep.restarts, float(np.vdot(prob.C, it.X)))
+    (HERE / "p4.json").write_text(json.dumps(p4, indent=1, sort_keys=True))
+
 
 if __name__ == "__main__":
     main()
