@@ -171,13 +171,25 @@ def make_device_problem(pd, cfgd, local, rows=None):
     return pd.DeviceProblem.sqeuclid_grid(cfgd["r"], cfgd["seed"], device=local, rows=rows)
 
 
-def make_host_problem(inst, cfgd, rows=None):
+def to_pinned(a):
+    """Copy a host array into page-locked memory (the e2e inputs come from pinned memory)."""
+    import torch
+    t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+    t.numpy()[...] = a
+    return t.numpy()
+
+
+def make_host_problem(inst, cfgd, rows=None, pinned=False):
     """Host (numpy) instance, or just its row shard, for the end-to-end run."""
     from types import SimpleNamespace
     if rows is None:
         if cfgd.get("kind") == "rect":
-            return inst.rect_problem(cfgd["seed"])
-        return inst.sqeuclid_problem(cfgd["r"], cfgd["seed"])
+            prob = inst.rect_problem(cfgd["seed"])
+        else:
+            prob = inst.sqeuclid_problem(cfgd["r"], cfgd["seed"])
+        if pinned:
+            prob.cost.entries = to_pinned(prob.C)
+        return prob
     r0, r1 = rows
     if cfgd.get("kind") == "rect":
         m, n = cfgd["m"], cfgd["n"]
@@ -187,6 +199,8 @@ def make_host_problem(inst, cfgd, rows=None):
         f, g = inst.whitenoise_marginals(cfgd["r"], cfgd["seed"])
         C, fro = inst.sqeuclid_grid_cost_rows(cfgd["r"], r0, r1), inst.sqeuclid_fro_norm(cfgd["r"])
     marg = float(np.linalg.norm(f) + np.linalg.norm(g))
+    if pinned:
+        C = to_pinned(C)
     return SimpleNamespace(C=C, f=f[r0:r1], g=g, m=r1 - r0, n=C.shape[1], cost_fro_norm=fro,
                            marginal_norm=marg, row0=r0, m_total=len(f))
 
@@ -295,17 +309,16 @@ def main():
     e2e = None
     host_prob = None
     if not args.no_e2e:
-        host_prob = make_host_problem(inst, cfgd, rows)
+        host_prob = make_host_problem(inst, cfgd, rows, pinned=True)
         if world == 1:
             _ = host_prob.cost_fro_norm, host_prob.marginal_norm
             del dp
-            pd.release_handles()
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
         if world == 1:
             it, rep_e = pd.solve(host_prob, pd.SolverConfig(tol=cfgd["tol"]), device=local)
-            api = "paper_2407_19689_b200.solve(OTProblem numpy, SolverConfig(tol))"
+            api = "paper_2407_19689_b200.solve(OTProblem with C in pinned host memory, SolverConfig(tol)) -> numpy X"
         else:
             dph = pd.DeviceProblem.from_host(host_prob, local)
             dph.m_total, dph.row0 = host_prob.m_total, host_prob.row0

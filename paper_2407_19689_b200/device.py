@@ -196,8 +196,8 @@ class Handle:
             torch.cuda.synchronize(self.device)
         _lib.check(self.lib.pdot_set_slot(self.ptr, slot, Xp, ld if Xp else self.n, pp, qp))
 
-    def get_slot(self, slot: int, want_X=True):
-        X = np.empty((self.m, self.n)) if want_X else None
+    def get_slot(self, slot: int, want_X=True, out=None):
+        X = (out if out is not None else np.empty((self.m, self.n))) if want_X else None
         p = np.empty(self.m)
         q = np.empty(self.n)
         _lib.check(self.lib.pdot_get_slot(self.ptr, slot, X.ctypes.data if want_X else None, self.n,

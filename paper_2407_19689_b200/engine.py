@@ -56,6 +56,28 @@ def _events(h) -> list:
             return out
 
 
+class _Prefault:
+    """Allocate the host output plan and first-touch its pages on background
+    threads while the GPU iterates: a device->host copy into fresh pageable
+    memory runs at ~4 GB/s (page faults), into touched pages at ~19 GB/s."""
+
+    def __init__(self, shape, nthreads: int = 16):
+        import threading
+        self.arr = np.empty(shape)
+        rows = np.array_split(np.arange(shape[0]), nthreads) if shape[0] else []
+        self.threads = [threading.Thread(target=self._touch, args=(r,), daemon=True) for r in rows if len(r)]
+        for t in self.threads:
+            t.start()
+
+    def _touch(self, r):
+        self.arr[r[0]:r[-1] + 1].fill(0.0)
+
+    def result(self):
+        for t in self.threads:
+            t.join()
+        return self.arr
+
+
 def assemble_report(h, res, config: SolverConfig, trace: SolveTrace | None, round_slot: bool = True):
     """Trace events + device result -> SolveReport (pdhg.py:380-399)."""
     lib = h.lib
@@ -125,6 +147,7 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
         h.set_slot(0, None, None, None)
     stepwise = trace is not None
     cfg = config_struct(config, trace_level=1 if trace is not None else 0, poll_passes=poll_passes)
+    out = _Prefault((dp.m, dp.n)) if not return_device and dp.m * dp.n >= (1 << 22) else None
     res = _lib.Result()
     lib = h.lib
     if not stepwise:
@@ -158,7 +181,7 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
     report._e2e_s = elapsed  # noqa: SLF001
     if return_device:
         return (int(res.final_slot), h), report
-    X, p, q = h.get_slot(res.final_slot)
+    X, p, q = h.get_slot(res.final_slot, out=None if out is None else out.result())
     return Iterate(X, p, q), report
 
 
