@@ -161,7 +161,7 @@ def run_reference(args, cfgd):
                                    f"instance build {build_s:.1f}s excluded"},
         "e2e": {"value": ips, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -205,7 +205,31 @@ def make_host_problem(inst, cfgd, rows=None, pinned=False):
                            marginal_norm=marg, row0=r0, m_total=len(f))
 
 
+_JSON_FD = None
+
+
+def emit(line: dict) -> None:
+    """Print the one JSON line on the real stdout (everything else goes to stderr)."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is not None:
+        os.write(_JSON_FD, data)
+    else:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+
+
+def quiet_stdout() -> None:
+    """Point fd 1 at stderr so library banners (NCCL's version line, ...) cannot
+    interleave with the JSON line; emit() writes to the saved descriptor."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
 def main():
+    quiet_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=300)
@@ -215,11 +239,15 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tol", action="store_true", help="skip the time-to-tolerance solve")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the row-sharded pass sequence even on 1 GPU (1-rank NCCL communicator)")
     args = ap.parse_args()
     cfgd = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfgd)
     args.warmup = max(3, args.warmup)
+    if args.sharded:
+        os.environ["PDOT_FORCE_SPLIT"] = "1"
 
     import torch
     import torch.distributed as dist
@@ -247,9 +275,10 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         return float(tt.item())
 
-    rows = shard_rows(m, n, world, rank) if world > 1 else None
+    sharded = world > 1 or args.sharded
+    rows = shard_rows(m, n, world, rank) if sharded else None
     dp = make_device_problem(pd, cfgd, local, rows)
-    if world > 1:
+    if sharded:
         solver = ShardedSolver(dp, world, rank)
         h = solver.h
 
@@ -310,13 +339,13 @@ def main():
     host_prob = None
     if not args.no_e2e:
         host_prob = make_host_problem(inst, cfgd, rows, pinned=True)
-        if world == 1:
+        if not sharded:
             _ = host_prob.cost_fro_norm, host_prob.marginal_norm
             del dp
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        if world == 1:
+        if not sharded:
             it, rep_e = pd.solve(host_prob, pd.SolverConfig(tol=cfgd["tol"]), device=local)
             api = "paper_2407_19689_b200.solve(OTProblem with C in pinned host memory, SolverConfig(tol)) -> numpy X"
         else:
@@ -355,7 +384,7 @@ def main():
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (on-device cost generator, seeded marginals)",
             "config": {"workload": cfgd["workload"], "m": m, "n": n, "global_batch": 1, "seq_len": 0,
-                       "parallelism": f"rows{world}" if world > 1 else "single",
+                       "parallelism": f"rows{world}" if sharded else "single",
                        "l2_policy": "inputs larger than L2 (C, X, average streamed every pass)",
                        "timed_window": f"iterations {args.warmup + 1}..{args.warmup + steps_done} of the solve, tol test disabled"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -369,7 +398,7 @@ def main():
             "cpu_baseline": cpu,
         }
         line.update(extra)
-        print(json.dumps(line), flush=True)
+        emit(line)
     if solver is not None:
         solver.close()
     if world > 1:

@@ -56,6 +56,7 @@ struct pdot_solver {
   int64_t gstride = 0;
   void* nccl_comm = nullptr;  // ncclComm_t when nranks > 1 and a communicator was attached
   bool virtual_shards = false;  // exchange driven by the host (single-GPU emulation)
+  bool force_split = false;     // 1-rank communicator exercising the multi-GPU pass sequence
 };
 
 namespace {
@@ -281,7 +282,7 @@ int shard_geometry(int64_t m_total, int64_t TM, int nranks, int rank, int64_t* T
   return PDOT_OK;
 }
 
-bool split_mode(const pdot_solver* h) { return h->nranks > 1; }
+bool split_mode(const pdot_solver* h) { return h->nranks > 1 || h->force_split; }
 
 // all-gather of the per-group partials (in place: every rank owns a contiguous chunk)
 int exchange(pdot_solver* h) {
@@ -996,7 +997,13 @@ int pdot_nccl_unique_id(void* out128) {
 
 int pdot_comm_init(pdot_solver* h, const void* id128) {
   if (!h || !id128) return set_err(PDOT_EINVAL, "null argument");
-  if (h->nranks == 1) return PDOT_OK;
+  if (h->nranks == 1) {
+    // a 1-rank communicator: only useful to exercise the split pass sequence
+    // (K2a -> ncclAllGather -> K2b) on one GPU; PDOT_FORCE_SPLIT=1 enables it
+    const char* e = getenv("PDOT_FORCE_SPLIT");
+    if (!e || atoi(e) == 0) return PDOT_OK;
+    h->force_split = true;
+  }
   if (!nccl().ok) return set_err(PDOT_ENCCL, "libnccl.so.2 could not be loaded");
   DeviceGuard dg(h->device);
   NcclId id;
@@ -1006,6 +1013,10 @@ int pdot_comm_init(pdot_solver* h, const void* id128) {
   if (r != 0) return nccl_fail(r, "ncclCommInitRank");
   h->nccl_comm = comm;
   h->virtual_shards = false;
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
   return PDOT_OK;
 }
 
