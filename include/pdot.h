@@ -101,6 +101,13 @@ int pdot_geometry(const pdot_solver* h, int64_t* ldx, int64_t* row_tile, int64_t
  * the handle; ldc must be even. */
 int pdot_set_problem(pdot_solver* h, const double* C_dev, int64_t ldc, const double* f_dev,
                      const double* g_dev, double cost_fro_norm, double marginal_norm);
+/* Matrix-free variant: C_ij is generated in registers from
+ * grid coordinates (kind/a as in pdot_gen_cost) instead of being streamed from
+ * HBM -- 32 instead of 40 bytes per plan entry per pass, and no m x n cost
+ * buffer at all.  The generated values are exact integers, so results are
+ * bit-identical to binding the explicit matrix. */
+int pdot_set_problem_implicit(pdot_solver* h, int kind, const int64_t* a, const double* f_dev,
+                              const double* g_dev, double cost_fro_norm, double marginal_norm);
 /* Load (X, p, q) into slot `slot` (0..5).  X_any may be NULL for zeros. */
 int pdot_set_slot(pdot_solver* h, int slot, const double* X_any, int64_t ldX, const double* p_any,
                   const double* q_any);

@@ -30,7 +30,7 @@ COST_SQEUCLID_GRID, COST_L1_GRID, COST_L1_RECT = 0, 1, 2
 # every symbol include/pdot.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "pdot_last_error", "pdot_version", "pdot_create", "pdot_destroy", "pdot_geometry",
-    "pdot_set_problem", "pdot_set_slot", "pdot_get_slot", "pdot_slot_ptrs", "pdot_solve",
+    "pdot_set_problem", "pdot_set_problem_implicit", "pdot_set_slot", "pdot_get_slot", "pdot_slot_ptrs", "pdot_solve",
     "pdot_begin", "pdot_advance", "pdot_finish", "pdot_resume", "pdot_get_events", "pdot_round",
     "pdot_unit_step", "pdot_unit_bound", "pdot_unit_kkt", "pdot_unit_apply_A", "pdot_apply_At",
     "pdot_gen_cost", "pdot_gen_cost_rows", "pdot_fro_norm", "pdot_time_stream_kernel",
@@ -84,6 +84,7 @@ _SIGS = {
     "pdot_geometry": ([_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
                        ctypes.POINTER(_I64)], ctypes.c_int),
     "pdot_set_problem": ([_P, _P, _I64, _P, _P, _D, _D], ctypes.c_int),
+    "pdot_set_problem_implicit": ([_P, ctypes.c_int, ctypes.POINTER(_I64), _P, _P, _D, _D], ctypes.c_int),
     "pdot_set_slot": ([_P, ctypes.c_int, _P, _I64, _P, _P], ctypes.c_int),
     "pdot_get_slot": ([_P, ctypes.c_int, _P, _I64, _P, _P], ctypes.c_int),
     "pdot_slot_ptrs": ([_P, ctypes.c_int, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P)],

@@ -199,7 +199,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
     column_sums<1>(c, b, col, j, smem, mode);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       c.cols_out[j] = col[0];
-      if (c.C) {
+      if (c.C || c.cost_kind > 0) {
         const Slot& sx = c.slot[c.sX];
         const double qj = sx.q[j], gj = c.g[j];
         const double pc = col[0] - gj;
@@ -291,7 +291,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
       row_sums<1>(c, ok ? i : c.m, row);
       if (ok) {
         c.rows_out[i] = row[0];
-        if (c.C) {
+        if (c.C || c.cost_kind > 0) {
           const double pi = c.slot[c.sX].p[i], fi = c.f[i];
           const double pr = row[0] - fi;
           vals[0] += pr * pr;

@@ -110,6 +110,10 @@ struct Ctl {
   const double* C;
   const double* f;
   const double* g;
+  // implicit (matrix-free) cost: C == nullptr and cost_kind > 0 -> C_ij generated
+  // from grid coordinates in registers (exact integers, identical to the explicit C)
+  int32_t cost_kind;       // 0 explicit, 1 sq-Euclidean grid, 2 L1 grid, 3 L1 rectangular
+  int64_t cost_a[4];
   Slot slot[kNSlot];
   double* colpart;    // [T][NQ][ldx]
   double* rowpart;    // [U][NQ][m]
@@ -200,6 +204,39 @@ __device__ __forceinline__ double div_by_count(double x, double k, double rk) {
   const double r = __fma_rn(-q0, k, x);
   return __fma_rn(r, rk, q0);
 }
+
+// C_ij of the generated cost families from row/column coordinates (pdot_gen_cost).
+enum CostKind : int { COST_EXPLICIT = 0, COST_SQEUCLID = 1, COST_L1GRID = 2, COST_L1RECT = 3 };
+
+struct CostGen {
+  int kind;
+  int64_t a0, a1, a2, a3;
+  int64_t row0;  // global index of local row 0 (row shards)
+  __device__ __forceinline__ double2 row_coord(int64_t i_local) const {
+    const int64_t i = row0 + i_local;
+    if (kind == COST_L1RECT) return make_double2((double)(2 * (i / a1)), (double)(2 * (i % a1)));
+    return make_double2((double)(i / a0), (double)(i % a0));
+  }
+  __device__ __forceinline__ double2 col_coord(int64_t j) const {
+    if (kind == COST_L1RECT) return make_double2((double)(j / a3), (double)(j % a3));
+    return make_double2((double)(j / a0), (double)(j % a0));
+  }
+  // row coordinates advance incrementally row by row (no division in the loop)
+  __device__ __forceinline__ void next_row(double2& r) const {
+    const double step = (kind == COST_L1RECT) ? 2.0 : 1.0;
+    const double wrap = (kind == COST_L1RECT) ? (double)(2 * a1) : (double)a0;
+    r.y += step;
+    if (r.y == wrap) {
+      r.y = 0.0;
+      r.x += step;
+    }
+  }
+  __device__ __forceinline__ double cost(double2 r, double2 cc) const {
+    const double da = r.x - cc.x, db = r.y - cc.y;  // exact (small integers)
+    if (kind == COST_SQEUCLID) return da * da + db * db;
+    return fabs(da) + fabs(db);
+  }
+};
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;

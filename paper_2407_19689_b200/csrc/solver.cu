@@ -608,6 +608,32 @@ int pdot_set_problem(pdot_solver* h, const double* C_dev, int64_t ldc, const dou
   if (((uintptr_t)C_dev & 15) != 0) return set_err(PDOT_EINVAL, "C must be 16-byte aligned");
   h->host.C = C_dev;
   h->host.ldc = ldc;
+  h->host.cost_kind = pdot::COST_EXPLICIT;
+  h->host.f = f_dev;
+  h->host.g = g_dev;
+  h->host.cost_fro = cost_fro_norm;
+  h->host.marg_norm = marginal_norm;
+  h->problem_set = true;
+  return PDOT_OK;
+}
+
+int pdot_set_problem_implicit(pdot_solver* h, int kind, const int64_t* a, const double* f_dev,
+                              const double* g_dev, double cost_fro_norm, double marginal_norm) {
+  if (!h || !a || !f_dev || !g_dev) return set_err(PDOT_EINVAL, "null argument");
+  const int64_t m_total = h->m_total, n = h->n;
+  if (kind == PDOT_COST_SQEUCLID_GRID || kind == PDOT_COST_L1_GRID) {
+    if (a[0] != a[1] || a[0] * a[1] != n || m_total != n) return set_err(PDOT_EINVAL, "grid cost needs m = n = r*r");
+  } else if (kind == PDOT_COST_L1_RECT) {
+    if (a[0] * a[1] != m_total || a[2] * a[3] != n) return set_err(PDOT_EINVAL, "rect cost shape mismatch");
+  } else {
+    return set_err(PDOT_EINVAL, "unknown cost kind");
+  }
+  h->host.C = nullptr;
+  h->host.ldc = h->ldx;
+  h->host.cost_kind = kind == PDOT_COST_SQEUCLID_GRID ? pdot::COST_SQEUCLID
+                      : kind == PDOT_COST_L1_GRID     ? pdot::COST_L1GRID
+                                                      : pdot::COST_L1RECT;
+  for (int i = 0; i < 4; ++i) h->host.cost_a[i] = a[i];
   h->host.f = f_dev;
   h->host.g = g_dev;
   h->host.cost_fro = cost_fro_norm;
@@ -873,7 +899,11 @@ static int unit_kkt_impl(pdot_solver* h, bool with_cost, double scale_R, double*
   Ctl& c = h->host;
   unit_ctl(h);
   const double* Csave = c.C;
-  if (!with_cost) c.C = nullptr;
+  const int32_t kind_save = c.cost_kind;
+  if (!with_cost) {
+    c.C = nullptr;
+    c.cost_kind = pdot::COST_EXPLICIT;
+  }
   c.sX = 0;
   c.scale_R = scale_R;
   c.kkt_write_viol = (viol_any && with_cost) ? 1 : 0;
@@ -881,6 +911,7 @@ static int unit_kkt_impl(pdot_solver* h, bool with_cost, double scale_R, double*
   c.op = pdot::OP_KKT;
   int rc = upload_ctl(h);
   c.C = Csave;
+  c.cost_kind = kind_save;
   if (rc) return rc;
   if ((rc = run_pass(h, pdot::OP_KKT))) return rc;
   double o[10];

@@ -33,7 +33,18 @@ struct Geo {
   int rows;     // rows in this tile
   int64_t j;    // first of this lane's two columns
   bool v0, v1;  // column validity
+  CostGen gen;  // implicit cost (gen.kind > 0 when C is generated, not read)
 };
+
+// the cost pair (i, j..j+1): streamed from HBM, or generated from coordinates
+__device__ __forceinline__ double2 cost_pair(const double* C, const Geo& g, int64_t i) {
+  if (C) return ld_stream2(C + i * g.ldc + g.j);
+  if (g.gen.kind > 0) {
+    const double2 r = g.gen.row_coord(i);
+    return make_double2(g.gen.cost(r, g.gen.col_coord(g.j)), g.gen.cost(r, g.gen.col_coord(g.j + 1)));
+  }
+  return make_double2(0.0, 0.0);
+}
 
 // ---------------------------------------------------------------------------
 // OP_STEP: the fused PDHG trial step (+ running average, + KKT dual violation
@@ -118,7 +129,7 @@ struct KktOp {
     cl.q1 = (g.v1 && q) ? q[g.j + 1] : 0.0;
   }
   __device__ __forceinline__ void load(Frag& fr, const Geo& g, int64_t i) const {
-    fr.c = C ? ld_stream2(C + i * g.ldc + g.j) : make_double2(0.0, 0.0);
+    fr.c = cost_pair(C, g, i);
     fr.x = ld_stream2(X + i * g.ldx + g.j);
     fr.p = p ? __ldg(p + i) : 0.0;
   }
@@ -197,7 +208,7 @@ struct RoundOp {
   }
   __device__ __forceinline__ void load(Frag& fr, const Geo& g, int64_t i) const {
     fr.x = ld_stream2(X + i * g.ldx + g.j);
-    fr.c = (stage == 3) ? ld_stream2(C + i * g.ldc + g.j) : make_double2(0.0, 0.0);
+    fr.c = (stage == 3) ? cost_pair(C, g, i) : make_double2(0.0, 0.0);
     fr.r = (stage >= 1) ? __ldg(rs + i) : 1.0;  // stage 0 sums X itself
     fr.e = (stage == 3) ? __ldg(er + i) : 0.0;
   }
@@ -271,6 +282,9 @@ __device__ __forceinline__ Geo make_geo(const Ctl& c, bool worker) {
   g.j = (int64_t)blockIdx.x * kTileN + warp * 64 + lane * 2;
   g.v0 = worker && g.j < c.n;
   g.v1 = worker && g.j + 1 < c.n;
+  g.gen.kind = c.C ? 0 : c.cost_kind;
+  g.gen.a0 = c.cost_a[0]; g.gen.a1 = c.cost_a[1]; g.gen.a2 = c.cost_a[2]; g.gen.a3 = c.cost_a[3];
+  g.gen.row0 = c.row0;
   return g;
 }
 
@@ -392,11 +406,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+template <bool IMPLICIT>
 __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigned char* smem) {
   constexpr int NQ = StepOp::NQ, NS = StepOp::NS, R = kStageRows;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool worker = warp < kWarps;
-  const Geo g = make_geo(c, worker);
+  Geo g = make_geo(c, worker);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kStages;
   unsigned char* stages = smem + kBarBytes;
@@ -409,6 +424,8 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
   const int64_t vcols = imin64(kTileN, c.n - col0);
   const uint32_t rowbytes = (uint32_t)(((vcols + 1) & ~1LL) * 8);
   const uint32_t pbytes = (uint32_t)(((g.rows + 1) & ~1) * 8);
+  constexpr bool implicit_c = IMPLICIT;       // cost generated in registers (g.gen)
+  const int kfirst = implicit_c ? 1 : 0;      // first streamed matrix (0 = C)
   const int nmat = op.with_avg ? 3 : 2;
 
   if (threadIdx.x == 0) {
@@ -430,13 +447,14 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
   if (!worker) {
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
-      const double* src[3] = {op.C + g.i0 * c.ldc + col0, op.X + g.i0 * c.ldx + col0, op.A + g.i0 * c.ldx + col0};
+      const double* src[3] = {implicit_c ? nullptr : op.C + g.i0 * c.ldc + col0, op.X + g.i0 * c.ldx + col0,
+                              op.A + g.i0 * c.ldx + col0};
       const int64_t ld[3] = {c.ldc, c.ldx, c.ldx};
       for (int it = 0; it < nst; ++it) {
         const int s = it % kStages;
         if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) + 1) & 1);
         const int nr = min(R, g.rows - it * R);
-        uint32_t tx = (uint32_t)(nr * nmat) * rowbytes;
+        uint32_t tx = (uint32_t)(nr * (nmat - kfirst)) * rowbytes;
         if (it == 0) tx += 2 * pbytes;
         mbar_expect_tx(&full[s], tx);
         if (it == 0) {
@@ -446,7 +464,7 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
         unsigned char* dst = stages + s * kStageBytes;
         for (int r = 0; r < nr; ++r) {
           const int64_t row = (int64_t)it * R + r;
-          for (int k = 0; k < nmat; ++k)
+          for (int k = kfirst; k < nmat; ++k)
             bulk_g2s(dst + (r * 3 + k) * kRowBytes, src[k] + row * ld[k], rowbytes, &full[s], pol);
         }
       }
@@ -455,6 +473,13 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
     StepOp::Col cl;
     op.load_col(cl, g);
     const int off = (warp * 64 + lane * 2) * 8;  // byte offset of the column pair in a staged row
+    double2 cj0 = make_double2(0.0, 0.0), cj1 = make_double2(0.0, 0.0);  // column coordinates (implicit C)
+    double2 rcoord = make_double2(0.0, 0.0);                            // current row's coordinates
+    if (implicit_c) {
+      cj0 = g.gen.col_coord(g.j);
+      cj1 = g.gen.col_coord(g.j + 1);
+      rcoord = g.gen.row_coord(g.i0);
+    }
     const bool fast = op.with_avg && g.rows == c.TM && vcols == kTileN;
     if (fast) {
       // full tile: no masks, running output pointers
@@ -467,7 +492,13 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
         double rv[R * NQ];
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
-          const double2 cc = *reinterpret_cast<const double2*>(st + (rr * 3 + 0) * kRowBytes + off);
+          double2 cc;
+          if (implicit_c) {
+            cc = make_double2(g.gen.cost(rcoord, cj0), g.gen.cost(rcoord, cj1));
+            g.gen.next_row(rcoord);
+          } else {
+            cc = *reinterpret_cast<const double2*>(st + (rr * 3 + 0) * kRowBytes + off);
+          }
           const double2 xx = *reinterpret_cast<const double2*>(st + (rr * 3 + 1) * kRowBytes + off);
           const double2 aa = *reinterpret_cast<const double2*>(st + (rr * 3 + 2) * kRowBytes + off);
           const double pi = pbuf[it * R + rr], pai = pabuf[it * R + rr];
@@ -503,7 +534,12 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
           for (int q = 0; q < NQ; ++q) o0[q] = o1[q] = 0.0;
           if (r < g.rows && g.v0) {
             StepOp::Frag fr;
-            fr.c = *reinterpret_cast<const double2*>(st + (rr * 3 + 0) * kRowBytes + off);
+            if (implicit_c) {
+              fr.c = make_double2(g.gen.cost(rcoord, cj0), g.gen.cost(rcoord, cj1));
+              g.gen.next_row(rcoord);
+            } else {
+              fr.c = *reinterpret_cast<const double2*>(st + (rr * 3 + 0) * kRowBytes + off);
+            }
             fr.x = *reinterpret_cast<const double2*>(st + (rr * 3 + 1) * kRowBytes + off);
             fr.a = op.with_avg ? *reinterpret_cast<const double2*>(st + (rr * 3 + 2) * kRowBytes + off)
                                : make_double2(0.0, 0.0);
@@ -542,13 +578,15 @@ __global__ void __launch_bounds__(kBlockThreads, PDOT_MINB) stream_kernel(const 
       o.Xn = c.slot[c.sXn].X; o.An = c.slot[c.sAn].X;
       o.p = sx.p; o.q = sx.q; o.pa = sa.p; o.qa = sa.q;
       o.tau = c.tau; o.kd = c.kd; o.rkd = c.rkd; o.with_avg = !c.unit || c.unit_avg;
-      step_tma(o, c, smem_raw);
+      if (o.C) step_tma<false>(o, c, smem_raw);
+      else step_tma<true>(o, c, smem_raw);
       break;
     }
     case OP_KKT: {
       KktOp o;
       const Slot& sx = c.slot[c.sX];
-      o.C = c.C; o.X = sx.X; o.p = c.C ? sx.p : nullptr; o.q = c.C ? sx.q : nullptr;
+      const bool has_cost = c.C != nullptr || c.cost_kind > 0;
+      o.C = c.C; o.X = sx.X; o.p = has_cost ? sx.p : nullptr; o.q = has_cost ? sx.q : nullptr;
       o.viol = c.kkt_write_viol ? c.viol_out : nullptr;
       tile_pass(o, c, smem);
       break;

@@ -57,10 +57,16 @@ class DeviceProblem:
         self.device = device
         self.host = host
         self.m_total, self.row0 = self.m, 0
+        self.cost_kind, self.cost_args = None, None
 
     @property
     def ldc(self) -> int:
-        return int(self.C_t.stride(0))
+        return int(self.C_t.stride(0)) if self.C_t is not None else even(self.n)
+
+    @property
+    def implicit(self) -> bool:
+        """True when C is generated in-kernel from grid coordinates (no cost buffer)."""
+        return self.C_t is None
 
     @classmethod
     def from_host(cls, prob, device: int = 0) -> "DeviceProblem":
@@ -71,22 +77,26 @@ class DeviceProblem:
 
     @classmethod
     def generated(cls, kind: int, m: int, n: int, shape_args, f: np.ndarray, g: np.ndarray,
-                  device: int = 0, fro: float | None = None, rows=None) -> "DeviceProblem":
+                  device: int = 0, fro: float | None = None, rows=None, implicit: bool = False) -> "DeviceProblem":
         """Cost built on the device (pdot_gen_cost_rows), marginals from the host.
 
         ``rows = (row0, row1)`` builds only that row shard (C rows and f entries);
         ``fro`` is the exact ||C||_F of the FULL matrix (instances.*_fro_norm),
-        so every shard and GPU count sees the same KKT normaliser."""
+        so every shard and GPU count sees the same KKT normaliser.  With
+        ``implicit=True`` no cost buffer is allocated: the kernels generate C_ij
+        from grid coordinates (matrix-free variant)."""
         require_cuda(device)
         lib = _lib.load()
         row0, row1 = (0, m) if rows is None else rows
-        C_t = torch.empty((row1 - row0, even(n)), dtype=torch.float64, device=f"cuda:{device}")
-        args = (ctypes.c_int64 * 4)(*shape_args)
-        torch.cuda.synchronize(device)
-        _lib.check(lib.pdot_gen_cost_rows(C_t.data_ptr(), row0, row1 - row0, n, C_t.stride(0), kind, args))
+        C_t = None
+        if not implicit:
+            C_t = torch.empty((row1 - row0, even(n)), dtype=torch.float64, device=f"cuda:{device}")
+            args = (ctypes.c_int64 * 4)(*shape_args)
+            torch.cuda.synchronize(device)
+            _lib.check(lib.pdot_gen_cost_rows(C_t.data_ptr(), row0, row1 - row0, n, C_t.stride(0), kind, args))
         if fro is None:
-            if rows is not None:
-                raise ValueError("a row shard needs the exact full-matrix Frobenius norm")
+            if rows is not None or implicit:
+                raise ValueError("a row shard / implicit cost needs the exact full-matrix Frobenius norm")
             out = ctypes.c_double()
             _lib.check(lib.pdot_fro_norm(C_t.data_ptr(), m, n, C_t.stride(0), ctypes.byref(out)))
             fro = out.value
@@ -94,31 +104,35 @@ class DeviceProblem:
         dp = cls(C_t, _h2d_vector(f[row0:row1], device), _h2d_vector(g, device), row1 - row0, n, fro, marg,
                  device)
         dp.m_total, dp.row0 = m, row0
+        dp.cost_kind, dp.cost_args = kind, tuple(shape_args)
         return dp
 
     @classmethod
-    def sqeuclid_grid(cls, r: int, seed: int, device: int = 0, rows=None) -> "DeviceProblem":
+    def sqeuclid_grid(cls, r: int, seed: int, device: int = 0, rows=None, implicit: bool = False) -> "DeviceProblem":
         """Configs C1/C2/C3/C5: whitenoise marginals, exact squared-Euclidean grid cost."""
         from .instances import sqeuclid_fro_norm, whitenoise_marginals
         f, g = whitenoise_marginals(r, seed)
         return cls.generated(_lib.COST_SQEUCLID_GRID, r * r, r * r, (r, r, 0, 0), f, g, device,
-                             fro=sqeuclid_fro_norm(r), rows=rows)
+                             fro=sqeuclid_fro_norm(r), rows=rows, implicit=implicit)
 
     @classmethod
-    def rect_l1(cls, seed: int, src=(64, 128), dst=(128, 256), device: int = 0, rows=None) -> "DeviceProblem":
+    def rect_l1(cls, seed: int, src=(64, 128), dst=(128, 256), device: int = 0, rows=None,
+                implicit: bool = False) -> "DeviceProblem":
         """Config C4: rectangular L1 cost with sparse-support marginals."""
         from .instances import rect_l1_fro_norm, sparse_marginals
         m, n = src[0] * src[1], dst[0] * dst[1]
         f = sparse_marginals(m, 2 * seed)
         g = sparse_marginals(n, 2 * seed + 1)
         return cls.generated(_lib.COST_L1_RECT, m, n, (src[0], src[1], dst[0], dst[1]), f, g, device,
-                             fro=rect_l1_fro_norm(src, dst), rows=rows)
+                             fro=rect_l1_fro_norm(src, dst), rows=rows, implicit=implicit)
 
     def row_shard(self, row0: int, row1: int) -> "DeviceProblem":
         """View of rows [row0, row1) of this (full) problem: C rows and f entries."""
-        dp = DeviceProblem(self.C_t[row0:row1], self.f_t[row0:row1], self.g_t, row1 - row0, self.n,
+        C = None if self.C_t is None else self.C_t[row0:row1]
+        dp = DeviceProblem(C, self.f_t[row0:row1], self.g_t, row1 - row0, self.n,
                            self.cost_fro_norm, self.marginal_norm, self.device)
         dp.m_total, dp.row0 = self.m, row0
+        dp.cost_kind, dp.cost_args = self.cost_kind, self.cost_args
         return dp
 
 
@@ -165,8 +179,13 @@ class Handle:
 
     def bind(self, dp: DeviceProblem) -> None:
         torch.cuda.synchronize(dp.device)
-        _lib.check(self.lib.pdot_set_problem(self.ptr, dp.C_t.data_ptr(), dp.ldc, dp.f_t.data_ptr(),
-                                             dp.g_t.data_ptr(), dp.cost_fro_norm, dp.marginal_norm))
+        if dp.implicit:
+            args = (ctypes.c_int64 * 4)(*dp.cost_args)
+            _lib.check(self.lib.pdot_set_problem_implicit(self.ptr, dp.cost_kind, args, dp.f_t.data_ptr(),
+                                                          dp.g_t.data_ptr(), dp.cost_fro_norm, dp.marginal_norm))
+        else:
+            _lib.check(self.lib.pdot_set_problem(self.ptr, dp.C_t.data_ptr(), dp.ldc, dp.f_t.data_ptr(),
+                                                 dp.g_t.data_ptr(), dp.cost_fro_norm, dp.marginal_norm))
         self.bound_problem = dp  # keep the borrowed buffers alive
 
     def set_slot(self, slot: int, X=None, p=None, q=None) -> None:

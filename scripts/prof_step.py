@@ -16,8 +16,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--r", type=int, default=128)
 ap.add_argument("--iters", type=int, default=30)
 ap.add_argument("--kernel-launches", type=int, default=3)
+ap.add_argument("--implicit", action="store_true")
 a = ap.parse_args()
-dp = pd.DeviceProblem.sqeuclid_grid(a.r, 0)
+dp = pd.DeviceProblem.sqeuclid_grid(a.r, 0, implicit=a.implicit)
 (slot, h), rep = pd.solve_device(dp, pd.SolverConfig(tol=1e-12, max_iters=a.iters))
 ms = ctypes.c_double()
 import torch  # noqa: E402
