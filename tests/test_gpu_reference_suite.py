@@ -366,3 +366,19 @@ def test_nonfinite_raises(pd):
     bad = pd.Iterate(np.array([[np.inf, 0.0], [0.0, 0.5]]), np.zeros(2), np.zeros(2))
     with pytest.raises(RuntimeError):
         pd.solve(prob, pd.SolverConfig(tol=1e-6, restart_mode=pd.FIXED_BETA), initial=bad)
+
+
+def test_acceptance12_cli_byte_identical(tmp_path):
+    """`gen` + two `solve --deterministic` runs write byte-identical reports
+    (test_acceptance.py:335-351, through this package's CLI)."""
+    from paper_2407_19689_b200.cli import main as cli_main
+    inst_file = tmp_path / "inst.txt"
+    assert cli_main(["gen", "--class", "cauchy_like", "--resolution", "4", "--norm", "l2", "--seed", "3",
+                     "--out", str(inst_file)]) == 0
+    payloads = []
+    for name in ("r1.json", "r2.json"):
+        out = tmp_path / name
+        assert cli_main(["solve", "--instance", str(inst_file), "--method", "pdot", "--tol", "1e-6",
+                         "--deterministic", "--out", str(out)]) == 0
+        payloads.append(out.read_bytes())
+    assert payloads[0] == payloads[1]
