@@ -385,7 +385,8 @@ def main():
                "h2d_bytes_per_step": h2d // iters, "d2h_bytes_per_step": d2h // iters,
                "seconds": e2e_s, "iterations": rep_e.iterations, "h2d_bytes_per_call": h2d,
                "d2h_bytes_per_call": d2h, "api": api,
-               "rounded_objective": rep_e.rounded_objective, "termination_reason": rep_e.termination_reason}
+               "rounded_objective": rep_e.rounded_objective, "termination_reason": rep_e.termination_reason,
+               "phases": getattr(rep_e, "_phases", None)}
         del it
 
     cpu = None

@@ -57,17 +57,32 @@ def _events(h) -> list:
 
 
 class _Prefault:
-    """Allocate the host output plan and first-touch its pages on background
-    threads while the GPU iterates: a device->host copy into fresh pageable
-    memory runs at ~4 GB/s (page faults), into touched pages at ~19 GB/s."""
+    """Prepare the host output plan on background threads while the GPU
+    iterates.  Default: first-touch fresh pageable pages, so the final
+    device->host copy runs at ~19 GB/s instead of ~4 GB/s into untouched
+    memory.  PDOT_OUTPUT_PINNED=1 allocates page-locked memory instead (a
+    ~49 GB/s DMA), but cudaHostAlloc during the solve stalls the graph
+    launches (measured: loop 3.1 s -> 3.8 s at C3), so it is opt-in."""
 
     def __init__(self, shape, nthreads: int = 16):
+        import os
         import threading
-        self.arr = np.empty(shape)
-        rows = np.array_split(np.arange(shape[0]), nthreads) if shape[0] else []
-        self.threads = [threading.Thread(target=self._touch, args=(r,), daemon=True) for r in rows if len(r)]
+        self.shape = shape
+        self.arr = None
+        self.pinned = os.environ.get("PDOT_OUTPUT_PINNED", "0") == "1"
+        if self.pinned:
+            self.threads = [threading.Thread(target=self._alloc_pinned, daemon=True)]
+        else:
+            self.arr = np.empty(shape)
+            rows = np.array_split(np.arange(shape[0]), nthreads) if shape[0] else []
+            self.threads = [threading.Thread(target=self._touch, args=(r,), daemon=True) for r in rows if len(r)]
         for t in self.threads:
             t.start()
+
+    def _alloc_pinned(self):
+        from .device import torch
+        self._t = torch.empty(self.shape, dtype=torch.float64, pin_memory=True)
+        self.arr = self._t.numpy()
 
     def _touch(self, r):
         self.arr[r[0]:r[-1] + 1].fill(0.0)
@@ -136,15 +151,18 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
     pair is returned in place of numpy arrays; see ``solve_device``).
     """
     t_start = time.perf_counter()
+    phases = {}
     if config is None:
         config = SolverConfig()
     dp = as_device_problem(prob, device)
+    phases["h2d_problem_s"] = time.perf_counter() - t_start
     h = get_handle(dp.m, dp.n, dp.device)
     h.bind(dp)
     if initial is not None:
         h.set_slot(0, initial.X, initial.p, initial.q)
     else:
         h.set_slot(0, None, None, None)
+    phases["setup_s"] = time.perf_counter() - t_start - phases["h2d_problem_s"]
     stepwise = trace is not None
     cfg = config_struct(config, trace_level=1 if trace is not None else 0, poll_passes=poll_passes)
     out = _Prefault((dp.m, dp.n)) if not return_device and dp.m * dp.n >= (1 << 22) else None
@@ -176,12 +194,20 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
             X, p, q = h.get_slot(prog.roles[0])
             trace.restart_points.append(Iterate(X, p, q))
     elapsed = time.perf_counter() - t_start
+    phases["loop_s"] = float(res.elapsed_s)
 
+    t1 = time.perf_counter()
     report = assemble_report(h, res, config, trace)
+    phases["round_report_s"] = time.perf_counter() - t1
     report._e2e_s = elapsed  # noqa: SLF001
+    report._phases = phases  # noqa: SLF001
     if return_device:
         return (int(res.final_slot), h), report
-    X, p, q = h.get_slot(res.final_slot, out=None if out is None else out.result())
+    t2 = time.perf_counter()
+    X = None if out is None else out.result()
+    phases["prefault_wait_s"] = time.perf_counter() - t2
+    X, p, q = h.get_slot(res.final_slot, out=X)
+    phases["d2h_plan_s"] = time.perf_counter() - t2 - phases["prefault_wait_s"]
     return Iterate(X, p, q), report
 
 
