@@ -184,6 +184,20 @@ int pdot_set_virtual(pdot_solver* h, int on);
 int pdot_shard_pass(pdot_solver* h, int phase, pdot_progress* prog);
 int pdot_exchange_local(pdot_solver** hs, int count);
 
+/* ---- log-domain Sinkhorn baseline (sinkhorn.py:58-130) ----
+ * Runs on the bound explicit cost; leaves the plan exp((phi+psi-C)/eps) in
+ * slot 0's X and the potentials (phi, psi) in slot 0's (p, q).  res->reason
+ * and res->iterations follow the reference's loop. */
+typedef struct {
+  double penalty;
+  double tol;
+  int64_t max_iters;
+  double time_limit_s;
+  int32_t poll_iters;  /* iterations per host poll (0: 16) */
+} pdot_sinkhorn_config;
+int pdot_sinkhorn_solve(pdot_solver* h, const pdot_sinkhorn_config* cfg, double elapsed_before_s,
+                        pdot_result* res);
+
 /* ---- instance generation on the device ---- */
 #define PDOT_COST_SQEUCLID_GRID 0 /* a = (r, r): (di^2 + dj^2) on an r x r grid   */
 #define PDOT_COST_L1_GRID 1       /* a = (r, r): |di| + |dj|                      */

@@ -10,6 +10,7 @@ from .config import (ABSOLUTE, ADAPTIVE, FIXED_BETA, RELATIVE, SolverConfig, Sol
                      default_stepsize, primal_weight_update, should_restart)
 from .device import DeviceProblem, release_handles
 from .engine import solve, solve_device
+from .entropic import Potentials, SinkhornConfig, sinkhorn_report_gap, sinkhorn_solve
 from .instances import CostMatrix, InstanceError, Marginal, OTProblem, make_problem
 from .records import Iterate, KKTReport, SolveReport
 from .units import (adaptive_stepsize, apply_A, apply_At, duality_gap, kkt_error, pdhg_step,
@@ -21,7 +22,7 @@ __all__ = [
     "solve", "solve_device", "CostMatrix", "InstanceError", "Marginal", "OTProblem", "make_problem",
     "Iterate", "KKTReport", "SolveReport", "adaptive_stepsize", "apply_A", "apply_At", "duality_gap",
     "kkt_error", "pdhg_step", "restart_candidate", "round_to_feasible", "rounded_objective",
-    "stepsize_bound",
+    "stepsize_bound", "Potentials", "SinkhornConfig", "sinkhorn_report_gap", "sinkhorn_solve",
 ]
 
 __version__ = "0.1.0"

@@ -36,6 +36,7 @@ EXPORTS = (
     "pdot_gen_cost", "pdot_gen_cost_rows", "pdot_fro_norm", "pdot_time_stream_kernel",
     "pdot_kernel_launches", "pdot_time_finalize", "pdot_shard_rows", "pdot_create_shard", "pdot_shard_info",
     "pdot_nccl_unique_id", "pdot_comm_init", "pdot_set_virtual", "pdot_shard_pass", "pdot_exchange_local",
+    "pdot_sinkhorn_solve",
 )
 
 
@@ -59,6 +60,11 @@ class Result(ctypes.Structure):
         ("omega", ctypes.c_double), ("scale_R", ctypes.c_double), ("elapsed_s", ctypes.c_double),
         ("device_s", ctypes.c_double),
     ]
+
+
+class SinkhornCfg(ctypes.Structure):
+    _fields_ = [("penalty", ctypes.c_double), ("tol", ctypes.c_double), ("max_iters", ctypes.c_int64),
+                ("time_limit_s", ctypes.c_double), ("poll_iters", ctypes.c_int32)]
 
 
 class Event(ctypes.Structure):
@@ -118,6 +124,7 @@ _SIGS = {
     "pdot_set_virtual": ([_P, ctypes.c_int], ctypes.c_int),
     "pdot_shard_pass": ([_P, ctypes.c_int, ctypes.POINTER(Progress)], ctypes.c_int),
     "pdot_exchange_local": ([ctypes.POINTER(_P), ctypes.c_int], ctypes.c_int),
+    "pdot_sinkhorn_solve": ([_P, ctypes.POINTER(SinkhornCfg), _D, ctypes.POINTER(Result)], ctypes.c_int),
 }
 
 _lib = None
@@ -155,7 +162,7 @@ def check(rc: int) -> None:
     if rc == PDOT_EINVAL:
         raise ValueError(msg)
     if rc == PDOT_ENONFINITE:
-        raise RuntimeError("numerical failure: non-finite iterate")
+        raise RuntimeError(msg if "potential" in msg else "numerical failure: non-finite iterate")
     if rc == PDOT_ELINESEARCH:
         raise RuntimeError("step-size line search failed to find an admissible eta")
     raise RuntimeError(f"libpdot error {rc}: {msg}")

@@ -1,0 +1,56 @@
+// The pdot_solver handle (shared by the C-ABI translation units).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <string>
+#include <vector>
+
+#include "../../include/pdot.h"
+#include "pdot_internal.cuh"
+
+using pdot::Ctl;
+
+struct pdot_solver {
+  int device = 0;
+  int64_t m = 0, n = 0, ldx = 0, TM = 0, T = 0, U = 0, CB = 0;
+  cudaStream_t stream = nullptr;
+  Ctl host{};
+  Ctl* dev = nullptr;
+  double* slot_mem = nullptr;
+  double* work = nullptr;
+  unsigned* counter = nullptr;
+  pdot::Status* status_h = nullptr;
+  pdot::Status* status_d = nullptr;
+  pdot::Event* ring_h = nullptr;
+  pdot::Event* ring_d = nullptr;
+  int64_t ring_tail = 0;
+  std::vector<pdot_event> events;
+  cudaGraphExec_t graph = nullptr;
+  int graph_L = 0;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  int64_t launches = 0;
+  bool problem_set = false;
+  std::chrono::steady_clock::time_point wall0;
+  double elapsed_before = 0.0;
+  int poll_L = 8;
+  Ctl saved{};          // control block of the last solve (unit calls reuse the device block)
+  bool has_saved = false;
+  // ---- row sharding ----
+  int nranks = 1, rank = 0;
+  int64_t m_total = 0, row0 = 0;
+  double* gbuf = nullptr;
+  int64_t gstride = 0;
+  void* nccl_comm = nullptr;  // ncclComm_t when nranks > 1 and a communicator was attached
+  bool virtual_shards = false;  // exchange driven by the host (single-GPU emulation)
+  bool force_split = false;     // 1-rank communicator exercising the multi-GPU pass sequence
+};
+
+
+namespace pdot {
+// error helpers shared with sinkhorn.cu (defined in solver.cu)
+int set_error(int code, const std::string& msg);
+int cuda_error(cudaError_t e, const char* what, int line);
+}  // namespace pdot

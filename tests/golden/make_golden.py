@@ -123,7 +123,28 @@ def instance_cases():
     return out
 
 
+def sinkhorn_cases():
+    """Reference Sinkhorn runs (pins oracle/sinkhorn_oracle.py, checks the GPU)."""
+    rng = np.random.default_rng(99)
+    cases = [("rand5x4", random_problem(rng, 5, 4), 0.05, 1e-8),
+             ("grid8_l1", ot.grid_problem("cauchy_like", 8, "l1", seed=2), 0.05, 1e-6),
+             ("shapes16_l2", ot.grid_problem("shapes", 16, "l2", seed=11), 0.01, 1e-4)]
+    f = inst.sparse_marginals(128, 3)
+    g = inst.sparse_marginals(256, 4)
+    cases.append(("rect_sparse", ref_problem(inst.rect_l1_cost((8, 16), (16, 16)) / 10.0, f, g), 0.05, 1e-6))
+    arrays, meta = {}, {}
+    for name, prob, pen, tol in cases:
+        plan, pot, rep = ot.sinkhorn_solve(prob, ot.SinkhornConfig(penalty=pen, tol=tol, deterministic=True))
+        arrays.update({name + "_C": prob.C, name + "_f": prob.f, name + "_g": prob.g, name + "_plan": plan,
+                       name + "_phi": pot.phi, name + "_psi": pot.psi})
+        meta[name] = dict(penalty=pen, tol=tol, report=json.loads(rep.to_json()))
+        print("sinkhorn", name, rep.iterations, rep.termination_reason)
+    np.savez_compressed(HERE / "sinkhorn.npz", **arrays)
+    (HERE / "sinkhorn.json").write_text(json.dumps(meta, indent=1, sort_keys=True))
+
+
 def main():
+    sinkhorn_cases()
     np.savez_compressed(HERE / "instances.npz", **instance_cases())
     np.savez_compressed(HERE / "elements.npz", **element_cases())
     arrays = {}

@@ -106,3 +106,18 @@ def test_instance_generators_match_reference():
             assert np.array_equal(prob.C, G[f"{kind}_{norm}_C"]), (kind, norm)
             assert np.array_equal(prob.f, G[f"{kind}_{norm}_f"]), (kind, norm)
             assert np.array_equal(prob.g, G[f"{kind}_{norm}_g"]), (kind, norm)
+
+
+def test_sinkhorn_oracle_bit_identical():
+    """oracle/sinkhorn_oracle.py reproduces the reference's sinkhorn_solve."""
+    from oracle.sinkhorn_oracle import oracle_sinkhorn
+    A = np.load(GOLD / "sinkhorn.npz")
+    meta = json.loads((GOLD / "sinkhorn.json").read_text())
+    for name, m in meta.items():
+        prob = raw_problem(A[name + "_C"], A[name + "_f"], A[name + "_g"])
+        plan, phi, psi, rep = oracle_sinkhorn(prob, m["penalty"], m["tol"])
+        ref = m["report"]
+        for key in ("iterations", "termination_reason", "final_relative_kkt", "rounded_objective", "duality_gap"):
+            assert rep[key] == ref[key], (name, key, rep[key], ref[key])
+        assert np.array_equal(plan, A[name + "_plan"]), name
+        assert np.array_equal(phi, A[name + "_phi"]) and np.array_equal(psi, A[name + "_psi"]), name
