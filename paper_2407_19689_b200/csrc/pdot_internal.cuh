@@ -251,5 +251,6 @@ void launch_stream_pass(const Ctl* ctl_dev, const Ctl& ctl_host, int force_op, c
 enum FinMode : int { FIN_FUSED = 0, FIN_A = 1, FIN_B = 2 };
 void launch_finalize_pass(Ctl* ctl_dev, const Ctl& ctl_host, int force_op, int mode, cudaStream_t s);
 size_t stream_smem_bytes(int64_t TM);
+void prepare_stream_kernel();
 
 }  // namespace pdot

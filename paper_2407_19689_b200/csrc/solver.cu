@@ -532,7 +532,8 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     pdot_destroy(h);
     return rc;
   }
-  // kernel attributes once, outside any capture
+  // kernel attributes (per device), outside any capture
+  pdot::prepare_stream_kernel();
   pdot::launch_stream_pass(h->dev, h->host, pdot::OP_NONE, h->stream);
   if ((e = cudaStreamSynchronize(h->stream)) != cudaSuccess) {
     int rc = cuda_fail(e, "pdot_create warmup", __LINE__);

@@ -53,7 +53,7 @@ __device__ __forceinline__ double2 cost_pair(const double* C, const Geo& g, int6
 //   scalars:    0 |d|^2, 1 <C,X+>, 2 <C,A'>, 3 |X+|^2, 4 |viol(p,q)|^2, 5 |viol(pa,qa)|^2
 // ---------------------------------------------------------------------------
 struct StepOp {
-  static constexpr int NQ = 4, NS = 6, RB = 2;
+  static constexpr int NQ = 4, NS = 6;
   const double* C;
   const double* X;
   const double* A;
@@ -624,13 +624,13 @@ size_t stream_smem_bytes(int64_t TM) {
   return kBarBytes + (size_t)kStages * kStageBytes + 2 * TM * sizeof(double) + rowbuf;
 }
 
+void prepare_stream_kernel() {
+  // per device: called from pdot_create_shard with the handle's device current
+  cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+}
+
 void launch_stream_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaStream_t s) {
-  static bool attr_set = false;
   const size_t smem = stream_smem_bytes(h.TM);
-  if (!attr_set) {
-    cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    attr_set = true;
-  }
   dim3 grid((unsigned)h.U, (unsigned)h.T);
   stream_kernel<<<grid, kBlockThreads, smem, s>>>(ctl_dev, force_op);
 }

@@ -253,8 +253,10 @@ def get_handle(m: int, n: int, device: int = 0) -> Handle:
 
 
 def release_handles() -> None:
-    for h in list(_HANDLES.values()):
-        h.close()
+    """Drop the cache's references; a handle is destroyed once no caller holds
+    it (a solve_device result keeps its handle alive)."""
+    import gc
     _HANDLES.clear()
+    gc.collect()
     if torch is not None and torch.cuda.is_available():
         torch.cuda.empty_cache()

@@ -1,0 +1,87 @@
+"""Edge shapes and inputs on the GPU path, checked against the CPU oracle:
+single rows/columns, odd n, partial tiles in both directions, zero-mass
+marginal entries, warm starts, the implicit-cost guard rails."""
+
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _raw(C, f, g):
+    return SimpleNamespace(C=C, f=f, g=g, m=C.shape[0], n=C.shape[1],
+                           cost_fro_norm=float(np.linalg.norm(C)),
+                           marginal_norm=float(np.linalg.norm(f) + np.linalg.norm(g)))
+
+
+def _problem(rng, m, n, zero_frac=0.0):
+    C = rng.random((m, n)) * 3
+    f = rng.random(m) + 0.05
+    g = rng.random(n) + 0.05
+    if zero_frac:
+        f[rng.random(m) < zero_frac] = 0.0
+        g[rng.random(n) < zero_frac] = 0.0
+        f[0] = max(f[0], 0.1)
+        g[0] = max(g[0], 0.1)
+    return _raw(C, f / f.sum(), g / g.sum())
+
+
+@pytest.mark.parametrize("m,n", [(1, 3000), (3000, 1), (129, 513), (257, 1025), (7, 4099), (1030, 6)])
+def test_step_and_kkt_edge_shapes(m, n):
+    import paper_2407_19689_b200 as pd
+    from oracle import pdot_oracle as O
+    rng = np.random.default_rng(m * 7919 + n)
+    prob = _problem(rng, m, n)
+    X = rng.random((m, n)) / (m * n)
+    X[rng.random((m, n)) < 0.3] = 0.0
+    p, q = rng.standard_normal(m) * 0.1, rng.standard_normal(n) * 0.1
+    nxt = pd.pdhg_step(prob, pd.Iterate(X, p, q), 0.3, 0.7)
+    Xn, pn, qn = O.primal_dual_step(prob.C, prob.f, prob.g, X, p, q, 0.3, 0.7)
+    assert np.array_equal(nxt.X, Xn)
+    np.testing.assert_allclose(nxt.p, pn, rtol=0, atol=1e-12 * max(1, np.abs(pn).max()))
+    np.testing.assert_allclose(nxt.q, qn, rtol=0, atol=1e-12 * max(1, np.abs(qn).max()))
+    rep = pd.kkt_error(prob, pd.Iterate(X, p, q), 1.5)
+    ref = O.kkt_blocks(prob.C, prob.f, prob.g, X, p, q, prob.cost_fro_norm, prob.marginal_norm, 1.5)
+    assert rep.relative_composite == pytest.approx(ref["relative_composite"], rel=1e-11)
+    assert np.array_equal(rep.dual_violation, ref["dual_violation"])
+
+
+@pytest.mark.parametrize("m,n", [(1, 200), (200, 1), (33, 70)])
+def test_solve_edge_shapes_against_oracle(m, n):
+    import paper_2407_19689_b200 as pd
+    from oracle import pdot_oracle as O
+    rng = np.random.default_rng(m + 1000 * n)
+    prob = _problem(rng, m, n, zero_frac=0.2)
+    cfg = pd.SolverConfig(tol=1e-6, deterministic=True)
+    it, rep = pd.solve(prob, cfg)
+    _, ref = O.oracle_solve(prob, cfg)
+    assert rep.termination_reason == ref["termination_reason"] == "tolerance"
+    assert rep.final_relative_kkt <= 1e-6
+    assert abs(rep.iterations - ref["iterations"]) <= 0.5 * ref["iterations"] + 10
+    assert rep.rounded_objective == pytest.approx(ref["rounded_objective"], rel=1e-3, abs=1e-6)
+    Xf = pd.round_to_feasible(prob, it.X)
+    np.testing.assert_allclose(Xf.sum(axis=1), prob.f, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(Xf.sum(axis=0), prob.g, rtol=0, atol=1e-12)
+
+
+def test_warm_start_continues_from_iterate():
+    import paper_2407_19689_b200 as pd
+    from paper_2407_19689_b200 import instances as inst
+    prob = inst.sqeuclid_problem(8, 3)
+    it1, rep1 = pd.solve(prob, pd.SolverConfig(tol=1e-3))
+    it2, rep2 = pd.solve(prob, pd.SolverConfig(tol=1e-3), initial=it1)
+    assert rep2.iterations == 0 and rep2.solved  # already at tolerance
+    _, rep3 = pd.solve(prob, pd.SolverConfig(tol=1e-6), initial=it1)
+    _, rep4 = pd.solve(prob, pd.SolverConfig(tol=1e-6))
+    assert rep3.solved and rep4.solved
+
+
+def test_implicit_guard_rails():
+    import paper_2407_19689_b200 as pd
+    dp = pd.DeviceProblem.sqeuclid_grid(8, 0, implicit=True)
+    with pytest.raises(ValueError):
+        pd.sinkhorn_solve(dp)
+    it, rep = pd.solve(dp, pd.SolverConfig(tol=1e-4))
+    assert rep.solved
