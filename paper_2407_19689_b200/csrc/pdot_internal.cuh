@@ -89,7 +89,7 @@ struct Ctl {
   // ---- step state ----
   double eta, omega, tau, sigma, kd, rkd;   // rkd = RN(1/kd)
   // ---- counters ----
-  int64_t total, inner, outer, passes, halvings, rejected, restarts_pending;
+  int64_t total, inner, outer, passes, halvings, rejected;
   // ---- KKT bookkeeping ----
   double epoch_kkt, prev_cand, best_kkt, best_rel, scale_R;
   int32_t pending;          // KKT of the current iterate awaits this pass's dual violation
@@ -144,12 +144,11 @@ __device__ __forceinline__ void st_stream2(double* p, double2 v) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
-__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
-
 // Transposed butterfly: V independent per-lane values (V a power of two, <= 32)
-// are summed across the warp.  Afterwards lane L holds the total of value
-// index (L >> s) & (V-1) with s = log2(32 / V)... computed by owner_index().
-// Every sum follows the same fixed tree, so results are deterministic.
+// are summed across the warp with one shuffle per value per halving step.
+// Afterwards lane L holds the total of value index L >> (5 - log2 V)
+// (transpose_owner_index); lanes with the low bits clear write it out
+// (transpose_is_writer).  Every sum follows the same fixed tree.
 template <int V>
 __device__ __forceinline__ void warp_transpose_sum(double (&v)[V]) {
   const int lane = threadIdx.x & 31;

@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _lib
 from .config import SolverConfig
-from .device import DeviceProblem, Handle, torch
+from .device import DeviceProblem, Handle
 from .engine import assemble_report, config_struct
 from .records import Iterate
 
