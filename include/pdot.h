@@ -126,6 +126,8 @@ typedef struct {
   int32_t roles[4];  /* slots holding: current iterate, running average, restart anchor, best */
   int32_t op;        /* next pass: 0 step, 1 restart distance, 2 start KKT */
   int64_t iterations, restarts, passes;
+  int32_t avg_written; /* the pass just run wrote the running-average matrix of the last */
+  int32_t avg_slot;    /* accepted iterate into slot avg_slot (it is computed one pass late) */
 } pdot_progress;
 
 /* Validate cfg (pdhg.py:61-75), load the control block; slot 0 holds the start point. */

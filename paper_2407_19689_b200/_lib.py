@@ -74,7 +74,8 @@ class Event(ctypes.Structure):
 
 class Progress(ctypes.Structure):
     _fields_ = [("done", ctypes.c_int32), ("roles", ctypes.c_int32 * 4), ("op", ctypes.c_int32),
-                ("iterations", ctypes.c_int64), ("restarts", ctypes.c_int64), ("passes", ctypes.c_int64)]
+                ("iterations", ctypes.c_int64), ("restarts", ctypes.c_int64), ("passes", ctypes.c_int64),
+                ("avg_written", ctypes.c_int32), ("avg_slot", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p

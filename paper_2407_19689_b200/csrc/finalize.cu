@@ -185,7 +185,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
       vals[6] = qn * qn;
       if (!c.unit || c.unit_avg) {
         const double qaj = sa.q[j];
-        const double qan = qaj + div_by_count(qn - qaj, c.kd, c.rkd);  // pdhg.py:317
+        const double qan = qaj + div_by_count(qn - qaj, c.kd_dual, c.rkd_dual);  // pdhg.py:317
         c.slot[c.sAn].q[j] = qan;
         const double pca = col[3] - gj;
         vals[3] = pca * pca;
@@ -277,7 +277,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
         vals[6] += pn * pn;
         if (!c.unit || c.unit_avg) {
           const double pai = sa.p[i];
-          const double pan = pai + div_by_count(pn - pai, c.kd, c.rkd);  // pdhg.py:316
+          const double pan = pai + div_by_count(pn - pai, c.kd_dual, c.rkd_dual);  // pdhg.py:316
           c.slot[c.sAn].p[i] = pan;
           const double pra = row[3] - fi;
           vals[3] += pra * pra;
@@ -444,8 +444,8 @@ __device__ double kkt_metric(const Ctl& c, double psq, double dsq, double pobj, 
 
 __device__ int pick_free(const Ctl& c, int avoid) {
   for (int s = 0; s < kNSlot; ++s)
-    if (s != c.sX && s != c.sA && s != c.sZ && s != c.sB && s != avoid) return s;
-  return -1;  // unreachable with kNSlot = 6
+    if (s != c.sX && s != c.sA && s != c.sZ && s != c.sB && s != avoid && !(c.lagA && s == c.sAsrc)) return s;
+  return -1;  // unreachable with kNSlot = 7 (at most 5 roles + the two outputs)
 }
 
 __device__ void prepare_step(Ctl& c) {
@@ -453,8 +453,10 @@ __device__ void prepare_step(Ctl& c) {
   c.sAn = pick_free(c, c.sXn);
   c.tau = c.eta / c.omega;     // pdhg.py:86-87
   c.sigma = c.eta * c.omega;   // pdhg.py:90-91
-  c.kd = (double)(c.inner + 1);
-  c.rkd = 1.0 / c.kd;
+  c.kd = (double)c.inner;      // lazy matrix average of the current iterate (k >= 1 when lagA)
+  c.rkd = c.inner > 0 ? 1.0 / c.kd : 1.0;
+  c.kd_dual = (double)(c.inner + 1);  // dual average of the trial iterate (pdhg.py:316-317)
+  c.rkd_dual = 1.0 / c.kd_dual;
   c.op = OP_STEP;
 }
 
@@ -477,7 +479,8 @@ __device__ void do_restart(Ctl& c, int cand_slot, double cand_kkt) {
   ring_push(c, EV_RESTART, (int)c.inner, cand_kkt, c.omega, 0.0);
   c.outer += 1;
   c.inner = 0;
-  c.sX = c.sA = c.sZ = cand_slot;
+  c.sX = c.sA = c.sZ = c.sAsrc = cand_slot;
+  c.lagA = 0;
   c.epoch_kkt = cand_kkt;
   c.prev_cand = cand_kkt;
   c.pending = 0;
@@ -505,12 +508,18 @@ __device__ bool limits_hit(Ctl& c, const Sums& S) {
 }
 
 __device__ void control_step(Ctl& c, const Sums& S) {
-  // ---- 1. resolve the KKT of the input iterate (evaluated at pdhg.py:331-378)
+  // the average matrix of the input iterate, if lagging, was written by this pass
+  c.avg_written = c.lagA;
+  c.avg_slot = c.sA;
+  c.lagA = 0;
+  // ---- 1. resolve the KKT of the input iterate (evaluated at pdhg.py:331-378):
+  //         current-iterate primal parts from the pass that created it, the
+  //         average's primal parts and both dual violations from this pass
   if (c.pending) {
     c.pending = 0;
     double rel_cur, rel_avg;
     const double kc = kkt_metric(c, c.pend_psq_cur, S.R[11], c.pend_pobj_cur, c.pend_dobj_cur, &rel_cur);
-    const double ka = kkt_metric(c, c.pend_psq_avg, S.R[12], c.pend_pobj_avg, c.pend_dobj_avg, &rel_avg);
+    const double ka = kkt_metric(c, S.R[3] + S.K[3], S.R[12], S.R[9], c.pend_dobj_avg, &rel_avg);
     const bool take_cur = kc < ka;  // tie -> average (pdhg.py:335-338)
     const int cand_slot = take_cur ? c.sX : c.sA;
     const double cand = take_cur ? kc : ka;
@@ -570,7 +579,9 @@ __device__ void control_step(Ctl& c, const Sums& S) {
   c.total += 1;
   c.inner += 1;
   c.sX = c.sXn;
+  c.sAsrc = c.sA;  // its matrix is the previous average; the next pass writes sAn's
   c.sA = c.sAn;
+  c.lagA = 1;
   // pdhg.py:319-322
   const double nrm = sqrt((S.R[10] + S.R[6]) + S.K[6]);
   if (!isfinite(nrm)) {
@@ -583,14 +594,13 @@ __device__ void control_step(Ctl& c, const Sums& S) {
     c.pend_psq_cur = S.R[2] + S.K[2];
     c.pend_pobj_cur = S.R[8];
     c.pend_dobj_cur = S.R[4] + S.K[4];
-    c.pend_psq_avg = S.R[3] + S.K[3];
-    c.pend_pobj_avg = S.R[9];
     c.pend_dobj_avg = S.R[5] + S.K[5];
   }
   prepare_step(c);
 }
 
 __device__ void control_dist(Ctl& c, const Sums& S) {
+  c.avg_written = 0;
   // pdhg.py:353-362 + primal_weight_update pdhg.py:174-186
   const double dX = sqrt(S.R[2]);
   const double dpq = sqrt(S.R[0] + S.K[0]);
@@ -601,6 +611,7 @@ __device__ void control_dist(Ctl& c, const Sums& S) {
 }
 
 __device__ void control_start(Ctl& c, const Sums& S) {
+  c.avg_written = 0;
   // pdhg.py:278-296
   const double nrm = sqrt((S.R[5] + S.R[2]) + S.K[2]);
   c.scale_R = nrm > 1.0 ? nrm : 1.0;
@@ -611,7 +622,8 @@ __device__ void control_start(Ctl& c, const Sums& S) {
   const double k0 = kkt_metric(c, psq, dsq, pobj, dobj, &rel);
   c.epoch_kkt = c.prev_cand = c.best_kkt = k0;
   c.best_rel = rel;
-  c.sA = c.sZ = c.sB = c.sX;
+  c.sA = c.sZ = c.sB = c.sAsrc = c.sX;
+  c.lagA = 0;
   c.pending = 0;
   ring_push(c, EV_START, 0, k0, rel, 0.0);
   if (k0 <= c.tol) {

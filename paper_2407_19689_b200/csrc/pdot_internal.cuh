@@ -19,7 +19,7 @@ constexpr int kTileN = kWarps * 64;       // 512 columns per tile (each lane: 2 
 constexpr int kMaxNQ = 4;                 // row/col quantities per pass (STEP: e, d, X+, A')
 constexpr int kMaxNS = 8;                 // per-tile scalar partials
 constexpr int kGroups = 8;                // row-tile groups of the hierarchical reduction
-constexpr int kNSlot = 6;
+constexpr int kNSlot = 7;
 constexpr int kRedThreads = 256;          // finalize-kernel block size
 constexpr int kMaxRowScal = 16;           // per-row-tile scalar partials (finalize)
 constexpr int kMaxColScal = 8;            // per-column-block scalar partials (finalize)
@@ -87,18 +87,26 @@ struct Ctl {
   uint64_t deadline_ns;    // %globaltimer deadline (0 = none)
   int32_t stop_request;    // host may set to force a time-limit stop
   // ---- step state ----
-  double eta, omega, tau, sigma, kd, rkd;   // rkd = RN(1/kd)
+  double eta, omega, tau, sigma;
+  double kd, rkd;            // lazy matrix average: k of the iterate being averaged, RN(1/k)
+  double kd_dual, rkd_dual;  // eager dual average: k of the trial iterate
   // ---- counters ----
   int64_t total, inner, outer, passes, halvings, rejected;
   // ---- KKT bookkeeping ----
   double epoch_kkt, prev_cand, best_kkt, best_rel, scale_R;
   int32_t pending;          // KKT of the current iterate awaits this pass's dual violation
   double pend_psq_cur, pend_pobj_cur, pend_dobj_cur;
-  double pend_psq_avg, pend_pobj_avg, pend_dobj_avg;
+  double pend_dobj_avg;
   double cand_kkt, cand_rel;   // candidate that triggered the pending restart
   double final_rel;
   // ---- roles ----
   int32_t sX, sA, sZ, sB, sXn, sAn, sCand, sFinal;
+  // Lazy running average: after an accepted step the average slot sA holds the
+  // new dual average (p, q) but its matrix is written by the NEXT pass from the
+  // accepted iterate and the previous average matrix in slot sAsrc (lagA = 1).
+  // A rejected trial's re-run then streams only C and X (24 instead of 40 B/entry).
+  int32_t sAsrc, lagA;
+  int32_t avg_written, avg_slot;  // this pass wrote the average matrix into avg_slot (trace)
   int32_t op, done, reason, error;
   int32_t round_stage;
   int32_t kkt_write_viol;   // unit kkt_error: also write the dual-violation matrix

@@ -697,7 +697,11 @@ int pdot_begin(pdot_solver* h, const pdot_config* cfg, double elapsed_before_s) 
   c.trace_level = cfg->trace_level;
   c.eta = cfg->eta0 > 0 ? cfg->eta0 : 1.0 / (2.0 * sqrt((double)(h->m_total + h->n)));  // pdhg.py:225-227
   c.omega = cfg->omega0;
-  c.tau = c.sigma = c.kd = c.rkd = 0.0;
+  c.tau = c.sigma = c.kd = c.rkd = c.kd_dual = c.rkd_dual = 0.0;
+  c.sAsrc = 0;
+  c.lagA = 0;
+  c.avg_written = 0;
+  c.avg_slot = 0;
   c.total = c.inner = c.outer = c.passes = c.halvings = c.rejected = 0;
   c.pending = 0;
   c.sX = c.sA = c.sZ = c.sB = c.sFinal = 0;
@@ -752,6 +756,8 @@ int pdot_advance(pdot_solver* h, int64_t max_passes, pdot_progress* prog) {
     prog->iterations = c.total;
     prog->restarts = c.outer;
     prog->passes = c.passes;
+    prog->avg_written = c.avg_written;
+    prog->avg_slot = c.avg_slot;
   }
   return PDOT_OK;
 }
@@ -841,8 +847,13 @@ int pdot_unit_step(pdot_solver* h, double tau, double sigma, double k) {
   unit_ctl(h);
   const bool avg = k > 0;
   c.unit_avg = avg ? 1 : 0;
-  c.sX = 0; c.sA = avg ? 2 : 0; c.sXn = 1; c.sAn = avg ? 3 : 2;
-  c.tau = tau; c.sigma = sigma; c.kd = avg ? k : 1.0; c.rkd = 1.0 / c.kd;
+  // with k: average matrix in slot 2 -> slot 3 (from the input iterate), average
+  // duals in slot 3 updated in place from the trial duals (the loop's lazy/eager split)
+  c.sX = 0; c.sXn = 1;
+  c.sAsrc = avg ? 2 : 0; c.sA = avg ? 3 : 0; c.sAn = avg ? 3 : 2;
+  c.tau = tau; c.sigma = sigma;
+  c.kd = avg ? k : 1.0; c.rkd = 1.0 / c.kd;
+  c.kd_dual = c.kd; c.rkd_dual = c.rkd;
   c.op = pdot::OP_STEP;
   if (int rc = upload_ctl(h)) return rc;
   if (int rc = run_pass(h, pdot::OP_STEP)) return rc;
@@ -968,8 +979,9 @@ int pdot_time_stream_kernel(pdot_solver* h, int iters, double* ms_per_launch) {
   c.done = 0;
   c.status = nullptr;
   c.ring = nullptr;
-  c.sX = 0; c.sA = 1; c.sXn = 2; c.sAn = 3;
-  c.tau = 1e-3; c.sigma = 1e-3; c.kd = 3.0; c.rkd = 1.0 / 3.0;
+  // a full (lagged-average) STEP pass: X, previous average, outputs all distinct
+  c.sX = 0; c.sAsrc = 1; c.sA = 3; c.sXn = 2; c.sAn = 4; c.lagA = 1;
+  c.tau = 1e-3; c.sigma = 1e-3; c.kd = 3.0; c.rkd = 1.0 / 3.0; c.kd_dual = 4.0; c.rkd_dual = 0.25;
   c.op = pdot::OP_STEP;
   if (int rc = upload_ctl(h)) return rc;
   for (int i = 0; i < 2; ++i) pdot::launch_stream_pass(h->dev, h->host, pdot::OP_STEP, h->stream);
@@ -1068,6 +1080,8 @@ int pdot_shard_pass(pdot_solver* h, int phase, pdot_progress* prog) {
     prog->iterations = c.total;
     prog->restarts = c.outer;
     prog->passes = c.passes;
+    prog->avg_written = c.avg_written;
+    prog->avg_slot = c.avg_slot;
   }
   return PDOT_OK;
 }
@@ -1097,9 +1111,9 @@ int pdot_time_finalize(pdot_solver* h, int iters, double* ms_per_launch) {
   DeviceGuard dg(h->device);
   Ctl& c = h->host;
   unit_ctl(h);
-  c.sX = 0; c.sA = 1; c.sXn = 2; c.sAn = 3;
+  c.sX = 0; c.sA = 1; c.sXn = 2; c.sAn = 3; c.sAsrc = 4;
   c.unit_avg = 1;
-  c.tau = 1e-3; c.sigma = 1e-3; c.kd = 3.0; c.rkd = 1.0 / 3.0;
+  c.tau = 1e-3; c.sigma = 1e-3; c.kd = 3.0; c.rkd = 1.0 / 3.0; c.kd_dual = 4.0; c.rkd_dual = 0.25;
   c.op = pdot::OP_STEP;
   if (int rc = upload_ctl(h)) return rc;
   pdot::launch_stream_pass(h->dev, h->host, pdot::OP_STEP, h->stream);

@@ -64,7 +64,7 @@ struct StepOp {
   const double* pa;
   const double* qa;
   double tau, kd, rkd;
-  bool with_avg;
+  bool with_avg;  // this pass also writes the (lagged) average matrix
 
   struct Col { double q0, q1, qa0, qa1; };
   struct Frag { double2 c, x, a; double p, pa; };
@@ -75,7 +75,10 @@ struct StepOp {
     cl.qa0 = g.v0 ? qa[g.j] : 0.0;
     cl.qa1 = g.v1 ? qa[g.j + 1] : 0.0;
   }
-  // One plan entry.  o = {e, d, X+, A'}; s = the six scalar sums.
+  // One plan entry.  o = {e, d, X+, A}; s = the six scalar sums.  AVG: this pass
+  // also forms the (lagged) running mean of the input iterate; a re-run after a
+  // rejected trial does not, and leaves o[3] and s[2] at zero.
+  template <bool AVG = true>
   __device__ __forceinline__ void elem(double c, double x, double a, double pi, double qj, double pai,
                                        double qaj, double (&o)[NQ], double (&s)[NS]) const {
     const double pq = pi + qj;                  // apply_At
@@ -83,24 +86,32 @@ struct StepOp {
     const double xn = relu_np(x - tau * sres);  // projected primal step
     const double d = xn - x;                    // displacement
     const double e = (xn + xn) - x;             // 2 X+ - X  (xn + xn == 2.0*xn exactly)
-    const double an = a + div_by_count(xn - a, kd, rkd);  // running mean
     const double vc = relu_np(pq - c);          // dual violation, current (p,q)
     const double va = relu_np((pai + qaj) - c); // dual violation, average (pa,qa)
-    o[0] = e; o[1] = d; o[2] = xn; o[3] = an;
+    o[0] = e; o[1] = d; o[2] = xn;
     s[0] = sqr_acc(s[0], d);
     s[1] = mul_acc(s[1], c, xn);
-    s[2] = mul_acc(s[2], c, an);
     s[3] = sqr_acc(s[3], xn);
     s[4] = sqr_acc(s[4], vc);
     s[5] = sqr_acc(s[5], va);
+    if (AVG) {
+      const double an = a + div_by_count(x - a, kd, rkd);  // running mean of the accepted iterate x (lazy)
+      o[3] = an;
+      s[2] = mul_acc(s[2], c, an);
+    } else {
+      o[3] = 0.0;
+    }
   }
   // masked variant for edge tiles and the unit (no running average) call
   __device__ __forceinline__ void compute(const Frag& fr, const Geo& g, int64_t i, const Col& cl,
                                           double (&o0)[NQ], double (&o1)[NQ], double (&s)[NS]) const {
-    const double2 a = with_avg ? fr.a : make_double2(0.0, 0.0);
-    if (g.v0) elem(fr.c.x, fr.x.x, a.x, fr.p, cl.q0, fr.pa, cl.qa0, o0, s);
-    if (g.v1) elem(fr.c.y, fr.x.y, a.y, fr.p, cl.q1, fr.pa, cl.qa1, o1, s);
-    if (!with_avg) { o0[3] = 0.0; o1[3] = 0.0; }
+    if (with_avg) {
+      if (g.v0) elem<true>(fr.c.x, fr.x.x, fr.a.x, fr.p, cl.q0, fr.pa, cl.qa0, o0, s);
+      if (g.v1) elem<true>(fr.c.y, fr.x.y, fr.a.y, fr.p, cl.q1, fr.pa, cl.qa1, o1, s);
+    } else {
+      if (g.v0) elem<false>(fr.c.x, fr.x.x, 0.0, fr.p, cl.q0, fr.pa, cl.qa0, o0, s);
+      if (g.v1) elem<false>(fr.c.y, fr.x.y, 0.0, fr.p, cl.q1, fr.pa, cl.qa1, o1, s);
+    }
     if (g.v0) {
       st_stream2(Xn + i * g.ldx + g.j, make_double2(o0[2], g.v1 ? o1[2] : 0.0));
       if (with_avg) st_stream2(An + i * g.ldx + g.j, make_double2(o0[3], g.v1 ? o1[3] : 0.0));
@@ -406,7 +417,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-template <bool IMPLICIT>
+template <bool IMPLICIT, bool AVG>
 __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigned char* smem) {
   constexpr int NQ = StepOp::NQ, NS = StepOp::NS, R = kStageRows;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -426,7 +437,7 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
   const uint32_t pbytes = (uint32_t)(((g.rows + 1) & ~1) * 8);
   constexpr bool implicit_c = IMPLICIT;       // cost generated in registers (g.gen)
   const int kfirst = implicit_c ? 1 : 0;      // first streamed matrix (0 = C)
-  const int nmat = op.with_avg ? 3 : 2;
+  const int nmat = AVG ? 3 : 2;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -480,7 +491,7 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
       cj1 = g.gen.col_coord(g.j + 1);
       rcoord = g.gen.row_coord(g.i0);
     }
-    const bool fast = op.with_avg && g.rows == c.TM && vcols == kTileN;
+    const bool fast = g.rows == c.TM && vcols == kTileN;
     if (fast) {
       // full tile: no masks, running output pointers
       double* xo = op.Xn + g.i0 * c.ldx + g.j;
@@ -500,13 +511,14 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
             cc = *reinterpret_cast<const double2*>(st + (rr * 3 + 0) * kRowBytes + off);
           }
           const double2 xx = *reinterpret_cast<const double2*>(st + (rr * 3 + 1) * kRowBytes + off);
-          const double2 aa = *reinterpret_cast<const double2*>(st + (rr * 3 + 2) * kRowBytes + off);
+          const double2 aa = AVG ? *reinterpret_cast<const double2*>(st + (rr * 3 + 2) * kRowBytes + off)
+                                 : make_double2(0.0, 0.0);
           const double pi = pbuf[it * R + rr], pai = pabuf[it * R + rr];
           double o0[NQ], o1[NQ];
-          op.elem(cc.x, xx.x, aa.x, pi, cl.q0, pai, cl.qa0, o0, sacc);
-          op.elem(cc.y, xx.y, aa.y, pi, cl.q1, pai, cl.qa1, o1, sacc);
+          op.template elem<AVG>(cc.x, xx.x, aa.x, pi, cl.q0, pai, cl.qa0, o0, sacc);
+          op.template elem<AVG>(cc.y, xx.y, aa.y, pi, cl.q1, pai, cl.qa1, o1, sacc);
           st_stream2(xo, make_double2(o0[2], o1[2]));
-          st_stream2(ao, make_double2(o0[3], o1[3]));
+          if (AVG) st_stream2(ao, make_double2(o0[3], o1[3]));
           xo += c.ldx;
           ao += c.ldx;
 #pragma unroll
@@ -541,8 +553,8 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
               fr.c = *reinterpret_cast<const double2*>(st + (rr * 3 + 0) * kRowBytes + off);
             }
             fr.x = *reinterpret_cast<const double2*>(st + (rr * 3 + 1) * kRowBytes + off);
-            fr.a = op.with_avg ? *reinterpret_cast<const double2*>(st + (rr * 3 + 2) * kRowBytes + off)
-                               : make_double2(0.0, 0.0);
+            fr.a = AVG ? *reinterpret_cast<const double2*>(st + (rr * 3 + 2) * kRowBytes + off)
+                       : make_double2(0.0, 0.0);
             fr.p = pbuf[r];
             fr.pa = pabuf[r];
             op.compute(fr, g, g.i0 + r, cl, o0, o1, sacc);
@@ -574,12 +586,20 @@ __global__ void __launch_bounds__(kBlockThreads, PDOT_MINB) stream_kernel(const 
       StepOp o;
       const Slot& sx = c.slot[c.sX];
       const Slot& sa = c.slot[c.sA];
-      o.C = c.C; o.X = sx.X; o.A = sa.X;
-      o.Xn = c.slot[c.sXn].X; o.An = c.slot[c.sAn].X;
+      o.C = c.C; o.X = sx.X;
+      o.A = c.slot[c.sAsrc].X;   // previous average matrix (lazy update input)
+      o.An = sa.X;               // average matrix of the current iterate (output)
+      o.Xn = c.slot[c.sXn].X;
       o.p = sx.p; o.q = sx.q; o.pa = sa.p; o.qa = sa.q;
-      o.tau = c.tau; o.kd = c.kd; o.rkd = c.rkd; o.with_avg = !c.unit || c.unit_avg;
-      if (o.C) step_tma<false>(o, c, smem_raw);
-      else step_tma<true>(o, c, smem_raw);
+      o.tau = c.tau; o.kd = c.kd; o.rkd = c.rkd;
+      o.with_avg = c.unit ? c.unit_avg != 0 : c.lagA != 0;
+      if (o.C) {
+        if (o.with_avg) step_tma<false, true>(o, c, smem_raw);
+        else step_tma<false, false>(o, c, smem_raw);
+      } else {
+        if (o.with_avg) step_tma<true, true>(o, c, smem_raw);
+        else step_tma<true, false>(o, c, smem_raw);
+      }
       break;
     }
     case OP_KKT: {

@@ -174,25 +174,27 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
         _lib.check(lib.pdot_begin(h.ptr, ctypes.byref(cfg), time.perf_counter() - t_start))
         prog = _lib.Progress()
         seen_iter = seen_outer = 0
+        avg_duals = []  # dual parts of the averages, known at acceptance (the matrix comes a pass later)
         while True:
             _lib.check(lib.pdot_advance(h.ptr, 1, ctypes.byref(prog)))
-            if prog.done:
-                break
+            if trace.record_inner and prog.avg_written and avg_duals:
+                A, _, _ = h.get_slot(prog.avg_slot)
+                pa, qa = avg_duals.pop(0)
+                trace.inner_averages.append(Iterate(A, pa, qa))
             if prog.restarts > seen_outer:
                 seen_outer = prog.restarts
                 X, p, q = h.get_slot(prog.roles[0])
                 trace.restart_points.append(Iterate(X, p, q))
+            if prog.done:
+                break
             if prog.iterations > seen_iter:
                 seen_iter = prog.iterations
                 if trace.record_inner:
                     X, p, q = h.get_slot(prog.roles[0])
                     trace.inner_iterates.append(Iterate(X, p, q))
-                    X, p, q = h.get_slot(prog.roles[1])
-                    trace.inner_averages.append(Iterate(X, p, q))
+                    _, pa, qa = h.get_slot(prog.roles[1], want_X=False)
+                    avg_duals.append((pa, qa))
         _lib.check(lib.pdot_finish(h.ptr, ctypes.byref(res)))
-        if prog.restarts > seen_outer:  # a restart on the very last pass
-            X, p, q = h.get_slot(prog.roles[0])
-            trace.restart_points.append(Iterate(X, p, q))
     elapsed = time.perf_counter() - t_start
     phases["loop_s"] = float(res.elapsed_s)
 

@@ -68,13 +68,17 @@ def pdhg_step(prob, it: Iterate, tau: float, sigma: float) -> Iterate:
 
 
 def step_and_average(prob, it: Iterate, avg: Iterate, tau: float, sigma: float, k: int):
-    """pdhg_step plus the running-mean update avg + (next - avg)/k of pdhg.py:314-317,
-    in the fused kernel the solve loop runs.  Returns (next, new_average)."""
+    """One fused STEP pass as the solve loop runs it: the trial ``next =
+    pdhg_step(it)`` plus the running-mean updates of pdhg.py:314-317 with count
+    k -- the average MATRIX of the input iterate, ``avg.X + (it.X - avg.X)/k``
+    (computed one pass late in the loop), and the average DUALS of the trial,
+    ``avg.p + (next.p - avg.p)/k``.  Returns (next, new_average)."""
     if k < 1:
         raise ValueError("k must be >= 1")
     dp, h = _bound_handle(prob)
     h.set_slot(0, it.X, it.p, it.q)
     h.set_slot(2, avg.X, avg.p, avg.q)
+    h.set_slot(3, None, avg.p, avg.q)
     _lib.check(h.lib.pdot_unit_step(h.ptr, float(tau), float(sigma), float(k)))
     X, p, q = h.get_slot(1)
     A, pa, qa = h.get_slot(3)

@@ -124,8 +124,9 @@ def test_step_matches_oracle_large(pd):
 
 
 def test_running_average_bit_identical(pd):
-    """A' = A + (X+ - A)/k in the fused kernel (Markstein division with a
-    precomputed 1/k) is bit-identical to numpy's IEEE division, for many k."""
+    """A' = A + (X - A)/k in the fused kernel (Markstein division with a
+    precomputed 1/k) is bit-identical to numpy's IEEE division, for many k;
+    the dual average uses the trial duals as the solve loop does."""
     from oracle import pdot_oracle as O
     from paper_2407_19689_b200 import instances as inst
     from paper_2407_19689_b200.units import step_and_average
@@ -143,7 +144,7 @@ def test_running_average_bit_identical(pd):
         Xn, _, _ = O.primal_dual_step(prob.C, prob.f, prob.g, X, p, q, 0.02, 0.3)
         assert np.array_equal(nxt.X, Xn)
         ref = A.copy()
-        ref += (Xn - ref) / k          # pdhg.py:315, numpy IEEE division
+        ref += (X - ref) / k           # pdhg.py:315 (average of the input iterate), IEEE division
         assert np.array_equal(av.X, ref), k
         rp = pa.copy()
         rp += (nxt.p - rp) / k         # pdhg.py:316 on the GPU's own p+
