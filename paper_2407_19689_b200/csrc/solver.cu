@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -284,6 +285,49 @@ int launch_pass(pdot_solver* h, int op) {
   return PDOT_OK;
 }
 
+// Device -> pageable host copy of an m x n matrix through the pinned double
+// buffer: chunk k+1 is DMA'd while host threads copy chunk k out (page faults of
+// fresh destination pages are taken in parallel too).
+int d2h_matrix_bounced(pdot_solver* h, double* dst, int64_t ldd, const double* src, int64_t lds, int64_t m,
+                       int64_t n) {
+  const int64_t row_bytes = n * (int64_t)sizeof(double);
+  const int64_t rows_per = std::max<int64_t>(1, (int64_t)h->bounce_bytes / row_bytes);
+  const int64_t nchunks = (m + rows_per - 1) / rows_per;
+  const unsigned nthreads = 8;
+  auto copy_out = [&](int64_t k) {
+    const int64_t r0 = k * rows_per, rows = std::min(rows_per, m - r0);
+    const char* b = reinterpret_cast<const char*>(h->bounce[k & 1]);
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < nthreads; ++t) {
+      const int64_t a = rows * t / nthreads, e = rows * (t + 1) / nthreads;
+      pool.emplace_back([=]() {
+        for (int64_t r = a; r < e; ++r)
+          memcpy(dst + (r0 + r) * ldd, b + r * row_bytes, (size_t)row_bytes);
+      });
+    }
+    for (auto& th : pool) th.join();
+  };
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int64_t r0 = k * rows_per, rows = std::min(rows_per, m - r0);
+    CK(cudaMemcpy2DAsync(h->bounce[k & 1], (size_t)row_bytes, src + r0 * lds, (size_t)lds * sizeof(double),
+                         (size_t)row_bytes, (size_t)rows, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaEventRecord(h->bounce_ev[k & 1], h->stream));
+    if (k > 0) copy_out(k - 1);  // overlaps with the DMA of chunk k
+    CK(cudaEventSynchronize(h->bounce_ev[k & 1]));
+  }
+  if (nchunks > 0) copy_out(nchunks - 1);
+  return PDOT_OK;
+}
+
+bool is_pageable_host(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
 void drain_ring(pdot_solver* h) {
   const int64_t head = h->status_h->ring_head;
   for (int64_t t = h->ring_tail; t < head; ++t) {
@@ -475,6 +519,17 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     return rc;
   }
   memset((void*)h->status_h, 0, sizeof(pdot::Status));
+  if ((size_t)m * n * sizeof(double) >= ((size_t)64 << 20)) {  // plans of >= 64 MB
+    h->bounce_bytes = (size_t)64 << 20;
+    for (int i = 0; i < 2; ++i) {
+      if ((e = cudaHostAlloc(&h->bounce[i], h->bounce_bytes, cudaHostAllocDefault)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&h->bounce_ev[i], cudaEventDisableTiming)) != cudaSuccess) {
+        int rc = cuda_fail(e, "pdot_create bounce buffers", __LINE__);
+        pdot_destroy(h);
+        return rc;
+      }
+    }
+  }
   if ((e = cudaMemsetAsync(h->slot_mem, 0, bytes_slots, h->stream)) != cudaSuccess ||
       (e = cudaMemsetAsync(h->work, 0, (size_t)w_total * sizeof(double), h->stream)) != cudaSuccess ||
       (e = cudaMemsetAsync(h->counter, 0, sizeof(unsigned) * 4, h->stream)) != cudaSuccess) {
@@ -555,6 +610,10 @@ int pdot_destroy(pdot_solver* h) {
   if (h->work) cudaFree(h->work);
   if (h->counter) cudaFree(h->counter);
   if (h->status_h) cudaFreeHost(h->status_h);
+  for (int i = 0; i < 2; ++i) {
+    if (h->bounce[i]) cudaFreeHost(h->bounce[i]);
+    if (h->bounce_ev[i]) cudaEventDestroy(h->bounce_ev[i]);
+  }
   if (h->ring_h) cudaFreeHost(h->ring_h);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
@@ -647,7 +706,11 @@ int pdot_get_slot(pdot_solver* h, int slot, double* X_any, int64_t ldX, double* 
   const pdot::Slot& s = h->host.slot[slot];
   if (X_any) {
     if (ldX < h->n) return set_err(PDOT_EINVAL, "X: leading dimension must be >= n");
-    if (int rc = copy_matrix(X_any, ldX, s.X, h->ldx, h->m, h->n, h->stream)) return rc;
+    if (h->bounce[0] && is_pageable_host(X_any)) {
+      if (int rc = d2h_matrix_bounced(h, X_any, ldX, s.X, h->ldx, h->m, h->n)) return rc;
+    } else if (int rc = copy_matrix(X_any, ldX, s.X, h->ldx, h->m, h->n, h->stream)) {
+      return rc;
+    }
   }
   if (p_any)
     if (int rc = copy_vec(p_any, s.p, h->m, h->stream)) return rc;

@@ -46,6 +46,12 @@ struct pdot_solver {
   void* nccl_comm = nullptr;  // ncclComm_t when nranks > 1 and a communicator was attached
   bool virtual_shards = false;  // exchange driven by the host (single-GPU emulation)
   bool force_split = false;     // 1-rank communicator exercising the multi-GPU pass sequence
+  // pinned double buffer for device->pageable-host copies of large matrices
+  // (allocated at handle creation for large plans): DMA at pinned speed
+  // overlapped with a multi-threaded copy-out
+  double* bounce[2] = {nullptr, nullptr};
+  size_t bounce_bytes = 0;
+  cudaEvent_t bounce_ev[2] = {nullptr, nullptr};
 };
 
 
