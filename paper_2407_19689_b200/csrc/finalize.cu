@@ -657,12 +657,12 @@ __device__ void control_unit(Ctl& c, int op, const Sums& S) {
     c.out[1] = S.R[10]; // |X+|^2
   } else if (op == OP_ROUND) {
     if (c.round_stage == 2) {
-      c.out[20] = S.R[0];                       // total deficit
-      c.out[21] = S.R[0] <= 1e-14 ? 0.0 : 1.0;  // rounding.py:36
+      c.out[OUT_ROUND_TOTAL] = S.R[0];                         // total deficit
+      c.out[OUT_ROUND_CORRECT] = S.R[0] <= 1e-14 ? 0.0 : 1.0;  // rounding.py:36
     } else if (c.round_stage == 3) {
-      c.out[22] = S.R[3];            // <C, X_feas>
-      c.out[23] = S.R[1] + S.K[0];   // f.p + g.q
-      c.out[19] = S.R[2] + S.K[1];   // l1 marginal violation of X_feas
+      c.out[OUT_ROUND_OBJ] = S.R[3];             // <C, X_feas>
+      c.out[OUT_ROUND_DUAL] = S.R[1] + S.K[0];   // f.p + g.q
+      c.out[OUT_ROUND_L1VIOL] = S.R[2] + S.K[1]; // l1 marginal violation of X_feas
     }
   }
 }

@@ -34,6 +34,17 @@ enum Op : int {
   OP_NONE = 5,
 };
 
+// Ctl::out[] layout.  Unit KKT: [0..9] = gap, composite, relative, pobj, dobj,
+// primal_sq, dual_sq, |X|^2, |p|^2, |q|^2.  Unit bound: [0..4] = bound, |dX|^2,
+// |dp|^2, |dq|^2, coupling.  Rounding stages use the named slots below.
+enum OutSlot : int {
+  OUT_ROUND_L1VIOL = 19,  // l1 marginal violation of X_feas       (stage 3)
+  OUT_ROUND_TOTAL = 20,   // total row deficit sum(err_r)           (stage 2)
+  OUT_ROUND_CORRECT = 21, // 1 if the rank-one correction applies   (stage 2)
+  OUT_ROUND_OBJ = 22,     // <C, X_feas>                            (stage 3)
+  OUT_ROUND_DUAL = 23,    // f.p + g.q of the rounded slot          (stage 3)
+};
+
 enum Reason : int { R_NONE = 0, R_TOL = 1, R_ITER = 2, R_TIME = 3 };
 enum Err : int { E_OK = 0, E_NONFINITE = 1, E_LINESEARCH = 2 };
 
@@ -110,7 +121,7 @@ struct Ctl {
   int32_t op, done, reason, error;
   int32_t round_stage;
   int32_t kkt_write_viol;   // unit kkt_error: also write the dual-violation matrix
-  // ---- unit-call outputs ----
+  // ---- unit-call outputs (indices: OutSlot) ----
   double out[24];
   // ---- ring ----
   int64_t ring_head;

@@ -887,13 +887,13 @@ int pdot_round(pdot_solver* h, int slot, double* Xf_any, int64_t ldX, double* ou
     h->launches += 1;
     if (int rc = run_pass(h, pdot::OP_ROUND)) return rc;
   }
-  double outv[5];
-  CK(cudaMemcpyAsync(outv, &h->dev->out[19], 5 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  double outv[24];
+  CK(cudaMemcpyAsync(outv, h->dev->out, sizeof(outv), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   if (out3) {
-    out3[0] = outv[3];  // <C, X_feas>
-    out3[1] = outv[4];  // f.p + g.q
-    out3[2] = outv[0];  // l1 marginal violation
+    out3[0] = outv[pdot::OUT_ROUND_OBJ];
+    out3[1] = outv[pdot::OUT_ROUND_DUAL];
+    out3[2] = outv[pdot::OUT_ROUND_L1VIOL];
   }
   if (Xf_any) {
     if (ldX < h->n) return set_err(PDOT_EINVAL, "X_feas: leading dimension must be >= n");

@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(kBlockThreads, PDOT_MINB) stream_kernel(const 
       RoundOp o;
       o.C = c.C; o.X = c.slot[c.sX].X;
       o.rs = c.vec_a; o.cs = c.vec_b; o.er = c.vec_a + c.m; o.ec = c.vec_b + c.ldx;
-      o.tot = c.out[20]; o.stage = c.round_stage; o.correct = c.out[21] != 0.0;
+      o.tot = c.out[OUT_ROUND_TOTAL]; o.stage = c.round_stage; o.correct = c.out[OUT_ROUND_CORRECT] != 0.0;
       o.out = c.viol_out;
       tile_pass(o, c, smem);
       break;

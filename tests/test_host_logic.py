@@ -96,3 +96,39 @@ class TestRecords:
         assert prob.f.tolist() == [0.25, 0.75] and prob.g.sum() == 1.0
         with pytest.raises(pd.InstanceError):
             pd.make_problem(np.ones((2, 2)), [1.0, -1.0], [1.0, 1.0])
+
+
+class TestShardGeometry:
+    """Python mirror (shard.py) == C ABI (pdot_shard_rows) over many shapes; the
+    shards tile the rows and align with the 8 reduction groups."""
+
+    def test_python_matches_c(self):
+        import ctypes
+
+        from paper_2407_19689_b200 import _lib
+        from paper_2407_19689_b200.shard import row_tile, shard_rows
+        lib = _lib.load()
+        for m, n in [(1024, 1024), (4096, 4096), (16384, 16384), (8192, 32768), (65536, 65536),
+                     (2048, 96), (1024, 100000), (3000 * 8 * 16, 700)]:
+            tm = row_tile(m, n)
+            T = -(-m // tm)
+            for R in (1, 2, 4, 8):
+                if R > 1 and T % 8:
+                    continue
+                prev = 0
+                for r in range(R):
+                    a, b = ctypes.c_int64(), ctypes.c_int64()
+                    assert lib.pdot_shard_rows(m, n, R, r, ctypes.byref(a), ctypes.byref(b)) == 0
+                    assert (a.value, b.value) == shard_rows(m, n, R, r)
+                    assert a.value == prev and (a.value // tm) % (T // 8 if R > 1 else 1) == 0
+                    prev = b.value
+                assert prev == m
+
+    def test_rejects_bad_shard_counts(self):
+        import pytest as _pytest
+
+        from paper_2407_19689_b200.shard import shard_rows
+        with _pytest.raises(ValueError):
+            shard_rows(1024, 1024, 3, 0)
+        with _pytest.raises(ValueError):
+            shard_rows(1000, 1000, 2, 0)  # 8 tiles of 128 rows? 1000 rows -> not a multiple of 8 tiles
