@@ -183,6 +183,14 @@ int pdot_comm_init(pdot_solver* h, const void* id128);
  * through phase 0 (stream + group partials), pdot_exchange_local, phase 1
  * (combine + controller). */
 int pdot_set_virtual(pdot_solver* h, int on);
+/* Peer-memory exchange instead of NCCL: the finalize kernel stores its group
+ * partials straight into every rank's exchange buffer over NVLink and publishes
+ * a sequence flag; the combine kernel acquires every rank's flag (bounded spin,
+ * PDOT_ENCCL after 20 s).  Ranks share their buffers through CUDA IPC handles
+ * (64 bytes each, exchanged by the host); single-GPU emulation links handles. */
+int pdot_ipc_handle(pdot_solver* h, void* out64);
+int pdot_p2p_open(pdot_solver* h, const void* handles64, int count);
+int pdot_p2p_link_local(pdot_solver** hs, int count);
 int pdot_shard_pass(pdot_solver* h, int phase, pdot_progress* prog);
 int pdot_exchange_local(pdot_solver** hs, int count);
 

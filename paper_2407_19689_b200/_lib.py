@@ -36,7 +36,7 @@ EXPORTS = (
     "pdot_gen_cost", "pdot_gen_cost_rows", "pdot_fro_norm", "pdot_time_stream_kernel",
     "pdot_kernel_launches", "pdot_time_finalize", "pdot_shard_rows", "pdot_create_shard", "pdot_shard_info",
     "pdot_nccl_unique_id", "pdot_comm_init", "pdot_set_virtual", "pdot_shard_pass", "pdot_exchange_local",
-    "pdot_sinkhorn_solve",
+    "pdot_sinkhorn_solve", "pdot_ipc_handle", "pdot_p2p_open", "pdot_p2p_link_local",
 )
 
 
@@ -126,6 +126,9 @@ _SIGS = {
     "pdot_shard_pass": ([_P, ctypes.c_int, ctypes.POINTER(Progress)], ctypes.c_int),
     "pdot_exchange_local": ([ctypes.POINTER(_P), ctypes.c_int], ctypes.c_int),
     "pdot_sinkhorn_solve": ([_P, ctypes.POINTER(SinkhornCfg), _D, ctypes.POINTER(Result)], ctypes.c_int),
+    "pdot_ipc_handle": ([_P, _P], ctypes.c_int),
+    "pdot_p2p_open": ([_P, _P, ctypes.c_int], ctypes.c_int),
+    "pdot_p2p_link_local": ([ctypes.POINTER(_P), ctypes.c_int], ctypes.c_int),
 }
 
 _lib = None

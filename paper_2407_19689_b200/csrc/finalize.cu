@@ -54,6 +54,61 @@ __device__ __forceinline__ double pair8(const double* g) {
 }
 
 // ---------------------------------------------------------------------------
+// peer-memory exchange (c.p2p): per-exchange parity buffers + sequence flags
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long* xcounter(const Ctl& c) {
+  return reinterpret_cast<unsigned long long*>(c.xpeer[c.rank] + 2 * (size_t)kGroups * c.gstride) +
+         2 * kMaxRanks;
+}
+__device__ __forceinline__ int64_t xseq_next(const Ctl& c) { return (int64_t)__ldcg(xcounter(c)) + 1; }
+__device__ __forceinline__ int xparity(const Ctl& c) { return (int)(xseq_next(c) & 1); }
+__device__ __forceinline__ double* xgroups(const Ctl& c, int r) {
+  return c.xpeer[r] + (size_t)xparity(c) * kGroups * c.gstride;
+}
+__device__ __forceinline__ unsigned long long* xflag(const Ctl& c, int r_owner, int r_src) {
+  unsigned long long* f = reinterpret_cast<unsigned long long*>(c.xpeer[r_owner] + 2 * (size_t)kGroups * c.gstride);
+  return f + xparity(c) * kMaxRanks + r_src;
+}
+// the group buffer K2b combines: the local exchange buffer of this parity, or gbuf
+__device__ __forceinline__ const double* combine_groups(const Ctl& c) {
+  return c.p2p ? xgroups(c, c.rank) : c.gbuf;
+}
+// group partial store: into every rank's buffer (p2p) or the local gbuf
+__device__ __forceinline__ void store_group2(const Ctl& c, int64_t off, double2 v) {
+  if (c.p2p) {
+    for (int r = 0; r < c.nranks; ++r) *reinterpret_cast<double2*>(xgroups(c, r) + off) = v;
+  } else {
+    *reinterpret_cast<double2*>(c.gbuf + off) = v;
+  }
+}
+__device__ __forceinline__ void store_group1(const Ctl& c, int64_t off, double v) {
+  if (c.p2p) {
+    for (int r = 0; r < c.nranks; ++r) xgroups(c, r)[off] = v;
+  } else {
+    c.gbuf[off] = v;
+  }
+}
+// K2b: wait until every rank has published this exchange (bounded spin)
+__device__ void wait_exchange(Ctl& c) {
+  if (threadIdx.x == 0) {
+    const int64_t want = xseq_next(c);
+    const uint64_t t0 = globaltimer_ns();
+    for (int r = 0; r < c.nranks; ++r) {
+      unsigned long long v;
+      for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(xflag(c, c.rank, r)) : "memory");
+        if ((int64_t)v >= want) break;
+        if (globaltimer_ns() - t0 > 20000000000ull) {  // 20 s: a rank is gone; fail instead of hanging
+          atomicExch(&c.xerror, 1);
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
 // column blocks
 // ---------------------------------------------------------------------------
 // Sum of the column partials of reduction group g over its row tiles, in tile
@@ -86,8 +141,7 @@ __device__ void column_group_partials(const Ctl& c, int b) {
   group_column_sum<NQ>(c, g, j, acc);
   if (j < c.n) {
 #pragma unroll
-    for (int q = 0; q < NQ; ++q)
-      *reinterpret_cast<double2*>(c.gbuf + g * c.gstride + q * c.ldx + j) = acc[q];
+    for (int q = 0; q < NQ; ++q) store_group2(c, g * c.gstride + q * c.ldx + j, acc[q]);
   }
 }
 
@@ -104,7 +158,7 @@ __device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_o
       for (int q = 0; q < NQ; ++q) {
         double g8[kGroups];
 #pragma unroll
-        for (int gi = 0; gi < kGroups; ++gi) g8[gi] = __ldcg(c.gbuf + gi * c.gstride + q * c.ldx + j_out);
+        for (int gi = 0; gi < kGroups; ++gi) g8[gi] = __ldcg(combine_groups(c) + gi * c.gstride + q * c.ldx + j_out);
         col[q] = pair8(g8);
       }
     } else {
@@ -375,7 +429,16 @@ __device__ void group_scalar_partials(Ctl& c) {
   if (s < kMaxRowScal && g < c.g1) {
     double v = group_row_scalar(c, s, g, 0) + group_row_scalar(c, s, g, 1);
     if (s == kMaxRowScal - 1) v = (g == c.g0 && local_stop(c)) ? 1.0 : 0.0;
-    c.gbuf[g * c.gstride + 4 * c.ldx + s] = v;
+    store_group1(c, g * c.gstride + 4 * c.ldx + s, v);
+  }
+  if (c.p2p) {  // publish after every block's stores (each fenced at system scope before its ticket)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const unsigned long long seq = (unsigned long long)xseq_next(c);
+      for (int r = 0; r < c.nranks; ++r)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(xflag(c, r, c.rank)), "l"(seq) : "memory");
+    }
   }
 }
 
@@ -398,7 +461,7 @@ __device__ void reduce_blocks(const Ctl& c, Sums* S, double* smem, int mode) {
     const int s = tid;
     double g8[kGroups];
     for (int g = 0; g < kGroups; ++g)
-      g8[g] = (mode == FIN_B) ? __ldcg(c.gbuf + g * c.gstride + 4 * c.ldx + s)
+      g8[g] = (mode == FIN_B) ? __ldcg(combine_groups(c) + g * c.gstride + 4 * c.ldx + s)
                               : smem[s * 16 + g * 2] + smem[s * 16 + g * 2 + 1];
     S->R[s] = pair8(g8);
   } else if (tid >= 32 && tid < 32 + kMaxColScal) {
@@ -411,7 +474,7 @@ __device__ void reduce_blocks(const Ctl& c, Sums* S, double* smem, int mode) {
   if (tid == 0) {
     if (mode == FIN_B) {
       double any = 0.0;
-      for (int g = 0; g < kGroups; ++g) any += __ldcg(c.gbuf + g * c.gstride + 4 * c.ldx + kMaxRowScal - 1);
+      for (int g = 0; g < kGroups; ++g) any += __ldcg(combine_groups(c) + g * c.gstride + 4 * c.ldx + kMaxRowScal - 1);
       S->stop_any = any > 0.0;
     } else {
       S->stop_any = local_stop(c);
@@ -676,6 +739,7 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   if (c.done) return;
   const int op = force_op >= 0 ? force_op : c.op;
   if (op == OP_NONE) return;
+  if (mode == FIN_B && c.p2p) wait_exchange(c);
   if ((int64_t)blockIdx.x < c.CB) {
     if (mode == FIN_A) {
       if (op == OP_STEP) column_group_partials<4>(c, blockIdx.x);
@@ -687,7 +751,8 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
     row_block(c, op, (int)(blockIdx.x - c.CB), smem);
   }
 
-  __threadfence();
+  if (mode == FIN_A && c.p2p) __threadfence_system();  // remote group stores before the ticket
+  else __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) is_last = atomicAdd(c.counter, 1u) == gridDim.x - 1;
   __syncthreads();
@@ -707,13 +772,19 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   __syncthreads();
   reduce_blocks(cs, &S, smem, mode);
   if (threadIdx.x == 0) {
-    if (cs.unit) {
+    if (mode == FIN_B && cs.p2p) {
+      *xcounter(cs) += 1ull;  // this exchange is consumed (same count on every rank)
+      if (cs.xerror) fail(cs, E_EXCHANGE);
+    }
+    if (!cs.done && cs.unit) {
       control_unit(cs, op, S);
-    } else {
-      cs.passes += 1;
-      if (op == OP_STEP) control_step(cs, S);
-      else if (op == OP_DIST) control_dist(cs, S);
-      else if (op == OP_KKT) control_start(cs, S);
+    } else if (!cs.unit) {
+      if (!cs.done) {  // (done here only when this pass's exchange failed)
+        cs.passes += 1;
+        if (op == OP_STEP) control_step(cs, S);
+        else if (op == OP_DIST) control_dist(cs, S);
+        else if (op == OP_KKT) control_start(cs, S);
+      }
       // publish to the host mirror (read by the host only after the pass's
       // completion event, which orders these mapped-memory writes)
       if (cs.status) {

@@ -46,7 +46,8 @@ enum OutSlot : int {
 };
 
 enum Reason : int { R_NONE = 0, R_TOL = 1, R_ITER = 2, R_TIME = 3 };
-enum Err : int { E_OK = 0, E_NONFINITE = 1, E_LINESEARCH = 2 };
+enum Err : int { E_OK = 0, E_NONFINITE = 1, E_LINESEARCH = 2, E_EXCHANGE = 3 };
+constexpr int kMaxRanks = 8;
 
 enum EvType : int { EV_START = 1, EV_ACCEPT = 2, EV_CAND = 3, EV_RESTART = 4, EV_REJECT = 5 };
 
@@ -90,6 +91,14 @@ struct Ctl {
   int32_t nranks, rank;
   double* gbuf;            // [kGroups][gstride]: per-group column sums (4 x ldx) + 16 scalars
   int64_t gstride;
+  // peer-memory exchange (p2p = 1): every rank's exchange buffer, mapped into this
+  // rank's address space: [2 parities][kGroups][gstride] doubles, [2][kMaxRanks]
+  // uint64 sequence flags, then this rank's own exchange counter (device-only:
+  // host uploads of this block never reset it).  K2a stores its groups into all
+  // ranks' buffers and publishes counter+1; K2b acquires every rank's flag,
+  // combines locally and advances the counter.
+  double* xpeer[8];
+  int32_t p2p, xerror;
   double cost_fro, marg_norm;
   double tol, beta, beta_suff, beta_nec, beta_art, theta, eps_zero;
   int64_t max_iters, kkt_stride;

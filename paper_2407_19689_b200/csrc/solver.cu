@@ -261,6 +261,7 @@ bool split_mode(const pdot_solver* h) { return h->nranks > 1 || h->force_split; 
 // all-gather of the per-group partials (in place: every rank owns a contiguous chunk)
 int exchange(pdot_solver* h) {
   if (h->virtual_shards) return PDOT_OK;  // the host copies between handles
+  if (h->host.p2p) return PDOT_OK;        // the finalize kernels exchanged over peer memory
   if (!h->nccl_comm) return set_err(PDOT_ESTATE, "sharded handle without a communicator");
   const int per = pdot::kGroups / h->nranks;
   const size_t count = (size_t)per * h->gstride;
@@ -420,6 +421,8 @@ int result_from_ctl(pdot_solver* h, pdot_result* res, double wall_s) {
     return set_err(PDOT_ENONFINITE, "numerical failure: non-finite iterate");
   if (c.error == pdot::E_LINESEARCH)
     return set_err(PDOT_ELINESEARCH, "step-size line search failed to find an admissible eta");
+  if (c.error == pdot::E_EXCHANGE)
+    return set_err(PDOT_ENCCL, "peer-memory exchange timed out (a rank stopped participating)");
   return PDOT_OK;
 }
 
@@ -530,6 +533,16 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
       }
     }
   }
+  if (nranks > 1) {  // peer-memory exchange buffer (separate allocation: shareable by CUDA IPC)
+    h->xbuf_bytes = (size_t)(2 * pdot::kGroups * h->gstride) * sizeof(double) +
+                    (2 * pdot::kMaxRanks + 1) * sizeof(unsigned long long);
+    if ((e = cudaMalloc(&h->xbuf, h->xbuf_bytes)) != cudaSuccess ||
+        (e = cudaMemsetAsync(h->xbuf, 0, h->xbuf_bytes, h->stream)) != cudaSuccess) {
+      int rc = cuda_fail(e, "pdot_create exchange buffer", __LINE__);
+      pdot_destroy(h);
+      return rc;
+    }
+  }
   if ((e = cudaMemsetAsync(h->slot_mem, 0, bytes_slots, h->stream)) != cudaSuccess ||
       (e = cudaMemsetAsync(h->work, 0, (size_t)w_total * sizeof(double), h->stream)) != cudaSuccess ||
       (e = cudaMemsetAsync(h->counter, 0, sizeof(unsigned) * 4, h->stream)) != cudaSuccess) {
@@ -605,6 +618,9 @@ int pdot_destroy(pdot_solver* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->graph) cudaGraphExecDestroy(h->graph);
   if (h->nccl_comm && nccl().ok) nccl().comm_destroy(h->nccl_comm);
+  for (int r = 0; r < pdot::kMaxRanks; ++r)
+    if (h->ipc_opened[r]) cudaIpcCloseMemHandle(h->ipc_opened[r]);
+  if (h->xbuf) cudaFree(h->xbuf);
   if (h->dev) cudaFree(h->dev);
   if (h->slot_mem) cudaFree(h->slot_mem);
   if (h->work) cudaFree(h->work);
@@ -1189,6 +1205,56 @@ int pdot_time_finalize(pdot_solver* h, int iters, double* ms_per_launch) {
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, h->t0, h->t1));
   if (ms_per_launch) *ms_per_launch = ms / iters;
+  return PDOT_OK;
+}
+
+int pdot_ipc_handle(pdot_solver* h, void* out64) {
+  if (!h || !out64) return set_err(PDOT_EINVAL, "null argument");
+  if (!h->xbuf) return set_err(PDOT_EINVAL, "peer-memory exchange needs a sharded handle");
+  DeviceGuard dg(h->device);
+  cudaIpcMemHandle_t ih;
+  CK(cudaIpcGetMemHandle(&ih, h->xbuf));
+  memcpy(out64, &ih, sizeof(ih));
+  return PDOT_OK;
+}
+
+int pdot_p2p_open(pdot_solver* h, const void* handles64, int count) {
+  if (!h || !handles64 || count != h->nranks) return set_err(PDOT_EINVAL, "need one IPC handle per rank");
+  DeviceGuard dg(h->device);
+  const char* base = static_cast<const char*>(handles64);
+  for (int r = 0; r < count; ++r) {
+    if (r == h->rank) {
+      h->host.xpeer[r] = h->xbuf;
+      continue;
+    }
+    cudaIpcMemHandle_t ih;
+    memcpy(&ih, base + (size_t)r * sizeof(ih), sizeof(ih));
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess));
+    h->ipc_opened[r] = p;
+    h->host.xpeer[r] = static_cast<double*>(p);
+  }
+  h->host.p2p = 1;
+  h->host.xerror = 0;
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  return upload_ctl(h);
+}
+
+int pdot_p2p_link_local(pdot_solver** hs, int count) {
+  if (!hs || count < 2) return set_err(PDOT_EINVAL, "bad argument");
+  for (int i = 0; i < count; ++i)
+    if (!hs[i] || hs[i]->nranks != count || hs[i]->rank != i || !hs[i]->xbuf || hs[i]->device != hs[0]->device)
+      return set_err(PDOT_EINVAL, "pdot_p2p_link_local: handles must be ranks 0..count-1 on one device");
+  for (int i = 0; i < count; ++i) {
+    for (int r = 0; r < count; ++r) hs[i]->host.xpeer[r] = hs[r]->xbuf;
+    hs[i]->host.p2p = 1;
+    hs[i]->host.xerror = 0;
+    DeviceGuard dg(hs[i]->device);
+    if (int rc = upload_ctl(hs[i])) return rc;
+  }
   return PDOT_OK;
 }
 

@@ -49,6 +49,9 @@ struct pdot_solver {
   // pinned double buffer for device->pageable-host copies of large matrices
   // (allocated at handle creation for large plans): DMA at pinned speed
   // overlapped with a multi-threaded copy-out
+  double* xbuf = nullptr;       // peer-memory exchange buffer (sharded handles)
+  size_t xbuf_bytes = 0;
+  void* ipc_opened[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   double* bounce[2] = {nullptr, nullptr};
   size_t bounce_bytes = 0;
   cudaEvent_t bounce_ev[2] = {nullptr, nullptr};

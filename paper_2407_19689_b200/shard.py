@@ -9,11 +9,18 @@ the combine, the q-update and the controller then run identically on every
 GPU, and the iterates are bit-identical to the single-GPU solve (checked by
 ``tests/test_gpu_shard.py`` with the single-GPU emulation below).
 
-Transport: NCCL ``ncclAllGather`` (torch's libnccl, over NVLink/NVSwitch)
-issued by libpdot on its own stream inside the captured CUDA graph; the
-unique id travels over the caller's ``torch.distributed`` group.  For tests
-on one GPU, ``solve_virtual`` steps R shard handles on the same device and
-moves the exchange buffers with device copies.
+Transports:
+* ``nccl`` (default): ``ncclAllGather`` (torch's libnccl, over NVLink/NVSwitch)
+  issued by libpdot on its own stream inside the captured CUDA graph; the
+  unique id travels over the caller's ``torch.distributed`` group.
+* ``p2p``: the finalize kernel itself stores its group partials into every
+  rank's exchange buffer (CUDA IPC-mapped peer memory) and publishes a
+  sequence flag with release semantics; the combine kernel acquires all flags.
+  The collective is fused into the compute kernel; no NCCL call per pass.
+For tests on one GPU, ``solve_virtual`` steps R shard handles on the same
+device: ``copy`` moves the exchange buffers with device copies, ``p2p`` runs
+the peer-store path with the handles linked to each other (every writer
+completes before any reader starts, so no kernel ever waits on another).
 """
 
 from __future__ import annotations
@@ -68,7 +75,7 @@ def _bind_shard(h: Handle, dp: DeviceProblem) -> None:
 
 
 def solve_virtual(dp: DeviceProblem, config: SolverConfig | None = None, nshards: int = 2,
-                  initial: Iterate | None = None):
+                  initial: Iterate | None = None, transport: str = "copy"):
     """Single-GPU emulation of an R-shard solve (test path).
 
     Returns the gathered full iterate and the report of shard 0.  Every shard
@@ -86,16 +93,21 @@ def solve_virtual(dp: DeviceProblem, config: SolverConfig | None = None, nshards
         else:
             sl = slice(h.row0, h.row0 + h.m)
             h.set_slot(0, initial.X[sl], initial.p[sl], initial.q)
+    arr = (ctypes.c_void_p * nshards)(*[h.ptr.value for h in hs])
+    if transport == "p2p":
+        _lib.check(hs[0].lib.pdot_p2p_link_local(arr, nshards))
+    elif transport != "copy":
+        raise ValueError(f"unknown transport {transport!r}")
     cfg = config_struct(config, trace_level=0)
     for h in hs:
         _lib.check(h.lib.pdot_begin(h.ptr, ctypes.byref(cfg), 0.0))
-    arr = (ctypes.c_void_p * nshards)(*[h.ptr.value for h in hs])
     progs = [_lib.Progress() for _ in hs]
     lib = hs[0].lib
     while True:
         for h in hs:
             _lib.check(lib.pdot_shard_pass(h.ptr, 0, None))
-        _lib.check(lib.pdot_exchange_local(arr, nshards))
+        if transport == "copy":
+            _lib.check(lib.pdot_exchange_local(arr, nshards))
         for h, pr in zip(hs, progs):
             _lib.check(lib.pdot_shard_pass(h.ptr, 1, ctypes.byref(pr)))
         state = {(p.done, p.iterations, p.restarts, p.passes, tuple(p.roles)) for p in progs}
@@ -145,9 +157,15 @@ class ShardedSolver:
     rows=shard_rows(...))`` or ``full.row_shard(...)``).
     """
 
-    def __init__(self, dp: DeviceProblem, nranks: int, rank: int, group=None):
+    def __init__(self, dp: DeviceProblem, nranks: int, rank: int, group=None, transport: str | None = None):
+        import os
         self.h = Handle(dp.m_total, dp.n, dp.device, nranks, rank)
         _bind_shard(self.h, dp)
+        self.transport = transport or os.environ.get("PDOT_EXCHANGE", "nccl")
+        if self.transport == "p2p" and nranks > 1:
+            self._open_p2p(group)
+            self.dp = dp
+            return
         if nranks == 1:  # a 1-rank communicator (PDOT_FORCE_SPLIT tests the split pass sequence)
             buf = (ctypes.c_char * 128)()
             _lib.check(self.h.lib.pdot_nccl_unique_id(buf))
@@ -157,6 +175,16 @@ class ShardedSolver:
         idbuf = ctypes.create_string_buffer(ident, 128)
         _lib.check(self.h.lib.pdot_comm_init(self.h.ptr, idbuf))
         self.dp = dp
+
+    def _open_p2p(self, group):
+        """Share every rank's exchange buffer through CUDA IPC handles."""
+        import torch.distributed as dist
+        buf = (ctypes.c_char * 64)()
+        _lib.check(self.h.lib.pdot_ipc_handle(self.h.ptr, buf))
+        handles = [None] * self.h.nranks
+        dist.all_gather_object(handles, bytes(buf.raw), group=group)
+        joined = ctypes.create_string_buffer(b"".join(handles), 64 * self.h.nranks)
+        _lib.check(self.h.lib.pdot_p2p_open(self.h.ptr, joined, self.h.nranks))
 
     def solve(self, config: SolverConfig | None = None, initial: Iterate | None = None):
         """Local rows of the final iterate (+ replicated q) and the report."""
