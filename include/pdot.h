@@ -228,6 +228,17 @@ int pdot_time_finalize(pdot_solver* h, int iters, double* ms_per_launch);
 /* Number of kernels launched so far by this handle (graph nodes count individually). */
 int64_t pdot_kernel_launches(const pdot_solver* h);
 
+/* ---- block screening of the STEP pass (csrc/screen.cu) ----
+ * Same results bit for bit (pdhg.py:121-129 / kkt.py:56-94 arithmetic is
+ * unchanged); the pass only skips 8 x 16 cells whose every output and every
+ * reduction term is exactly +0.  On by default (PDOT_SCREEN=0 disables it for
+ * new handles); toggling rebuilds the min-C table and rescans the slots. */
+int pdot_set_screening(pdot_solver* h, int on);
+/* Counters since the last reset: out8 = {screened passes, active cells, tiles
+ * visited, bytes moved by K1, K0 metadata bytes, summed K1 ns (%globaltimer),
+ * screening on, cells per plan}. */
+int pdot_screen_stats(pdot_solver* h, int reset, unsigned long long* out8);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,7 +10,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "lib" / "libpdot.so"
-SOURCES = ["stream.cu", "finalize.cu", "solver.cu", "sinkhorn.cu"]
+SOURCES = ["stream.cu", "screen.cu", "finalize.cu", "solver.cu", "sinkhorn.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [
@@ -24,7 +24,7 @@ FLAGS = [
 
 def build_library(verbose: bool = False, force: bool = False) -> Path:
     srcs = [CSRC / s for s in SOURCES]
-    deps = srcs + [CSRC / "pdot_internal.cuh", CSRC / "solver_internal.h", PKG.parent / "include" / "pdot.h"]
+    deps = srcs + [CSRC / "pdot_internal.cuh", CSRC / "pass_ops.cuh", CSRC / "solver_internal.h", PKG.parent / "include" / "pdot.h"]
     if OUT.exists() and not force and all(OUT.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return OUT
     OUT.parent.mkdir(parents=True, exist_ok=True)

@@ -120,7 +120,9 @@ __device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j,
   const int64_t ta = imax64((int64_t)g * c.GS, c.t0);
   const int64_t tb = imin64(imin64((int64_t)(g + 1) * c.GS, c.Tg), c.t0 + c.T);
   if (j >= c.n) return;
+  const int64_t u = j / kTileN;
   for (int64_t t = ta; t < tb; ++t) {
+    if (!c.tileflag[(t - c.t0) * c.U + u]) continue;  // screened-out tile: all partials +0
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const double2 v = __ldcg(reinterpret_cast<const double2*>(c.colpart + ((t - c.t0) * NQ + q) * c.ldx + j));
@@ -197,20 +199,9 @@ __device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ]) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) row[q] = 0.0;
   if (i >= c.m) return;
-  constexpr int B = 4;
-  int64_t u = 0;
-  for (; u + B <= c.U; u += B) {
-    double v[B][NQ];
-#pragma unroll
-    for (int k = 0; k < B; ++k)
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) v[k][q] = __ldcg(c.rowpart + ((u + k) * NQ + q) * c.m + i);
-#pragma unroll
-    for (int k = 0; k < B; ++k)
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) row[q] += v[k][q];
-  }
-  for (; u < c.U; ++u) {
+  const uint8_t* tf = c.tileflag + (i / c.TM) * c.U;
+  for (int64_t u = 0; u < c.U; ++u) {
+    if (!tf[u]) continue;  // screened-out tile: all partials +0
 #pragma unroll
     for (int q = 0; q < NQ; ++q) row[q] += __ldcg(c.rowpart + (u * NQ + q) * c.m + i);
   }
@@ -224,6 +215,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
   if (op == OP_STEP) {
     double col[4];
     column_sums<4>(c, b, col, j, smem, mode);
+    double qb = -INFINITY, qab = -INFINITY;  // screening bounds of q+ and the dual average
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       const Slot& sx = c.slot[c.sX];
       const Slot& sa = c.slot[c.sA];
@@ -231,6 +223,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
       const double qn = qj + c.sigma * (gj - col[0]);        // pdhg.py:128
       const double dq = qn - qj;                              // pdhg.py:141
       c.slot[c.sXn].q[j] = qn;
+      qb = qn;
       vals[0] = dq * dq;
       vals[1] = dq * col[1];
       const double pcx = col[2] - gj;                         // kkt.py:69
@@ -241,12 +234,27 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
         const double qaj = sa.q[j];
         const double qan = qaj + div_by_count(qn - qaj, c.kd_dual, c.rkd_dual);  // pdhg.py:317
         c.slot[c.sAn].q[j] = qan;
+        qab = qan;
         const double pca = col[3] - gj;
         vals[3] = pca * pca;
         vals[5] = gj * qan;
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) c.cols_out[q * c.ldx + j] = col[q];
+    }
+    if (threadIdx.x < kColsPerBlock) {  // NaN-propagating maxima over each 16-column cell
+      const int lane = threadIdx.x & 31;
+      const unsigned gm = 0xffffu << (lane & 16);
+#pragma unroll
+      for (int msk = 1; msk < kCell; msk <<= 1) {
+        qb = max_nan(qb, __shfl_xor_sync(gm, qb, msk));
+        qab = max_nan(qab, __shfl_xor_sync(gm, qab, msk));
+      }
+      const int64_t cell = ((int64_t)b * kColsPerBlock + threadIdx.x) / kCell;
+      if ((threadIdx.x & (kCell - 1)) == 0 && cell < c.ncells) {
+        c.qmax[c.sXn * c.ncells + cell] = qb;
+        if (!c.unit || c.unit_avg) c.qmax[c.sAn * c.ncells + cell] = qab;
+      }
     }
   } else if (op == OP_KKT) {
     double col[1];
@@ -316,6 +324,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
     if (op == OP_STEP) {
       double row[4];
       row_sums<4>(c, ok ? i : c.m, row);
+      double pb = -INFINITY, pab = -INFINITY;  // screening bounds of p+ and the dual average
       if (ok) {
         const Slot& sx = c.slot[c.sX];
         const Slot& sa = c.slot[c.sA];
@@ -323,6 +332,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
         const double pn = pi + c.sigma * (fi - row[0]);       // pdhg.py:127
         const double dp = pn - pi;                             // pdhg.py:140
         c.slot[c.sXn].p[i] = pn;
+        pb = pn;
         vals[0] += dp * dp;
         vals[1] += dp * row[1];
         const double prx = row[2] - fi;                        // kkt.py:68
@@ -333,12 +343,27 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
           const double pai = sa.p[i];
           const double pan = pai + div_by_count(pn - pai, c.kd_dual, c.rkd_dual);  // pdhg.py:316
           c.slot[c.sAn].p[i] = pan;
+          pab = pan;
           const double pra = row[3] - fi;
           vals[3] += pra * pra;
           vals[5] += fi * pan;
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) c.rows_out[q * c.m + i] = row[q];
+      }
+      {  // NaN-propagating maxima over each 8-row band (TM is a multiple of 8)
+        const int lane = threadIdx.x & 31;
+        const unsigned gm = 0xffu << (lane & 24);
+#pragma unroll
+        for (int msk = 1; msk < kBand; msk <<= 1) {
+          pb = max_nan(pb, __shfl_xor_sync(gm, pb, msk));
+          pab = max_nan(pab, __shfl_xor_sync(gm, pab, msk));
+        }
+        const int64_t band = i / kBand;
+        if ((r & (kBand - 1)) == 0 && band < c.nbands) {
+          c.pmax[c.sXn * c.nbands + band] = pb;
+          if (!c.unit || c.unit_avg) c.pmax[c.sAn * c.nbands + band] = pab;
+        }
       }
     } else if (op == OP_KKT) {
       double row[1];
@@ -391,7 +416,8 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
   // tile scalars of this row tile (sum over column tiles, in order)
   if (threadIdx.x < ns) {
     double acc = 0.0;
-    for (int64_t u = 0; u < c.U; ++u) acc += __ldcg(c.tilescal + ((int64_t)t * c.U + u) * kMaxNS + threadIdx.x);
+    for (int64_t u = 0; u < c.U; ++u)
+      if (c.tileflag[(int64_t)t * c.U + u]) acc += __ldcg(c.tilescal + ((int64_t)t * c.U + u) * kMaxNS + threadIdx.x);
     c.rowblk[(int64_t)t * kMaxRowScal + nr + threadIdx.x] = acc;
   }
 }
@@ -802,7 +828,10 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   __syncthreads();
   unsigned long long* gwo = reinterpret_cast<unsigned long long*>(ctlp);
   for (int i = threadIdx.x; i < kWords; i += blockDim.x) gwo[i] = cw[i];
-  if (threadIdx.x == 0) *cs.counter = 0u;
+  if (threadIdx.x == 0) {
+    *cs.counter = 0u;
+    if (cs.tcount) *cs.tcount = 0u;  // the screened tile list of this pass is consumed
+  }
 }
 
 }  // namespace

@@ -25,6 +25,36 @@ constexpr int kMaxRowScal = 16;           // per-row-tile scalar partials (final
 constexpr int kMaxColScal = 8;            // per-column-block scalar partials (finalize)
 constexpr int kRingCap = 1 << 16;         // trace/event ring entries (host mapped)
 
+// Block screening of the STEP pass (screen.cu).  The plan is cut
+// into cells of kBand rows x kCell columns; a warp strip is kStrip = 4 cells.
+// A cell is SKIPPABLE in a pass when X and the lagged average are zero there
+// and neither dual pair violates it: RN(max p + max q) <= min C over the cell
+// (same for the averaged duals).  Then every output and every reduction term
+// of the cell is exactly +0, so skipping it leaves all results bit-identical.
+constexpr int kBand = 8;
+constexpr int kCell = 16;
+constexpr int kStrip = 64;
+constexpr int kCellsPerStrip = kStrip / kCell;  // 4: one byte each in a 32-bit word
+// per-cell flags of a K0 unit word (one byte per cell)
+enum UnitFlag : uint32_t { U_ACT = 1, U_LDX = 2, U_LDA = 4, U_ZX = 8, U_ZA = 16 };
+// screening statistics (uint64 counters, accumulated over a solve)
+enum ScreenStat : int {
+  ST_PASSES = 0,    // screened STEP passes
+  ST_CELLS = 1,     // active cells processed by K1
+  ST_TILES = 2,     // tiles visited by K1
+  ST_BYTES = 3,     // bytes K1 moved (cell loads/stores + tile partials)
+  ST_META = 4,      // bytes K0 read/wrote (screen metadata)
+  ST_K1_NS = 5,     // summed K1 durations (%globaltimer, first CTA start -> last CTA end)
+  ST_K0_NS = 6,     // summed K0 durations
+  ST_T0 = 7,        // scratch: start / end stamps / done-CTA counters of the running pass
+  ST_T1 = 8,
+  ST_DONE1 = 9,
+  ST_T0K0 = 10,
+  ST_T1K0 = 11,
+  ST_DONE0 = 12,
+  ST_COUNT = 16,
+};
+
 enum Op : int {
   OP_STEP = 0,   // trial step + running average + dual-violation of the input iterate
   OP_DIST = 1,   // ||cand - anchor||^2 at an adaptive restart
@@ -153,6 +183,18 @@ struct Ctl {
   double* vec_a;      // scratch m (rounding row scale / error)
   double* vec_b;      // scratch n (rounding col scale / error)
   double* viol_out;   // unit kkt: dual-violation matrix (ldx) or null
+  // ---- block screening (screen != 0: STEP passes run K0 screen + K1 sparse) ----
+  int32_t screen, nbt;       // nbt = bands per tile = TM / kBand
+  int64_t nbands, ncells, nstrips;
+  const double* minc;        // [nbands][ncells]  min C over each cell (-inf if any entry is not finite)
+  uint32_t* occ;             // [kNSlot][nbands][nstrips] per-cell "X has a nonzero bit pattern" bytes
+  double* pmax;              // [kNSlot][nbands]  NaN-propagating max of p over each band
+  double* qmax;              // [kNSlot][ncells]  ... of q over each cell (-inf for cells past n)
+  uint32_t* unitw;           // [T][U][8 strips][nbt] K0 -> K1 unit words
+  uint8_t* tileflag;         // [T][U] the tile's K1 partials are valid (0: all its partials are +0)
+  int32_t* tlist;            // [T*U] tiles K1 must visit this pass
+  unsigned int* tcount;      // length of tlist (K0 appends, K2 resets)
+  unsigned long long* sstat; // [ST_COUNT]
   unsigned int* counter;   // last-block-done counter for the finalize kernel
   Status* status;          // host mapped
   Event* ring;             // host mapped, kRingCap entries
@@ -217,6 +259,9 @@ __host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { retur
 __device__ __forceinline__ double sqr_acc(double acc, double x) { return __fma_rn(x, x, acc); }
 __device__ __forceinline__ double mul_acc(double acc, double x, double y) { return __fma_rn(x, y, acc); }
 
+// max that propagates NaN (screening bounds: a NaN dual must keep its cells active)
+__device__ __forceinline__ double max_nan(double a, double b) { return (a > b || a != a) ? a : b; }
+
 // numpy np.maximum(x, 0.0) for a scalar: NaN propagates, -0.0 stays -0.0
 __device__ __forceinline__ double relu_np(double x) { return x < 0.0 ? 0.0 : x; }
 
@@ -279,5 +324,11 @@ enum FinMode : int { FIN_FUSED = 0, FIN_A = 1, FIN_B = 2 };
 void launch_finalize_pass(Ctl* ctl_dev, const Ctl& ctl_host, int force_op, int mode, cudaStream_t s);
 size_t stream_smem_bytes(int64_t TM);
 void prepare_stream_kernel();
+// block-screened pass (screen.cu): K0 screen + K1 sparse walker
+void launch_screened_pass(const Ctl* ctl_dev, const Ctl& ctl_host, int force_op, cudaStream_t s);
+void prepare_sparse_kernel();
+// screening metadata: min C per cell, per-slot occupancy and dual bounds
+void launch_minc_build(const Ctl& ctl_host, double* minc, cudaStream_t s);
+void launch_slot_meta(const Ctl& ctl_host, int slot, bool scan_occ, cudaStream_t s);
 
 }  // namespace pdot

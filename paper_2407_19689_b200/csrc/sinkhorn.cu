@@ -327,6 +327,11 @@ extern "C" int pdot_sinkhorn_solve(pdot_solver* h, const pdot_sinkhorn_config* c
   sk_plan_kernel<<<148 * 16, 256, 0, s>>>(c.C, c.ldc, h->m, h->n, c.f, c.g, phi[fin], psi[fin], cfg->penalty,
                                           c.slot[0].X, h->ldx);
   h->launches += 1;
+  // slot 0 now holds the Sinkhorn plan and potentials; slots 4/5 the potential
+  // buffers: refresh their screening metadata for later PDHG passes
+  pdot::launch_slot_meta(c, 0, true, s);
+  pdot::launch_slot_meta(c, 4, false, s);
+  pdot::launch_slot_meta(c, 5, false, s);
   SKCK(cudaGetLastError());
   SKCK(cudaStreamSynchronize(s));
 #undef SKCK

@@ -272,17 +272,59 @@ int exchange(pdot_solver* h) {
 }
 
 // one pass: K1, then K2 (single GPU) or K2a -> exchange -> K2b (row shards)
-int launch_pass(pdot_solver* h, int op) {
+// K1 of a pass: the dense TMA walker, or K0 screen + K1 sparse walker
+int launch_k1(pdot_solver* h, int op) {
+  if (h->host.screen) {
+    pdot::launch_screened_pass(h->dev, h->host, op, h->stream);
+    return 2;
+  }
   pdot::launch_stream_pass(h->dev, h->host, op, h->stream);
+  return 1;
+}
+
+int launch_pass(pdot_solver* h, int op) {
+  h->launches += launch_k1(h, op);
   if (!split_mode(h)) {
     pdot::launch_finalize_pass(h->dev, h->host, op, pdot::FIN_FUSED, h->stream);
-    h->launches += 2;
+    h->launches += 1;
   } else {
     pdot::launch_finalize_pass(h->dev, h->host, op, pdot::FIN_A, h->stream);
     if (int rc = exchange(h)) return rc;
     pdot::launch_finalize_pass(h->dev, h->host, op, pdot::FIN_B, h->stream);
-    h->launches += 3;
+    h->launches += 2;
   }
+  return PDOT_OK;
+}
+
+// kernels per pass (graph replays count launches without re-launching)
+int launches_per_pass(const pdot_solver* h) { return (h->host.screen ? 2 : 1) + (split_mode(h) ? 2 : 1); }
+
+// screening metadata of one slot after its matrix / duals were written outside
+// the STEP kernels: occupancy scanned from the data (or cleared for a zero
+// matrix) and the dual bounds recomputed
+void slot_meta(pdot_solver* h, int slot, bool X_written, bool X_zero) {
+  const Ctl& c = h->host;
+  uint32_t* occ = c.occ + (int64_t)slot * c.nbands * c.nstrips;
+  if (X_zero) cudaMemsetAsync(occ, 0, (size_t)c.nbands * c.nstrips * sizeof(uint32_t), h->stream);
+  pdot::launch_slot_meta(c, slot, X_written && !X_zero, h->stream);
+}
+
+// the slot matrix holds arbitrary data: every cell may be nonzero
+void occ_invalidate(pdot_solver* h, int slot) {
+  const Ctl& c = h->host;
+  cudaMemsetAsync(c.occ + (int64_t)slot * c.nbands * c.nstrips, 0x01,
+                  (size_t)c.nbands * c.nstrips * sizeof(uint32_t), h->stream);
+}
+
+// (re)build min C for the bound problem when screening is on
+int screen_setup(pdot_solver* h) {
+  Ctl& c = h->host;
+  c.screen = 0;
+  if (!h->screen_on || !h->problem_set) return PDOT_OK;
+  pdot::launch_minc_build(c, h->minc_buf, h->stream);
+  CK(cudaGetLastError());
+  c.minc = h->minc_buf;
+  c.screen = 1;
   return PDOT_OK;
 }
 
@@ -380,7 +422,7 @@ int drive(pdot_solver* h, int L) {
   int64_t i = 0;
   for (;;) {
     CK(cudaGraphLaunch(h->graph, h->stream));
-    h->launches += (split_mode(h) ? 3 : 2) * L;
+    h->launches += launches_per_pass(h) * L;
     CK(cudaEventRecord(h->ev[i & 1], h->stream));
     if (i > 0) {
       CK(cudaEventSynchronize(h->ev[(i - 1) & 1]));
@@ -533,6 +575,51 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
       }
     }
   }
+  {  // block-screening metadata (screen.cu): a few MB even at 16384^2
+    const int64_t nbands = (m + pdot::kBand - 1) / pdot::kBand;
+    const int64_t ncells = (n + pdot::kCell - 1) / pdot::kCell;
+    const int64_t nstrips = (n + pdot::kStrip - 1) / pdot::kStrip;
+    const int64_t nbt = TM / pdot::kBand;
+    const int64_t tiles = h->T * h->U;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+      const size_t o = off;
+      off += (bytes + 255) & ~(size_t)255;
+      return o;
+    };
+    const size_t o_minc = take(nbands * ncells * sizeof(double));
+    const size_t o_occ = take(pdot::kNSlot * nbands * nstrips * sizeof(uint32_t));
+    const size_t o_pmax = take(pdot::kNSlot * nbands * sizeof(double));
+    const size_t o_qmax = take(pdot::kNSlot * ncells * sizeof(double));
+    const size_t o_unit = take(tiles * pdot::kWarps * nbt * sizeof(uint32_t));
+    const size_t o_tflag = take(tiles);
+    const size_t o_tlist = take(tiles * sizeof(int32_t));
+    const size_t o_tcount = take(sizeof(unsigned));
+    const size_t o_stat = take(pdot::ST_COUNT * sizeof(unsigned long long));
+    char* base = nullptr;
+    if ((e = cudaMalloc(&base, off)) != cudaSuccess || (e = cudaMemsetAsync(base, 0, off, h->stream)) != cudaSuccess) {
+      int rc = cuda_fail(e, "pdot_create screening metadata", __LINE__);
+      pdot_destroy(h);
+      return rc;
+    }
+    h->screen_mem = base;
+    h->minc_buf = reinterpret_cast<double*>(base + o_minc);
+    Ctl& c = h->host;
+    c.nbt = (int32_t)nbt;
+    c.nbands = nbands;
+    c.ncells = ncells;
+    c.nstrips = nstrips;
+    c.occ = reinterpret_cast<uint32_t*>(base + o_occ);
+    c.pmax = reinterpret_cast<double*>(base + o_pmax);
+    c.qmax = reinterpret_cast<double*>(base + o_qmax);
+    c.unitw = reinterpret_cast<uint32_t*>(base + o_unit);
+    c.tileflag = reinterpret_cast<uint8_t*>(base + o_tflag);
+    c.tlist = reinterpret_cast<int32_t*>(base + o_tlist);
+    c.tcount = reinterpret_cast<unsigned*>(base + o_tcount);
+    c.sstat = reinterpret_cast<unsigned long long*>(base + o_stat);
+    const char* env = getenv("PDOT_SCREEN");
+    h->screen_on = !(env && atoi(env) == 0);
+  }
   if (nranks > 1) {  // peer-memory exchange buffer (separate allocation: shareable by CUDA IPC)
     h->xbuf_bytes = (size_t)(2 * pdot::kGroups * h->gstride) * sizeof(double) +
                     (2 * pdot::kMaxRanks + 1) * sizeof(unsigned long long);
@@ -550,8 +637,7 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     pdot_destroy(h);
     return rc;
   }
-  Ctl& c = h->host;
-  memset(&c, 0, sizeof(Ctl));
+  Ctl& c = h->host;  // value-initialised with the handle; the screening fields are already set
   c.m = m;
   c.n = n;
   c.ldx = h->ldx;
@@ -602,6 +688,7 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
   }
   // kernel attributes (per device), outside any capture
   pdot::prepare_stream_kernel();
+  pdot::prepare_sparse_kernel();
   pdot::launch_stream_pass(h->dev, h->host, pdot::OP_NONE, h->stream);
   if ((e = cudaStreamSynchronize(h->stream)) != cudaSuccess) {
     int rc = cuda_fail(e, "pdot_create warmup", __LINE__);
@@ -624,6 +711,7 @@ int pdot_destroy(pdot_solver* h) {
   if (h->dev) cudaFree(h->dev);
   if (h->slot_mem) cudaFree(h->slot_mem);
   if (h->work) cudaFree(h->work);
+  if (h->screen_mem) cudaFree(h->screen_mem);
   if (h->counter) cudaFree(h->counter);
   if (h->status_h) cudaFreeHost(h->status_h);
   for (int i = 0; i < 2; ++i) {
@@ -663,7 +751,8 @@ int pdot_set_problem(pdot_solver* h, const double* C_dev, int64_t ldc, const dou
   h->host.cost_fro = cost_fro_norm;
   h->host.marg_norm = marginal_norm;
   h->problem_set = true;
-  return PDOT_OK;
+  DeviceGuard dg(h->device);
+  return screen_setup(h);
 }
 
 int pdot_set_problem_implicit(pdot_solver* h, int kind, const int64_t* a, const double* f_dev,
@@ -688,7 +777,8 @@ int pdot_set_problem_implicit(pdot_solver* h, int kind, const int64_t* a, const 
   h->host.cost_fro = cost_fro_norm;
   h->host.marg_norm = marginal_norm;
   h->problem_set = true;
-  return PDOT_OK;
+  DeviceGuard dg(h->device);
+  return screen_setup(h);
 }
 
 int pdot_set_slot(pdot_solver* h, int slot, const double* X_any, int64_t ldX, const double* p_any,
@@ -712,6 +802,8 @@ int pdot_set_slot(pdot_solver* h, int slot, const double* X_any, int64_t ldX, co
   } else {
     CK(cudaMemsetAsync(s.q, 0, h->n * sizeof(double), h->stream));
   }
+  slot_meta(h, slot, true, X_any == nullptr);
+  CK(cudaGetLastError());
   CK(cudaStreamSynchronize(h->stream));
   return PDOT_OK;
 }
@@ -912,6 +1004,7 @@ int pdot_round(pdot_solver* h, int slot, double* Xf_any, int64_t ldX, double* ou
     out3[2] = outv[pdot::OUT_ROUND_L1VIOL];
   }
   if (Xf_any) {
+    occ_invalidate(h, scratch);  // X_feas now lives in the scratch slot
     if (ldX < h->n) return set_err(PDOT_EINVAL, "X_feas: leading dimension must be >= n");
     if (int rc = copy_matrix(Xf_any, ldX, c.slot[scratch].X, h->ldx, h->m, h->n, h->stream)) return rc;
     CK(cudaStreamSynchronize(h->stream));
@@ -978,6 +1071,7 @@ static int unit_kkt_impl(pdot_solver* h, bool with_cost, double scale_R, double*
   c.cost_kind = kind_save;
   if (rc) return rc;
   if ((rc = run_pass(h, pdot::OP_KKT))) return rc;
+  if (c.kkt_write_viol) occ_invalidate(h, 1);  // the violation matrix lives in slot 1
   double o[10];
   CK(cudaMemcpyAsync(o, &h->dev->out[0], 10 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   if (rows_any && (rc = copy_vec(rows_any, c.rows_out, h->m, h->stream))) return rc;
@@ -1063,11 +1157,13 @@ int pdot_time_stream_kernel(pdot_solver* h, int iters, double* ms_per_launch) {
   c.tau = 1e-3; c.sigma = 1e-3; c.kd = 3.0; c.rkd = 1.0 / 3.0; c.kd_dual = 4.0; c.rkd_dual = 0.25;
   c.op = pdot::OP_STEP;
   if (int rc = upload_ctl(h)) return rc;
+  // always the dense TMA walker: this is the 40 B/entry roofline probe
   for (int i = 0; i < 2; ++i) pdot::launch_stream_pass(h->dev, h->host, pdot::OP_STEP, h->stream);
   CK(cudaEventRecord(h->t0, h->stream));
   for (int i = 0; i < iters; ++i) pdot::launch_stream_pass(h->dev, h->host, pdot::OP_STEP, h->stream);
   CK(cudaEventRecord(h->t1, h->stream));
   h->launches += iters + 2;
+  for (int s = 0; s < pdot::kNSlot; ++s) occ_invalidate(h, s);  // the dense walker kept no occupancy
   CK(cudaEventSynchronize(h->t1));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, h->t0, h->t1));
@@ -1136,9 +1232,9 @@ int pdot_shard_pass(pdot_solver* h, int phase, pdot_progress* prog) {
   if (!h || h->nranks == 1) return set_err(PDOT_EINVAL, "pdot_shard_pass needs a sharded handle");
   DeviceGuard dg(h->device);
   if (phase == 0) {
-    pdot::launch_stream_pass(h->dev, h->host, -1, h->stream);
+    h->launches += launch_k1(h, -1);
     pdot::launch_finalize_pass(h->dev, h->host, -1, pdot::FIN_A, h->stream);
-    h->launches += 2;
+    h->launches += 1;
   } else {
     pdot::launch_finalize_pass(h->dev, h->host, -1, pdot::FIN_B, h->stream);
     h->launches += 1;
@@ -1195,7 +1291,7 @@ int pdot_time_finalize(pdot_solver* h, int iters, double* ms_per_launch) {
   c.tau = 1e-3; c.sigma = 1e-3; c.kd = 3.0; c.rkd = 1.0 / 3.0; c.kd_dual = 4.0; c.rkd_dual = 0.25;
   c.op = pdot::OP_STEP;
   if (int rc = upload_ctl(h)) return rc;
-  pdot::launch_stream_pass(h->dev, h->host, pdot::OP_STEP, h->stream);
+  launch_k1(h, pdot::OP_STEP);
   for (int i = 0; i < 2; ++i) pdot::launch_finalize_pass(h->dev, h->host, pdot::OP_STEP, pdot::FIN_FUSED, h->stream);
   CK(cudaEventRecord(h->t0, h->stream));
   for (int i = 0; i < iters; ++i) pdot::launch_finalize_pass(h->dev, h->host, pdot::OP_STEP, pdot::FIN_FUSED, h->stream);
@@ -1255,6 +1351,43 @@ int pdot_p2p_link_local(pdot_solver** hs, int count) {
     DeviceGuard dg(hs[i]->device);
     if (int rc = upload_ctl(hs[i])) return rc;
   }
+  return PDOT_OK;
+}
+
+int pdot_set_screening(pdot_solver* h, int on) {
+  if (!h) return set_err(PDOT_EINVAL, "null handle");
+  DeviceGuard dg(h->device);
+  const bool was = h->host.screen != 0;
+  h->screen_on = on != 0;
+  if (int rc = screen_setup(h)) return rc;
+  if (h->host.screen && !was) {
+    // the dense walker kept no occupancy: rescan every slot (memory is the truth)
+    for (int s = 0; s < pdot::kNSlot; ++s) slot_meta(h, s, true, false);
+  }
+  if (h->graph) {  // the pass topology changed
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(h->stream));
+  return PDOT_OK;
+}
+
+int pdot_screen_stats(pdot_solver* h, int reset, unsigned long long* out8) {
+  if (!h || !out8) return set_err(PDOT_EINVAL, "null argument");
+  DeviceGuard dg(h->device);
+  unsigned long long st[pdot::ST_COUNT];
+  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaMemcpy(st, h->host.sstat, sizeof(st), cudaMemcpyDeviceToHost));
+  out8[0] = st[pdot::ST_PASSES];
+  out8[1] = st[pdot::ST_CELLS];
+  out8[2] = st[pdot::ST_TILES];
+  out8[3] = st[pdot::ST_BYTES];
+  out8[4] = st[pdot::ST_META];
+  out8[5] = st[pdot::ST_K1_NS];
+  out8[6] = (unsigned long long)h->host.screen;
+  out8[7] = (unsigned long long)(h->host.nbands * h->host.ncells);
+  if (reset) CK(cudaMemset(h->host.sstat, 0, 7 * sizeof(unsigned long long)));
   return PDOT_OK;
 }
 

@@ -53,6 +53,10 @@ struct pdot_solver {
   size_t xbuf_bytes = 0;
   void* ipc_opened[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   double* bounce[2] = {nullptr, nullptr};
+  // block screening (screen.cu): metadata allocation, min C of the bound problem
+  char* screen_mem = nullptr;
+  double* minc_buf = nullptr;
+  bool screen_on = true;        // PDOT_SCREEN=0 or pdot_set_screening(h, 0) selects the dense walker
   size_t bounce_bytes = 0;
   cudaEvent_t bounce_ev[2] = {nullptr, nullptr};
 };

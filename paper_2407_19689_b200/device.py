@@ -173,6 +173,7 @@ class Handle:
         self.ldx = ldx.value
         self.bytes = 6 * 8 * m * self.ldx
         self.bound_problem = None
+        self.screen = None  # None: the library default (PDOT_SCREEN, on unless set to 0)
 
     def close(self):
         if self.ptr:
@@ -195,6 +196,19 @@ class Handle:
             _lib.check(self.lib.pdot_set_problem(self.ptr, dp.C_t.data_ptr(), dp.ldc, dp.f_t.data_ptr(),
                                                  dp.g_t.data_ptr(), dp.cost_fro_norm, dp.marginal_norm))
         self.bound_problem = dp  # keep the borrowed buffers alive
+        if _SCREEN is not None and _SCREEN != self.screen:
+            self.set_screening(_SCREEN)
+
+    def set_screening(self, on: bool) -> None:
+        """Block screening of the STEP pass (bit-identical results)."""
+        _lib.check(self.lib.pdot_set_screening(self.ptr, 1 if on else 0))
+        self.screen = bool(on)
+
+    def screen_stats(self, reset: bool = False) -> dict:
+        out = (ctypes.c_ulonglong * 8)()
+        _lib.check(self.lib.pdot_screen_stats(self.ptr, 1 if reset else 0, out))
+        keys = ("passes", "active_cells", "tiles", "k1_bytes", "k0_bytes", "k1_ns", "screen_on", "cells_per_plan")
+        return dict(zip(keys, (int(v) for v in out)))
 
     def set_slot(self, slot: int, X=None, p=None, q=None) -> None:
         keep = []
@@ -237,6 +251,15 @@ class Handle:
 
 _HANDLES: dict = {}
 _BIG = 1 << 30
+_SCREEN = None
+
+
+def set_screening(on) -> None:
+    """Process-wide override of block screening for handles bound from now on:
+    True / False, or None for the library default (on; PDOT_SCREEN=0 turns it
+    off).  Results are bit-identical either way; tests flip it to prove that."""
+    global _SCREEN
+    _SCREEN = None if on is None else bool(on)
 
 
 def get_handle(m: int, n: int, device: int = 0) -> Handle:

@@ -1,0 +1,149 @@
+"""Block screening of the STEP pass (csrc/screen.cu) must not change a single bit.
+
+A screened pass skips 8x16 cells whose every output and reduction term is
+exactly +0 (zero plan and lagged average there, no dual violation by the
+current or averaged duals), so solves with screening on and off must agree
+bit for bit: reports, iterates (compared as int64 bit patterns, so -0.0 and
++0.0 differ), traces.  The dense TMA walker is the reference here; its own
+parity with the oracle is covered by test_gpu_solve / test_gpu_units.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def pd():
+    import paper_2407_19689_b200 as pd
+    from paper_2407_19689_b200 import device
+    yield pd
+    device.set_screening(None)
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
+
+
+def _same_iterate(a, b):
+    return (np.array_equal(_bits(a.X), _bits(b.X)) and np.array_equal(_bits(a.p), _bits(b.p))
+            and np.array_equal(_bits(a.q), _bits(b.q)))
+
+
+def _solve_both(pd, prob, cfg, initial=None, trace=False):
+    from paper_2407_19689_b200 import device
+    out = []
+    for on in (False, True):
+        device.set_screening(on)
+        tr = pd.SolveTrace(record_inner=trace) if trace else None
+        it, rep = pd.solve(prob, cfg, initial=initial, trace=tr)
+        out.append((it, rep, tr))
+    return out
+
+
+def _raw(C, f, g):
+    from types import SimpleNamespace
+    return SimpleNamespace(C=C, f=f, g=g, m=C.shape[0], n=C.shape[1], cost_fro_norm=float(np.linalg.norm(C)),
+                           marginal_norm=float(np.linalg.norm(f) + np.linalg.norm(g)))
+
+
+def _random_problem(m, n, seed):
+    rng = np.random.default_rng(seed)
+    C = rng.random((m, n))
+    f = rng.random(m) + 0.1
+    g = rng.random(n) + 0.1
+    return _raw(C, f / f.sum(), g / g.sum())
+
+
+CASES = [
+    ("sqeuclid_r8", lambda inst: inst.sqeuclid_problem(8, 1), dict(tol=1e-6)),
+    ("sqeuclid_r16", lambda inst: inst.sqeuclid_problem(16, 0), dict(tol=1e-5)),
+    ("c1_seed0", lambda inst: inst.sqeuclid_problem(32, 0), dict(tol=1e-4)),
+    ("l1_grid_r16", lambda inst: inst.grid_problem("whitenoise", 16, "l1", 3), dict(tol=1e-5)),
+    ("rect_sparse", lambda inst: inst.rect_problem(2, src_shape=(8, 16), dst_shape=(16, 32)), dict(tol=1e-5)),
+    ("random_37x53", lambda inst: _random_problem(37, 53, 4), dict(tol=1e-6)),
+    ("random_1x9", lambda inst: _random_problem(1, 9, 5), dict(tol=1e-7)),
+    ("random_9x1", lambda inst: _random_problem(9, 1, 6), dict(tol=1e-7)),
+    ("fixed_mode", lambda inst: inst.sqeuclid_problem(8, 2), dict(tol=1e-5, restart_mode="fixed")),
+    ("stride_abs", lambda inst: inst.sqeuclid_problem(8, 3), dict(tol=1e-5, kkt_stride=3, kkt_mode="absolute")),
+    ("iter_limit", lambda inst: inst.sqeuclid_problem(16, 4), dict(tol=1e-9, max_iters=150)),
+]
+
+
+@pytest.mark.parametrize("name,make,kw", CASES, ids=[c[0] for c in CASES])
+def test_screened_solve_bit_identical(pd, name, make, kw):
+    from paper_2407_19689_b200 import instances as inst
+    prob = make(inst)
+    cfg = pd.SolverConfig(deterministic=True, **kw)
+    (it0, r0, _), (it1, r1, _) = _solve_both(pd, prob, cfg)
+    assert r0.to_json() == r1.to_json(), name
+    assert _same_iterate(it0, it1), name
+
+
+def test_screened_warm_start_and_trace(pd):
+    """Warm start from a dense random plan (every cell occupied at first) and
+    the stepwise trace path (snapshots of every iterate and average)."""
+    from paper_2407_19689_b200 import instances as inst
+    prob = inst.sqeuclid_problem(8, 5)
+    rng = np.random.default_rng(7)
+    init = pd.Iterate(rng.random((64, 64)) * 1e-3, rng.standard_normal(64) * 0.01, rng.standard_normal(64) * 0.01)
+    cfg = pd.SolverConfig(tol=1e-5, deterministic=True)
+    (it0, r0, t0), (it1, r1, t1) = _solve_both(pd, prob, cfg, initial=init, trace=True)
+    assert r0.to_json() == r1.to_json()
+    assert _same_iterate(it0, it1)
+    assert len(t0.inner_iterates) == len(t1.inner_iterates) == r0.iterations
+    for a, b in zip(t0.inner_iterates + t0.inner_averages + t0.restart_points,
+                    t1.inner_iterates + t1.inner_averages + t1.restart_points):
+        assert _same_iterate(a, b)
+
+
+def test_screened_implicit_cost(pd):
+    prob = pd.DeviceProblem.sqeuclid_grid(32, 2, implicit=True)
+    cfg = pd.SolverConfig(tol=1e-4, deterministic=True)
+    (it0, r0, _), (it1, r1, _) = _solve_both(pd, prob, cfg)
+    assert r0.to_json() == r1.to_json()
+    assert _same_iterate(it0, it1)
+
+
+@pytest.mark.parametrize("k", [0, 3])
+def test_screened_unit_step(pd, k):
+    """pdhg_step (and the averaged unit step) through the screened walker, on a
+    sparse plan and on a dense one, against the dense walker."""
+    from paper_2407_19689_b200 import device, instances as inst, units
+    prob = inst.sqeuclid_problem(8, 1)
+    rng = np.random.default_rng(3)
+    X = np.zeros((64, 64))
+    X[rng.integers(0, 64, 40), rng.integers(0, 64, 40)] = rng.random(40)
+    for plan in (X, rng.random((64, 64))):
+        it = pd.Iterate(plan, rng.standard_normal(64) * 5, rng.standard_normal(64) * 5)
+        res = []
+        for on in (False, True):
+            device.set_screening(on)
+            if k:
+                avg = pd.Iterate(plan * 0.5, it.p * 0.3, it.q * 0.3)
+                res.append(units.step_and_average(prob, it, avg, 0.01, 0.5, k))
+            else:
+                res.append(pd.pdhg_step(prob, it, 0.01, 0.5))
+        if k:
+            (n0, a0), (n1, a1) = res
+            assert _same_iterate(n0, n1) and _same_iterate(a0, a1)
+        else:
+            assert _same_iterate(res[0], res[1])
+
+
+def test_screening_engages(pd):
+    """At C1 the screened passes must touch a small part of the plan."""
+    from paper_2407_19689_b200 import device
+    device.set_screening(True)
+    dp = pd.DeviceProblem.sqeuclid_grid(32, 0)
+    h = device.get_handle(dp.m, dp.n, dp.device)
+    h.bind(dp)
+    h.screen_stats(reset=True)
+    _, rep = pd.solve(dp, pd.SolverConfig(tol=1e-4, deterministic=True))
+    st = h.screen_stats()
+    assert st["screen_on"] == 1
+    assert st["passes"] >= rep.iterations
+    frac = st["active_cells"] / (st["passes"] * st["cells_per_plan"])
+    print("C1 active cell fraction", frac, st)
+    assert frac < 0.3
