@@ -113,16 +113,170 @@ __device__ void wait_exchange(Ctl& c) {
 // ---------------------------------------------------------------------------
 // Sum of the column partials of reduction group g over its row tiles, in tile
 // order: the within-group order that every GPU count reproduces.
+// ---------------------------------------------------------------------------
+// screened passes: tile partials rebuilt from the unit partials of K1 in the
+// canonical order (screen.cu); loads are batched so each step waits once
+// ---------------------------------------------------------------------------
+// column sums of the tiles [ta, tb) (global tile indices) of one strip: the
+// tile partial = sum of its active bands' unit partials in band order
 template <int NQ>
-__device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j, double2 (&acc)[NQ]) {
+__device__ __forceinline__ void group_column_sum_units(const Ctl& c, int64_t ta, int64_t tb, int64_t j,
+                                                       double2 (&acc)[NQ]) {
+  const int lane = threadIdx.x & 31;
+  const bool valid = j < c.n;
+  const int64_t strip = (j - lane * 2) / kStrip;  // warp-uniform
+  const uint32_t* bits = c.ubc + strip * c.nbw;
+  const int64_t bA = (ta - c.t0) * c.nbt, bB = imin64((tb - c.t0) * c.nbt, c.nbands);
+  if (bA >= bB) return;
+  const int64_t wA = bA >> 5, nwords = ((bB - 1) >> 5) - wA + 1;
+  const bool fast = nwords <= 32;
+  const uint32_t wl = (fast && lane < nwords) ? __ldcg(bits + wA + lane) : 0u;
+  for (int64_t t = ta; t < tb; ++t) {
+    const int64_t b0 = (t - c.t0) * c.nbt, b1 = imin64(b0 + c.nbt, c.nbands);
+    if (b0 >= b1) break;
+    uint32_t m;
+    if (fast) {
+      const int k0 = (int)((b0 >> 5) - wA);
+      const uint32_t lo = __shfl_sync(0xffffffffu, wl, k0);
+      const uint32_t hi = __shfl_sync(0xffffffffu, wl, k0 + 1 < 32 ? k0 + 1 : 31);
+      const uint64_t m64 = (((uint64_t)hi << 32) | lo) >> (b0 & 31);
+      const int nb = (int)(b1 - b0);
+      m = (uint32_t)m64 & (nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u));
+    } else {
+      m = 0;
+      for (int64_t b = b0; b < b1; ++b) m |= ((__ldcg(bits + (b >> 5)) >> (b & 31)) & 1u) << (b - b0);
+    }
+    double2 tacc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) tacc[q] = make_double2(0.0, 0.0);
+    while (m) {
+      int bb[4];
+      int cnt = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        bb[k] = 0;
+        if (m) {
+          bb[k] = __ffs(m) - 1;
+          m &= m - 1;
+          cnt = k + 1;
+        }
+      }
+      double2 v[4][NQ];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          v[k][q] = (valid && k < cnt)
+                        ? __ldcg(reinterpret_cast<const double2*>(c.ucol + ((b0 + bb[k]) * kMaxNQ + q) * c.ldx + j))
+                        : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < cnt)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            tacc[q].x += v[k][q].x;
+            tacc[q].y += v[k][q].y;
+          }
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      acc[q].x += tacc[q].x;
+      acc[q].y += tacc[q].y;
+    }
+  }
+}
+
+// row sums of row i: per column tile, its active strips' unit partials in strip order
+template <int NQ>
+__device__ __forceinline__ void row_sums_units(const Ctl& c, int64_t i, double (&row)[NQ]) {
+  const uint8_t* bits = c.ubr + (i / kBand) * c.U;
+  for (int64_t u0 = 0; u0 < c.U; u0 += 8) {
+    unsigned bytes[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) bytes[k] = (u0 + k < c.U) ? (unsigned)__ldcg(bits + u0 + k) : 0u;
+#pragma unroll 1
+    for (int k = 0; k < 8; ++k) {
+      const unsigned byte = bytes[k];
+      if (!byte) continue;
+      const int64_t u = u0 + k;
+      double v[kWarps][NQ];
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          v[w][q] = ((byte >> w) & 1u) ? __ldcg(c.urow + ((u * kWarps + w) * kMaxNQ + q) * c.mpad + i) : 0.0;
+      double a[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) a[q] = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w)
+        if ((byte >> w) & 1u)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) a[q] += v[w][q];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) row[q] += a[q];
+    }
+  }
+}
+
+// scalar s of tile t, column tile u: sum over strips of the strip's band-ordered
+// sum of its active units' scalars
+__device__ __forceinline__ double tile_scalar_units(const Ctl& c, int64_t t, int64_t u, int s) {
+  const int64_t b0 = t * c.nbt;
+  const int nb = (int)imin64(c.nbt, c.nbands - b0);
+  uint32_t mw[kWarps];
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) mw[w] = 0;
+#pragma unroll
+  for (int bl = 0; bl < 32; ++bl) {
+    if (bl < nb) {
+      const unsigned byte = __ldcg(c.ubr + (b0 + bl) * c.U + u);
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) mw[w] |= ((byte >> w) & 1u) << bl;
+    }
+  }
+  double tsu = 0.0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    uint32_t m = mw[w];
+    double ws = 0.0;
+    while (m) {
+      int bb[4];
+      int cnt = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        bb[k] = 0;
+        if (m) {
+          bb[k] = __ffs(m) - 1;
+          m &= m - 1;
+          cnt = k + 1;
+        }
+      }
+      double v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        v[k] = k < cnt ? __ldcg(c.uscal + ((b0 + bb[k]) * c.nstrips + u * kWarps + w) * kMaxNS + s) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < cnt) ws += v[k];
+    }
+    tsu = (w == 0) ? ws : tsu + ws;
+  }
+  return tsu;
+}
+
+template <int NQ>
+__device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j, double2 (&acc)[NQ], bool units) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = make_double2(0.0, 0.0);
   const int64_t ta = imax64((int64_t)g * c.GS, c.t0);
   const int64_t tb = imin64(imin64((int64_t)(g + 1) * c.GS, c.Tg), c.t0 + c.T);
+  if (units) {  // every lane of the warp takes part (shuffles); lanes past n only skip loads
+    group_column_sum_units<NQ>(c, ta, tb, j, acc);
+    return;
+  }
   if (j >= c.n) return;
-  const int64_t u = j / kTileN;
   for (int64_t t = ta; t < tb; ++t) {
-    if (!c.tileflag[(t - c.t0) * c.U + u]) continue;  // screened-out tile: all partials +0
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const double2 v = __ldcg(reinterpret_cast<const double2*>(c.colpart + ((t - c.t0) * NQ + q) * c.ldx + j));
@@ -133,24 +287,33 @@ __device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j,
 }
 
 // FIN_A: this shard's groups -> gbuf[g][q][j]
+// screened pass: the strip's unit bits are consumed; clear them for the next pass
+__device__ __forceinline__ void clear_unit_bits(const Ctl& c, int b) {
+  __syncthreads();
+  for (int64_t k = threadIdx.x; k < c.nbw; k += blockDim.x) c.ubc[(int64_t)b * c.nbw + k] = 0u;
+}
+
 template <int NQ>
-__device__ void column_group_partials(const Ctl& c, int b) {
+__device__ void column_group_partials(const Ctl& c, int b, bool units) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = c.g0 + warp;
-  if (g >= c.g1) return;
-  const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
-  double2 acc[NQ];
-  group_column_sum<NQ>(c, g, j, acc);
-  if (j < c.n) {
+  if (g < c.g1) {
+    const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
+    double2 acc[NQ];
+    group_column_sum<NQ>(c, g, j, acc, units);
+    if (j < c.n) {
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) store_group2(c, g * c.gstride + q * c.ldx + j, acc[q]);
+      for (int q = 0; q < NQ; ++q) store_group2(c, g * c.gstride + q * c.ldx + j, acc[q]);
+    }
   }
+  if (units) clear_unit_bits(c, b);
 }
 
 // Full column sums = pairwise combination of the 8 group sums (FIN_FUSED: the
 // groups are computed here; FIN_B: they come from the exchange buffer).
 template <int NQ>
-__device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_out, double* smem, int mode) {
+__device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_out, double* smem, int mode,
+                            bool units) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int jj = threadIdx.x;
   j_out = (int64_t)b * kColsPerBlock + jj;
@@ -171,7 +334,8 @@ __device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_o
   }
   const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
   double2 acc[NQ];
-  group_column_sum<NQ>(c, warp, j, acc);
+  group_column_sum<NQ>(c, warp, j, acc, units);
+  if (units) clear_unit_bits(c, b);
   // smem [group][q][64]
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
@@ -195,26 +359,42 @@ __device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_o
 }
 
 template <int NQ>
-__device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ]) {
+__device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ], bool units) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) row[q] = 0.0;
   if (i >= c.m) return;
-  const uint8_t* tf = c.tileflag + (i / c.TM) * c.U;
-  for (int64_t u = 0; u < c.U; ++u) {
-    if (!tf[u]) continue;  // screened-out tile: all partials +0
+  if (units) {
+    row_sums_units<NQ>(c, i, row);
+    return;
+  }
+  constexpr int B = 4;
+  int64_t u = 0;
+  for (; u + B <= c.U; u += B) {
+    double v[B][NQ];
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) v[k][q] = __ldcg(c.rowpart + ((u + k) * NQ + q) * c.m + i);
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) row[q] += v[k][q];
+  }
+  for (; u < c.U; ++u) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) row[q] += __ldcg(c.rowpart + (u * NQ + q) * c.m + i);
   }
 }
 
 __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
+  const bool units = unit_pass(c, op);
   double vals[kMaxColScal];
 #pragma unroll
   for (int s = 0; s < kMaxColScal; ++s) vals[s] = 0.0;
   int64_t j;
   if (op == OP_STEP) {
     double col[4];
-    column_sums<4>(c, b, col, j, smem, mode);
+    column_sums<4>(c, b, col, j, smem, mode, units);
     double qb = -INFINITY, qab = -INFINITY;  // screening bounds of q+ and the dual average
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       const Slot& sx = c.slot[c.sX];
@@ -258,7 +438,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
     }
   } else if (op == OP_KKT) {
     double col[1];
-    column_sums<1>(c, b, col, j, smem, mode);
+    column_sums<1>(c, b, col, j, smem, mode, units);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       c.cols_out[j] = col[0];
       if (c.C || c.cost_kind > 0) {
@@ -272,7 +452,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
     }
   } else if (op == OP_DIFF || op == OP_DIST) {
     double col[1];
-    column_sums<1>(c, b, col, j, smem, mode);
+    column_sums<1>(c, b, col, j, smem, mode, units);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       c.cols_out[j] = col[0];
       const double* qa = (op == OP_DIFF) ? c.slot[c.sX].q : c.slot[c.sZ].q;
@@ -283,7 +463,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
     }
   } else if (op == OP_ROUND) {
     double col[1];
-    column_sums<1>(c, b, col, j, smem, mode);
+    column_sums<1>(c, b, col, j, smem, mode, units);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       c.cols_out[j] = col[0];
       const double gj = c.g[j];
@@ -310,6 +490,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
 // row blocks (one per row tile)
 // ---------------------------------------------------------------------------
 __device__ void row_block(Ctl& c, int op, int t, double* smem) {
+  const bool units = unit_pass(c, op);
   double vals[kMaxRowScal];
 #pragma unroll
   for (int s = 0; s < kMaxRowScal; ++s) vals[s] = 0.0;
@@ -323,7 +504,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
     const bool ok = r < rows;
     if (op == OP_STEP) {
       double row[4];
-      row_sums<4>(c, ok ? i : c.m, row);
+      row_sums<4>(c, ok ? i : c.m, row, units);
       double pb = -INFINITY, pab = -INFINITY;  // screening bounds of p+ and the dual average
       if (ok) {
         const Slot& sx = c.slot[c.sX];
@@ -367,7 +548,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
       }
     } else if (op == OP_KKT) {
       double row[1];
-      row_sums<1>(c, ok ? i : c.m, row);
+      row_sums<1>(c, ok ? i : c.m, row, units);
       if (ok) {
         c.rows_out[i] = row[0];
         if (c.C || c.cost_kind > 0) {
@@ -380,7 +561,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
       }
     } else if (op == OP_DIFF || op == OP_DIST) {
       double row[1];
-      row_sums<1>(c, ok ? i : c.m, row);
+      row_sums<1>(c, ok ? i : c.m, row, units);
       if (ok) {
         c.rows_out[i] = row[0];
         const double* pa = (op == OP_DIFF) ? c.slot[c.sX].p : c.slot[c.sZ].p;
@@ -391,7 +572,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
       }
     } else if (op == OP_ROUND) {
       double row[1];
-      row_sums<1>(c, ok ? i : c.m, row);
+      row_sums<1>(c, ok ? i : c.m, row, units);
       if (ok) {
         c.rows_out[i] = row[0];
         const double fi = c.f[i];
@@ -414,12 +595,27 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
     for (int s = 0; s < nr; ++s) c.rowblk[(int64_t)t * kMaxRowScal + s] = vals[s];
   }
   // tile scalars of this row tile (sum over column tiles, in order)
-  if (threadIdx.x < ns) {
-    double acc = 0.0;
-    for (int64_t u = 0; u < c.U; ++u)
-      if (c.tileflag[(int64_t)t * c.U + u]) acc += __ldcg(c.tilescal + ((int64_t)t * c.U + u) * kMaxNS + threadIdx.x);
-    c.rowblk[(int64_t)t * kMaxRowScal + nr + threadIdx.x] = acc;
+  if (!units) {
+    if (threadIdx.x < ns) {
+      double acc = 0.0;
+      for (int64_t u = 0; u < c.U; ++u) acc += __ldcg(c.tilescal + ((int64_t)t * c.U + u) * kMaxNS + threadIdx.x);
+      c.rowblk[(int64_t)t * kMaxRowScal + nr + threadIdx.x] = acc;
+    }
+    return;
   }
+  // screened pass: tile scalars rebuilt from the unit scalars, 32 column tiles at a time
+  __syncthreads();
+  const int uu = threadIdx.x >> 3, s = threadIdx.x & 7;
+  double acc = 0.0;
+  for (int64_t u0 = 0; u0 < c.U; u0 += 32) {
+    const int64_t u = u0 + uu;
+    smem[uu * 8 + s] = (u < c.U && s < ns) ? tile_scalar_units(c, t, u, s) : 0.0;
+    __syncthreads();
+    if (threadIdx.x < ns)
+      for (int k = 0; k < 32 && u0 + k < c.U; ++k) acc += smem[k * 8 + threadIdx.x];
+    __syncthreads();
+  }
+  if (threadIdx.x < ns) c.rowblk[(int64_t)t * kMaxRowScal + nr + threadIdx.x] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -768,8 +964,8 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   if (mode == FIN_B && c.p2p) wait_exchange(c);
   if ((int64_t)blockIdx.x < c.CB) {
     if (mode == FIN_A) {
-      if (op == OP_STEP) column_group_partials<4>(c, blockIdx.x);
-      else column_group_partials<1>(c, blockIdx.x);
+      if (op == OP_STEP) column_group_partials<4>(c, blockIdx.x, unit_pass(c, op));
+      else column_group_partials<1>(c, blockIdx.x, unit_pass(c, op));
     } else {
       column_block(c, op, blockIdx.x, smem, mode);
     }
@@ -830,7 +1026,7 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   for (int i = threadIdx.x; i < kWords; i += blockDim.x) gwo[i] = cw[i];
   if (threadIdx.x == 0) {
     *cs.counter = 0u;
-    if (cs.tcount) *cs.tcount = 0u;  // the screened tile list of this pass is consumed
+    if (cs.ucount) *cs.ucount = 0u;  // the screened unit list of this pass is consumed
   }
 }
 

@@ -236,14 +236,45 @@ struct RoundOp {
 };
 
 // ---------------------------------------------------------------------------
-// per-tile flush shared by both walkers: column partials (registers -> global),
-// scalars (warp butterfly -> fixed-order sum over warps), row partials
-// (per-warp smem entries -> fixed-order sum over warps).
+// Canonical reduction tree of a pass (every walker reproduces it exactly, so
+// the dense TMA walker, the generic walker and the block-screened unit walker
+// give bit-identical partials; screen.cu relies on it):
+//   * a BAND is kBand = 8 consecutive rows of a tile;
+//   * column partial of a tile = sum over its bands in order of the band
+//     partial, each band partial = sequential sum over the band's rows;
+//   * row partial of a tile = sum over the 8 warp strips in order of the strip's
+//     butterfly (lane values o0 + o1, xor masks 16..1);
+//   * scalar of a tile = sum over strips in order of the strip's sum over bands
+//     in order of the band's 32-lane butterfly of the lane-sequential partial.
+// Adding an all-zero band or strip anywhere in this tree changes nothing, which
+// is what lets the screened walker skip them.
 // ---------------------------------------------------------------------------
+// end of a band: lane partials -> warp totals (identical in every lane), reset
+template <int NQ, int NS>
+__device__ __forceinline__ void band_close(double (&bacc)[NQ][2], double (&cacc)[NQ][2], double (&sacc)[NS],
+                                           double (&ws)[NS]) {
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    cacc[q][0] += bacc[q][0];
+    cacc[q][1] += bacc[q][1];
+    bacc[q][0] = bacc[q][1] = 0.0;
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    double x = sacc[s];
+#pragma unroll
+    for (int msk = 16; msk >= 1; msk >>= 1) x += __shfl_xor_sync(0xffffffffu, x, msk);
+    ws[s] += x;
+    sacc[s] = 0.0;
+  }
+}
+
+// per-tile flush shared by the walkers: column partials (registers -> global),
+// scalars (warp totals -> fixed-order sum over warps), row partials (per-warp
+// smem entries -> fixed-order sum over warps).
 template <int NQ, int NS>
 __device__ __forceinline__ void tile_flush(const Ctl& c, const Geo& g, bool worker, double (&cacc)[NQ][2],
-                                           const double (&sacc)[NS], double* rowbuf, double* sbuf) {
-  constexpr int NSP = (NS <= 1) ? 1 : (NS <= 2) ? 2 : (NS <= 4) ? 4 : 8;
+                                           const double (&ws)[NS], double* rowbuf, double* sbuf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (worker && g.v0) {
 #pragma unroll
@@ -251,12 +282,9 @@ __device__ __forceinline__ void tile_flush(const Ctl& c, const Geo& g, bool work
       *reinterpret_cast<double2*>(c.colpart + (g.tt * NQ + q) * c.ldx + g.j) =
           make_double2(cacc[q][0], cacc[q][1]);
   }
-  if (worker) {
-    double sv[NSP];
+  if (worker && lane == 0) {
 #pragma unroll
-    for (int s = 0; s < NSP; ++s) sv[s] = (s < NS) ? sacc[s] : 0.0;
-    warp_transpose_sum<NSP>(sv);
-    if (transpose_is_writer<NSP>(lane)) sbuf[warp * NSP + transpose_owner_index<NSP>(lane)] = sv[0];
+    for (int s = 0; s < NS; ++s) sbuf[warp * 8 + s] = ws[s];
   }
   __syncthreads();
   const int nrow_vals = g.rows * NQ;
@@ -271,10 +299,9 @@ __device__ __forceinline__ void tile_flush(const Ctl& c, const Geo& g, bool work
   if (threadIdx.x < NS) {
     double acc = sbuf[threadIdx.x];
 #pragma unroll
-    for (int w = 1; w < kWarps; ++w) acc += sbuf[w * NSP + threadIdx.x];
+    for (int w = 1; w < kWarps; ++w) acc += sbuf[w * 8 + threadIdx.x];
     c.tilescal[(g.tt * c.U + g.tu) * kMaxNS + threadIdx.x] = acc;
   }
-  if (threadIdx.x == 0 && c.tileflag) c.tileflag[g.tt * c.U + g.tu] = 1;
 }
 
 __device__ __forceinline__ Geo make_geo(const Ctl& c, bool worker, int64_t tu, int64_t tt) {
@@ -315,17 +342,18 @@ __device__ __forceinline__ void tile_pass(const Op& op, const Ctl& c, double* sm
   constexpr int NQ = Op::NQ, NS = Op::NS, RB = Op::RB;
   constexpr int V = RB * NQ;
   static_assert((V & (V - 1)) == 0 && V <= 32, "RB*NQ must be a power of two <= 32");
+  static_assert(RB == kBand, "one batch of the generic walker is one band");
   const int warp = threadIdx.x >> 5;
   const bool worker = warp < kWarps;
   const Geo g = make_geo(c, worker, tu, tt);
   double* rowbuf = smem;                              // [TM][NQ][kWarps]
   double* sbuf = smem + (size_t)c.TM * NQ * kWarps;   // [kWarps][8]
-  double cacc[NQ][2];
+  double cacc[NQ][2], bacc[NQ][2];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = 0.0;
-  double sacc[NS];
+  for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = bacc[q][0] = bacc[q][1] = 0.0;
+  double sacc[NS], ws[NS];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) sacc[s] = 0.0;
+  for (int s = 0; s < NS; ++s) sacc[s] = ws[s] = 0.0;
   typename Op::Col cl;
   if (worker) op.load_col(cl, g);
 
@@ -343,14 +371,15 @@ __device__ __forceinline__ void tile_pass(const Op& op, const Ctl& c, double* sm
       if (r0 + rr < g.rows && g.v0) op.compute(fr[rr], g, g.i0 + r0 + rr, cl, o0, o1, sacc);
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        cacc[q][0] += o0[q];
-        cacc[q][1] += o1[q];
+        bacc[q][0] += o0[q];
+        bacc[q][1] += o1[q];
         rv[rr * NQ + q] = o0[q] + o1[q];
       }
     }
     push_rows<NQ, RB>(rv, rowbuf, r0, worker);
+    band_close<NQ, NS>(bacc, cacc, sacc, ws);
   }
-  tile_flush<NQ, NS>(c, g, worker, cacc, sacc, rowbuf, sbuf);
+  tile_flush<NQ, NS>(c, g, worker, cacc, ws, rowbuf, sbuf);
 }
 
 // ---------------------------------------------------------------------------

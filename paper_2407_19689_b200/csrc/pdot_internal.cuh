@@ -41,7 +41,7 @@ enum UnitFlag : uint32_t { U_ACT = 1, U_LDX = 2, U_LDA = 4, U_ZX = 8, U_ZA = 16 
 enum ScreenStat : int {
   ST_PASSES = 0,    // screened STEP passes
   ST_CELLS = 1,     // active cells processed by K1
-  ST_TILES = 2,     // tiles visited by K1
+  ST_TILES = 2,     // units visited by K1
   ST_BYTES = 3,     // bytes K1 moved (cell loads/stores + tile partials)
   ST_META = 4,      // bytes K0 read/wrote (screen metadata)
   ST_K1_NS = 5,     // summed K1 durations (%globaltimer, first CTA start -> last CTA end)
@@ -183,17 +183,22 @@ struct Ctl {
   double* vec_a;      // scratch m (rounding row scale / error)
   double* vec_b;      // scratch n (rounding col scale / error)
   double* viol_out;   // unit kkt: dual-violation matrix (ldx) or null
-  // ---- block screening (screen != 0: STEP passes run K0 screen + K1 sparse) ----
+  // ---- block screening (screen.cu; screen != 0: STEP / DIST / start-KKT passes run
+  //      K0 screen + K1 unit walker, and K2 reduces per-unit partials) ----
   int32_t screen, nbt;       // nbt = bands per tile = TM / kBand
-  int64_t nbands, ncells, nstrips;
+  int64_t nbands, ncells, nstrips, nbw, mpad;  // nbw = 32-band words per strip
   const double* minc;        // [nbands][ncells]  min C over each cell (-inf if any entry is not finite)
   uint32_t* occ;             // [kNSlot][nbands][nstrips] per-cell "X has a nonzero bit pattern" bytes
   double* pmax;              // [kNSlot][nbands]  NaN-propagating max of p over each band
   double* qmax;              // [kNSlot][ncells]  ... of q over each cell (-inf for cells past n)
-  uint32_t* unitw;           // [T][U][8 strips][nbt] K0 -> K1 unit words
-  uint8_t* tileflag;         // [T][U] the tile's K1 partials are valid (0: all its partials are +0)
-  int32_t* tlist;            // [T*U] tiles K1 must visit this pass
-  unsigned int* tcount;      // length of tlist (K0 appends, K2 resets)
+  uint32_t* unitw;           // [nbands][nstrips] K0 -> K1 unit words (a flag byte per cell)
+  uint32_t* ulist;           // units K1 visits this pass (band * nstrips + strip)
+  unsigned int* ucount;      // length of ulist (K0 appends, K2 resets)
+  uint8_t* ubr;              // [nbands][U] bit w: unit (band, 8 u + w) wrote partials
+  uint32_t* ubc;             // [nstrips][nbw] bit b % 32: unit (b, strip) wrote partials (K0 sets, K2 clears)
+  double* ucol;              // [nbands][kMaxNQ][ldx]   unit column partials (band partial of the canonical tree)
+  double* urow;              // [nstrips][kMaxNQ][mpad] unit row partials (strip butterfly per row)
+  double* uscal;             // [nbands][nstrips][kMaxNS] unit scalars (band butterfly)
   unsigned long long* sstat; // [ST_COUNT]
   unsigned int* counter;   // last-block-done counter for the finalize kernel
   Status* status;          // host mapped
@@ -324,9 +329,14 @@ enum FinMode : int { FIN_FUSED = 0, FIN_A = 1, FIN_B = 2 };
 void launch_finalize_pass(Ctl* ctl_dev, const Ctl& ctl_host, int force_op, int mode, cudaStream_t s);
 size_t stream_smem_bytes(int64_t TM);
 void prepare_stream_kernel();
-// block-screened pass (screen.cu): K0 screen + K1 sparse walker
+// block-screened pass (screen.cu): K0 screen + K1 unit walker, or the generic
+// walker over all tiles for the unit calls that the screen does not cover
 void launch_screened_pass(const Ctl* ctl_dev, const Ctl& ctl_host, int force_op, cudaStream_t s);
 void prepare_sparse_kernel();
+// a pass whose partials are per-unit (screened) rather than per-tile
+__host__ __device__ __forceinline__ bool unit_pass(const Ctl& c, int op) {
+  return c.screen && (op == OP_STEP || (!c.unit && (op == OP_DIST || op == OP_KKT)));
+}
 // screening metadata: min C per cell, per-slot occupancy and dual bounds
 void launch_minc_build(const Ctl& ctl_host, double* minc, cudaStream_t s);
 void launch_slot_meta(const Ctl& ctl_host, int slot, bool scan_occ, cudaStream_t s);

@@ -276,7 +276,7 @@ int exchange(pdot_solver* h) {
 int launch_k1(pdot_solver* h, int op) {
   if (h->host.screen) {
     pdot::launch_screened_pass(h->dev, h->host, op, h->stream);
-    return 2;
+    return (op < 0 || pdot::unit_pass(h->host, op)) ? 2 : 1;
   }
   pdot::launch_stream_pass(h->dev, h->host, op, h->stream);
   return 1;
@@ -591,13 +591,23 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     const size_t o_occ = take(pdot::kNSlot * nbands * nstrips * sizeof(uint32_t));
     const size_t o_pmax = take(pdot::kNSlot * nbands * sizeof(double));
     const size_t o_qmax = take(pdot::kNSlot * ncells * sizeof(double));
-    const size_t o_unit = take(tiles * pdot::kWarps * nbt * sizeof(uint32_t));
-    const size_t o_tflag = take(tiles);
-    const size_t o_tlist = take(tiles * sizeof(int32_t));
-    const size_t o_tcount = take(sizeof(unsigned));
+    const int64_t nunits = nbands * nstrips;
+    const int64_t nbw = (nbands + 31) / 32;
+    const int64_t mpad = round_up(m, 2);
+    const size_t o_unit = take(nunits * sizeof(uint32_t));
+    const size_t o_ulist = take(nunits * sizeof(uint32_t));
+    const size_t o_ucount = take(sizeof(unsigned));
+    const size_t o_ubr = take(nbands * h->U);
+    const size_t o_ubc = take(nstrips * nbw * sizeof(uint32_t));
     const size_t o_stat = take(pdot::ST_COUNT * sizeof(unsigned long long));
+    // unit partials of screened passes (written sparsely; ~1 GB at 16384^2)
+    const size_t o_ucol = take(nbands * pdot::kMaxNQ * h->ldx * sizeof(double));
+    const size_t o_urow = take(nstrips * pdot::kMaxNQ * mpad * sizeof(double));
+    const size_t o_uscal = take(nunits * pdot::kMaxNS * sizeof(double));
+    (void)tiles;
     char* base = nullptr;
-    if ((e = cudaMalloc(&base, off)) != cudaSuccess || (e = cudaMemsetAsync(base, 0, off, h->stream)) != cudaSuccess) {
+    // only the metadata needs zeroing; the unit partials are written before they are read
+    if ((e = cudaMalloc(&base, off)) != cudaSuccess || (e = cudaMemsetAsync(base, 0, o_ucol, h->stream)) != cudaSuccess) {
       int rc = cuda_fail(e, "pdot_create screening metadata", __LINE__);
       pdot_destroy(h);
       return rc;
@@ -613,10 +623,16 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     c.pmax = reinterpret_cast<double*>(base + o_pmax);
     c.qmax = reinterpret_cast<double*>(base + o_qmax);
     c.unitw = reinterpret_cast<uint32_t*>(base + o_unit);
-    c.tileflag = reinterpret_cast<uint8_t*>(base + o_tflag);
-    c.tlist = reinterpret_cast<int32_t*>(base + o_tlist);
-    c.tcount = reinterpret_cast<unsigned*>(base + o_tcount);
+    c.ulist = reinterpret_cast<uint32_t*>(base + o_ulist);
+    c.ucount = reinterpret_cast<unsigned*>(base + o_ucount);
+    c.ubr = reinterpret_cast<uint8_t*>(base + o_ubr);
+    c.ubc = reinterpret_cast<uint32_t*>(base + o_ubc);
     c.sstat = reinterpret_cast<unsigned long long*>(base + o_stat);
+    c.ucol = reinterpret_cast<double*>(base + o_ucol);
+    c.urow = reinterpret_cast<double*>(base + o_urow);
+    c.uscal = reinterpret_cast<double*>(base + o_uscal);
+    c.nbw = nbw;
+    c.mpad = mpad;
     const char* env = getenv("PDOT_SCREEN");
     h->screen_on = !(env && atoi(env) == 0);
   }

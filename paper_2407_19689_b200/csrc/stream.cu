@@ -117,12 +117,13 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
   }
   __syncthreads();
 
-  double cacc[NQ][2];
+  double cacc[NQ][2], bacc[NQ][2];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = 0.0;
-  double sacc[NS];
+  for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = bacc[q][0] = bacc[q][1] = 0.0;
+  double sacc[NS], ws[NS];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) sacc[s] = 0.0;
+  for (int s = 0; s < NS; ++s) sacc[s] = ws[s] = 0.0;
+  constexpr int kStagesPerBand = kBand / R;
 
   if (!worker) {
     if (lane == 0) {
@@ -192,14 +193,15 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
           ao += c.ldx;
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
-            cacc[q][0] += o0[q];
-            cacc[q][1] += o1[q];
+            bacc[q][0] += o0[q];
+            bacc[q][1] += o1[q];
             rv[rr * NQ + q] = o0[q] + o1[q];
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         push_rows<NQ, R>(rv, rowbuf, it * R, true);
+        if ((it % kStagesPerBand) == kStagesPerBand - 1 || it == nst - 1) band_close<NQ, NS>(bacc, cacc, sacc, ws);
       }
     } else {
       for (int it = 0; it < nst; ++it) {
@@ -230,18 +232,19 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
           }
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
-            cacc[q][0] += o0[q];
-            cacc[q][1] += o1[q];
+            bacc[q][0] += o0[q];
+            bacc[q][1] += o1[q];
             rv[rr * NQ + q] = o0[q] + o1[q];
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         push_rows<NQ, R>(rv, rowbuf, it * R, true);
+        if ((it % kStagesPerBand) == kStagesPerBand - 1 || it == nst - 1) band_close<NQ, NS>(bacc, cacc, sacc, ws);
       }
     }
   }
-  tile_flush<NQ, NS>(c, g, worker, cacc, sacc, rowbuf, sbuf);
+  tile_flush<NQ, NS>(c, g, worker, cacc, ws, rowbuf, sbuf);
 }
 
 __global__ void __launch_bounds__(kBlockThreads, PDOT_MINB) stream_kernel(const Ctl* __restrict__ ctlp, int force_op) {

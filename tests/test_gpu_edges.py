@@ -59,7 +59,10 @@ def test_solve_edge_shapes_against_oracle(m, n):
     _, ref = O.oracle_solve(prob, cfg)
     assert rep.termination_reason == ref["termination_reason"] == "tolerance"
     assert rep.final_relative_kkt <= 1e-6
-    assert abs(rep.iterations - ref["iterations"]) <= 0.5 * ref["iterations"] + 10
+    # iteration counts of these small random instances are chaotic in the reduction
+    # order: for 33x70 the oracle itself takes 1376..3052 iterations
+    # under eight random summation orders plus long-double and reversed sums
+    assert ref["iterations"] / 2.5 - 10 <= rep.iterations <= 2.5 * ref["iterations"] + 10
     assert rep.rounded_objective == pytest.approx(ref["rounded_objective"], rel=1e-3, abs=1e-6)
     Xf = pd.round_to_feasible(prob, it.X)
     np.testing.assert_allclose(Xf.sum(axis=1), prob.f, rtol=0, atol=1e-12)
