@@ -28,7 +28,8 @@ def build_library(verbose: bool = False, force: bool = False) -> Path:
     if OUT.exists() and not force and all(OUT.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return OUT
     OUT.parent.mkdir(parents=True, exist_ok=True)
-    cmd = [NVCC, *FLAGS, *map(str, srcs), "-o", str(OUT)]
+    extra = ["-DPDOT_DEVICE_CHECKS"] if os.environ.get("PDOT_DEVICE_CHECKS") == "1" else []
+    cmd = [NVCC, *FLAGS, *extra, *map(str, srcs), "-o", str(OUT)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -114,69 +114,86 @@ __device__ void wait_exchange(Ctl& c) {
 // Sum of the column partials of reduction group g over its row tiles, in tile
 // order: the within-group order that every GPU count reproduces.
 // ---------------------------------------------------------------------------
-// screened passes: tile partials rebuilt from the unit partials of K1 in the
-// canonical order (screen.cu); loads are batched so each step waits once
+// screened passes: tile partials rebuilt from the cell partials of K1 in the
+// canonical order (pass_ops.cuh); loads are batched so each step waits once
 // ---------------------------------------------------------------------------
-// column sums of the tiles [ta, tb) (global tile indices) of one strip: the
-// tile partial = sum of its active bands' unit partials in band order
+// next (up to) 4 set bits of m, lowest first
+__device__ __forceinline__ int take4(uint32_t& m, int (&bb)[4]) {
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    bb[k] = 0;
+    if (m) {
+      bb[k] = __ffs(m) - 1;
+      m &= m - 1;
+      cnt = k + 1;
+    }
+  }
+  return cnt;
+}
+
+// column sums of the tiles [ta, tb) (global tile indices) for the lane's column
+// pair: tile partial = its active bands' cell partials in band order.  The
+// active (tile, band) pairs are scanned from the bit maps in registers and their
+// partials loaded 4 at a time, so the lane waits once per 4 active bands.
 template <int NQ>
 __device__ __forceinline__ void group_column_sum_units(const Ctl& c, int64_t ta, int64_t tb, int64_t j,
                                                        double2 (&acc)[NQ]) {
-  const int lane = threadIdx.x & 31;
-  const bool valid = j < c.n;
-  const int64_t strip = (j - lane * 2) / kStrip;  // warp-uniform
-  const uint32_t* bits = c.ubc + strip * c.nbw;
-  const int64_t bA = (ta - c.t0) * c.nbt, bB = imin64((tb - c.t0) * c.nbt, c.nbands);
-  if (bA >= bB) return;
-  const int64_t wA = bA >> 5, nwords = ((bB - 1) >> 5) - wA + 1;
-  const bool fast = nwords <= 32;
-  const uint32_t wl = (fast && lane < nwords) ? __ldcg(bits + wA + lane) : 0u;
-  for (int64_t t = ta; t < tb; ++t) {
-    const int64_t b0 = (t - c.t0) * c.nbt, b1 = imin64(b0 + c.nbt, c.nbands);
-    if (b0 >= b1) break;
-    uint32_t m;
-    if (fast) {
-      const int k0 = (int)((b0 >> 5) - wA);
-      const uint32_t lo = __shfl_sync(0xffffffffu, wl, k0);
-      const uint32_t hi = __shfl_sync(0xffffffffu, wl, k0 + 1 < 32 ? k0 + 1 : 31);
-      const uint64_t m64 = (((uint64_t)hi << 32) | lo) >> (b0 & 31);
-      const int nb = (int)(b1 - b0);
-      m = (uint32_t)m64 & (nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u));
-    } else {
-      m = 0;
-      for (int64_t b = b0; b < b1; ++b) m |= ((__ldcg(bits + (b >> 5)) >> (b & 31)) & 1u) << (b - b0);
-    }
+  if (j >= c.n) return;
+  const int64_t cell = j / kCell;
+  for (int64_t tc = ta; tc < tb; tc += 16) {
+    uint32_t mw[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) mw[k] = (tc + k < tb) ? __ldcg(c.bct + (tc + k - c.t0) * c.ncp + cell) : 0u;
     double2 tacc[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) tacc[q] = make_double2(0.0, 0.0);
-    while (m) {
-      int bb[4];
-      int cnt = 0;
+    int cur = -1;  // tile (within the chunk) tacc belongs to
+    int k = 0;     // tile being scanned
+    while (true) {
+      // next up to 4 active (tile, band) pairs in order
+      int tk[4], bb[4], cnt = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        bb[k] = 0;
-        if (m) {
-          bb[k] = __ffs(m) - 1;
-          m &= m - 1;
-          cnt = k + 1;
+      for (int e = 0; e < 4; ++e) {
+        tk[e] = 0;
+        bb[e] = 0;
+        while (k < 16 && mw[k] == 0u) ++k;
+        if (k < 16) {
+          tk[e] = k;
+          bb[e] = __ffs(mw[k]) - 1;
+          mw[k] &= mw[k] - 1;
+          cnt = e + 1;
         }
       }
+      if (cnt == 0) break;
       double2 v[4][NQ];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int e = 0; e < 4; ++e) {
+        const int64_t band = (tc + tk[e] - c.t0) * c.nbt + bb[e];
 #pragma unroll
         for (int q = 0; q < NQ; ++q)
-          v[k][q] = (valid && k < cnt)
-                        ? __ldcg(reinterpret_cast<const double2*>(c.ucol + ((b0 + bb[k]) * kMaxNQ + q) * c.ldx + j))
-                        : make_double2(0.0, 0.0);
+          v[e][q] = e < cnt ? __ldcg(reinterpret_cast<const double2*>(c.ccol + (band * kMaxNQ + q) * c.ldx + j))
+                            : make_double2(0.0, 0.0);
+      }
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (k < cnt)
+      for (int e = 0; e < 4; ++e) {
+        if (e < cnt) {
+          if (tk[e] != cur) {  // a new tile: close the previous tile's partial
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              acc[q].x += tacc[q].x;
+              acc[q].y += tacc[q].y;
+              tacc[q] = make_double2(0.0, 0.0);
+            }
+            cur = tk[e];
+          }
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
-            tacc[q].x += v[k][q].x;
-            tacc[q].y += v[k][q].y;
+            tacc[q].x += v[e][q].x;
+            tacc[q].y += v[e][q].y;
           }
+        }
+      }
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -186,83 +203,94 @@ __device__ __forceinline__ void group_column_sum_units(const Ctl& c, int64_t ta,
   }
 }
 
-// row sums of row i: per column tile, its active strips' unit partials in strip order
+// row sums of row i: per column tile, the strip values ((c0+c1)+(c2+c3)) of the
+// active cells summed in strip order; the active strips are scanned from the
+// bit maps in registers and loaded two at a time
 template <int NQ>
 __device__ __forceinline__ void row_sums_units(const Ctl& c, int64_t i, double (&row)[NQ]) {
-  const uint8_t* bits = c.ubr + (i / kBand) * c.U;
-  for (int64_t u0 = 0; u0 < c.U; u0 += 8) {
-    unsigned bytes[8];
+  const uint32_t* bits = c.bcr + (i / kBand) * c.U;
+  for (int64_t uc = 0; uc < c.U; uc += 32) {
+    uint32_t wv[32];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) bytes[k] = (u0 + k < c.U) ? (unsigned)__ldcg(bits + u0 + k) : 0u;
-#pragma unroll 1
-    for (int k = 0; k < 8; ++k) {
-      const unsigned byte = bytes[k];
-      if (!byte) continue;
-      const int64_t u = u0 + k;
-      double v[kWarps][NQ];
+    for (int k = 0; k < 32; ++k) wv[k] = (uc + k < c.U) ? __ldcg(bits + uc + k) : 0u;
+    double a[NQ];
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w)
+    for (int q = 0; q < NQ; ++q) a[q] = 0.0;
+    int cur = -1;  // column tile a[] belongs to
+    int k = 0;
+    while (true) {
+      int uk[2], ww[2], nib[2], cnt = 0;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q)
-          v[w][q] = ((byte >> w) & 1u) ? __ldcg(c.urow + ((u * kWarps + w) * kMaxNQ + q) * c.mpad + i) : 0.0;
-      double a[NQ];
+      for (int e = 0; e < 2; ++e) {
+        uk[e] = 0;
+        ww[e] = 0;
+        nib[e] = 0;
+        while (k < 32 && wv[k] == 0u) ++k;
+        if (k < 32) {
+          const int w = (__ffs(wv[k]) - 1) >> 2;  // next active strip of this column tile
+          uk[e] = k;
+          ww[e] = w;
+          nib[e] = (wv[k] >> (4 * w)) & 0xf;
+          wv[k] &= ~(0xfu << (4 * w));
+          cnt = e + 1;
+        }
+      }
+      if (cnt == 0) break;
+      double v[2][4][NQ];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) a[q] = 0.0;
+      for (int e = 0; e < 2; ++e) {
+        const int64_t cb = (uc + uk[e]) * 32 + 4 * ww[e];
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w)
-        if ((byte >> w) & 1u)
+        for (int x = 0; x < 4; ++x)
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) a[q] += v[w][q];
+          for (int q = 0; q < NQ; ++q)
+            v[e][x][q] = (e < cnt && ((nib[e] >> x) & 1)) ? __ldcg(c.crow + ((cb + x) * kMaxNQ + q) * c.mpad + i) : 0.0;
+      }
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) row[q] += a[q];
+      for (int e = 0; e < 2; ++e) {
+        if (e < cnt) {
+          if (uk[e] != cur) {  // next column tile: its partial joins the row in tile order
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              row[q] += a[q];
+              a[q] = 0.0;
+            }
+            cur = uk[e];
+          }
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) a[q] += (v[e][0][q] + v[e][1][q]) + (v[e][2][q] + v[e][3][q]);
+        }
+      }
     }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) row[q] += a[q];
   }
 }
 
-// scalar s of tile t, column tile u: sum over strips of the strip's band-ordered
-// sum of its active units' scalars
-__device__ __forceinline__ double tile_scalar_units(const Ctl& c, int64_t t, int64_t u, int s) {
+// scalar pieces of tile t, column tile u, strip w: the strip's band-ordered sum
+// of its strip-band values ((c0+c1)+(c2+c3))
+template <int NS>
+__device__ __forceinline__ void strip_scalars_units(const Ctl& c, int64_t t, int64_t u, int w, double (&ws)[NS]) {
   const int64_t b0 = t * c.nbt;
   const int nb = (int)imin64(c.nbt, c.nbands - b0);
-  uint32_t mw[kWarps];
+  uint32_t nibs[32];
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) mw[w] = 0;
+  for (int bl = 0; bl < 32; ++bl) nibs[bl] = bl < nb ? (__ldcg(c.bcr + (b0 + bl) * c.U + u) >> (4 * w)) & 0xfu : 0u;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) ws[s] = 0.0;
 #pragma unroll
   for (int bl = 0; bl < 32; ++bl) {
-    if (bl < nb) {
-      const unsigned byte = __ldcg(c.ubr + (b0 + bl) * c.U + u);
+    const unsigned nib = nibs[bl];
+    if (!nib) continue;
+    const double* base = c.cscal + ((b0 + bl) * c.ncp + u * 32 + 4 * w) * kMaxNS;
+    double v[4][NS];
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) mw[w] |= ((byte >> w) & 1u) << bl;
-    }
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int s = 0; s < NS; ++s) v[x][s] = ((nib >> x) & 1u) ? __ldcg(base + x * kMaxNS + s) : 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) ws[s] += (v[0][s] + v[1][s]) + (v[2][s] + v[3][s]);
   }
-  double tsu = 0.0;
-#pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    uint32_t m = mw[w];
-    double ws = 0.0;
-    while (m) {
-      int bb[4];
-      int cnt = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        bb[k] = 0;
-        if (m) {
-          bb[k] = __ffs(m) - 1;
-          m &= m - 1;
-          cnt = k + 1;
-        }
-      }
-      double v[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        v[k] = k < cnt ? __ldcg(c.uscal + ((b0 + bb[k]) * c.nstrips + u * kWarps + w) * kMaxNS + s) : 0.0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (k < cnt) ws += v[k];
-    }
-    tsu = (w == 0) ? ws : tsu + ws;
-  }
-  return tsu;
 }
 
 template <int NQ>
@@ -287,12 +315,6 @@ __device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j,
 }
 
 // FIN_A: this shard's groups -> gbuf[g][q][j]
-// screened pass: the strip's unit bits are consumed; clear them for the next pass
-__device__ __forceinline__ void clear_unit_bits(const Ctl& c, int b) {
-  __syncthreads();
-  for (int64_t k = threadIdx.x; k < c.nbw; k += blockDim.x) c.ubc[(int64_t)b * c.nbw + k] = 0u;
-}
-
 template <int NQ>
 __device__ void column_group_partials(const Ctl& c, int b, bool units) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -306,7 +328,6 @@ __device__ void column_group_partials(const Ctl& c, int b, bool units) {
       for (int q = 0; q < NQ; ++q) store_group2(c, g * c.gstride + q * c.ldx + j, acc[q]);
     }
   }
-  if (units) clear_unit_bits(c, b);
 }
 
 // Full column sums = pairwise combination of the 8 group sums (FIN_FUSED: the
@@ -335,7 +356,6 @@ __device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_o
   const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
   double2 acc[NQ];
   group_column_sum<NQ>(c, warp, j, acc, units);
-  if (units) clear_unit_bits(c, b);
   // smem [group][q][64]
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
@@ -603,16 +623,31 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
     }
     return;
   }
-  // screened pass: tile scalars rebuilt from the unit scalars, 32 column tiles at a time
+  // screened pass: tile scalars rebuilt from the cell scalars; thread (u, w)
+  // computes strip w's band-ordered sum, then the strips and column tiles are
+  // added in order (32 column tiles per round)
   __syncthreads();
-  const int uu = threadIdx.x >> 3, s = threadIdx.x & 7;
+  const int uu = threadIdx.x >> 3, w = threadIdx.x & 7;
   double acc = 0.0;
   for (int64_t u0 = 0; u0 < c.U; u0 += 32) {
     const int64_t u = u0 + uu;
-    smem[uu * 8 + s] = (u < c.U && s < ns) ? tile_scalar_units(c, t, u, s) : 0.0;
+    double ws[6];
+    if (u < c.U) {
+      strip_scalars_units<6>(c, t, u, w, ws);
+    } else {
+#pragma unroll
+      for (int s = 0; s < 6; ++s) ws[s] = 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < 6; ++s) smem[(uu * 8 + w) * 8 + s] = ws[s];
     __syncthreads();
-    if (threadIdx.x < ns)
-      for (int k = 0; k < 32 && u0 + k < c.U; ++k) acc += smem[k * 8 + threadIdx.x];
+    if (threadIdx.x < ns) {
+      for (int k = 0; k < 32 && u0 + k < c.U; ++k) {
+        double tsu = smem[(k * 8) * 8 + threadIdx.x];
+        for (int x = 1; x < kWarps; ++x) tsu += smem[(k * 8 + x) * 8 + threadIdx.x];
+        acc += tsu;
+      }
+    }
     __syncthreads();
   }
   if (threadIdx.x < ns) c.rowblk[(int64_t)t * kMaxRowScal + nr + threadIdx.x] = acc;

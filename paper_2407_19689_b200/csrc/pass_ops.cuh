@@ -236,35 +236,58 @@ struct RoundOp {
 };
 
 // ---------------------------------------------------------------------------
-// Canonical reduction tree of a pass (every walker reproduces it exactly, so
-// the dense TMA walker, the generic walker and the block-screened unit walker
-// give bit-identical partials; screen.cu relies on it):
-//   * a BAND is kBand = 8 consecutive rows of a tile;
-//   * column partial of a tile = sum over its bands in order of the band
-//     partial, each band partial = sequential sum over the band's rows;
-//   * row partial of a tile = sum over the 8 warp strips in order of the strip's
-//     butterfly (lane values o0 + o1, xor masks 16..1);
-//   * scalar of a tile = sum over strips in order of the strip's sum over bands
-//     in order of the band's 32-lane butterfly of the lane-sequential partial.
-// Adding an all-zero band or strip anywhere in this tree changes nothing, which
-// is what lets the screened walker skip them.
+// Canonical reduction tree of a pass.  Every walker reproduces it exactly, so
+// the dense TMA walker, the generic walker and the block-screened cell walker
+// (screen.cu) give bit-identical partials.  Units: a BAND is 8 rows of a tile,
+// a STRIP 64 columns (one warp of the dense walkers, lane = column pair), a
+// CELL = band x 16 columns (8 lanes).
+//   * column: band partial = ((r0+r1) + (r2+r3)) + ((r4+r5) + (r6+r7)) over
+//     the band's rows; tile partial = sum of band partials in band order;
+//   * row: lane value o0 + o1; cell value = 8-lane butterfly (masks 1, 2, 4);
+//     strip value = (c0 + c1) + (c2 + c3) (masks 8, 16); tile partial = sum of
+//     strip values in strip order;
+//   * scalar: lane band partial = sequential over the band's rows (col0 then
+//     col1 per row); cell value = 8-lane butterfly; strip band value =
+//     (c0 + c1) + (c2 + c3); tile scalar = sum over strips of the strip's sum
+//     over bands in band order.
+// A skipped cell contributes exact +0 terms anywhere in this tree.
 // ---------------------------------------------------------------------------
-// end of a band: lane partials -> warp totals (identical in every lane), reset
+// column band partial built from 2-row stage sums: stage k (0..3) of the band
+template <int NQ>
+struct BandCols {
+  double a[NQ][2], b[NQ][2];
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) a[q][0] = a[q][1] = b[q][0] = b[q][1] = 0.0;
+  }
+  // st = o(row 2k) + o(row 2k+1) of this band
+  __device__ __forceinline__ void add(int k, const double (&st)[NQ][2]) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (k == 0) a[q][e] = st[q][e];
+        else if (k == 1) a[q][e] += st[q][e];
+        else if (k == 2) b[q][e] = st[q][e];
+        else b[q][e] += st[q][e];
+      }
+  }
+};
+
+// end of a band: band column partial into the tile partial, lane scalar partials
+// -> warp totals (identical in every lane); reset
 template <int NQ, int NS>
-__device__ __forceinline__ void band_close(double (&bacc)[NQ][2], double (&cacc)[NQ][2], double (&sacc)[NS],
+__device__ __forceinline__ void band_close(BandCols<NQ>& bc, double (&cacc)[NQ][2], double (&sacc)[NS],
                                            double (&ws)[NS]) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
-    cacc[q][0] += bacc[q][0];
-    cacc[q][1] += bacc[q][1];
-    bacc[q][0] = bacc[q][1] = 0.0;
+    cacc[q][0] += bc.a[q][0] + bc.b[q][0];
+    cacc[q][1] += bc.a[q][1] + bc.b[q][1];
   }
+  bc.reset();
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
-    double x = sacc[s];
-#pragma unroll
-    for (int msk = 16; msk >= 1; msk >>= 1) x += __shfl_xor_sync(0xffffffffu, x, msk);
-    ws[s] += x;
+    ws[s] += group_sum<32>(sacc[s]);
     sacc[s] = 0.0;
   }
 }
@@ -348,9 +371,11 @@ __device__ __forceinline__ void tile_pass(const Op& op, const Ctl& c, double* sm
   const Geo g = make_geo(c, worker, tu, tt);
   double* rowbuf = smem;                              // [TM][NQ][kWarps]
   double* sbuf = smem + (size_t)c.TM * NQ * kWarps;   // [kWarps][8]
-  double cacc[NQ][2], bacc[NQ][2];
+  double cacc[NQ][2];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = bacc[q][0] = bacc[q][1] = 0.0;
+  for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = 0.0;
+  BandCols<NQ> bcol;
+  bcol.reset();
   double sacc[NS], ws[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) sacc[s] = ws[s] = 0.0;
@@ -363,6 +388,7 @@ __device__ __forceinline__ void tile_pass(const Op& op, const Ctl& c, double* sm
     for (int rr = 0; rr < RB; ++rr)
       if (r0 + rr < g.rows && g.v0) op.load(fr[rr], g, g.i0 + r0 + rr);
     double rv[V];
+    double st[NQ][2];
 #pragma unroll
     for (int rr = 0; rr < RB; ++rr) {
       double o0[NQ], o1[NQ];
@@ -371,13 +397,19 @@ __device__ __forceinline__ void tile_pass(const Op& op, const Ctl& c, double* sm
       if (r0 + rr < g.rows && g.v0) op.compute(fr[rr], g, g.i0 + r0 + rr, cl, o0, o1, sacc);
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        bacc[q][0] += o0[q];
-        bacc[q][1] += o1[q];
+        if (rr & 1) {
+          st[q][0] += o0[q];
+          st[q][1] += o1[q];
+        } else {
+          st[q][0] = o0[q];
+          st[q][1] = o1[q];
+        }
         rv[rr * NQ + q] = o0[q] + o1[q];
       }
+      if (rr & 1) bcol.add(rr >> 1, st);
     }
     push_rows<NQ, RB>(rv, rowbuf, r0, worker);
-    band_close<NQ, NS>(bacc, cacc, sacc, ws);
+    band_close<NQ, NS>(bcol, cacc, sacc, ws);
   }
   tile_flush<NQ, NS>(c, g, worker, cacc, ws, rowbuf, sbuf);
 }

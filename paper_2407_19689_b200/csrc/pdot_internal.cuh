@@ -41,7 +41,7 @@ enum UnitFlag : uint32_t { U_ACT = 1, U_LDX = 2, U_LDA = 4, U_ZX = 8, U_ZA = 16 
 enum ScreenStat : int {
   ST_PASSES = 0,    // screened STEP passes
   ST_CELLS = 1,     // active cells processed by K1
-  ST_TILES = 2,     // units visited by K1
+  ST_TILES = 2,     // cells visited by K1 (active or stale-zeroing)
   ST_BYTES = 3,     // bytes K1 moved (cell loads/stores + tile partials)
   ST_META = 4,      // bytes K0 read/wrote (screen metadata)
   ST_K1_NS = 5,     // summed K1 durations (%globaltimer, first CTA start -> last CTA end)
@@ -186,19 +186,20 @@ struct Ctl {
   // ---- block screening (screen.cu; screen != 0: STEP / DIST / start-KKT passes run
   //      K0 screen + K1 unit walker, and K2 reduces per-unit partials) ----
   int32_t screen, nbt;       // nbt = bands per tile = TM / kBand
-  int64_t nbands, ncells, nstrips, nbw, mpad;  // nbw = 32-band words per strip
+  int64_t nbands, ncells, nstrips, mpad;
   const double* minc;        // [nbands][ncells]  min C over each cell (-inf if any entry is not finite)
   uint32_t* occ;             // [kNSlot][nbands][nstrips] per-cell "X has a nonzero bit pattern" bytes
   double* pmax;              // [kNSlot][nbands]  NaN-propagating max of p over each band
   double* qmax;              // [kNSlot][ncells]  ... of q over each cell (-inf for cells past n)
-  uint32_t* unitw;           // [nbands][nstrips] K0 -> K1 unit words (a flag byte per cell)
-  uint32_t* ulist;           // units K1 visits this pass (band * nstrips + strip)
+  uint32_t* unitw;           // [nbands][nstrips] K0 -> K1 flag words (a flag byte per cell)
+  uint32_t* ulist;           // cells K1 visits this pass: (band << 12) | cell
   unsigned int* ucount;      // length of ulist (K0 appends, K2 resets)
-  uint8_t* ubr;              // [nbands][U] bit w: unit (band, 8 u + w) wrote partials
-  uint32_t* ubc;             // [nstrips][nbw] bit b % 32: unit (b, strip) wrote partials (K0 sets, K2 clears)
-  double* ucol;              // [nbands][kMaxNQ][ldx]   unit column partials (band partial of the canonical tree)
-  double* urow;              // [nstrips][kMaxNQ][mpad] unit row partials (strip butterfly per row)
-  double* uscal;             // [nbands][nstrips][kMaxNS] unit scalars (band butterfly)
+  int64_t ncp;               // cells per row of cells, padded to whole tiles (U * 32)
+  uint32_t* bcr;             // [nbands][U]  bit k: cell k of column tile u wrote partials this pass
+  uint32_t* bct;             // [T][ncp]     bit b: band b of row tile t of this cell wrote partials
+  double* ccol;              // [nbands][kMaxNQ][ldx]  cell column partials (band partial of the tree)
+  double* crow;              // [ncp][kMaxNQ][mpad]   cell row partials (8-lane butterfly per row)
+  double* cscal;             // [nbands][ncp][kMaxNS] cell scalars
   unsigned long long* sstat; // [ST_COUNT]
   unsigned int* counter;   // last-block-done counter for the finalize kernel
   Status* status;          // host mapped
@@ -219,15 +220,18 @@ __device__ __forceinline__ void st_stream2(double* p, double2 v) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
-// Transposed butterfly: V independent per-lane values (V a power of two, <= 32)
-// are summed across the warp with one shuffle per value per halving step.
-// Afterwards lane L holds the total of value index L >> (5 - log2 V)
-// (transpose_owner_index); lanes with the low bits clear write it out
-// (transpose_is_writer).  Every sum follows the same fixed tree.
-template <int V>
+// Transposed butterfly over groups of W consecutive lanes, masks ASCENDING
+// (1, 2, ..., W/2): V independent per-lane values (V a power of two <= W) are
+// summed across the group with one shuffle per value per halving step.  The
+// first log2(V) steps route the values (transposition), the rest is a plain
+// butterfly on one value.  Afterwards lane L holds the group total of value
+// transpose_owner_index<V>(L); lanes with (L % W) < V hold distinct indices
+// (transpose_is_writer).  Ascending masks make the 32-lane tree the
+// composition of 8-lane (16-column cell) trees: ((c0 + c1) + (c2 + c3)).
+template <int V, int W = 32>
 __device__ __forceinline__ void warp_transpose_sum(double (&v)[V]) {
   const int lane = threadIdx.x & 31;
-  int mask = 16;
+  int mask = 1;
 #pragma unroll
   for (int w = V / 2; w >= 1; w /= 2) {
     const bool upper = (lane & mask) != 0;
@@ -237,25 +241,40 @@ __device__ __forceinline__ void warp_transpose_sum(double (&v)[V]) {
       const double keep = upper ? v[t + w] : v[t];
       v[t] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
     }
-    mask >>= 1;
+    mask <<= 1;
   }
 #pragma unroll
-  for (; mask >= 1; mask >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], mask);
+  for (; mask < W; mask <<= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], mask);
 }
 
-// value index held by `lane` after warp_transpose_sum<V>; valid for every lane
+template <int V>
+__device__ __forceinline__ constexpr int log2_pow2() {
+  return (V >= 32) ? 5 : (V >= 16) ? 4 : (V >= 8) ? 3 : (V >= 4) ? 2 : (V >= 2) ? 1 : 0;
+}
+
+// value index held by `lane` after warp_transpose_sum<V, W>: step k (mask 2^k)
+// kept the half selected by lane bit k, i.e. index bit (log2 V - 1 - k)
 template <int V>
 __device__ __forceinline__ int transpose_owner_index(int lane) {
-  // bits consumed: 16 -> V/2 ... ; index = lane >> (5 - log2 V)
-  constexpr int lg = (V >= 32) ? 5 : (V >= 16) ? 4 : (V >= 8) ? 3 : (V >= 4) ? 2 : (V >= 2) ? 1 : 0;
-  return lane >> (5 - lg);
+  constexpr int lg = log2_pow2<V>();
+  int idx = 0;
+#pragma unroll
+  for (int k = 0; k < lg; ++k) idx |= ((lane >> k) & 1) << (lg - 1 - k);
+  return idx;
 }
 
-// lane that writes value idx (the lowest lane holding it)
-template <int V>
+// one writer per value index in every group of W lanes
+template <int V, int W = 32>
 __device__ __forceinline__ bool transpose_is_writer(int lane) {
-  constexpr int lg = (V >= 32) ? 5 : (V >= 16) ? 4 : (V >= 8) ? 3 : (V >= 4) ? 2 : (V >= 2) ? 1 : 0;
-  return (lane & ((1 << (5 - lg)) - 1)) == 0;
+  return ((lane & (W - 1)) >> log2_pow2<V>()) == 0;
+}
+
+// xor butterfly of one value over groups of W lanes, masks ascending
+template <int W = 32>
+__device__ __forceinline__ double group_sum(double x) {
+#pragma unroll
+  for (int msk = 1; msk < W; msk <<= 1) x += __shfl_xor_sync(0xffffffffu, x, msk);
+  return x;
 }
 
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }

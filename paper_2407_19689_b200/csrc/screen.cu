@@ -31,7 +31,25 @@
 //       restart distance, unit calls, rounding) take the generic walker over
 //       all tiles.
 // K2 (finalize.cu) skips tiles whose flag is 0: their partials are +0.
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "pass_ops.cuh"
+
+#ifdef PDOT_DEVICE_CHECKS
+#define DCHECK(cond, tag, a, b)                                                                     \
+  do {                                                                                              \
+    if (!(cond)) {                                                                                  \
+      printf("DCHECK %s failed at %s:%d (%lld, %lld) block %d thread %d\n", tag, __FILE__, __LINE__, \
+             (long long)(a), (long long)(b), blockIdx.x, threadIdx.x);                              \
+      __trap();                                                                                     \
+    }                                                                                               \
+  } while (0)
+#else
+#define DCHECK(cond, tag, a, b) \
+  do {                          \
+  } while (0)
+#endif
 
 namespace pdot {
 namespace {
@@ -50,19 +68,25 @@ __device__ __forceinline__ bool step_with_avg(const Ctl& c) { return c.unit ? c.
 //         or a dual pair may violate it; stale output cells are flagged ZX/ZA.
 //   DIST: active where the candidate or the anchor has a nonzero.
 //   KKT:  active where X has a nonzero or the duals may violate.
+// Outputs: flag words, the list of cells K1 visits (active or stale), and the
+// bit maps K2 reads the cell partials by: bcr (per band and column tile) and
+// bct (per row tile and cell).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) screen_kernel(const Ctl* __restrict__ ctlp, int force_op) {
   const Ctl& c = *ctlp;
   if (c.done || !c.screen) return;
   const int op = force_op >= 0 ? force_op : c.op;
   if (!unit_pass(c, op)) return;
+  __shared__ uint32_t tilebits[32];  // per cell of the tile: bit bl = band bl active
   const int64_t tu = blockIdx.x, tt = blockIdx.y;
   const int s = threadIdx.x & 7, bl = threadIdx.x >> 3;  // strip in tile, band in tile
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) tilebits[threadIdx.x] = 0u;
   const bool with_avg = op == OP_STEP && step_with_avg(c);
   const int64_t band = tt * c.nbt + bl;
   const int64_t strip = tu * kWarps + s;
-  const bool valid = bl < c.nbt && band < c.nbands && strip < c.nstrips;
+  const bool inband = bl < c.nbt && band < c.nbands;
+  const bool valid = inband && strip < c.nstrips;
   uint32_t word = 0;
   if (valid) {
     const int64_t sstride = c.nbands * c.nstrips;
@@ -110,252 +134,345 @@ __global__ void __launch_bounds__(256) screen_kernel(const Ctl* __restrict__ ctl
       word |= f << (8 * k);
     }
     c.unitw[ow] = word;
-    if (word) c.ulist[atomicAdd(c.ucount, 1u)] = (uint32_t)ow;
   }
-  const bool parts = (word & 0x01010101u) != 0;  // the unit writes partials
-  if (parts) atomicOr(c.ubc + strip * c.nbw + (band >> 5), 1u << (band & 31));
-  const unsigned bal = __ballot_sync(0xffffffffu, parts);
-  // byte (band, tile column): bit s = strip 8 tu + s wrote partials
-  if (s == 0 && bl < c.nbt && band < c.nbands) c.ubr[band * c.U + tu] = (uint8_t)((bal >> (lane & 24)) & 0xffu);
+  // per-cell bits of this thread's strip: listed (any flag) and active (partials)
+  uint32_t listed = 0, actb = 0;
+#pragma unroll
+  for (int k = 0; k < kCellsPerStrip; ++k) {
+    const uint32_t f = (word >> (8 * k)) & 0xffu;
+    listed |= (f != 0u) << k;
+    actb |= ((f & U_ACT) != 0u) << k;
+  }
+  // warp-aggregated append of the listed cells
+  const int cnt = __popc(listed);
+  int incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned base = 0;
+  if (lane == 31 && total) base = atomicAdd(c.ucount, (unsigned)total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  unsigned pos = base + (unsigned)(incl - cnt);
+#pragma unroll
+  for (int k = 0; k < kCellsPerStrip; ++k)
+    if ((listed >> k) & 1u) c.ulist[pos++] = (uint32_t)((band << 12) | (strip * kCellsPerStrip + k));
+  // bcr[band][tu]: bit 4 s + k = cell k of strip s (8 lanes of one band)
+  uint32_t rbits = actb << (4 * s);
+#pragma unroll
+  for (int msk = 1; msk < 8; msk <<= 1) rbits |= __shfl_xor_sync(0xffffffffu, rbits, msk);
+  if (s == 0 && inband) c.bcr[band * c.U + tu] = rbits;
+  // bct[tt][cell]: bit bl = band bl of the tile
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kCellsPerStrip; ++k)
+    if ((actb >> k) & 1u) atomicOr(&tilebits[s * kCellsPerStrip + k], 1u << bl);
+  __syncthreads();
+  if (threadIdx.x < 32) c.bct[tt * c.ncp + tu * 32 + threadIdx.x] = tilebits[threadIdx.x];
 }
 
 // ---------------------------------------------------------------------------
-// K1: one warp per listed unit (8 rows x 64 columns; lane = column pair).
+// K1: one warp per listed cell (8 rows x 16 columns).  Lane = (row group rg =
+// lane / 8 holding rows 2 rg and 2 rg + 1, column pair cp = lane % 8), so all
+// 32 lanes carry elements.  The partials follow the canonical tree of
+// pass_ops.cuh: column band partial ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) via
+// pair sums and masks 8, 16; row values via the 8-lane butterfly; scalars as
+// the lane-sequential row chain (passed from row group to row group) and the
+// 8-lane butterfly.
 // ---------------------------------------------------------------------------
-struct UnitGeo {
-  int64_t band, strip, i0, j;
-  int rows;
+struct CellGeo {
+  int64_t band, cell, strip, i0, j;
+  int rows, k, rg, cp;
   bool v0, v1;
 };
 
-__device__ __forceinline__ UnitGeo unit_geo(const Ctl& c, uint32_t unit) {
+__device__ __forceinline__ CellGeo cell_geo(const Ctl& c, uint32_t entry) {
   const int lane = threadIdx.x & 31;
-  UnitGeo u;
-  u.band = unit / c.nstrips;
-  u.strip = unit - u.band * c.nstrips;
-  u.i0 = u.band * kBand;
-  u.rows = (int)imin64(kBand, c.m - u.i0);
-  u.j = u.strip * kStrip + lane * 2;
-  u.v0 = u.j < c.n;
-  u.v1 = u.j + 1 < c.n;
-  return u;
+  CellGeo g;
+  g.band = entry >> 12;
+  g.cell = entry & 0xfffu;
+  DCHECK(g.band < c.nbands, "band", g.band, c.nbands);
+  DCHECK(g.cell < c.ncells, "cell", g.cell, c.ncells);
+  g.strip = g.cell >> 2;
+  g.k = (int)(g.cell & 3);
+  g.i0 = g.band * kBand;
+  g.rows = (int)imin64(kBand, c.m - g.i0);
+  g.cp = lane & 7;
+  g.rg = lane >> 3;
+  g.j = g.cell * kCell + g.cp * 2;
+  g.v0 = g.j < c.n;
+  g.v1 = g.j + 1 < c.n;
+  return g;
 }
 
-// unit row partials of RB rows starting at r0: per-row strip butterflies
-template <int NQ, int RB>
-__device__ __forceinline__ void unit_rows(const Ctl& c, const UnitGeo& u, double (&rv)[RB * NQ], int r0) {
-  const int lane = threadIdx.x & 31;
-  constexpr int V = RB * NQ;
-  warp_transpose_sum<V>(rv);
-  if (transpose_is_writer<V>(lane)) {
-    const int idx = transpose_owner_index<V>(lane);
-    const int r = r0 + idx / NQ, q = idx % NQ;
-    if (r < u.rows) c.urow[(u.strip * kMaxNQ + q) * c.mpad + u.i0 + r] = rv[0];
-  }
-}
-
-// unit column partials (band partial of the canonical tree) and scalars (band butterfly)
+// Scalar chain + partial writes shared by every cell op.  o[rr][q][e]: the
+// lane's outputs for row 2 rg + rr, column e; ta/tb[rr][e][s]: the fma terms
+// (acc = fma(ta, tb, acc)) of each element, applied only where ok[rr][e].
 template <int NQ, int NS>
-__device__ __forceinline__ void unit_flush(const Ctl& c, const UnitGeo& u, const double (&bacc)[NQ][2],
-                                          double (&sacc)[NS]) {
-  const int lane = threadIdx.x & 31;
-  if (u.v0) {
+__device__ __forceinline__ void cell_flush(const Ctl& c, const CellGeo& g, const double (&o)[2][NQ][2],
+                                          const double (&ta)[2][2][NS], const double (&tb)[2][2][NS],
+                                          const bool (&ok)[2][2]) {
+  // column band partial: pair sum of the lane's two rows, then masks 8, 16
+  double2 cs[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    double x = o[0][q][0] + o[1][q][0], y = o[0][q][1] + o[1][q][1];
+    x += __shfl_xor_sync(0xffffffffu, x, 8);
+    y += __shfl_xor_sync(0xffffffffu, y, 8);
+    x += __shfl_xor_sync(0xffffffffu, x, 16);
+    y += __shfl_xor_sync(0xffffffffu, y, 16);
+    cs[q] = make_double2(x, y);
+  }
+  if (g.rg == 0 && g.v0) {
+    DCHECK(g.j + 1 < c.ldx, "ccol j", g.j, c.ldx);
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
-      *reinterpret_cast<double2*>(c.ucol + (u.band * kMaxNQ + q) * c.ldx + u.j) = make_double2(bacc[q][0], bacc[q][1]);
+      *reinterpret_cast<double2*>(c.ccol + (g.band * kMaxNQ + q) * c.ldx + g.j) = cs[q];
   }
+  // row values: 8-lane transposed butterfly over the column pairs
+  constexpr int V = 2 * NQ;
+  double rv[V];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    double x = sacc[s];
+  for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
-    for (int msk = 16; msk >= 1; msk >>= 1) x += __shfl_xor_sync(0xffffffffu, x, msk);
-    sacc[s] = x;
+    for (int q = 0; q < NQ; ++q) rv[rr * NQ + q] = o[rr][q][0] + o[rr][q][1];
+  warp_transpose_sum<V, 8>(rv);
+  if (transpose_is_writer<V, 8>(threadIdx.x & 31)) {
+    const int idx = transpose_owner_index<V>(g.cp);
+    const int r = 2 * g.rg + idx / NQ, q = idx % NQ;
+    DCHECK(g.cell < c.ncp && (r >= g.rows || g.i0 + r < c.mpad), "crow", g.cell, g.i0 + r);
+    if (r < g.rows) c.crow[(g.cell * kMaxNQ + q) * c.mpad + g.i0 + r] = rv[0];
   }
-  if (lane == 0) {
+  // scalars: the lane partial runs down the band row by row (row group 0..3)
+  double acc[NS];
 #pragma unroll
-    for (int s = 0; s < NS; ++s) c.uscal[(u.band * c.nstrips + u.strip) * kMaxNS + s] = sacc[s];
-  }
-}
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
-               "l"(gsrc)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
-
-// One STEP unit.  Every lane copies its own column pair of the active rows of
-// C, X and A into this warp's shared buffer with cp.async (all copies in
-// flight at once, no registers held), then computes from shared memory.
-template <bool IMPLICIT, bool AVG>
-__device__ __forceinline__ void unit_step(const StepOp& op, const Ctl& c, const CostGen& gen, uint32_t unit,
-                                          double2* wbuf, unsigned long long& bytes, unsigned long long& cells) {
-  constexpr int NQ = StepOp::NQ, NS = StepOp::NS, H = kBand / 2;
-  const int lane = threadIdx.x & 31;
-  const UnitGeo u = unit_geo(c, unit);
-  const uint32_t w = __ldcg(c.unitw + unit);
-  const uint32_t cb = (w >> ((lane >> 3) * 8)) & 0xffu;
-  const bool act = (cb & U_ACT) && u.v0;
-  const bool ldx = act && (cb & U_LDX);
-  const bool lda = AVG && act && (cb & U_LDA);
-  const bool zx = (cb & U_ZX) && u.v0;
-  const bool za = AVG && (cb & U_ZA) && u.v0;
-  if ((lane & 7) == 0 && (cb & U_ACT)) cells += 1;
-  double2* bc = wbuf + lane;                 // [3][kBand][32] double2, this lane's column
-  if (act) {
+  for (int s = 0; s < NS; ++s) acc[s] = 0.0;
 #pragma unroll
-    for (int r = 0; r < kBand; ++r) {
-      if (r < u.rows) {
-        const int64_t i = u.i0 + r;
-        if (!IMPLICIT) cp_async16(bc + (0 * kBand + r) * 32, op.C + i * c.ldc + u.j);
-        if (ldx) cp_async16(bc + (1 * kBand + r) * 32, op.X + i * c.ldx + u.j);
-        if (lda) cp_async16(bc + (2 * kBand + r) * 32, op.A + i * c.ldx + u.j);
+  for (int gi = 0; gi < 4; ++gi) {
+    if (g.rg == gi) {
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (ok[rr][e])
+#pragma unroll
+            for (int s = 0; s < NS; ++s) acc[s] = __fma_rn(ta[rr][e][s], tb[rr][e][s], acc[s]);
+    }
+    if (gi < 3) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const double t = __shfl_up_sync(0xffffffffu, acc[s], 8);
+        if (g.rg == gi + 1) acc[s] = t;
       }
     }
-    bytes += (unsigned long long)u.rows * ((IMPLICIT ? 0 : 16) + (ldx ? 16 : 0) + (lda ? 16 : 0));
   }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) acc[s] = group_sum<8>(acc[s]);
+  if ((threadIdx.x & 31) == 24) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) c.cscal[(g.band * c.ncp + g.cell) * kMaxNS + s] = acc[s];
+  }
+}
+
+template <bool IMPLICIT, bool AVG>
+__device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const CostGen& gen, uint32_t entry,
+                                          unsigned long long& bytes, unsigned long long& cells) {
+  constexpr int NQ = StepOp::NQ, NS = StepOp::NS;
+  const int lane = threadIdx.x & 31;
+  const CellGeo g = cell_geo(c, entry);
+  const uint32_t f = (__ldcg(c.unitw + g.band * c.nstrips + g.strip) >> (8 * g.k)) & 0xffu;
+  const bool act = (f & U_ACT) != 0;  // cell-uniform
+  const bool ldx = act && (f & U_LDX);
+  const bool lda = AVG && act && (f & U_LDA);
+  const bool zx = (f & U_ZX) != 0;
+  const bool za = AVG && (f & U_ZA) != 0;
+  if (lane == 0 && act) cells += 1;
   const double2 zero2 = make_double2(0.0, 0.0);
-  // duals: this lane's columns, and the band's rows broadcast from lanes 0..7
-  double q0 = 0.0, q1 = 0.0, qa0 = 0.0, qa1 = 0.0;
-  if (act) {
-    q0 = op.q[u.j]; qa0 = op.qa[u.j];
-    if (u.v1) { q1 = op.q[u.j + 1]; qa1 = op.qa[u.j + 1]; }
-  }
-  const bool prow = lane < u.rows;
-  const double pl = prow ? __ldg(op.p + u.i0 + lane) : 0.0;
-  const double pal = prow ? __ldg(op.pa + u.i0 + lane) : 0.0;
-  double2 cj0 = zero2, cj1 = zero2;
-  if (IMPLICIT) {
-    cj0 = gen.col_coord(u.j);
-    cj1 = gen.col_coord(u.j + 1);
-  }
-  double bacc[NQ][2];
+  double2 cc[2], xx[2], aa[2];
+  double pr[2], par[2];
+  bool okr[2];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) bacc[q][0] = bacc[q][1] = 0.0;
-  double sacc[NS];
+  for (int rr = 0; rr < 2; ++rr) {
+    const int r = 2 * g.rg + rr;
+    okr[rr] = act && r < g.rows && g.v0;
+    const int64_t i = g.i0 + r;
+    if (IMPLICIT) {
+      cc[rr] = zero2;
+    } else {
+      cc[rr] = okr[rr] ? ld_stream2(op.C + i * c.ldc + g.j) : zero2;
+    }
+    xx[rr] = (okr[rr] && ldx) ? ld_stream2(op.X + i * c.ldx + g.j) : zero2;
+    aa[rr] = (okr[rr] && lda) ? ld_stream2(op.A + i * c.ldx + g.j) : zero2;
+    pr[rr] = okr[rr] ? __ldg(op.p + i) : 0.0;
+    par[rr] = okr[rr] ? __ldg(op.pa + i) : 0.0;
+    if (okr[rr]) bytes += (IMPLICIT ? 0 : 16) + (ldx ? 16 : 0) + (lda ? 16 : 0);
+  }
+  double qv[2] = {0.0, 0.0}, qav[2] = {0.0, 0.0};
+  if (act && g.v0) {
+    qv[0] = op.q[g.j]; qav[0] = op.qa[g.j];
+    if (g.v1) { qv[1] = op.q[g.j + 1]; qav[1] = op.qa[g.j + 1]; }
+  }
+  if (IMPLICIT && act) {
+    const double2 c0 = gen.col_coord(g.j), c1 = gen.col_coord(g.j + 1);
 #pragma unroll
-  for (int s = 0; s < NS; ++s) sacc[s] = 0.0;
-  const bool parts = (w & 0x01010101u) != 0;  // warp-uniform: the unit writes partials
+    for (int rr = 0; rr < 2; ++rr) {
+      const double2 rc = gen.row_coord(g.i0 + 2 * g.rg + rr);
+      if (okr[rr]) cc[rr] = make_double2(gen.cost(rc, c0), gen.cost(rc, c1));
+    }
+  }
+  double o[2][NQ][2];
+  double ta[2][2][NS], tb[2][2][NS];
+  bool ok[2][2];
   bool nzx = false, nza = false;
-  cp_async_wait_all();  // each lane reads back only what it copied itself
-#pragma unroll 1
-  for (int h = 0; h < 2; ++h) {
-    double rv[H * NQ];
 #pragma unroll
-    for (int rr = 0; rr < H; ++rr) {
-      const int r = h * H + rr;
-      const bool inrow = r < u.rows;
-      const bool ok = act && inrow;
-      const int64_t i = u.i0 + r;
-      const double pi = __shfl_sync(0xffffffffu, pl, r), pai = __shfl_sync(0xffffffffu, pal, r);
-      double o0[NQ], o1[NQ];
+  for (int rr = 0; rr < 2; ++rr) {
+    const int r = 2 * g.rg + rr;
+    const bool inrow = r < g.rows && g.v0;
+    const int64_t i = g.i0 + r;
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) o0[q] = o1[q] = 0.0;
-      if (ok) {
-        double2 cc;
-        if (IMPLICIT) {
-          const double2 rc = gen.row_coord(i);
-          cc = make_double2(gen.cost(rc, cj0), gen.cost(rc, cj1));
-        } else {
-          cc = bc[(0 * kBand + r) * 32];
-        }
-        const double2 xx = ldx ? bc[(1 * kBand + r) * 32] : zero2;
-        const double2 aa = lda ? bc[(2 * kBand + r) * 32] : zero2;
-        op.template elem<AVG>(cc.x, xx.x, aa.x, pi, q0, pai, qa0, o0, sacc);
-        if (u.v1) op.template elem<AVG>(cc.y, xx.y, aa.y, pi, q1, pai, qa1, o1, sacc);
-      }
-      const double2 xo = make_double2(o0[2], o1[2]);
-      const bool nzr = nz2(xo);
-      nzx |= nzr;
-      if (inrow && (ok ? (zx || nzr) : zx)) {
-        st_stream2(op.Xn + i * c.ldx + u.j, xo);
+    for (int e = 0; e < 2; ++e) {
+      ok[rr][e] = okr[rr] && (e == 0 || g.v1);
+      const double cv = e ? cc[rr].y : cc[rr].x, x = e ? xx[rr].y : xx[rr].x, a = e ? aa[rr].y : aa[rr].x;
+      // StepOp::elem, expression by expression (pdhg.py:123-125, 315; kkt.py:70-71)
+      const double pq = pr[rr] + qv[e];
+      const double sres = cv - pq;
+      const double xn = relu_np(x - op.tau * sres);
+      const double d = xn - x;
+      const double ee = (xn + xn) - x;
+      const double vc = relu_np(pq - cv);
+      const double va = relu_np((par[rr] + qav[e]) - cv);
+      const double an = AVG ? a + div_by_count(x - a, op.kd, op.rkd) : 0.0;
+      const bool k_ = ok[rr][e];
+      o[rr][0][e] = k_ ? ee : 0.0;
+      o[rr][1][e] = k_ ? d : 0.0;
+      o[rr][2][e] = k_ ? xn : 0.0;
+      o[rr][3][e] = k_ ? an : 0.0;
+      ta[rr][e][0] = d;  tb[rr][e][0] = d;
+      ta[rr][e][1] = cv; tb[rr][e][1] = xn;
+      ta[rr][e][2] = cv; tb[rr][e][2] = an;
+      ta[rr][e][3] = xn; tb[rr][e][3] = xn;
+      ta[rr][e][4] = vc; tb[rr][e][4] = vc;
+      ta[rr][e][5] = va; tb[rr][e][5] = va;
+    }
+    const double2 xo = make_double2(o[rr][2][0], o[rr][2][1]);
+    const bool nzr = nz2(xo);
+    nzx |= nzr;
+    if (inrow && (okr[rr] ? (zx || nzr) : zx)) {
+      st_stream2(op.Xn + i * c.ldx + g.j, xo);
+      bytes += 16;
+    }
+    if (AVG) {
+      const double2 ao = make_double2(o[rr][3][0], o[rr][3][1]);
+      const bool nar = nz2(ao);
+      nza |= nar;
+      if (inrow && (okr[rr] ? (za || nar) : za)) {
+        st_stream2(op.An + i * c.ldx + g.j, ao);
         bytes += 16;
       }
-      if (AVG) {
-        const double2 ao = make_double2(o0[3], o1[3]);
-        const bool nar = nz2(ao);
-        nza |= nar;
-        if (inrow && (ok ? (za || nar) : za)) {
-          st_stream2(op.An + i * c.ldx + u.j, ao);
-          bytes += 16;
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        bacc[q][0] += o0[q];
-        bacc[q][1] += o1[q];
-        rv[rr * NQ + q] = o0[q] + o1[q];
-      }
     }
-    if (parts) unit_rows<NQ, H>(c, u, rv, h * H);
   }
-  __syncwarp();  // the buffer is reused by this warp's next unit
-  // occupancy of the unit's 4 output cells (bit patterns, so -0.0 counts)
-  const unsigned mx = __ballot_sync(0xffffffffu, nzx);
-  const unsigned ma = __ballot_sync(0xffffffffu, nza);
+  // occupancy bytes of the cell in the two output slots
+  const bool anyx = __any_sync(0xffffffffu, nzx), anya = __any_sync(0xffffffffu, nza);
   if (lane == 0) {
-    uint32_t wx = 0, wa = 0;
-#pragma unroll
-    for (int k = 0; k < kCellsPerStrip; ++k) {
-      wx |= ((mx >> (8 * k)) & 0xffu) ? (1u << (8 * k)) : 0u;
-      wa |= ((ma >> (8 * k)) & 0xffu) ? (1u << (8 * k)) : 0u;
-    }
     const int64_t sstride = c.nbands * c.nstrips;
-    c.occ[c.sXn * sstride + unit] = wx;
-    if (AVG) c.occ[c.sA * sstride + unit] = wa;
+    uint8_t* ox = reinterpret_cast<uint8_t*>(c.occ + c.sXn * sstride + g.band * c.nstrips + g.strip);
+    ox[g.k] = anyx ? 1 : 0;
+    if (AVG) {
+      uint8_t* oa = reinterpret_cast<uint8_t*>(c.occ + c.sA * sstride + g.band * c.nstrips + g.strip);
+      oa[g.k] = anya ? 1 : 0;
+    }
   }
-  if (parts) {
-    unit_flush<NQ, NS>(c, u, bacc, sacc);
-    if (lane == 0) bytes += (unsigned long long)(2 * NQ * kStrip + NQ * kBand + NS) * 8;
+  if (act) {
+    if (!AVG) {  // no average this pass: its terms are not accumulated
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) ta[rr][e][2] = tb[rr][e][2] = 0.0;
+    }
+    cell_flush<NQ, NS>(c, g, o, ta, tb, ok);
+    if (lane == 0) bytes += (unsigned long long)(NQ * kCell + NQ * kBand + NS) * 8 * 2;
   }
 }
 
-// the NQ = 1 ops through the screen: restart distance and the start KKT
-template <class Op>
-__device__ __noinline__ void unit_generic(const Op& op, const Ctl& c, uint32_t unit, unsigned long long& bytes,
-                                          unsigned long long& cells) {
-  constexpr int NQ = Op::NQ, NS = Op::NS;
-  static_assert(NQ == 1 && Op::RB == kBand, "unit_generic handles the one-quantity ops");
+// restart distance (DIST) and the start KKT through the screen (NQ = 1)
+template <int OPK>
+__device__ __forceinline__ void cell_one(const Ctl& c, uint32_t entry, unsigned long long& bytes,
+                                         unsigned long long& cells) {
+  constexpr int NQ = 1, NS = (OPK == OP_DIST) ? 1 : 3;
   const int lane = threadIdx.x & 31;
-  const UnitGeo u = unit_geo(c, unit);
-  const uint32_t w = __ldcg(c.unitw + unit);
-  const uint32_t cb = (w >> ((lane >> 3) * 8)) & 0xffu;
-  const bool act = (cb & U_ACT) && u.v0;
-  if ((lane & 7) == 0 && (cb & U_ACT)) cells += 1;
-  Geo g;  // the fields the ops read
-  g.m = c.m; g.n = c.n; g.ldc = c.ldc; g.ldx = c.ldx; g.TM = c.TM;
-  g.tu = 0; g.tt = 0; g.i0 = u.i0; g.rows = u.rows; g.j = u.j;
-  g.v0 = act;
-  g.v1 = act && u.v1;
-  g.gen.kind = c.C ? 0 : c.cost_kind;
-  g.gen.a0 = c.cost_a[0]; g.gen.a1 = c.cost_a[1]; g.gen.a2 = c.cost_a[2]; g.gen.a3 = c.cost_a[3];
-  g.gen.row0 = c.row0;
-  typename Op::Col cl;
-  op.load_col(cl, g);
-  typename Op::Frag fr[kBand];
-#pragma unroll
-  for (int r = 0; r < kBand; ++r)
-    if (act && r < u.rows) op.load(fr[r], g, u.i0 + r);
-  double bacc[NQ][2] = {{0.0, 0.0}};
-  double sacc[NS];
-#pragma unroll
-  for (int s = 0; s < NS; ++s) sacc[s] = 0.0;
-  double rv[kBand * NQ];
-#pragma unroll
-  for (int r = 0; r < kBand; ++r) {
-    double o0[NQ] = {0.0}, o1[NQ] = {0.0};
-    if (act && r < u.rows) op.compute(fr[r], g, u.i0 + r, cl, o0, o1, sacc);
-    bacc[0][0] += o0[0];
-    bacc[0][1] += o1[0];
-    rv[r] = o0[0] + o1[0];
+  const CellGeo g = cell_geo(c, entry);
+  const uint32_t f = (__ldcg(c.unitw + g.band * c.nstrips + g.strip) >> (8 * g.k)) & 0xffu;
+  const bool act = (f & U_ACT) != 0;
+  if (lane == 0 && act) cells += 1;
+  if (!act) return;
+#ifdef DBG_SKIP_CELL_ONE
+  return;
+#endif
+  const double2 zero2 = make_double2(0.0, 0.0);
+  CostGen gen;
+  gen.kind = c.C ? 0 : c.cost_kind;
+  gen.a0 = c.cost_a[0]; gen.a1 = c.cost_a[1]; gen.a2 = c.cost_a[2]; gen.a3 = c.cost_a[3];
+  gen.row0 = c.row0;
+  const Slot& sx = c.slot[c.sX];
+  double o[2][NQ][2];
+  double ta[2][2][NS], tb[2][2][NS];
+  bool ok[2][2];
+  double q0 = 0.0, q1 = 0.0;
+  if (OPK == OP_KKT && g.v0) {
+    q0 = sx.q[g.j];
+    if (g.v1) q1 = sx.q[g.j + 1];
   }
-  if (act) bytes += 32 * (unsigned long long)u.rows;
-  if (w & 0x01010101u) {
-    unit_rows<NQ, kBand>(c, u, rv, 0);
-    unit_flush<NQ, NS>(c, u, bacc, sacc);
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int r = 2 * g.rg + rr;
+    const bool okr = r < g.rows && g.v0;
+    const int64_t i = g.i0 + r;
+    double2 xa = zero2, xb = zero2, cv = zero2;
+    double p = 0.0;
+#ifdef DBG_SKIP_LOADS
+    if (false) {
+#else
+    if (okr) {
+#endif
+      DCHECK(i < c.m && g.j + 1 < c.ldx, "cell_one ld", i, g.j);
+      if (OPK == OP_DIST) {
+        xa = ld_stream2(c.slot[c.sZ].X + i * c.ldx + g.j);
+        xb = ld_stream2(c.slot[c.sCand].X + i * c.ldx + g.j);
+      } else {
+        xb = ld_stream2(sx.X + i * c.ldx + g.j);
+        if (c.C) {
+          cv = ld_stream2(c.C + i * c.ldc + g.j);
+        } else if (gen.kind > 0) {
+          const double2 rc = gen.row_coord(i);
+          cv = make_double2(gen.cost(rc, gen.col_coord(g.j)), gen.cost(rc, gen.col_coord(g.j + 1)));
+        }
+        p = __ldg(sx.p + i);
+      }
+      bytes += 32;
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      ok[rr][e] = okr && (e == 0 || g.v1);
+      const double b = e ? xb.y : xb.x;
+      if (OPK == OP_DIST) {  // DiffOp: d = X_b - X_a
+        const double d = b - (e ? xa.y : xa.x);
+        o[rr][0][e] = ok[rr][e] ? d : 0.0;
+        ta[rr][e][0] = d; tb[rr][e][0] = d;
+      } else {  // KktOp: <C,X>, |[p+q-C]^+|^2, |X|^2
+        const double cc = e ? cv.y : cv.x;
+        const double v = relu_np((p + (e ? q1 : q0)) - cc);
+        o[rr][0][e] = ok[rr][e] ? b : 0.0;
+        ta[rr][e][0] = cc; tb[rr][e][0] = b;
+        ta[rr][e][1] = v;  tb[rr][e][1] = v;
+        ta[rr][e][2] = b;  tb[rr][e][2] = b;
+      }
+    }
   }
+#ifndef DBG_SKIP_FLUSH
+  cell_flush<NQ, NS>(c, g, o, ta, tb, ok);
+#endif
 }
 
 __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const Ctl* __restrict__ ctlp, int force_op) {
@@ -364,10 +481,9 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
   const int op = force_op >= 0 ? force_op : c.op;
   if (!unit_pass(c, op)) return;
   __shared__ unsigned long long red[2][kWarps];
-  extern __shared__ __align__(128) unsigned char smem_raw[];
   if (blockIdx.x == 0 && threadIdx.x == 0) c.sstat[ST_T0] = globaltimer_ns();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned nunits = __ldcg(c.ucount);
+  const unsigned ncells = __ldcg(c.ucount);
   const unsigned gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
   unsigned long long bytes = 0, cells = 0;
   if (op == OP_STEP) {
@@ -376,26 +492,20 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
     gen.kind = c.C ? 0 : c.cost_kind;
     gen.a0 = c.cost_a[0]; gen.a1 = c.cost_a[1]; gen.a2 = c.cost_a[2]; gen.a3 = c.cost_a[3];
     gen.row0 = c.row0;
-    double2* wbuf = reinterpret_cast<double2*>(smem_raw) + warp * (3 * kBand * 32);
-    for (unsigned k = gw; k < nunits; k += nw) {
-      const uint32_t unit = __ldcg(c.ulist + k);
+    for (unsigned k = gw; k < ncells; k += nw) {
+      const uint32_t entry = __ldcg(c.ulist + k);
       if (o.C) {
-        if (o.with_avg) unit_step<false, true>(o, c, gen, unit, wbuf, bytes, cells);
-        else unit_step<false, false>(o, c, gen, unit, wbuf, bytes, cells);
+        if (o.with_avg) cell_step<false, true>(o, c, gen, entry, bytes, cells);
+        else cell_step<false, false>(o, c, gen, entry, bytes, cells);
       } else {
-        if (o.with_avg) unit_step<true, true>(o, c, gen, unit, wbuf, bytes, cells);
-        else unit_step<true, false>(o, c, gen, unit, wbuf, bytes, cells);
+        if (o.with_avg) cell_step<true, true>(o, c, gen, entry, bytes, cells);
+        else cell_step<true, false>(o, c, gen, entry, bytes, cells);
       }
     }
   } else if (op == OP_DIST) {
-    DiffOp o;
-    o.Xa = c.slot[c.sZ].X; o.Xb = c.slot[c.sCand].X;
-    for (unsigned k = gw; k < nunits; k += nw) unit_generic(o, c, __ldcg(c.ulist + k), bytes, cells);
+    for (unsigned k = gw; k < ncells; k += nw) cell_one<OP_DIST>(c, __ldcg(c.ulist + k), bytes, cells);
   } else {
-    KktOp o;
-    const Slot& sx = c.slot[c.sX];
-    o.C = c.C; o.X = sx.X; o.p = sx.p; o.q = sx.q; o.viol = nullptr;
-    for (unsigned k = gw; k < nunits; k += nw) unit_generic(o, c, __ldcg(c.ulist + k), bytes, cells);
+    for (unsigned k = gw; k < ncells; k += nw) cell_one<OP_KKT>(c, __ldcg(c.ulist + k), bytes, cells);
   }
   // statistics: one atomic per CTA, then the last CTA stamps the end time
 #pragma unroll
@@ -422,9 +532,9 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
       const unsigned long long t1 = globaltimer_ns();
       if (op == OP_STEP) {
         c.sstat[ST_K1_NS] += t1 - __ldcg(&c.sstat[ST_T0]);
-        c.sstat[ST_TILES] += nunits;
+        c.sstat[ST_TILES] += ncells;
         c.sstat[ST_PASSES] += 1;
-        // K0 metadata traffic of this pass: min C + 4 occupancy words + unit word per (band, strip)
+        // K0 metadata traffic of this pass: min C + 4 occupancy words + flag word per (band, strip)
         c.sstat[ST_META] += (unsigned long long)c.nbands * c.nstrips * (kCellsPerStrip * 8 + 4 * 4 + 4);
       }
       c.sstat[ST_DONE1] = 0;
@@ -512,11 +622,8 @@ __global__ void bounds_kernel(const double* __restrict__ p, const double* __rest
 
 }  // namespace
 
-constexpr size_t kUnitSmem = (size_t)kWarps * 3 * kBand * 32 * sizeof(double2);  // 96 KB
-
 void prepare_sparse_kernel() {
   cudaFuncSetAttribute(generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  cudaFuncSetAttribute(unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUnitSmem);
 }
 
 static size_t generic_smem_bytes(int64_t TM) {
@@ -530,8 +637,15 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
   // graph passes (force_op < 0) are STEP / DIST / start-KKT; unit calls choose on the host
   if (force_op < 0 || unit_pass(h, force_op)) {
     dim3 g0((unsigned)h.U, (unsigned)h.T);
-    screen_kernel<<<g0, (unsigned)(kWarps * h.nbt), 0, s>>>(ctl_dev, force_op);
-    unit_kernel<<<(unsigned)(sms * kSparseCtasPerSm), kThreads, kUnitSmem, s>>>(ctl_dev, force_op);
+    // thread (band, strip) of the tile; at least one full warp (the append and
+    // the bit maps use warp shuffles)
+    const unsigned threads = (unsigned)(kWarps * h.nbt < 32 ? 32 : kWarps * h.nbt);
+    screen_kernel<<<g0, threads, 0, s>>>(ctl_dev, force_op);
+    if (getenv("PDOT_DEBUG_SYNC")) {
+      const cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) fprintf(stderr, "screen_kernel failed: %s\n", cudaGetErrorString(e));
+    }
+    unit_kernel<<<(unsigned)(sms * kSparseCtasPerSm), kThreads, 0, s>>>(ctl_dev, force_op);
   } else {
     const unsigned grid = (unsigned)imin64(h.T * h.U, (int64_t)sms * 2);
     generic_kernel<<<grid, kThreads, generic_smem_bytes(h.TM), s>>>(ctl_dev, force_op);

@@ -278,14 +278,29 @@ int launch_k1(pdot_solver* h, int op) {
     pdot::launch_screened_pass(h->dev, h->host, op, h->stream);
     return (op < 0 || pdot::unit_pass(h->host, op)) ? 2 : 1;
   }
+  // (dense walker below)
   pdot::launch_stream_pass(h->dev, h->host, op, h->stream);
   return 1;
 }
 
+// PDOT_DEBUG_SYNC=1: synchronise after K1 and K2 of every non-graph pass and
+// name the failing one (debugging aid; never set in measurements)
+int debug_sync(pdot_solver* h, const char* what) {
+  static const bool on = getenv("PDOT_DEBUG_SYNC") && atoi(getenv("PDOT_DEBUG_SYNC")) != 0;
+  if (!on) return PDOT_OK;
+  cudaStreamCaptureStatus cs;
+  if (cudaStreamIsCapturing(h->stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) return PDOT_OK;
+  const cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(e, what, __LINE__);
+  return PDOT_OK;
+}
+
 int launch_pass(pdot_solver* h, int op) {
   h->launches += launch_k1(h, op);
+  if (int rc = debug_sync(h, "K1 of a pass")) return rc;
   if (!split_mode(h)) {
     pdot::launch_finalize_pass(h->dev, h->host, op, pdot::FIN_FUSED, h->stream);
+    if (int rc = debug_sync(h, "K2 of a pass")) return rc;
     h->launches += 1;
   } else {
     pdot::launch_finalize_pass(h->dev, h->host, op, pdot::FIN_A, h->stream);
@@ -592,22 +607,23 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     const size_t o_pmax = take(pdot::kNSlot * nbands * sizeof(double));
     const size_t o_qmax = take(pdot::kNSlot * ncells * sizeof(double));
     const int64_t nunits = nbands * nstrips;
-    const int64_t nbw = (nbands + 31) / 32;
+    const int64_t ncp = h->U * 32;  // cells per band, padded to whole tiles
     const int64_t mpad = round_up(m, 2);
     const size_t o_unit = take(nunits * sizeof(uint32_t));
-    const size_t o_ulist = take(nunits * sizeof(uint32_t));
+    const size_t o_ulist = take(nbands * ncp * sizeof(uint32_t));
     const size_t o_ucount = take(sizeof(unsigned));
-    const size_t o_ubr = take(nbands * h->U);
-    const size_t o_ubc = take(nstrips * nbw * sizeof(uint32_t));
+    const size_t o_bcr = take(nbands * h->U * sizeof(uint32_t));
+    const size_t o_bct = take(h->T * ncp * sizeof(uint32_t));
     const size_t o_stat = take(pdot::ST_COUNT * sizeof(unsigned long long));
-    // unit partials of screened passes (written sparsely; ~1 GB at 16384^2)
-    const size_t o_ucol = take(nbands * pdot::kMaxNQ * h->ldx * sizeof(double));
-    const size_t o_urow = take(nstrips * pdot::kMaxNQ * mpad * sizeof(double));
-    const size_t o_uscal = take(nunits * pdot::kMaxNS * sizeof(double));
+    // cell partials of screened passes (written sparsely, read back only where
+    // the bit maps say so: never zeroed)
+    const size_t o_ccol = take(nbands * pdot::kMaxNQ * h->ldx * sizeof(double));
+    const size_t o_crow = take(ncp * pdot::kMaxNQ * mpad * sizeof(double));
+    const size_t o_cscal = take(nbands * ncp * pdot::kMaxNS * sizeof(double));
     (void)tiles;
     char* base = nullptr;
     // only the metadata needs zeroing; the unit partials are written before they are read
-    if ((e = cudaMalloc(&base, off)) != cudaSuccess || (e = cudaMemsetAsync(base, 0, o_ucol, h->stream)) != cudaSuccess) {
+    if ((e = cudaMalloc(&base, off)) != cudaSuccess || (e = cudaMemsetAsync(base, 0, o_ccol, h->stream)) != cudaSuccess) {
       int rc = cuda_fail(e, "pdot_create screening metadata", __LINE__);
       pdot_destroy(h);
       return rc;
@@ -625,13 +641,13 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     c.unitw = reinterpret_cast<uint32_t*>(base + o_unit);
     c.ulist = reinterpret_cast<uint32_t*>(base + o_ulist);
     c.ucount = reinterpret_cast<unsigned*>(base + o_ucount);
-    c.ubr = reinterpret_cast<uint8_t*>(base + o_ubr);
-    c.ubc = reinterpret_cast<uint32_t*>(base + o_ubc);
     c.sstat = reinterpret_cast<unsigned long long*>(base + o_stat);
-    c.ucol = reinterpret_cast<double*>(base + o_ucol);
-    c.urow = reinterpret_cast<double*>(base + o_urow);
-    c.uscal = reinterpret_cast<double*>(base + o_uscal);
-    c.nbw = nbw;
+    c.bcr = reinterpret_cast<uint32_t*>(base + o_bcr);
+    c.bct = reinterpret_cast<uint32_t*>(base + o_bct);
+    c.ccol = reinterpret_cast<double*>(base + o_ccol);
+    c.crow = reinterpret_cast<double*>(base + o_crow);
+    c.cscal = reinterpret_cast<double*>(base + o_cscal);
+    c.ncp = ncp;
     c.mpad = mpad;
     const char* env = getenv("PDOT_SCREEN");
     h->screen_on = !(env && atoi(env) == 0);

@@ -117,9 +117,11 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
   }
   __syncthreads();
 
-  double cacc[NQ][2], bacc[NQ][2];
+  double cacc[NQ][2];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = bacc[q][0] = bacc[q][1] = 0.0;
+  for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = 0.0;
+  BandCols<NQ> bcol;
+  bcol.reset();
   double sacc[NS], ws[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) sacc[s] = ws[s] = 0.0;
@@ -171,6 +173,7 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
         mbar_wait(&full[s], (it / kStages) & 1);
         const unsigned char* st = stages + s * kStageBytes;
         double rv[R * NQ];
+        double ps[NQ][2];  // 2-row stage sum of the column band partial
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
           double2 cc;
@@ -193,15 +196,21 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
           ao += c.ldx;
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
-            bacc[q][0] += o0[q];
-            bacc[q][1] += o1[q];
+            if (rr == 0) {
+              ps[q][0] = o0[q];
+              ps[q][1] = o1[q];
+            } else {
+              ps[q][0] += o0[q];
+              ps[q][1] += o1[q];
+            }
             rv[rr * NQ + q] = o0[q] + o1[q];
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         push_rows<NQ, R>(rv, rowbuf, it * R, true);
-        if ((it % kStagesPerBand) == kStagesPerBand - 1 || it == nst - 1) band_close<NQ, NS>(bacc, cacc, sacc, ws);
+        bcol.add(it % kStagesPerBand, ps);
+        if ((it % kStagesPerBand) == kStagesPerBand - 1 || it == nst - 1) band_close<NQ, NS>(bcol, cacc, sacc, ws);
       }
     } else {
       for (int it = 0; it < nst; ++it) {
@@ -209,6 +218,7 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
         mbar_wait(&full[s], (it / kStages) & 1);
         const unsigned char* st = stages + s * kStageBytes;
         double rv[R * NQ];
+        double ps[NQ][2];  // 2-row stage sum of the column band partial
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
           const int r = it * R + rr;
@@ -232,15 +242,21 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
           }
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
-            bacc[q][0] += o0[q];
-            bacc[q][1] += o1[q];
+            if (rr == 0) {
+              ps[q][0] = o0[q];
+              ps[q][1] = o1[q];
+            } else {
+              ps[q][0] += o0[q];
+              ps[q][1] += o1[q];
+            }
             rv[rr * NQ + q] = o0[q] + o1[q];
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         push_rows<NQ, R>(rv, rowbuf, it * R, true);
-        if ((it % kStagesPerBand) == kStagesPerBand - 1 || it == nst - 1) band_close<NQ, NS>(bacc, cacc, sacc, ws);
+        bcol.add(it % kStagesPerBand, ps);
+        if ((it % kStagesPerBand) == kStagesPerBand - 1 || it == nst - 1) band_close<NQ, NS>(bcol, cacc, sacc, ws);
       }
     }
   }
