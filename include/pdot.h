@@ -231,13 +231,15 @@ int64_t pdot_kernel_launches(const pdot_solver* h);
 /* ---- block screening of the STEP pass (csrc/screen.cu) ----
  * Same results bit for bit (pdhg.py:121-129 / kkt.py:56-94 arithmetic is
  * unchanged); the pass only skips 8 x 16 cells whose every output and every
- * reduction term is exactly +0.  On by default (PDOT_SCREEN=0 disables it for
- * new handles); toggling rebuilds the min-C table and rescans the slots. */
+ * reduction term is exactly +0.  On by default from 2^22 plan entries
+ * (PDOT_SCREEN=0/1 forces it for new handles); toggling rebuilds the min-C
+ * table and rescans the slots. */
 int pdot_set_screening(pdot_solver* h, int on);
-/* Counters since the last reset: out8 = {screened passes, active cells, tiles
- * visited, bytes moved by K1, K0 metadata bytes, summed K1 ns (%globaltimer),
- * screening on, cells per plan}. */
-int pdot_screen_stats(pdot_solver* h, int reset, unsigned long long* out8);
+/* Counters since the last reset: out12 = {screened STEP passes, active cells,
+ * cells visited, bytes moved by K1, K0 metadata bytes, summed K1 ns
+ * (%globaltimer), screening on, cells per plan, summed K2 ns up to the last
+ * block, summed K2 controller-tail ns, controller reduce / decide / publish ns}. */
+int pdot_screen_stats(pdot_solver* h, int reset, unsigned long long* out16);
 
 #ifdef __cplusplus
 }

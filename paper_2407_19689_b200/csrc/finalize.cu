@@ -49,6 +49,20 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* red /* [kWarps
   __syncthreads();
 }
 
+// sum of count values at p[0], p[stride], ... in order; loads issued 8 at a time
+__device__ __forceinline__ double seq_sum(const double* p, int64_t stride, int64_t count) {
+  double acc = 0.0;
+  for (int64_t k0 = 0; k0 < count; k0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = (k0 + k < count) ? __ldcg(p + (k0 + k) * stride) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k0 + k < count) acc += v[k];
+  }
+  return acc;
+}
+
 __device__ __forceinline__ double pair8(const double* g) {
   return ((g[0] + g[1]) + (g[2] + g[3])) + ((g[4] + g[5]) + (g[6] + g[7]));
 }
@@ -113,216 +127,45 @@ __device__ void wait_exchange(Ctl& c) {
 // ---------------------------------------------------------------------------
 // Sum of the column partials of reduction group g over its row tiles, in tile
 // order: the within-group order that every GPU count reproduces.
-// ---------------------------------------------------------------------------
-// screened passes: tile partials rebuilt from the cell partials of K1 in the
-// canonical order (pass_ops.cuh); loads are batched so each step waits once
-// ---------------------------------------------------------------------------
-// next (up to) 4 set bits of m, lowest first
-__device__ __forceinline__ int take4(uint32_t& m, int (&bb)[4]) {
-  int cnt = 0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    bb[k] = 0;
-    if (m) {
-      bb[k] = __ffs(m) - 1;
-      m &= m - 1;
-      cnt = k + 1;
-    }
-  }
-  return cnt;
-}
-
-// column sums of the tiles [ta, tb) (global tile indices) for the lane's column
-// pair: tile partial = its active bands' cell partials in band order.  The
-// active (tile, band) pairs are scanned from the bit maps in registers and their
-// partials loaded 4 at a time, so the lane waits once per 4 active bands.
 template <int NQ>
-__device__ __forceinline__ void group_column_sum_units(const Ctl& c, int64_t ta, int64_t tb, int64_t j,
-                                                       double2 (&acc)[NQ]) {
-  if (j >= c.n) return;
-  const int64_t cell = j / kCell;
-  for (int64_t tc = ta; tc < tb; tc += 16) {
-    uint32_t mw[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) mw[k] = (tc + k < tb) ? __ldcg(c.bct + (tc + k - c.t0) * c.ncp + cell) : 0u;
-    double2 tacc[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) tacc[q] = make_double2(0.0, 0.0);
-    int cur = -1;  // tile (within the chunk) tacc belongs to
-    int k = 0;     // tile being scanned
-    while (true) {
-      // next up to 4 active (tile, band) pairs in order
-      int tk[4], bb[4], cnt = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        tk[e] = 0;
-        bb[e] = 0;
-        while (k < 16 && mw[k] == 0u) ++k;
-        if (k < 16) {
-          tk[e] = k;
-          bb[e] = __ffs(mw[k]) - 1;
-          mw[k] &= mw[k] - 1;
-          cnt = e + 1;
-        }
-      }
-      if (cnt == 0) break;
-      double2 v[4][NQ];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t band = (tc + tk[e] - c.t0) * c.nbt + bb[e];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q)
-          v[e][q] = e < cnt ? __ldcg(reinterpret_cast<const double2*>(c.ccol + (band * kMaxNQ + q) * c.ldx + j))
-                            : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if (e < cnt) {
-          if (tk[e] != cur) {  // a new tile: close the previous tile's partial
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-              acc[q].x += tacc[q].x;
-              acc[q].y += tacc[q].y;
-              tacc[q] = make_double2(0.0, 0.0);
-            }
-            cur = tk[e];
-          }
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) {
-            tacc[q].x += v[e][q].x;
-            tacc[q].y += v[e][q].y;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      acc[q].x += tacc[q].x;
-      acc[q].y += tacc[q].y;
-    }
-  }
-}
-
-// row sums of row i: per column tile, the strip values ((c0+c1)+(c2+c3)) of the
-// active cells summed in strip order; the active strips are scanned from the
-// bit maps in registers and loaded two at a time
-template <int NQ>
-__device__ __forceinline__ void row_sums_units(const Ctl& c, int64_t i, double (&row)[NQ]) {
-  const uint32_t* bits = c.bcr + (i / kBand) * c.U;
-  for (int64_t uc = 0; uc < c.U; uc += 32) {
-    uint32_t wv[32];
-#pragma unroll
-    for (int k = 0; k < 32; ++k) wv[k] = (uc + k < c.U) ? __ldcg(bits + uc + k) : 0u;
-    double a[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) a[q] = 0.0;
-    int cur = -1;  // column tile a[] belongs to
-    int k = 0;
-    while (true) {
-      int uk[2], ww[2], nib[2], cnt = 0;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        uk[e] = 0;
-        ww[e] = 0;
-        nib[e] = 0;
-        while (k < 32 && wv[k] == 0u) ++k;
-        if (k < 32) {
-          const int w = (__ffs(wv[k]) - 1) >> 2;  // next active strip of this column tile
-          uk[e] = k;
-          ww[e] = w;
-          nib[e] = (wv[k] >> (4 * w)) & 0xf;
-          wv[k] &= ~(0xfu << (4 * w));
-          cnt = e + 1;
-        }
-      }
-      if (cnt == 0) break;
-      double v[2][4][NQ];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int64_t cb = (uc + uk[e]) * 32 + 4 * ww[e];
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int q = 0; q < NQ; ++q)
-            v[e][x][q] = (e < cnt && ((nib[e] >> x) & 1)) ? __ldcg(c.crow + ((cb + x) * kMaxNQ + q) * c.mpad + i) : 0.0;
-      }
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        if (e < cnt) {
-          if (uk[e] != cur) {  // next column tile: its partial joins the row in tile order
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-              row[q] += a[q];
-              a[q] = 0.0;
-            }
-            cur = uk[e];
-          }
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) a[q] += (v[e][0][q] + v[e][1][q]) + (v[e][2][q] + v[e][3][q]);
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) row[q] += a[q];
-  }
-}
-
-// scalar pieces of tile t, column tile u, strip w: the strip's band-ordered sum
-// of its strip-band values ((c0+c1)+(c2+c3))
-template <int NS>
-__device__ __forceinline__ void strip_scalars_units(const Ctl& c, int64_t t, int64_t u, int w, double (&ws)[NS]) {
-  const int64_t b0 = t * c.nbt;
-  const int nb = (int)imin64(c.nbt, c.nbands - b0);
-  uint32_t nibs[32];
-#pragma unroll
-  for (int bl = 0; bl < 32; ++bl) nibs[bl] = bl < nb ? (__ldcg(c.bcr + (b0 + bl) * c.U + u) >> (4 * w)) & 0xfu : 0u;
-#pragma unroll
-  for (int s = 0; s < NS; ++s) ws[s] = 0.0;
-#pragma unroll
-  for (int bl = 0; bl < 32; ++bl) {
-    const unsigned nib = nibs[bl];
-    if (!nib) continue;
-    const double* base = c.cscal + ((b0 + bl) * c.ncp + u * 32 + 4 * w) * kMaxNS;
-    double v[4][NS];
-#pragma unroll
-    for (int x = 0; x < 4; ++x)
-#pragma unroll
-      for (int s = 0; s < NS; ++s) v[x][s] = ((nib >> x) & 1u) ? __ldcg(base + x * kMaxNS + s) : 0.0;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) ws[s] += (v[0][s] + v[1][s]) + (v[2][s] + v[3][s]);
-  }
-}
-
-template <int NQ>
-__device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j, double2 (&acc)[NQ], bool units) {
+__device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j, double2 (&acc)[NQ]) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = make_double2(0.0, 0.0);
   const int64_t ta = imax64((int64_t)g * c.GS, c.t0);
   const int64_t tb = imin64(imin64((int64_t)(g + 1) * c.GS, c.Tg), c.t0 + c.T);
-  if (units) {  // every lane of the warp takes part (shuffles); lanes past n only skip loads
-    group_column_sum_units<NQ>(c, ta, tb, j, acc);
-    return;
-  }
   if (j >= c.n) return;
-  for (int64_t t = ta; t < tb; ++t) {
+  // tiles whose flag is 0 were screened out entirely: their partials are +0
+  const uint8_t* flags = c.tileflag + (j / kTileN);
+  for (int64_t t0 = ta; t0 < tb; t0 += 4) {
+    double2 v[4][NQ];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const double2 v = __ldcg(reinterpret_cast<const double2*>(c.colpart + ((t - c.t0) * NQ + q) * c.ldx + j));
-      acc[q].x += v.x;
-      acc[q].y += v.y;
+    for (int k = 0; k < 4; ++k) {
+      const bool on = t0 + k < tb && __ldg(flags + (t0 + k - c.t0) * c.U);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        v[k][q] = on ? __ldcg(reinterpret_cast<const double2*>(c.colpart + ((t0 + k - c.t0) * NQ + q) * c.ldx + j))
+                     : make_double2(0.0, 0.0);
     }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (t0 + k < tb)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          acc[q].x += v[k][q].x;
+          acc[q].y += v[k][q].y;
+        }
   }
 }
 
 // FIN_A: this shard's groups -> gbuf[g][q][j]
 template <int NQ>
-__device__ void column_group_partials(const Ctl& c, int b, bool units) {
+__device__ void column_group_partials(const Ctl& c, int b) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = c.g0 + warp;
   if (g < c.g1) {
     const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
     double2 acc[NQ];
-    group_column_sum<NQ>(c, g, j, acc, units);
+    group_column_sum<NQ>(c, g, j, acc);
     if (j < c.n) {
 #pragma unroll
       for (int q = 0; q < NQ; ++q) store_group2(c, g * c.gstride + q * c.ldx + j, acc[q]);
@@ -333,8 +176,7 @@ __device__ void column_group_partials(const Ctl& c, int b, bool units) {
 // Full column sums = pairwise combination of the 8 group sums (FIN_FUSED: the
 // groups are computed here; FIN_B: they come from the exchange buffer).
 template <int NQ>
-__device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_out, double* smem, int mode,
-                            bool units) {
+__device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_out, double* smem, int mode) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int jj = threadIdx.x;
   j_out = (int64_t)b * kColsPerBlock + jj;
@@ -355,7 +197,7 @@ __device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_o
   }
   const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
   double2 acc[NQ];
-  group_column_sum<NQ>(c, warp, j, acc, units);
+  group_column_sum<NQ>(c, warp, j, acc);
   // smem [group][q][64]
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
@@ -379,42 +221,35 @@ __device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_o
 }
 
 template <int NQ>
-__device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ], bool units) {
+__device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ]) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) row[q] = 0.0;
   if (i >= c.m) return;
-  if (units) {
-    row_sums_units<NQ>(c, i, row);
-    return;
-  }
-  constexpr int B = 4;
-  int64_t u = 0;
-  for (; u + B <= c.U; u += B) {
-    double v[B][NQ];
+  const uint8_t* flags = c.tileflag + (i / c.TM) * c.U;  // screened-out tiles: partials +0
+  for (int64_t u0 = 0; u0 < c.U; u0 += 4) {
+    double v[4][NQ];
 #pragma unroll
-    for (int k = 0; k < B; ++k)
+    for (int k = 0; k < 4; ++k) {
+      const bool on = u0 + k < c.U && __ldg(flags + u0 + k);
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) v[k][q] = __ldcg(c.rowpart + ((u + k) * NQ + q) * c.m + i);
+      for (int q = 0; q < NQ; ++q) v[k][q] = on ? __ldcg(c.rowpart + ((u0 + k) * NQ + q) * c.m + i) : 0.0;
+    }
 #pragma unroll
-    for (int k = 0; k < B; ++k)
+    for (int k = 0; k < 4; ++k)
+      if (u0 + k < c.U)
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) row[q] += v[k][q];
-  }
-  for (; u < c.U; ++u) {
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) row[q] += __ldcg(c.rowpart + (u * NQ + q) * c.m + i);
+        for (int q = 0; q < NQ; ++q) row[q] += v[k][q];
   }
 }
 
 __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
-  const bool units = unit_pass(c, op);
   double vals[kMaxColScal];
 #pragma unroll
   for (int s = 0; s < kMaxColScal; ++s) vals[s] = 0.0;
   int64_t j;
   if (op == OP_STEP) {
     double col[4];
-    column_sums<4>(c, b, col, j, smem, mode, units);
+    column_sums<4>(c, b, col, j, smem, mode);
     double qb = -INFINITY, qab = -INFINITY;  // screening bounds of q+ and the dual average
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       const Slot& sx = c.slot[c.sX];
@@ -458,7 +293,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
     }
   } else if (op == OP_KKT) {
     double col[1];
-    column_sums<1>(c, b, col, j, smem, mode, units);
+    column_sums<1>(c, b, col, j, smem, mode);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       c.cols_out[j] = col[0];
       if (c.C || c.cost_kind > 0) {
@@ -472,7 +307,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
     }
   } else if (op == OP_DIFF || op == OP_DIST) {
     double col[1];
-    column_sums<1>(c, b, col, j, smem, mode, units);
+    column_sums<1>(c, b, col, j, smem, mode);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       c.cols_out[j] = col[0];
       const double* qa = (op == OP_DIFF) ? c.slot[c.sX].q : c.slot[c.sZ].q;
@@ -483,7 +318,7 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
     }
   } else if (op == OP_ROUND) {
     double col[1];
-    column_sums<1>(c, b, col, j, smem, mode, units);
+    column_sums<1>(c, b, col, j, smem, mode);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       c.cols_out[j] = col[0];
       const double gj = c.g[j];
@@ -510,7 +345,6 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
 // row blocks (one per row tile)
 // ---------------------------------------------------------------------------
 __device__ void row_block(Ctl& c, int op, int t, double* smem) {
-  const bool units = unit_pass(c, op);
   double vals[kMaxRowScal];
 #pragma unroll
   for (int s = 0; s < kMaxRowScal; ++s) vals[s] = 0.0;
@@ -524,7 +358,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
     const bool ok = r < rows;
     if (op == OP_STEP) {
       double row[4];
-      row_sums<4>(c, ok ? i : c.m, row, units);
+      row_sums<4>(c, ok ? i : c.m, row);
       double pb = -INFINITY, pab = -INFINITY;  // screening bounds of p+ and the dual average
       if (ok) {
         const Slot& sx = c.slot[c.sX];
@@ -568,7 +402,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
       }
     } else if (op == OP_KKT) {
       double row[1];
-      row_sums<1>(c, ok ? i : c.m, row, units);
+      row_sums<1>(c, ok ? i : c.m, row);
       if (ok) {
         c.rows_out[i] = row[0];
         if (c.C || c.cost_kind > 0) {
@@ -581,7 +415,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
       }
     } else if (op == OP_DIFF || op == OP_DIST) {
       double row[1];
-      row_sums<1>(c, ok ? i : c.m, row, units);
+      row_sums<1>(c, ok ? i : c.m, row);
       if (ok) {
         c.rows_out[i] = row[0];
         const double* pa = (op == OP_DIFF) ? c.slot[c.sX].p : c.slot[c.sZ].p;
@@ -592,7 +426,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
       }
     } else if (op == OP_ROUND) {
       double row[1];
-      row_sums<1>(c, ok ? i : c.m, row, units);
+      row_sums<1>(c, ok ? i : c.m, row);
       if (ok) {
         c.rows_out[i] = row[0];
         const double fi = c.f[i];
@@ -614,43 +448,23 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < nr; ++s) c.rowblk[(int64_t)t * kMaxRowScal + s] = vals[s];
   }
-  // tile scalars of this row tile (sum over column tiles, in order)
-  if (!units) {
-    if (threadIdx.x < ns) {
-      double acc = 0.0;
-      for (int64_t u = 0; u < c.U; ++u) acc += __ldcg(c.tilescal + ((int64_t)t * c.U + u) * kMaxNS + threadIdx.x);
-      c.rowblk[(int64_t)t * kMaxRowScal + nr + threadIdx.x] = acc;
-    }
-    return;
-  }
-  // screened pass: tile scalars rebuilt from the cell scalars; thread (u, w)
-  // computes strip w's band-ordered sum, then the strips and column tiles are
-  // added in order (32 column tiles per round)
-  __syncthreads();
-  const int uu = threadIdx.x >> 3, w = threadIdx.x & 7;
-  double acc = 0.0;
-  for (int64_t u0 = 0; u0 < c.U; u0 += 32) {
-    const int64_t u = u0 + uu;
-    double ws[6];
-    if (u < c.U) {
-      strip_scalars_units<6>(c, t, u, w, ws);
-    } else {
+  // tile scalars of this row tile (sum over column tiles, in order; screened-out tiles are +0)
+  if (threadIdx.x < ns) {
+    const uint8_t* flags = c.tileflag + (int64_t)t * c.U;
+    double acc = 0.0;
+    for (int64_t u0 = 0; u0 < c.U; u0 += 8) {
+      double v[8];
 #pragma unroll
-      for (int s = 0; s < 6; ++s) ws[s] = 0.0;
-    }
+      for (int k = 0; k < 8; ++k)
+        v[k] = (u0 + k < c.U && __ldg(flags + u0 + k))
+                   ? __ldcg(c.tilescal + ((int64_t)t * c.U + u0 + k) * kMaxNS + threadIdx.x)
+                   : 0.0;
 #pragma unroll
-    for (int s = 0; s < 6; ++s) smem[(uu * 8 + w) * 8 + s] = ws[s];
-    __syncthreads();
-    if (threadIdx.x < ns) {
-      for (int k = 0; k < 32 && u0 + k < c.U; ++k) {
-        double tsu = smem[(k * 8) * 8 + threadIdx.x];
-        for (int x = 1; x < kWarps; ++x) tsu += smem[(k * 8 + x) * 8 + threadIdx.x];
-        acc += tsu;
-      }
+      for (int k = 0; k < 8; ++k)
+        if (u0 + k < c.U) acc += v[k];
     }
-    __syncthreads();
+    c.rowblk[(int64_t)t * kMaxRowScal + nr + threadIdx.x] = acc;
   }
-  if (threadIdx.x < ns) c.rowblk[(int64_t)t * kMaxRowScal + nr + threadIdx.x] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -669,9 +483,7 @@ __device__ __forceinline__ double group_row_scalar(const Ctl& c, int s, int g, i
   const int64_t ga = (int64_t)g * c.GS, gb = imin64((int64_t)(g + 1) * c.GS, c.Tg);
   const int64_t mid = ga + (imax64(gb - ga, 0) + 1) / 2;
   const int64_t a = half ? mid : ga, e = half ? gb : mid;
-  double acc = 0.0;
-  for (int64_t t = a; t < e; ++t) acc += __ldcg(c.rowblk + (t - c.t0) * kMaxRowScal + s);
-  return acc;
+  return seq_sum(c.rowblk + (a - c.t0) * kMaxRowScal + s, kMaxRowScal, imax64(e - a, 0));
 }
 
 __device__ __forceinline__ bool local_stop(const Ctl& c) {
@@ -709,9 +521,7 @@ __device__ void reduce_blocks(const Ctl& c, Sums* S, double* smem, int mode) {
     const int s = tid >> 5, w = tid & 31;
     const int64_t per = (c.CB + 31) / 32;
     const int64_t b0 = w * per, b1 = imin64(c.CB, b0 + per);
-    double acc = 0.0;
-    for (int64_t b = b0; b < b1; ++b) acc += __ldcg(c.colblk + b * kMaxColScal + s);
-    smem[256 + tid] = acc;
+    smem[256 + tid] = seq_sum(c.colblk + b0 * kMaxColScal + s, kMaxColScal, imax64(b1 - b0, 0));
   }
   __syncthreads();
   if (tid < kMaxRowScal) {
@@ -992,15 +802,31 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   __shared__ Sums S;
   __shared__ int is_last;
   __shared__ Ctl cs;
-  Ctl& c = *ctlp;
-  if (c.done) return;
+  {
+    const Ctl& g = *ctlp;
+    if (g.done) return;
+    const int op0 = force_op >= 0 ? force_op : g.op;
+    if (op0 == OP_NONE) return;
+    if (mode == FIN_B && g.p2p) wait_exchange(*ctlp);
+  }
+  // Every block works on a shared-memory copy of the control block: its fields
+  // are then plain shared loads that no global store can alias (the blocks only
+  // write through the pointers it holds), and the controller reuses the copy.
+  constexpr int kWords = (int)(sizeof(Ctl) / sizeof(unsigned long long));
+  unsigned long long* cw = reinterpret_cast<unsigned long long*>(&cs);
+  {
+    const unsigned long long* gw = reinterpret_cast<const unsigned long long*>(ctlp);
+    for (int i = threadIdx.x; i < kWords; i += blockDim.x) cw[i] = __ldcg(gw + i);
+  }
+  __syncthreads();
+  Ctl& c = cs;
   const int op = force_op >= 0 ? force_op : c.op;
-  if (op == OP_NONE) return;
-  if (mode == FIN_B && c.p2p) wait_exchange(c);
+  const bool timed = op == OP_STEP && unit_pass(c, op) && c.sstat;  // K2 timing of screened STEP passes
+  if (timed && blockIdx.x == 0 && threadIdx.x == 0) c.sstat[ST_K2_T0] = globaltimer_ns();
   if ((int64_t)blockIdx.x < c.CB) {
     if (mode == FIN_A) {
-      if (op == OP_STEP) column_group_partials<4>(c, blockIdx.x, unit_pass(c, op));
-      else column_group_partials<1>(c, blockIdx.x, unit_pass(c, op));
+      if (op == OP_STEP) column_group_partials<4>(c, blockIdx.x);
+      else column_group_partials<1>(c, blockIdx.x);
     } else {
       column_block(c, op, blockIdx.x, smem, mode);
     }
@@ -1015,19 +841,19 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   __syncthreads();
   if (!is_last) return;
   __threadfence();
+  const uint64_t t_last = timed ? globaltimer_ns() : 0;
   if (mode == FIN_A) {
     group_scalar_partials(c);
     __syncthreads();
     if (threadIdx.x == 0) *c.counter = 0u;
     return;
   }
-  // the controller works on a shared-memory copy of the control block
-  constexpr int kWords = (int)(sizeof(Ctl) / sizeof(unsigned long long));
-  unsigned long long* cw = reinterpret_cast<unsigned long long*>(&cs);
-  const unsigned long long* gw = reinterpret_cast<const unsigned long long*>(ctlp);
-  for (int i = threadIdx.x; i < kWords; i += blockDim.x) cw[i] = __ldcg(gw + i);
+  // the controller works on the shared-memory copy and writes it back
+  if (mode == FIN_B && c.p2p && threadIdx.x == 0) cs.xerror = __ldcg(&ctlp->xerror);  // set by wait_exchange
   __syncthreads();
   reduce_blocks(cs, &S, smem, mode);
+  const uint64_t t_red = timed ? globaltimer_ns() : 0;
+  uint64_t t_logic = 0;
   if (threadIdx.x == 0) {
     if (mode == FIN_B && cs.p2p) {
       *xcounter(cs) += 1ull;  // this exchange is consumed (same count on every rank)
@@ -1042,6 +868,7 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
         else if (op == OP_DIST) control_dist(cs, S);
         else if (op == OP_KKT) control_start(cs, S);
       }
+      if (timed) t_logic = globaltimer_ns();
       // publish to the host mirror (read by the host only after the pass's
       // completion event, which orders these mapped-memory writes)
       if (cs.status) {
@@ -1061,7 +888,16 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   for (int i = threadIdx.x; i < kWords; i += blockDim.x) gwo[i] = cw[i];
   if (threadIdx.x == 0) {
     *cs.counter = 0u;
-    if (cs.ucount) *cs.ucount = 0u;  // the screened unit list of this pass is consumed
+    if (cs.ucount) *cs.ucount = 0u;  // the screened cell and tile lists of this pass are consumed
+    if (cs.tcount) *cs.tcount = 0u;
+    if (timed) {
+      const uint64_t t_end = globaltimer_ns();
+      cs.sstat[ST_K2_MAIN] += t_last - __ldcg(&cs.sstat[ST_K2_T0]);
+      cs.sstat[ST_K2_CTL] += t_end - t_last;
+      cs.sstat[ST_T0K0] += t_red - t_last;     // controller: copy-free reduction of the block partials
+      cs.sstat[ST_T1K0] += t_logic - t_red;    // controller: decisions
+      cs.sstat[ST_DONE0] += t_end - t_logic;   // controller: status mirror + control-block write-back
+    }
   }
 }
 

@@ -246,50 +246,60 @@ struct RoundOp {
 //   * row: lane value o0 + o1; cell value = 8-lane butterfly (masks 1, 2, 4);
 //     strip value = (c0 + c1) + (c2 + c3) (masks 8, 16); tile partial = sum of
 //     strip values in strip order;
-//   * scalar: lane band partial = sequential over the band's rows (col0 then
-//     col1 per row); cell value = 8-lane butterfly; strip band value =
+//   * scalar: lane stage partial = sequential over the stage's (2 rows) elements
+//     (row 2k col0, col1, row 2k+1 col0, col1) from +0; lane band partial =
+//     (s0 + s1) + (s2 + s3); cell value = 8-lane butterfly; strip band value =
 //     (c0 + c1) + (c2 + c3); tile scalar = sum over strips of the strip's sum
 //     over bands in band order.
 // A skipped cell contributes exact +0 terms anywhere in this tree.
 // ---------------------------------------------------------------------------
-// column band partial built from 2-row stage sums: stage k (0..3) of the band
-template <int NQ>
-struct BandCols {
-  double a[NQ][2], b[NQ][2];
+// Band accumulators of the canonical tree, fed once per 2-row STAGE (stage k =
+// rows 2k, 2k+1 of the band): column stage sums and the lane's stage scalar
+// partials (sequential over the stage's elements from +0) combine as
+// (s0 + s1) + (s2 + s3).
+template <int NQ, int NS>
+struct BandAcc {
+  double ca[NQ][2], cb[NQ][2], sa[NS], sb[NS];
   __device__ __forceinline__ void reset() {
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) a[q][0] = a[q][1] = b[q][0] = b[q][1] = 0.0;
+    for (int q = 0; q < NQ; ++q) ca[q][0] = ca[q][1] = cb[q][0] = cb[q][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) sa[s] = sb[s] = 0.0;
   }
-  // st = o(row 2k) + o(row 2k+1) of this band
-  __device__ __forceinline__ void add(int k, const double (&st)[NQ][2]) {
+  // ps = o(row 2k) + o(row 2k+1); sacc = the stage's scalar partials (reset here)
+  __device__ __forceinline__ void stage(int k, const double (&ps)[NQ][2], double (&sacc)[NS]) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        if (k == 0) a[q][e] = st[q][e];
-        else if (k == 1) a[q][e] += st[q][e];
-        else if (k == 2) b[q][e] = st[q][e];
-        else b[q][e] += st[q][e];
+        if (k == 0) ca[q][e] = ps[q][e];
+        else if (k == 1) ca[q][e] += ps[q][e];
+        else if (k == 2) cb[q][e] = ps[q][e];
+        else cb[q][e] += ps[q][e];
       }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (k == 0) sa[s] = sacc[s];
+      else if (k == 1) sa[s] += sacc[s];
+      else if (k == 2) sb[s] = sacc[s];
+      else sb[s] += sacc[s];
+      sacc[s] = 0.0;
+    }
   }
 };
 
-// end of a band: band column partial into the tile partial, lane scalar partials
-// -> warp totals (identical in every lane); reset
+// end of a band: band column partial into the tile partial, band scalar
+// partials -> warp totals (identical in every lane); reset
 template <int NQ, int NS>
-__device__ __forceinline__ void band_close(BandCols<NQ>& bc, double (&cacc)[NQ][2], double (&sacc)[NS],
-                                           double (&ws)[NS]) {
+__device__ __forceinline__ void band_close(BandAcc<NQ, NS>& ba, double (&cacc)[NQ][2], double (&ws)[NS]) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
-    cacc[q][0] += bc.a[q][0] + bc.b[q][0];
-    cacc[q][1] += bc.a[q][1] + bc.b[q][1];
+    cacc[q][0] += ba.ca[q][0] + ba.cb[q][0];
+    cacc[q][1] += ba.ca[q][1] + ba.cb[q][1];
   }
-  bc.reset();
 #pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    ws[s] += group_sum<32>(sacc[s]);
-    sacc[s] = 0.0;
-  }
+  for (int s = 0; s < NS; ++s) ws[s] += group_sum<32>(ba.sa[s] + ba.sb[s]);
+  ba.reset();
 }
 
 // per-tile flush shared by the walkers: column partials (registers -> global),
@@ -325,6 +335,7 @@ __device__ __forceinline__ void tile_flush(const Ctl& c, const Geo& g, bool work
     for (int w = 1; w < kWarps; ++w) acc += sbuf[w * 8 + threadIdx.x];
     c.tilescal[(g.tt * c.U + g.tu) * kMaxNS + threadIdx.x] = acc;
   }
+  if (threadIdx.x == 0 && c.tileflag) c.tileflag[g.tt * c.U + g.tu] = 1;
 }
 
 __device__ __forceinline__ Geo make_geo(const Ctl& c, bool worker, int64_t tu, int64_t tt) {
@@ -374,8 +385,8 @@ __device__ __forceinline__ void tile_pass(const Op& op, const Ctl& c, double* sm
   double cacc[NQ][2];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = 0.0;
-  BandCols<NQ> bcol;
-  bcol.reset();
+  BandAcc<NQ, NS> bacc;
+  bacc.reset();
   double sacc[NS], ws[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) sacc[s] = ws[s] = 0.0;
@@ -406,10 +417,10 @@ __device__ __forceinline__ void tile_pass(const Op& op, const Ctl& c, double* sm
         }
         rv[rr * NQ + q] = o0[q] + o1[q];
       }
-      if (rr & 1) bcol.add(rr >> 1, st);
+      if (rr & 1) bacc.stage(rr >> 1, st, sacc);
     }
     push_rows<NQ, RB>(rv, rowbuf, r0, worker);
-    band_close<NQ, NS>(bcol, cacc, sacc, ws);
+    band_close<NQ, NS>(bacc, cacc, ws);
   }
   tile_flush<NQ, NS>(c, g, worker, cacc, ws, rowbuf, sbuf);
 }

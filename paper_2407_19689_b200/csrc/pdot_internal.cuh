@@ -52,6 +52,9 @@ enum ScreenStat : int {
   ST_T0K0 = 10,
   ST_T1K0 = 11,
   ST_DONE0 = 12,
+  ST_K2_T0 = 13,    // K2 of screened STEP passes: start stamp (block 0),
+  ST_K2_MAIN = 14,  // summed time from start to the last block's ticket,
+  ST_K2_CTL = 15,   // summed time of the controller tail (last block)
   ST_COUNT = 16,
 };
 
@@ -197,6 +200,9 @@ struct Ctl {
   int64_t ncp;               // cells per row of cells, padded to whole tiles (U * 32)
   uint32_t* bcr;             // [nbands][U]  bit k: cell k of column tile u wrote partials this pass
   uint32_t* bct;             // [T][ncp]     bit b: band b of row tile t of this cell wrote partials
+  uint8_t* tileflag;         // [T][U] the tile's partials are valid (0: screened out, all +0)
+  int32_t* tlist;            // [T*U] tiles with active cells this pass (K1b assembles them)
+  unsigned int* tcount;      // length of tlist (K0 appends, K2 resets)
   double* ccol;              // [nbands][kMaxNQ][ldx]  cell column partials (band partial of the tree)
   double* crow;              // [ncp][kMaxNQ][mpad]   cell row partials (8-lane butterfly per row)
   double* cscal;             // [nbands][ncp][kMaxNS] cell scalars

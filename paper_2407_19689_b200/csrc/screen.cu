@@ -169,8 +169,13 @@ __global__ void __launch_bounds__(256) screen_kernel(const Ctl* __restrict__ ctl
 #pragma unroll
   for (int k = 0; k < kCellsPerStrip; ++k)
     if ((actb >> k) & 1u) atomicOr(&tilebits[s * kCellsPerStrip + k], 1u << bl);
-  __syncthreads();
+  const int any = __syncthreads_or(actb != 0u);
   if (threadIdx.x < 32) c.bct[tt * c.ncp + tu * 32 + threadIdx.x] = tilebits[threadIdx.x];
+  // the tile's partials are assembled by K1b, or are all +0 (flag 0)
+  if (threadIdx.x == 0) {
+    c.tileflag[tt * c.U + tu] = any ? 1 : 0;
+    if (any) c.tlist[atomicAdd(c.tcount, 1u)] = (int32_t)(tt * c.U + tu);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -207,13 +212,13 @@ __device__ __forceinline__ CellGeo cell_geo(const Ctl& c, uint32_t entry) {
   return g;
 }
 
-// Scalar chain + partial writes shared by every cell op.  o[rr][q][e]: the
-// lane's outputs for row 2 rg + rr, column e; ta/tb[rr][e][s]: the fma terms
-// (acc = fma(ta, tb, acc)) of each element, applied only where ok[rr][e].
+// Partial writes shared by every cell op.  o[rr][q][e]: the lane's outputs for
+// row 2 rg + rr, column e; sacc: the lane's stage scalar partials (its two rows,
+// element order), so the band partial is (s0 + s1) + (s2 + s3) over the row
+// groups (masks 8, 16) and the cell value the 8-lane butterfly on top.
 template <int NQ, int NS>
 __device__ __forceinline__ void cell_flush(const Ctl& c, const CellGeo& g, const double (&o)[2][NQ][2],
-                                          const double (&ta)[2][2][NS], const double (&tb)[2][2][NS],
-                                          const bool (&ok)[2][2]) {
+                                          const double (&sacc)[NS]) {
   // column band partial: pair sum of the lane's two rows, then masks 8, 16
   double2 cs[NQ];
 #pragma unroll
@@ -245,34 +250,18 @@ __device__ __forceinline__ void cell_flush(const Ctl& c, const CellGeo& g, const
     DCHECK(g.cell < c.ncp && (r >= g.rows || g.i0 + r < c.mpad), "crow", g.cell, g.i0 + r);
     if (r < g.rows) c.crow[(g.cell * kMaxNQ + q) * c.mpad + g.i0 + r] = rv[0];
   }
-  // scalars: the lane partial runs down the band row by row (row group 0..3)
-  double acc[NS];
+  // scalars: stage partials pairwise over the row groups, then over the column pairs
+  double sv[NS];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) acc[s] = 0.0;
-#pragma unroll
-  for (int gi = 0; gi < 4; ++gi) {
-    if (g.rg == gi) {
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (ok[rr][e])
-#pragma unroll
-            for (int s = 0; s < NS; ++s) acc[s] = __fma_rn(ta[rr][e][s], tb[rr][e][s], acc[s]);
-    }
-    if (gi < 3) {
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        const double t = __shfl_up_sync(0xffffffffu, acc[s], 8);
-        if (g.rg == gi + 1) acc[s] = t;
-      }
-    }
+  for (int s = 0; s < NS; ++s) {
+    double x = sacc[s];
+    x += __shfl_xor_sync(0xffffffffu, x, 8);
+    x += __shfl_xor_sync(0xffffffffu, x, 16);
+    sv[s] = group_sum<8>(x);
   }
+  if ((threadIdx.x & 31) == 0) {
 #pragma unroll
-  for (int s = 0; s < NS; ++s) acc[s] = group_sum<8>(acc[s]);
-  if ((threadIdx.x & 31) == 24) {
-#pragma unroll
-    for (int s = 0; s < NS; ++s) c.cscal[(g.band * c.ncp + g.cell) * kMaxNS + s] = acc[s];
+    for (int s = 0; s < NS; ++s) c.cscal[(g.band * c.ncp + g.cell) * kMaxNS + s] = sv[s];
   }
 }
 
@@ -323,40 +312,28 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const 
     }
   }
   double o[2][NQ][2];
-  double ta[2][2][NS], tb[2][2][NS];
-  bool ok[2][2];
+  double sacc[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) sacc[s] = 0.0;
   bool nzx = false, nza = false;
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
     const int r = 2 * g.rg + rr;
     const bool inrow = r < g.rows && g.v0;
     const int64_t i = g.i0 + r;
+    double o0[NQ], o1[NQ];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      ok[rr][e] = okr[rr] && (e == 0 || g.v1);
-      const double cv = e ? cc[rr].y : cc[rr].x, x = e ? xx[rr].y : xx[rr].x, a = e ? aa[rr].y : aa[rr].x;
-      // StepOp::elem, expression by expression (pdhg.py:123-125, 315; kkt.py:70-71)
-      const double pq = pr[rr] + qv[e];
-      const double sres = cv - pq;
-      const double xn = relu_np(x - op.tau * sres);
-      const double d = xn - x;
-      const double ee = (xn + xn) - x;
-      const double vc = relu_np(pq - cv);
-      const double va = relu_np((par[rr] + qav[e]) - cv);
-      const double an = AVG ? a + div_by_count(x - a, op.kd, op.rkd) : 0.0;
-      const bool k_ = ok[rr][e];
-      o[rr][0][e] = k_ ? ee : 0.0;
-      o[rr][1][e] = k_ ? d : 0.0;
-      o[rr][2][e] = k_ ? xn : 0.0;
-      o[rr][3][e] = k_ ? an : 0.0;
-      ta[rr][e][0] = d;  tb[rr][e][0] = d;
-      ta[rr][e][1] = cv; tb[rr][e][1] = xn;
-      ta[rr][e][2] = cv; tb[rr][e][2] = an;
-      ta[rr][e][3] = xn; tb[rr][e][3] = xn;
-      ta[rr][e][4] = vc; tb[rr][e][4] = vc;
-      ta[rr][e][5] = va; tb[rr][e][5] = va;
+    for (int q = 0; q < NQ; ++q) o0[q] = o1[q] = 0.0;
+    if (okr[rr]) {  // StepOp::elem in the dense walkers' element order
+      op.template elem<AVG>(cc[rr].x, xx[rr].x, aa[rr].x, pr[rr], qv[0], par[rr], qav[0], o0, sacc);
+      if (g.v1) op.template elem<AVG>(cc[rr].y, xx[rr].y, aa[rr].y, pr[rr], qv[1], par[rr], qav[1], o1, sacc);
     }
-    const double2 xo = make_double2(o[rr][2][0], o[rr][2][1]);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      o[rr][q][0] = o0[q];
+      o[rr][q][1] = o1[q];
+    }
+    const double2 xo = make_double2(o0[2], o1[2]);
     const bool nzr = nz2(xo);
     nzx |= nzr;
     if (inrow && (okr[rr] ? (zx || nzr) : zx)) {
@@ -364,7 +341,7 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const 
       bytes += 16;
     }
     if (AVG) {
-      const double2 ao = make_double2(o[rr][3][0], o[rr][3][1]);
+      const double2 ao = make_double2(o0[3], o1[3]);
       const bool nar = nz2(ao);
       nza |= nar;
       if (inrow && (okr[rr] ? (za || nar) : za)) {
@@ -385,94 +362,59 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const 
     }
   }
   if (act) {
-    if (!AVG) {  // no average this pass: its terms are not accumulated
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) ta[rr][e][2] = tb[rr][e][2] = 0.0;
-    }
-    cell_flush<NQ, NS>(c, g, o, ta, tb, ok);
+    cell_flush<NQ, NS>(c, g, o, sacc);
     if (lane == 0) bytes += (unsigned long long)(NQ * kCell + NQ * kBand + NS) * 8 * 2;
   }
 }
 
-// restart distance (DIST) and the start KKT through the screen (NQ = 1)
-template <int OPK>
-__device__ __forceinline__ void cell_one(const Ctl& c, uint32_t entry, unsigned long long& bytes,
+// restart distance (DIST) and the start KKT through the screen (NQ = 1), with
+// the dense walkers' per-row compute()
+template <class Op>
+__device__ __forceinline__ void cell_one(const Op& op, const Ctl& c, uint32_t entry, unsigned long long& bytes,
                                          unsigned long long& cells) {
-  constexpr int NQ = 1, NS = (OPK == OP_DIST) ? 1 : 3;
+  constexpr int NQ = Op::NQ, NS = Op::NS;
   const int lane = threadIdx.x & 31;
-  const CellGeo g = cell_geo(c, entry);
-  const uint32_t f = (__ldcg(c.unitw + g.band * c.nstrips + g.strip) >> (8 * g.k)) & 0xffu;
-  const bool act = (f & U_ACT) != 0;
-  if (lane == 0 && act) cells += 1;
-  if (!act) return;
-#ifdef DBG_SKIP_CELL_ONE
-  return;
-#endif
-  const double2 zero2 = make_double2(0.0, 0.0);
-  CostGen gen;
-  gen.kind = c.C ? 0 : c.cost_kind;
-  gen.a0 = c.cost_a[0]; gen.a1 = c.cost_a[1]; gen.a2 = c.cost_a[2]; gen.a3 = c.cost_a[3];
-  gen.row0 = c.row0;
-  const Slot& sx = c.slot[c.sX];
-  double o[2][NQ][2];
-  double ta[2][2][NS], tb[2][2][NS];
-  bool ok[2][2];
-  double q0 = 0.0, q1 = 0.0;
-  if (OPK == OP_KKT && g.v0) {
-    q0 = sx.q[g.j];
-    if (g.v1) q1 = sx.q[g.j + 1];
-  }
+  const CellGeo cg = cell_geo(c, entry);
+  const uint32_t f = (__ldcg(c.unitw + cg.band * c.nstrips + cg.strip) >> (8 * cg.k)) & 0xffu;
+  if (!(f & U_ACT)) return;  // cell-uniform
+  if (lane == 0) cells += 1;
+  Geo g;  // the fields the ops read
+  g.m = c.m; g.n = c.n; g.ldc = c.ldc; g.ldx = c.ldx; g.TM = c.TM;
+  g.tu = 0; g.tt = 0; g.i0 = cg.i0; g.rows = cg.rows; g.j = cg.j;
+  g.v0 = cg.v0;
+  g.v1 = cg.v1;
+  g.gen.kind = c.C ? 0 : c.cost_kind;
+  g.gen.a0 = c.cost_a[0]; g.gen.a1 = c.cost_a[1]; g.gen.a2 = c.cost_a[2]; g.gen.a3 = c.cost_a[3];
+  g.gen.row0 = c.row0;
+  typename Op::Col cl;
+  op.load_col(cl, g);
+  typename Op::Frag fr[2];
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
-    const int r = 2 * g.rg + rr;
-    const bool okr = r < g.rows && g.v0;
-    const int64_t i = g.i0 + r;
-    double2 xa = zero2, xb = zero2, cv = zero2;
-    double p = 0.0;
-#ifdef DBG_SKIP_LOADS
-    if (false) {
-#else
-    if (okr) {
-#endif
-      DCHECK(i < c.m && g.j + 1 < c.ldx, "cell_one ld", i, g.j);
-      if (OPK == OP_DIST) {
-        xa = ld_stream2(c.slot[c.sZ].X + i * c.ldx + g.j);
-        xb = ld_stream2(c.slot[c.sCand].X + i * c.ldx + g.j);
-      } else {
-        xb = ld_stream2(sx.X + i * c.ldx + g.j);
-        if (c.C) {
-          cv = ld_stream2(c.C + i * c.ldc + g.j);
-        } else if (gen.kind > 0) {
-          const double2 rc = gen.row_coord(i);
-          cv = make_double2(gen.cost(rc, gen.col_coord(g.j)), gen.cost(rc, gen.col_coord(g.j + 1)));
-        }
-        p = __ldg(sx.p + i);
-      }
+    const int r = 2 * cg.rg + rr;
+    if (r < cg.rows && cg.v0) {
+      op.load(fr[rr], g, cg.i0 + r);
       bytes += 32;
     }
+  }
+  double o[2][NQ][2];
+  double sacc[NS];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      ok[rr][e] = okr && (e == 0 || g.v1);
-      const double b = e ? xb.y : xb.x;
-      if (OPK == OP_DIST) {  // DiffOp: d = X_b - X_a
-        const double d = b - (e ? xa.y : xa.x);
-        o[rr][0][e] = ok[rr][e] ? d : 0.0;
-        ta[rr][e][0] = d; tb[rr][e][0] = d;
-      } else {  // KktOp: <C,X>, |[p+q-C]^+|^2, |X|^2
-        const double cc = e ? cv.y : cv.x;
-        const double v = relu_np((p + (e ? q1 : q0)) - cc);
-        o[rr][0][e] = ok[rr][e] ? b : 0.0;
-        ta[rr][e][0] = cc; tb[rr][e][0] = b;
-        ta[rr][e][1] = v;  tb[rr][e][1] = v;
-        ta[rr][e][2] = b;  tb[rr][e][2] = b;
-      }
+  for (int s = 0; s < NS; ++s) sacc[s] = 0.0;
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int r = 2 * cg.rg + rr;
+    double o0[NQ], o1[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) o0[q] = o1[q] = 0.0;
+    if (r < cg.rows && cg.v0) op.compute(fr[rr], g, cg.i0 + r, cl, o0, o1, sacc);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      o[rr][q][0] = o0[q];
+      o[rr][q][1] = o1[q];
     }
   }
-#ifndef DBG_SKIP_FLUSH
-  cell_flush<NQ, NS>(c, g, o, ta, tb, ok);
-#endif
+  cell_flush<NQ, NS>(c, cg, o, sacc);
 }
 
 __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const Ctl* __restrict__ ctlp, int force_op) {
@@ -503,9 +445,14 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
       }
     }
   } else if (op == OP_DIST) {
-    for (unsigned k = gw; k < ncells; k += nw) cell_one<OP_DIST>(c, __ldcg(c.ulist + k), bytes, cells);
+    DiffOp o;
+    o.Xa = c.slot[c.sZ].X; o.Xb = c.slot[c.sCand].X;
+    for (unsigned k = gw; k < ncells; k += nw) cell_one(o, c, __ldcg(c.ulist + k), bytes, cells);
   } else {
-    for (unsigned k = gw; k < ncells; k += nw) cell_one<OP_KKT>(c, __ldcg(c.ulist + k), bytes, cells);
+    KktOp o;
+    const Slot& sx = c.slot[c.sX];
+    o.C = c.C; o.X = sx.X; o.p = sx.p; o.q = sx.q; o.viol = nullptr;
+    for (unsigned k = gw; k < ncells; k += nw) cell_one(o, c, __ldcg(c.ulist + k), bytes, cells);
   }
   // statistics: one atomic per CTA, then the last CTA stamps the end time
 #pragma unroll
@@ -539,6 +486,130 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
       }
       c.sstat[ST_DONE1] = 0;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1b: assembles the per-tile partials of the canonical tree (the same layout
+// the dense walkers write: colpart / rowpart / tilescal) from the cell
+// partials, for every tile with an active cell.  One CTA per listed tile:
+//   columns: thread = column pair, band-ordered sum of its cell column;
+//   rows:    thread = row, strip-ordered sum of the strip values
+//            ((c0 + c1) + (c2 + c3)) of the row segment's active cells;
+//   scalars: thread (strip, scalar), band-ordered sum of strip-band values,
+//            then the strips in order.
+// ---------------------------------------------------------------------------
+template <int NQ, int NS>
+__device__ __forceinline__ void assemble_tile(const Ctl& c, int64_t tu, int64_t tt, double* sm) {
+  const int th = threadIdx.x;
+  const int64_t b0 = tt * c.nbt;
+  {  // columns
+    const int64_t j = tu * kTileN + th * 2;
+    if (j < c.n) {
+      uint32_t m = __ldg(c.bct + tt * c.ncp + j / kCell);
+      double2 acc[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) acc[q] = make_double2(0.0, 0.0);
+      while (m) {
+        int bb[4];
+        int cnt = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          bb[e] = 0;
+          if (m) {
+            bb[e] = __ffs(m) - 1;
+            m &= m - 1;
+            cnt = e + 1;
+          }
+        }
+        double2 v[4][NQ];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+            v[e][q] = e < cnt ? __ldg(reinterpret_cast<const double2*>(c.ccol + ((b0 + bb[e]) * kMaxNQ + q) * c.ldx + j))
+                              : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (e < cnt)
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              acc[q].x += v[e][q].x;
+              acc[q].y += v[e][q].y;
+            }
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) *reinterpret_cast<double2*>(c.colpart + (tt * NQ + q) * c.ldx + j) = acc[q];
+    }
+  }
+  for (int r = th; r < c.TM; r += blockDim.x) {  // rows
+    const int64_t i = tt * c.TM + r;
+    if (i >= c.m) break;
+    uint32_t word = __ldg(c.bcr + (i / kBand) * c.U + tu);
+    double acc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+    while (word) {
+      const int w = (__ffs(word) - 1) >> 2;  // next active strip, in order
+      const unsigned nib = (word >> (4 * w)) & 0xfu;
+      word &= ~(0xfu << (4 * w));
+      const int64_t cb = tu * 32 + 4 * w;
+      double v[4][NQ];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          v[x][q] = ((nib >> x) & 1u) ? __ldg(c.crow + ((cb + x) * kMaxNQ + q) * c.mpad + i) : 0.0;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) acc[q] += (v[0][q] + v[1][q]) + (v[2][q] + v[3][q]);
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) c.rowpart[(tu * NQ + q) * c.m + i] = acc[q];
+  }
+  {  // scalars: thread (strip w, scalar s)
+    const int w = th >> 3, s = th & 7;
+    double ws = 0.0;
+    if (w < kWarps && s < NS) {
+      const int nb = (int)imin64(c.nbt, c.nbands - b0);
+      uint32_t nibs[32];
+#pragma unroll
+      for (int bl = 0; bl < 32; ++bl) nibs[bl] = bl < nb ? (__ldg(c.bcr + (b0 + bl) * c.U + tu) >> (4 * w)) & 0xfu : 0u;
+#pragma unroll
+      for (int bl = 0; bl < 32; ++bl) {
+        const unsigned nib = nibs[bl];
+        if (!nib) continue;
+        const double* base = c.cscal + ((b0 + bl) * c.ncp + tu * 32 + 4 * w) * kMaxNS + s;
+        double v[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) v[x] = ((nib >> x) & 1u) ? __ldg(base + x * kMaxNS) : 0.0;
+        ws += (v[0] + v[1]) + (v[2] + v[3]);
+      }
+    }
+    if (th < 64) sm[th] = ws;
+    __syncthreads();
+    if (th < NS) {
+      double acc = sm[th];
+#pragma unroll
+      for (int x = 1; x < kWarps; ++x) acc += sm[x * 8 + th];
+      c.tilescal[(tt * c.U + tu) * kMaxNS + th] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) tile_kernel(const Ctl* __restrict__ ctlp, int force_op) {
+  __shared__ double sm[64];
+  const Ctl& c = *ctlp;
+  if (c.done || !c.screen) return;
+  const int op = force_op >= 0 ? force_op : c.op;
+  if (!unit_pass(c, op)) return;
+  const unsigned ntiles = __ldcg(c.tcount);
+  for (unsigned k = blockIdx.x; k < ntiles; k += gridDim.x) {
+    const int32_t tile = __ldcg(c.tlist + k);
+    const int64_t tu = tile % c.U, tt = tile / c.U;
+    if (op == OP_STEP) assemble_tile<4, 6>(c, tu, tt, sm);
+    else if (op == OP_DIST) assemble_tile<1, 1>(c, tu, tt, sm);
+    else assemble_tile<1, 3>(c, tu, tt, sm);
   }
 }
 
@@ -646,6 +717,7 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
       if (e != cudaSuccess) fprintf(stderr, "screen_kernel failed: %s\n", cudaGetErrorString(e));
     }
     unit_kernel<<<(unsigned)(sms * kSparseCtasPerSm), kThreads, 0, s>>>(ctl_dev, force_op);
+    tile_kernel<<<(unsigned)imin64(h.T * h.U, (int64_t)sms * 4), kThreads, 0, s>>>(ctl_dev, force_op);
   } else {
     const unsigned grid = (unsigned)imin64(h.T * h.U, (int64_t)sms * 2);
     generic_kernel<<<grid, kThreads, generic_smem_bytes(h.TM), s>>>(ctl_dev, force_op);

@@ -276,7 +276,7 @@ int exchange(pdot_solver* h) {
 int launch_k1(pdot_solver* h, int op) {
   if (h->host.screen) {
     pdot::launch_screened_pass(h->dev, h->host, op, h->stream);
-    return (op < 0 || pdot::unit_pass(h->host, op)) ? 2 : 1;
+    return (op < 0 || pdot::unit_pass(h->host, op)) ? 3 : 1;
   }
   // (dense walker below)
   pdot::launch_stream_pass(h->dev, h->host, op, h->stream);
@@ -312,7 +312,7 @@ int launch_pass(pdot_solver* h, int op) {
 }
 
 // kernels per pass (graph replays count launches without re-launching)
-int launches_per_pass(const pdot_solver* h) { return (h->host.screen ? 2 : 1) + (split_mode(h) ? 2 : 1); }
+int launches_per_pass(const pdot_solver* h) { return (h->host.screen ? 3 : 1) + (split_mode(h) ? 2 : 1); }
 
 // screening metadata of one slot after its matrix / duals were written outside
 // the STEP kernels: occupancy scanned from the data (or cleared for a zero
@@ -422,9 +422,12 @@ int build_graph(pdot_solver* h, int L) {
 }
 
 int auto_batch(const pdot_solver* h) {
-  // aim for ~10 ms of work per graph launch, 4..64 passes
-  const double est_us = 40.0 * (double)h->m * (double)h->n / 6.0e6 + 8.0;
-  int L = (int)(10000.0 / est_us);
+  // aim for ~10 ms of work per graph launch (dense walker), 4..64 passes; a
+  // screened pass costs about a twentieth of a dense one on sparse plans, so
+  // poll every ~2 ms there (the controller may finish mid-batch: the rest of
+  // the batch's kernels then exit at once)
+  const double est_us = (h->host.screen ? 2.0 : 40.0) * (double)h->m * (double)h->n / 6.0e6 + 8.0;
+  int L = (int)((h->host.screen ? 2000.0 : 10000.0) / est_us);
   if (L < 4) L = 4;
   if (L > 64) L = 64;
   return L;
@@ -614,6 +617,9 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     const size_t o_ucount = take(sizeof(unsigned));
     const size_t o_bcr = take(nbands * h->U * sizeof(uint32_t));
     const size_t o_bct = take(h->T * ncp * sizeof(uint32_t));
+    const size_t o_tflag = take(h->T * h->U);
+    const size_t o_tlist = take(h->T * h->U * sizeof(int32_t));
+    const size_t o_tcount = take(sizeof(unsigned));
     const size_t o_stat = take(pdot::ST_COUNT * sizeof(unsigned long long));
     // cell partials of screened passes (written sparsely, read back only where
     // the bit maps say so: never zeroed)
@@ -644,13 +650,19 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     c.sstat = reinterpret_cast<unsigned long long*>(base + o_stat);
     c.bcr = reinterpret_cast<uint32_t*>(base + o_bcr);
     c.bct = reinterpret_cast<uint32_t*>(base + o_bct);
+    c.tileflag = reinterpret_cast<uint8_t*>(base + o_tflag);
+    c.tlist = reinterpret_cast<int32_t*>(base + o_tlist);
+    c.tcount = reinterpret_cast<unsigned*>(base + o_tcount);
     c.ccol = reinterpret_cast<double*>(base + o_ccol);
     c.crow = reinterpret_cast<double*>(base + o_crow);
     c.cscal = reinterpret_cast<double*>(base + o_cscal);
     c.ncp = ncp;
     c.mpad = mpad;
+    // PDOT_SCREEN=0/1 forces the walker; by default the screened pass is used
+    // from 2^22 plan entries up (below that the plan is L2-resident and the
+    // single dense launch per pass wins, e.g. 1024^2)
     const char* env = getenv("PDOT_SCREEN");
-    h->screen_on = !(env && atoi(env) == 0);
+    h->screen_on = env ? atoi(env) != 0 : (double)m_total * (double)n >= (double)(1 << 22);
   }
   if (nranks > 1) {  // peer-memory exchange buffer (separate allocation: shareable by CUDA IPC)
     h->xbuf_bytes = (size_t)(2 * pdot::kGroups * h->gstride) * sizeof(double) +
@@ -1405,8 +1417,9 @@ int pdot_set_screening(pdot_solver* h, int on) {
   return PDOT_OK;
 }
 
-int pdot_screen_stats(pdot_solver* h, int reset, unsigned long long* out8) {
-  if (!h || !out8) return set_err(PDOT_EINVAL, "null argument");
+int pdot_screen_stats(pdot_solver* h, int reset, unsigned long long* out12) {
+  if (!h || !out12) return set_err(PDOT_EINVAL, "null argument");
+  unsigned long long* out8 = out12;
   DeviceGuard dg(h->device);
   unsigned long long st[pdot::ST_COUNT];
   CK(cudaStreamSynchronize(h->stream));
@@ -1419,7 +1432,16 @@ int pdot_screen_stats(pdot_solver* h, int reset, unsigned long long* out8) {
   out8[5] = st[pdot::ST_K1_NS];
   out8[6] = (unsigned long long)h->host.screen;
   out8[7] = (unsigned long long)(h->host.nbands * h->host.ncells);
-  if (reset) CK(cudaMemset(h->host.sstat, 0, 7 * sizeof(unsigned long long)));
+  out12[8] = st[pdot::ST_K2_MAIN];
+  out12[9] = st[pdot::ST_K2_CTL];
+  out12[10] = st[pdot::ST_T0K0];
+  out12[11] = st[pdot::ST_T1K0];
+  out12[12] = st[pdot::ST_DONE0];
+  if (reset) {
+    CK(cudaMemset(h->host.sstat, 0, 7 * sizeof(unsigned long long)));
+    CK(cudaMemset(h->host.sstat + pdot::ST_K2_MAIN, 0, 2 * sizeof(unsigned long long)));
+    CK(cudaMemset(h->host.sstat + pdot::ST_T0K0, 0, 3 * sizeof(unsigned long long)));
+  }
   return PDOT_OK;
 }
 

@@ -120,8 +120,8 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
   double cacc[NQ][2];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = 0.0;
-  BandCols<NQ> bcol;
-  bcol.reset();
+  BandAcc<NQ, NS> bacc;
+  bacc.reset();
   double sacc[NS], ws[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) sacc[s] = ws[s] = 0.0;
@@ -209,8 +209,8 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         push_rows<NQ, R>(rv, rowbuf, it * R, true);
-        bcol.add(it % kStagesPerBand, ps);
-        if ((it % kStagesPerBand) == kStagesPerBand - 1 || it == nst - 1) band_close<NQ, NS>(bcol, cacc, sacc, ws);
+        bacc.stage(it % kStagesPerBand, ps, sacc);
+        if ((it % kStagesPerBand) == kStagesPerBand - 1 || it == nst - 1) band_close<NQ, NS>(bacc, cacc, ws);
       }
     } else {
       for (int it = 0; it < nst; ++it) {
@@ -255,8 +255,8 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         push_rows<NQ, R>(rv, rowbuf, it * R, true);
-        bcol.add(it % kStagesPerBand, ps);
-        if ((it % kStagesPerBand) == kStagesPerBand - 1 || it == nst - 1) band_close<NQ, NS>(bcol, cacc, sacc, ws);
+        bacc.stage(it % kStagesPerBand, ps, sacc);
+        if ((it % kStagesPerBand) == kStagesPerBand - 1 || it == nst - 1) band_close<NQ, NS>(bacc, cacc, ws);
       }
     }
   }

@@ -1,6 +1,5 @@
-timeout 900 python -m pytest tests/test_gpu_screen.py -x -q 2>&1 | tail -2
-timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3
 timeout 600 python bench.py --no-cpu > gpurun_out/scr_c3.json 2> gpurun_out/scr_c3.err; echo c3 rc=$?
-tail -2 gpurun_out/scr_c3.err
-B="python bench.py --steps 120 --warmup 5 --no-tol --no-e2e --no-variant --no-cpu"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -c 2000 --csv --log-file gpurun_out/launches_unit_warm.csv $B > /dev/null 2>gpurun_out/ncu2.err; echo ncu2 rc=$?
+timeout 600 python bench.py --config c1 --no-cpu > gpurun_out/scr_c1.json 2> gpurun_out/scr_c1.err; echo c1 rc=$?
+PDOT_SCREEN=1 timeout 600 python bench.py --config c1 --no-cpu --no-e2e --no-variant > gpurun_out/scr_c1s.json 2> gpurun_out/scr_c1s.err; echo c1s rc=$?
+timeout 600 python bench.py --config c2 --no-cpu > gpurun_out/scr_c2.json 2> gpurun_out/scr_c2.err; echo c2 rc=$?
+PDOT_SCREEN=0 timeout 600 python bench.py --config c2 --no-cpu --no-e2e --no-variant > gpurun_out/scr_c2d.json 2> gpurun_out/scr_c2d.err; echo c2d rc=$?

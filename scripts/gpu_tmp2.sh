@@ -1,0 +1,1 @@
+timeout 600 python scripts/e2e_probe.py 128 2>&1 | tail -8

@@ -29,7 +29,7 @@ rows = []
 for k in range(max_passes):
     _lib.check(h.lib.pdot_advance(h.ptr, 1, ctypes.byref(prog)))
     st = h.screen_stats()
-    d = {key: st[key] - prev[key] for key in ("passes", "active_cells", "tiles", "k1_bytes", "k1_ns")}
+    d = {key: st[key] - prev[key] for key in ("passes", "active_cells", "cells_visited", "k1_bytes", "k1_ns", "k2_main_ns", "k2_ctl_ns", "ctl_reduce_ns", "ctl_logic_ns", "ctl_publish_ns")}
     prev = st
     d["it"] = prog.iterations
     d["frac"] = d["active_cells"] / st["cells_per_plan"]
@@ -42,9 +42,15 @@ steps = [x for x in rows if x["passes"]]
 summary = {"r": r, "iterations": res.iterations, "passes": len(rows),
            "mean_frac": sum(x["frac"] for x in steps) / len(steps),
            "mean_k1_us": sum(x["k1_ns"] for x in steps) / len(steps) / 1e3,
-           "mean_tiles": sum(x["tiles"] for x in steps) / len(steps),
+           "mean_cells_visited": sum(x["cells_visited"] for x in steps) / len(steps),
+           "mean_k2_main_us": sum(x["k2_main_ns"] for x in steps) / len(steps) / 1e3,
+           "mean_k2_ctl_us": sum(x["k2_ctl_ns"] for x in steps) / len(steps) / 1e3,
+           "mean_ctl_reduce_us": sum(x["ctl_reduce_ns"] for x in steps) / len(steps) / 1e3,
+           "mean_ctl_logic_us": sum(x["ctl_logic_ns"] for x in steps) / len(steps) / 1e3,
+           "mean_ctl_publish_us": sum(x["ctl_publish_ns"] for x in steps) / len(steps) / 1e3,
            "mean_k1_MB": sum(x["k1_bytes"] for x in steps) / len(steps) / 1e6}
 print(json.dumps(summary))
 for i in range(0, len(rows), max(1, len(rows) // 60)):
     x = rows[i]
-    print(i, x["it"], "frac %.4f tiles %d MB %.1f us %.1f" % (x["frac"], x["tiles"], x["k1_bytes"] / 1e6, x["k1_ns"] / 1e3))
+    print(i, x["it"], "frac %.4f cells %d MB %.1f K1 us %.1f K2 us %.1f + %.1f" % (
+        x["frac"], x["cells_visited"], x["k1_bytes"] / 1e6, x["k1_ns"] / 1e3, x["k2_main_ns"] / 1e3, x["k2_ctl_ns"] / 1e3))
