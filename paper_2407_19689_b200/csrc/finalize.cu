@@ -127,6 +127,15 @@ __device__ void wait_exchange(Ctl& c) {
 // ---------------------------------------------------------------------------
 // Sum of the column partials of reduction group g over its row tiles, in tile
 // order: the within-group order that every GPU count reproduces.
+// the flags of up to 32 consecutive tiles (stride apart) as a bit mask
+__device__ __forceinline__ uint32_t flag_mask(const uint8_t* f, int64_t stride, int64_t count) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    if (k < count && __ldg(f + k * stride)) m |= 1u << k;
+  return m;
+}
+
 template <int NQ>
 __device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j, double2 (&acc)[NQ]) {
 #pragma unroll
@@ -134,26 +143,39 @@ __device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j,
   const int64_t ta = imax64((int64_t)g * c.GS, c.t0);
   const int64_t tb = imin64(imin64((int64_t)(g + 1) * c.GS, c.Tg), c.t0 + c.T);
   if (j >= c.n) return;
-  // tiles whose flag is 0 were screened out entirely: their partials are +0
+  // tiles whose flag is 0 were screened out entirely: their partials are +0;
+  // the flags are read first, then the partials of the flagged tiles 4 at a time
   const uint8_t* flags = c.tileflag + (j / kTileN);
-  for (int64_t t0 = ta; t0 < tb; t0 += 4) {
-    double2 v[4][NQ];
+  for (int64_t tc = ta; tc < tb; tc += 32) {
+    uint32_t m = flag_mask(flags + (tc - c.t0) * c.U, c.U, tb - tc);
+    while (m) {
+      int tk[4];
+      int cnt = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const bool on = t0 + k < tb && __ldg(flags + (t0 + k - c.t0) * c.U);
-#pragma unroll
-      for (int q = 0; q < NQ; ++q)
-        v[k][q] = on ? __ldcg(reinterpret_cast<const double2*>(c.colpart + ((t0 + k - c.t0) * NQ + q) * c.ldx + j))
-                     : make_double2(0.0, 0.0);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (t0 + k < tb)
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          acc[q].x += v[k][q].x;
-          acc[q].y += v[k][q].y;
+      for (int e = 0; e < 4; ++e) {
+        tk[e] = 0;
+        if (m) {
+          tk[e] = __ffs(m) - 1;
+          m &= m - 1;
+          cnt = e + 1;
         }
+      }
+      double2 v[4][NQ];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          v[e][q] = e < cnt ? __ldcg(reinterpret_cast<const double2*>(c.colpart + ((tc + tk[e] - c.t0) * NQ + q) * c.ldx + j))
+                            : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < cnt)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            acc[q].x += v[e][q].x;
+            acc[q].y += v[e][q].y;
+          }
+    }
   }
 }
 
@@ -226,19 +248,31 @@ __device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ]) {
   for (int q = 0; q < NQ; ++q) row[q] = 0.0;
   if (i >= c.m) return;
   const uint8_t* flags = c.tileflag + (i / c.TM) * c.U;  // screened-out tiles: partials +0
-  for (int64_t u0 = 0; u0 < c.U; u0 += 4) {
-    double v[4][NQ];
+  for (int64_t uc = 0; uc < c.U; uc += 32) {
+    uint32_t m = flag_mask(flags + uc, 1, c.U - uc);
+    while (m) {
+      int uk[4];
+      int cnt = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const bool on = u0 + k < c.U && __ldg(flags + u0 + k);
+      for (int e = 0; e < 4; ++e) {
+        uk[e] = 0;
+        if (m) {
+          uk[e] = __ffs(m) - 1;
+          m &= m - 1;
+          cnt = e + 1;
+        }
+      }
+      double v[4][NQ];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) v[k][q] = on ? __ldcg(c.rowpart + ((u0 + k) * NQ + q) * c.m + i) : 0.0;
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) v[e][q] = e < cnt ? __ldcg(c.rowpart + ((uc + uk[e]) * NQ + q) * c.m + i) : 0.0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < cnt)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) row[q] += v[e][q];
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (u0 + k < c.U)
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) row[q] += v[k][q];
   }
 }
 
@@ -248,13 +282,16 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
   for (int s = 0; s < kMaxColScal; ++s) vals[s] = 0.0;
   int64_t j;
   if (op == OP_STEP) {
+    // the vectors of this thread's column, loaded before the (long) column sums
+    const int64_t jp = (int64_t)b * kColsPerBlock + threadIdx.x;
+    const bool own = threadIdx.x < kColsPerBlock && jp < c.n;
+    const double qj = own ? __ldcg(c.slot[c.sX].q + jp) : 0.0;
+    const double gj = own ? __ldg(c.g + jp) : 0.0;
+    const double qaj = own ? __ldcg(c.slot[c.sA].q + jp) : 0.0;
     double col[4];
     column_sums<4>(c, b, col, j, smem, mode);
     double qb = -INFINITY, qab = -INFINITY;  // screening bounds of q+ and the dual average
     if (threadIdx.x < kColsPerBlock && j < c.n) {
-      const Slot& sx = c.slot[c.sX];
-      const Slot& sa = c.slot[c.sA];
-      const double qj = sx.q[j], gj = c.g[j];
       const double qn = qj + c.sigma * (gj - col[0]);        // pdhg.py:128
       const double dq = qn - qj;                              // pdhg.py:141
       c.slot[c.sXn].q[j] = qn;
@@ -266,7 +303,6 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
       vals[4] = gj * qn;
       vals[6] = qn * qn;
       if (!c.unit || c.unit_avg) {
-        const double qaj = sa.q[j];
         const double qan = qaj + div_by_count(qn - qaj, c.kd_dual, c.rkd_dual);  // pdhg.py:317
         c.slot[c.sAn].q[j] = qan;
         qab = qan;
@@ -357,13 +393,14 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
     const int64_t i = i0 + r;
     const bool ok = r < rows;
     if (op == OP_STEP) {
+      // the vectors of this row, loaded before the (long) row sums
+      const double pi = ok ? __ldcg(c.slot[c.sX].p + i) : 0.0;
+      const double fi = ok ? __ldg(c.f + i) : 0.0;
+      const double pai = ok ? __ldcg(c.slot[c.sA].p + i) : 0.0;
       double row[4];
       row_sums<4>(c, ok ? i : c.m, row);
       double pb = -INFINITY, pab = -INFINITY;  // screening bounds of p+ and the dual average
       if (ok) {
-        const Slot& sx = c.slot[c.sX];
-        const Slot& sa = c.slot[c.sA];
-        const double pi = sx.p[i], fi = c.f[i];
         const double pn = pi + c.sigma * (fi - row[0]);       // pdhg.py:127
         const double dp = pn - pi;                             // pdhg.py:140
         c.slot[c.sXn].p[i] = pn;
@@ -375,7 +412,6 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
         vals[4] += fi * pn;
         vals[6] += pn * pn;
         if (!c.unit || c.unit_avg) {
-          const double pai = sa.p[i];
           const double pan = pai + div_by_count(pn - pai, c.kd_dual, c.rkd_dual);  // pdhg.py:316
           c.slot[c.sAn].p[i] = pan;
           pab = pan;
@@ -452,16 +488,28 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
   if (threadIdx.x < ns) {
     const uint8_t* flags = c.tileflag + (int64_t)t * c.U;
     double acc = 0.0;
-    for (int64_t u0 = 0; u0 < c.U; u0 += 8) {
-      double v[8];
+    for (int64_t uc = 0; uc < c.U; uc += 32) {
+      uint32_t m = flag_mask(flags + uc, 1, c.U - uc);
+      while (m) {
+        int uk[8];
+        int cnt = 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        v[k] = (u0 + k < c.U && __ldg(flags + u0 + k))
-                   ? __ldcg(c.tilescal + ((int64_t)t * c.U + u0 + k) * kMaxNS + threadIdx.x)
-                   : 0.0;
+        for (int e = 0; e < 8; ++e) {
+          uk[e] = 0;
+          if (m) {
+            uk[e] = __ffs(m) - 1;
+            m &= m - 1;
+            cnt = e + 1;
+          }
+        }
+        double v[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (u0 + k < c.U) acc += v[k];
+        for (int e = 0; e < 8; ++e)
+          v[e] = e < cnt ? __ldcg(c.tilescal + ((int64_t)t * c.U + uc + uk[e]) * kMaxNS + threadIdx.x) : 0.0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (e < cnt) acc += v[e];
+      }
     }
     c.rowblk[(int64_t)t * kMaxRowScal + nr + threadIdx.x] = acc;
   }
@@ -823,21 +871,27 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   const int op = force_op >= 0 ? force_op : c.op;
   const bool timed = op == OP_STEP && unit_pass(c, op) && c.sstat;  // K2 timing of screened STEP passes
   if (timed && blockIdx.x == 0 && threadIdx.x == 0) c.sstat[ST_K2_T0] = globaltimer_ns();
-  if ((int64_t)blockIdx.x < c.CB) {
+  if (timed && c.kdbg && threadIdx.x == 0) c.kdbg[blockIdx.x * 4 + 0] = globaltimer_ns();
+  // row blocks first (they carry the longer chains); FIN_B has column blocks only
+  const int64_t nrow_blocks = mode == FIN_B ? 0 : c.T;
+  if ((int64_t)blockIdx.x >= nrow_blocks) {
+    const int b = (int)(blockIdx.x - nrow_blocks);
     if (mode == FIN_A) {
-      if (op == OP_STEP) column_group_partials<4>(c, blockIdx.x);
-      else column_group_partials<1>(c, blockIdx.x);
+      if (op == OP_STEP) column_group_partials<4>(c, b);
+      else column_group_partials<1>(c, b);
     } else {
-      column_block(c, op, blockIdx.x, smem, mode);
+      column_block(c, op, b, smem, mode);
     }
   } else {
-    row_block(c, op, (int)(blockIdx.x - c.CB), smem);
+    row_block(c, op, (int)blockIdx.x, smem);
   }
 
+  if (timed && c.kdbg && threadIdx.x == 0) c.kdbg[blockIdx.x * 4 + 1] = globaltimer_ns();
   if (mode == FIN_A && c.p2p) __threadfence_system();  // remote group stores before the ticket
   else __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) is_last = atomicAdd(c.counter, 1u) == gridDim.x - 1;
+  if (timed && c.kdbg && threadIdx.x == 0) c.kdbg[blockIdx.x * 4 + 2] = globaltimer_ns();
   __syncthreads();
   if (!is_last) return;
   __threadfence();

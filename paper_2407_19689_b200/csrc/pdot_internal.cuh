@@ -207,6 +207,7 @@ struct Ctl {
   double* crow;              // [ncp][kMaxNQ][mpad]   cell row partials (8-lane butterfly per row)
   double* cscal;             // [nbands][ncp][kMaxNS] cell scalars
   unsigned long long* sstat; // [ST_COUNT]
+  unsigned long long* kdbg;  // PDOT_K2_TRACE=1: per-block K2 timestamps of the last screened STEP pass
   unsigned int* counter;   // last-block-done counter for the finalize kernel
   Status* status;          // host mapped
   Event* ring;             // host mapped, kRingCap entries

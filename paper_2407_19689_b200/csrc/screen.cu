@@ -216,52 +216,102 @@ __device__ __forceinline__ CellGeo cell_geo(const Ctl& c, uint32_t entry) {
 // row 2 rg + rr, column e; sacc: the lane's stage scalar partials (its two rows,
 // element order), so the band partial is (s0 + s1) + (s2 + s3) over the row
 // groups (masks 8, 16) and the cell value the 8-lane butterfly on top.
+// Transposed butterfly with an explicit mask order M[0..NM): the first log2(V)
+// masks route values (lane bit of mask k selects index bit log2(V)-1-k), the
+// rest add the remaining value.  Every sum is the xor-pairing tree of the masks
+// in order, the same tree a plain butterfly over those masks builds.
+template <int V, int NM>
+__device__ __forceinline__ void tsum(double (&v)[V], const int (&M)[NM]) {
+#pragma unroll
+  for (int k = 0, w = V / 2; k < NM; ++k) {
+    const int mask = M[k];
+    if (w >= 1) {
+      const bool upper = (threadIdx.x & mask) != 0;
+#pragma unroll
+      for (int t = 0; t < V / 2; ++t) {
+        if (t < w) {
+          const double send = upper ? v[t] : v[t + w];
+          const double keep = upper ? v[t + w] : v[t];
+          v[t] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+        }
+      }
+      w /= 2;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], mask);
+    }
+  }
+}
+// first value index held by this lane after tsum<V> (it holds indices idx .. idx + V/2^steps - 1)
+template <int V, int NM>
+__device__ __forceinline__ int tsum_index(const int (&M)[NM]) {
+  constexpr int lg = log2_pow2<V>();
+  int idx = 0;
+#pragma unroll
+  for (int k = 0; k < NM && k < lg; ++k) idx |= ((threadIdx.x & M[k]) ? 1 : 0) << (lg - 1 - k);
+  return idx;
+}
+
+// Partial writes shared by every cell op.  o[rr][q][e]: the lane's outputs for
+// row 2 rg + rr, column e; sacc: the lane's stage scalar partials (its two rows,
+// element order), so the band partial is (s0 + s1) + (s2 + s3) over the row
+// groups (masks 8, 16) and the cell value the 8-lane butterfly on top.  All
+// three reductions use transposed butterflies (a few shuffles per value).
 template <int NQ, int NS>
 __device__ __forceinline__ void cell_flush(const Ctl& c, const CellGeo& g, const double (&o)[2][NQ][2],
                                           const double (&sacc)[NS]) {
-  // column band partial: pair sum of the lane's two rows, then masks 8, 16
-  double2 cs[NQ];
+  // column band partial: pair sum of the lane's two rows, then masks 8, 16;
+  // afterwards lane (rg, cp) holds (x, y) of quantity q(rg) for its column pair
+  {
+    constexpr int V = 2 * NQ;
+    double v[V];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    double x = o[0][q][0] + o[1][q][0], y = o[0][q][1] + o[1][q][1];
-    x += __shfl_xor_sync(0xffffffffu, x, 8);
-    y += __shfl_xor_sync(0xffffffffu, y, 8);
-    x += __shfl_xor_sync(0xffffffffu, x, 16);
-    y += __shfl_xor_sync(0xffffffffu, y, 16);
-    cs[q] = make_double2(x, y);
-  }
-  if (g.rg == 0 && g.v0) {
-    DCHECK(g.j + 1 < c.ldx, "ccol j", g.j, c.ldx);
-#pragma unroll
-    for (int q = 0; q < NQ; ++q)
-      *reinterpret_cast<double2*>(c.ccol + (g.band * kMaxNQ + q) * c.ldx + g.j) = cs[q];
+    for (int q = 0; q < NQ; ++q) {
+      v[2 * q] = o[0][q][0] + o[1][q][0];
+      v[2 * q + 1] = o[0][q][1] + o[1][q][1];
+    }
+    constexpr int M[2] = {8, 16};
+    tsum<V, 2>(v, M);
+    const int idx = tsum_index<V, 2>(M);
+    if (g.v0) {
+      if (NQ == 4) {
+        *reinterpret_cast<double2*>(c.ccol + (g.band * kMaxNQ + idx / 2) * c.ldx + g.j) = make_double2(v[0], v[1]);
+      } else if (g.rg < 2) {  // NQ == 1: rg 0 holds x, rg 1 holds y
+        c.ccol[g.band * kMaxNQ * c.ldx + g.j + idx] = v[0];
+      }
+    }
   }
   // row values: 8-lane transposed butterfly over the column pairs
-  constexpr int V = 2 * NQ;
-  double rv[V];
+  {
+    constexpr int V = 2 * NQ;
+    double rv[V];
 #pragma unroll
-  for (int rr = 0; rr < 2; ++rr)
+    for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) rv[rr * NQ + q] = o[rr][q][0] + o[rr][q][1];
-  warp_transpose_sum<V, 8>(rv);
-  if (transpose_is_writer<V, 8>(threadIdx.x & 31)) {
-    const int idx = transpose_owner_index<V>(g.cp);
-    const int r = 2 * g.rg + idx / NQ, q = idx % NQ;
-    DCHECK(g.cell < c.ncp && (r >= g.rows || g.i0 + r < c.mpad), "crow", g.cell, g.i0 + r);
-    if (r < g.rows) c.crow[(g.cell * kMaxNQ + q) * c.mpad + g.i0 + r] = rv[0];
+      for (int q = 0; q < NQ; ++q) rv[rr * NQ + q] = o[rr][q][0] + o[rr][q][1];
+    warp_transpose_sum<V, 8>(rv);
+    if (transpose_is_writer<V, 8>(threadIdx.x & 31)) {
+      const int idx = transpose_owner_index<V>(g.cp);
+      const int r = 2 * g.rg + idx / NQ, q = idx % NQ;
+      DCHECK(g.cell < c.ncp && (r >= g.rows || g.i0 + r < c.mpad), "crow", g.cell, g.i0 + r);
+      if (r < g.rows) c.crow[(g.cell * kMaxNQ + q) * c.mpad + g.i0 + r] = rv[0];
+    }
   }
-  // scalars: stage partials pairwise over the row groups, then over the column pairs
-  double sv[NS];
+  // scalars: stage partials pairwise over the row groups (masks 8, 16), then
+  // the column pairs (masks 1, 2, 4)
+  {
+    constexpr int V = NS <= 1 ? 1 : NS <= 2 ? 2 : NS <= 4 ? 4 : 8;
+    double v[V];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    double x = sacc[s];
-    x += __shfl_xor_sync(0xffffffffu, x, 8);
-    x += __shfl_xor_sync(0xffffffffu, x, 16);
-    sv[s] = group_sum<8>(x);
-  }
-  if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-    for (int s = 0; s < NS; ++s) c.cscal[(g.band * c.ncp + g.cell) * kMaxNS + s] = sv[s];
+    for (int s = 0; s < V; ++s) v[s] = s < NS ? sacc[s] : 0.0;
+    constexpr int M[5] = {8, 16, 1, 2, 4};
+    tsum<V, 5>(v, M);
+    const int idx = tsum_index<V, 5>(M);
+    // every lane holds the total of index idx; the lanes with cp bits above the
+    // routing steps clear write it
+    constexpr int lg = log2_pow2<V>();
+    const int routed = lg >= 3 ? 1 : 0;  // mask 1 (cp bit 0) routed for V = 8
+    if (idx < NS && (g.cp >> routed) == 0)
+      c.cscal[(g.band * c.ncp + g.cell) * kMaxNS + idx] = v[0];
   }
 }
 

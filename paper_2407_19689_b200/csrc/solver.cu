@@ -661,6 +661,10 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     // PDOT_SCREEN=0/1 forces the walker; by default the screened pass is used
     // from 2^22 plan entries up (below that the plan is L2-resident and the
     // single dense launch per pass wins, e.g. 1024^2)
+    if (getenv("PDOT_K2_TRACE") && atoi(getenv("PDOT_K2_TRACE")) != 0) {
+      unsigned long long* kd = nullptr;
+      if (cudaMalloc(&kd, (size_t)(h->CB + h->T) * 4 * sizeof(unsigned long long)) == cudaSuccess) c.kdbg = kd;
+    }
     const char* env = getenv("PDOT_SCREEN");
     h->screen_on = env ? atoi(env) != 0 : (double)m_total * (double)n >= (double)(1 << 22);
   }
@@ -1396,6 +1400,17 @@ int pdot_p2p_link_local(pdot_solver** hs, int count) {
     if (int rc = upload_ctl(hs[i])) return rc;
   }
   return PDOT_OK;
+}
+
+// debugging aid (PDOT_K2_TRACE=1): per-block K2 timestamps {entry, work done,
+// ticket, 0} of the last screened STEP pass; returns the block count
+int pdot_debug_k2(pdot_solver* h, unsigned long long* out, int64_t cap) {
+  if (!h || !h->host.kdbg) return 0;
+  DeviceGuard dg(h->device);
+  const int64_t nb = h->CB + h->T;
+  const int64_t k = std::min<int64_t>(cap, nb * 4);
+  if (cudaMemcpy(out, h->host.kdbg, k * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return (int)nb;
 }
 
 int pdot_set_screening(pdot_solver* h, int on) {

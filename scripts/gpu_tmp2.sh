@@ -1,1 +1,1 @@
-timeout 600 python scripts/e2e_probe.py 128 2>&1 | tail -8
+timeout 300 python scripts/k2_trace.py 128 400 2>&1 | tail -4

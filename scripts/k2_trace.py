@@ -1,0 +1,34 @@
+"""Debug tooling: per-block K2 timeline of the last screened STEP pass (PDOT_K2_TRACE=1)."""
+import ctypes
+import os
+import sys
+
+os.environ["PDOT_K2_TRACE"] = "1"
+sys.path.insert(0, ".")
+import numpy as np  # noqa: E402
+import paper_2407_19689_b200 as pd  # noqa: E402
+from paper_2407_19689_b200 import _lib, device  # noqa: E402
+
+dp = pd.DeviceProblem.sqeuclid_grid(int(sys.argv[1]) if len(sys.argv) > 1 else 128, 0)
+it = int(sys.argv[2]) if len(sys.argv) > 2 else 400
+(_, h), rep = pd.solve_device(dp, pd.SolverConfig(tol=1e-12, max_iters=5))
+h.screen_stats(reset=True)
+(_, h), rep = pd.solve_device(dp, pd.SolverConfig(tol=1e-12, max_iters=it))
+lib = _lib.load()
+lib.pdot_debug_k2.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int64]
+buf = (ctypes.c_ulonglong * 8192)()
+nb = lib.pdot_debug_k2(h.ptr, buf, 8192)
+a = np.array(buf[:nb * 4], dtype=np.float64).reshape(nb, 4)
+t0 = a[:, 0].min()
+a[:, :3] -= t0
+T = dp.m // 128
+print("blocks", nb, "row blocks", T)
+for name, sl in (("row", slice(0, T)), ("column", slice(T, nb))):
+    x = a[sl]
+    print(f"{name}: entry {x[:,0].min():.0f}..{x[:,0].max():.0f} ns, work {np.median(x[:,1]-x[:,0]):.0f} "
+          f"(max {(x[:,1]-x[:,0]).max():.0f}) ns, ticket at {x[:,2].min():.0f}..{x[:,2].max():.0f} ns")
+st = h.screen_stats()
+p = max(1, st["passes"])
+print("per pass: K1 %.1f us, K2 to last ticket %.1f us, controller %.1f us (reduce %.1f, decide %.1f, publish %.1f)" % (
+    st["k1_ns"] / p / 1e3, st["k2_main_ns"] / p / 1e3, st["k2_ctl_ns"] / p / 1e3, st["ctl_reduce_ns"] / p / 1e3,
+    st["ctl_logic_ns"] / p / 1e3, st["ctl_publish_ns"] / p / 1e3))
