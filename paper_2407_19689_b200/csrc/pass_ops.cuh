@@ -288,17 +288,37 @@ struct BandAcc {
   }
 };
 
-// end of a band: band column partial into the tile partial, band scalar
-// partials -> warp totals (identical in every lane); reset
+// end of a band: band column partial into the tile partial; band scalar
+// partials -> warp totals with a transposed butterfly (masks 1..16), lane L
+// accumulating the scalar band_scalar_index(L) into ws; reset
+template <int NS>
+struct ScalPad {
+  static constexpr int V = NS <= 1 ? 1 : NS <= 2 ? 2 : NS <= 4 ? 4 : 8;
+};
+template <int NS>
+__device__ __forceinline__ int band_scalar_index() {
+  constexpr int M[5] = {1, 2, 4, 8, 16};
+  return tsum_index<ScalPad<NS>::V, 5>(M);
+}
+// lanes holding distinct scalars (the others hold copies)
+template <int NS>
+__device__ __forceinline__ bool band_scalar_writer() {
+  return ((threadIdx.x & 31) >> log2_pow2<ScalPad<NS>::V>()) == 0;
+}
 template <int NQ, int NS>
-__device__ __forceinline__ void band_close(BandAcc<NQ, NS>& ba, double (&cacc)[NQ][2], double (&ws)[NS]) {
+__device__ __forceinline__ void band_close(BandAcc<NQ, NS>& ba, double (&cacc)[NQ][2], double& ws) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     cacc[q][0] += ba.ca[q][0] + ba.cb[q][0];
     cacc[q][1] += ba.ca[q][1] + ba.cb[q][1];
   }
+  constexpr int V = ScalPad<NS>::V;
+  constexpr int M[5] = {1, 2, 4, 8, 16};
+  double v[V];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) ws[s] += group_sum<32>(ba.sa[s] + ba.sb[s]);
+  for (int s = 0; s < V; ++s) v[s] = s < NS ? ba.sa[s] + ba.sb[s] : 0.0;
+  tsum<V, 5>(v, M);
+  ws += v[0];
   ba.reset();
 }
 
@@ -307,7 +327,7 @@ __device__ __forceinline__ void band_close(BandAcc<NQ, NS>& ba, double (&cacc)[N
 // smem entries -> fixed-order sum over warps).
 template <int NQ, int NS>
 __device__ __forceinline__ void tile_flush(const Ctl& c, const Geo& g, bool worker, double (&cacc)[NQ][2],
-                                           const double (&ws)[NS], double* rowbuf, double* sbuf) {
+                                           double ws, double* rowbuf, double* sbuf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (worker && g.v0) {
 #pragma unroll
@@ -315,9 +335,9 @@ __device__ __forceinline__ void tile_flush(const Ctl& c, const Geo& g, bool work
       *reinterpret_cast<double2*>(c.colpart + (g.tt * NQ + q) * c.ldx + g.j) =
           make_double2(cacc[q][0], cacc[q][1]);
   }
-  if (worker && lane == 0) {
-#pragma unroll
-    for (int s = 0; s < NS; ++s) sbuf[warp * 8 + s] = ws[s];
+  if (worker && band_scalar_writer<NS>()) {
+    const int s = band_scalar_index<NS>();
+    if (s < NS) sbuf[warp * 8 + s] = ws;
   }
   __syncthreads();
   const int nrow_vals = g.rows * NQ;
@@ -387,9 +407,9 @@ __device__ __forceinline__ void tile_pass(const Op& op, const Ctl& c, double* sm
   for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = 0.0;
   BandAcc<NQ, NS> bacc;
   bacc.reset();
-  double sacc[NS], ws[NS];
+  double sacc[NS], ws = 0.0;
 #pragma unroll
-  for (int s = 0; s < NS; ++s) sacc[s] = ws[s] = 0.0;
+  for (int s = 0; s < NS; ++s) sacc[s] = 0.0;
   typename Op::Col cl;
   if (worker) op.load_col(cl, g);
 

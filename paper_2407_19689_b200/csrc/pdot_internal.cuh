@@ -276,6 +276,41 @@ __device__ __forceinline__ bool transpose_is_writer(int lane) {
   return ((lane & (W - 1)) >> log2_pow2<V>()) == 0;
 }
 
+// Transposed butterfly with an explicit mask order M[0..NM): the first log2(V)
+// masks route values (lane bit of mask k selects index bit log2(V)-1-k), the
+// rest add the remaining value.  Every sum is the xor-pairing tree of the masks
+// in order, the same tree a plain butterfly over those masks builds.
+template <int V, int NM>
+__device__ __forceinline__ void tsum(double (&v)[V], const int (&M)[NM]) {
+#pragma unroll
+  for (int k = 0, w = V / 2; k < NM; ++k) {
+    const int mask = M[k];
+    if (w >= 1) {
+      const bool upper = (threadIdx.x & mask) != 0;
+#pragma unroll
+      for (int t = 0; t < V / 2; ++t) {
+        if (t < w) {
+          const double send = upper ? v[t] : v[t + w];
+          const double keep = upper ? v[t + w] : v[t];
+          v[t] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+        }
+      }
+      w /= 2;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], mask);
+    }
+  }
+}
+// first value index held by this lane after tsum<V> (it holds indices idx .. idx + V/2^steps - 1)
+template <int V, int NM>
+__device__ __forceinline__ int tsum_index(const int (&M)[NM]) {
+  constexpr int lg = log2_pow2<V>();
+  int idx = 0;
+#pragma unroll
+  for (int k = 0; k < NM && k < lg; ++k) idx |= ((threadIdx.x & M[k]) ? 1 : 0) << (lg - 1 - k);
+  return idx;
+}
+
 // xor butterfly of one value over groups of W lanes, masks ascending
 template <int W = 32>
 __device__ __forceinline__ double group_sum(double x) {

@@ -122,9 +122,9 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
   for (int q = 0; q < NQ; ++q) cacc[q][0] = cacc[q][1] = 0.0;
   BandAcc<NQ, NS> bacc;
   bacc.reset();
-  double sacc[NS], ws[NS];
+  double sacc[NS], ws = 0.0;
 #pragma unroll
-  for (int s = 0; s < NS; ++s) sacc[s] = ws[s] = 0.0;
+  for (int s = 0; s < NS; ++s) sacc[s] = 0.0;
   constexpr int kStagesPerBand = kBand / R;
 
   if (!worker) {
@@ -168,7 +168,12 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
       // full tile: no masks, running output pointers
       double* xo = op.Xn + g.i0 * c.ldx + g.j;
       double* ao = op.An + g.i0 * c.ldx + g.j;
-      for (int it = 0; it < nst; ++it) {
+      // a full tile has whole bands: unroll the band's 4 stages so the stage
+      // index of the band accumulators is a compile-time constant
+      for (int it0 = 0; it0 < nst; it0 += kStagesPerBand) {
+#pragma unroll
+       for (int k = 0; k < kStagesPerBand; ++k) {
+        const int it = it0 + k;
         const int s = it % kStages;
         mbar_wait(&full[s], (it / kStages) & 1);
         const unsigned char* st = stages + s * kStageBytes;
@@ -209,8 +214,9 @@ __device__ __forceinline__ void step_tma(const StepOp& op, const Ctl& c, unsigne
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         push_rows<NQ, R>(rv, rowbuf, it * R, true);
-        bacc.stage(it % kStagesPerBand, ps, sacc);
-        if ((it % kStagesPerBand) == kStagesPerBand - 1 || it == nst - 1) band_close<NQ, NS>(bacc, cacc, ws);
+        bacc.stage(k, ps, sacc);
+       }
+        band_close<NQ, NS>(bacc, cacc, ws);
       }
     } else {
       for (int it = 0; it < nst; ++it) {
