@@ -872,6 +872,7 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   const bool timed = op == OP_STEP && unit_pass(c, op) && c.sstat;  // K2 timing of screened STEP passes
   if (timed && blockIdx.x == 0 && threadIdx.x == 0) c.sstat[ST_K2_T0] = globaltimer_ns();
   if (timed && c.kdbg && threadIdx.x == 0) c.kdbg[blockIdx.x * 4 + 0] = globaltimer_ns();
+  if (timed) tl_start(c.ktl, 3);
   // row blocks first (they carry the longer chains); FIN_B has column blocks only
   const int64_t nrow_blocks = mode == FIN_B ? 0 : c.T;
   if ((int64_t)blockIdx.x >= nrow_blocks) {
@@ -944,6 +945,15 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
     *cs.counter = 0u;
     if (cs.ucount) *cs.ucount = 0u;  // the screened cell and tile lists of this pass are consumed
     if (cs.tcount) *cs.tcount = 0u;
+    if (timed && cs.ktl) {  // pass timeline: K2 end, then reset it for the next pass
+      unsigned long long* tl = cs.ktl;
+      tl[7] = globaltimer_ns();
+      for (int k = 0; k < 8; ++k) tl[8 + k] = tl[k];  // keep the last complete pass
+      for (int k = 0; k < 4; ++k) {
+        tl[2 * k] = ~0ull;
+        tl[2 * k + 1] = 0ull;
+      }
+    }
     if (timed) {
       const uint64_t t_end = globaltimer_ns();
       cs.sstat[ST_K2_MAIN] += t_last - __ldcg(&cs.sstat[ST_K2_T0]);

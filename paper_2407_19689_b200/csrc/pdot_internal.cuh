@@ -208,6 +208,7 @@ struct Ctl {
   double* cscal;             // [nbands][ncp][kMaxNS] cell scalars
   unsigned long long* sstat; // [ST_COUNT]
   unsigned long long* kdbg;  // PDOT_K2_TRACE=1: per-block K2 timestamps of the last screened STEP pass
+  unsigned long long* ktl;   // PDOT_K2_TRACE=1: pass timeline {K0, K1, K1b, K2} x {first start, last end}
   unsigned int* counter;   // last-block-done counter for the finalize kernel
   Status* status;          // host mapped
   Event* ring;             // host mapped, kRingCap entries
@@ -380,6 +381,15 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+// debugging aid (PDOT_K2_TRACE=1): kernel k of a screened STEP pass records
+// its first block start / last block end in the pass timeline
+__device__ __forceinline__ void tl_start(unsigned long long* tl, int k) {
+  if (tl && threadIdx.x == 0) atomicMin(tl + 2 * k, (unsigned long long)globaltimer_ns());
+}
+__device__ __forceinline__ void tl_end(unsigned long long* tl, int k) {
+  if (tl && threadIdx.x == 0) atomicMax(tl + 2 * k + 1, (unsigned long long)globaltimer_ns());
 }
 
 // ---------------------------------------------------------------------------

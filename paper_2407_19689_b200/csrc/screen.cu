@@ -78,9 +78,12 @@ __global__ void __launch_bounds__(256) screen_kernel(const Ctl* __restrict__ ctl
   const int op = force_op >= 0 ? force_op : c.op;
   if (!unit_pass(c, op)) return;
   __shared__ uint32_t tilebits[32];  // per cell of the tile: bit bl = band bl active
+  __shared__ unsigned warp_base[8];  // cell-list offsets of the CTA's warps
+  unsigned long long* tl = op == OP_STEP ? c.ktl : nullptr;
+  tl_start(tl, 0);
   const int64_t tu = blockIdx.x, tt = blockIdx.y;
   const int s = threadIdx.x & 7, bl = threadIdx.x >> 3;  // strip in tile, band in tile
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < 32) tilebits[threadIdx.x] = 0u;
   const bool with_avg = op == OP_STEP && step_with_avg(c);
   const int64_t band = tt * c.nbt + bl;
@@ -91,24 +94,24 @@ __global__ void __launch_bounds__(256) screen_kernel(const Ctl* __restrict__ ctl
   if (valid) {
     const int64_t sstride = c.nbands * c.nstrips;
     const int64_t ow = band * c.nstrips + strip;
-    uint32_t ox = 0, oa = 0, zx = 0, za = 0;
-    double P = -INFINITY, Pa = -INFINITY;
-    bool bound = false;
-    if (op == OP_STEP) {
-      ox = __ldcg(c.occ + c.sX * sstride + ow);
-      oa = with_avg ? __ldcg(c.occ + c.sAsrc * sstride + ow) : 0u;
-      zx = __ldcg(c.occ + c.sXn * sstride + ow);
-      za = with_avg ? __ldcg(c.occ + c.sA * sstride + ow) : 0u;
-      P = __ldcg(c.pmax + c.sX * c.nbands + band);
-      Pa = __ldcg(c.pmax + c.sA * c.nbands + band);
-      bound = true;
-    } else if (op == OP_DIST) {
-      ox = __ldcg(c.occ + c.sCand * sstride + ow);  // X_b = candidate
-      oa = __ldcg(c.occ + c.sZ * sstride + ow);     // X_a = anchor
-    } else {  // OP_KKT of slot sX
-      ox = __ldcg(c.occ + c.sX * sstride + ow);
-      P = __ldcg(c.pmax + c.sX * c.nbands + band);
-      bound = true;
+    // every load of the unit is issued up front (one memory round trip)
+    const int sx = op == OP_DIST ? c.sCand : c.sX;
+    const uint32_t ox = __ldcg(c.occ + sx * sstride + ow);
+    const uint32_t oa = (op == OP_DIST || with_avg) ? __ldcg(c.occ + (op == OP_DIST ? c.sZ : c.sAsrc) * sstride + ow) : 0u;
+    const uint32_t zx = op == OP_STEP ? __ldcg(c.occ + c.sXn * sstride + ow) : 0u;
+    const uint32_t za = with_avg ? __ldcg(c.occ + c.sA * sstride + ow) : 0u;
+    const bool bound = op != OP_DIST;
+    const bool bound_avg = op == OP_STEP;
+    const double P = bound ? __ldcg(c.pmax + c.sX * c.nbands + band) : 0.0;
+    const double Pa = bound_avg ? __ldcg(c.pmax + c.sA * c.nbands + band) : 0.0;
+    double mc[kCellsPerStrip], Q[kCellsPerStrip], Qa[kCellsPerStrip];
+#pragma unroll
+    for (int k = 0; k < kCellsPerStrip; ++k) {
+      const int64_t cell = strip * kCellsPerStrip + k;
+      const bool ok = bound && cell < c.ncells;
+      mc[k] = ok ? __ldcg(c.minc + band * c.ncells + cell) : 0.0;
+      Q[k] = ok ? __ldcg(c.qmax + c.sX * c.ncells + cell) : 0.0;
+      Qa[k] = (ok && bound_avg) ? __ldcg(c.qmax + c.sA * c.ncells + cell) : 0.0;
     }
     // a non-finite step (tau) would turn 0 * inf into NaN: screen nothing
     const bool open = op == OP_STEP && !isfinite(c.tau);
@@ -118,17 +121,9 @@ __global__ void __launch_bounds__(256) screen_kernel(const Ctl* __restrict__ ctl
       if (cell >= c.ncells) break;
       const uint32_t bx = (ox >> (8 * k)) & 0xffu, ba = (oa >> (8 * k)) & 0xffu;
       const uint32_t bzx = (zx >> (8 * k)) & 0xffu, bza = (za >> (8 * k)) & 0xffu;
-      bool act = bx || ba || open;
-      if (bound && !act) {
-        const double mc = __ldcg(c.minc + band * c.ncells + cell);
-        const double Q = __ldcg(c.qmax + c.sX * c.ncells + cell);
-        // !(a <= b) keeps NaN bounds active
-        act = !(P + Q <= mc);
-        if (op == OP_STEP && !act) {
-          const double Qa = __ldcg(c.qmax + c.sA * c.ncells + cell);
-          act = !(Pa + Qa <= mc);
-        }
-      }
+      // !(a <= b) keeps NaN bounds active
+      const bool act = bx || ba || open || (bound && !(P + Q[k] <= mc[k])) ||
+                       (bound_avg && !(Pa + Qa[k] <= mc[k]));
       const uint32_t f = (act ? U_ACT : 0u) | (bx ? U_LDX : 0u) | (ba ? U_LDA : 0u) | (bzx ? U_ZX : 0u) |
                          (bza ? U_ZA : 0u);
       word |= f << (8 * k);
@@ -143,7 +138,7 @@ __global__ void __launch_bounds__(256) screen_kernel(const Ctl* __restrict__ ctl
     listed |= (f != 0u) << k;
     actb |= ((f & U_ACT) != 0u) << k;
   }
-  // warp-aggregated append of the listed cells
+  // CTA-aggregated append of the listed cells: warp scan, one atomic per CTA
   const int cnt = __popc(listed);
   int incl = cnt;
 #pragma unroll
@@ -151,31 +146,40 @@ __global__ void __launch_bounds__(256) screen_kernel(const Ctl* __restrict__ ctl
     const int y = __shfl_up_sync(0xffffffffu, incl, d);
     if (lane >= d) incl += y;
   }
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
-  unsigned base = 0;
-  if (lane == 31 && total) base = atomicAdd(c.ucount, (unsigned)total);
-  base = __shfl_sync(0xffffffffu, base, 31);
-  unsigned pos = base + (unsigned)(incl - cnt);
-#pragma unroll
-  for (int k = 0; k < kCellsPerStrip; ++k)
-    if ((listed >> k) & 1u) c.ulist[pos++] = (uint32_t)((band << 12) | (strip * kCellsPerStrip + k));
+  if (lane == 31) warp_base[warp] = (unsigned)incl;
   // bcr[band][tu]: bit 4 s + k = cell k of strip s (8 lanes of one band)
   uint32_t rbits = actb << (4 * s);
 #pragma unroll
   for (int msk = 1; msk < 8; msk <<= 1) rbits |= __shfl_xor_sync(0xffffffffu, rbits, msk);
   if (s == 0 && inband) c.bcr[band * c.U + tu] = rbits;
-  // bct[tt][cell]: bit bl = band bl of the tile
   __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    unsigned tot = 0;
+    for (int w = 0; w < nw; ++w) {
+      const unsigned t = warp_base[w];
+      warp_base[w] = tot;
+      tot += t;
+    }
+    const unsigned base = tot ? atomicAdd(c.ucount, tot) : 0u;
+    for (int w = 0; w < nw; ++w) warp_base[w] += base;
+  }
+  // bct[tt][cell]: bit bl = band bl of the tile
 #pragma unroll
   for (int k = 0; k < kCellsPerStrip; ++k)
     if ((actb >> k) & 1u) atomicOr(&tilebits[s * kCellsPerStrip + k], 1u << bl);
   const int any = __syncthreads_or(actb != 0u);
+  unsigned pos = warp_base[warp] + (unsigned)(incl - cnt);
+#pragma unroll
+  for (int k = 0; k < kCellsPerStrip; ++k)
+    if ((listed >> k) & 1u) c.ulist[pos++] = (uint32_t)((band << 12) | (strip * kCellsPerStrip + k));
   if (threadIdx.x < 32) c.bct[tt * c.ncp + tu * 32 + threadIdx.x] = tilebits[threadIdx.x];
   // the tile's partials are assembled by K1b, or are all +0 (flag 0)
   if (threadIdx.x == 0) {
     c.tileflag[tt * c.U + tu] = any ? 1 : 0;
     if (any) c.tlist[atomicAdd(c.tcount, 1u)] = (int32_t)(tt * c.U + tu);
   }
+  tl_end(tl, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -443,6 +447,8 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
   if (!unit_pass(c, op)) return;
   __shared__ unsigned long long red[2][kWarps];
   if (blockIdx.x == 0 && threadIdx.x == 0) c.sstat[ST_T0] = globaltimer_ns();
+  unsigned long long* tl = op == OP_STEP ? c.ktl : nullptr;
+  tl_start(tl, 1);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned ncells = __ldcg(c.ucount);
   const unsigned gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
@@ -506,6 +512,7 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
       c.sstat[ST_DONE1] = 0;
     }
   }
+  tl_end(tl, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -623,6 +630,8 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Ctl* __restrict__ 
   const int op = force_op >= 0 ? force_op : c.op;
   if (!unit_pass(c, op)) return;
   const unsigned ntiles = __ldcg(c.tcount);
+  unsigned long long* tl = op == OP_STEP ? c.ktl : nullptr;
+  tl_start(tl, 2);
   for (unsigned k = blockIdx.x; k < ntiles; k += gridDim.x) {
     const int32_t tile = __ldcg(c.tlist + k);
     const int64_t tu = tile % c.U, tt = tile / c.U;
@@ -630,6 +639,7 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Ctl* __restrict__ 
     else if (op == OP_DIST) assemble_tile<1, 1>(c, tu, tt, sm);
     else assemble_tile<1, 3>(c, tu, tt, sm);
   }
+  tl_end(tl, 2);
 }
 
 // the unit calls the screen does not cover (KKT of a unit call, DIFF, ROUND):

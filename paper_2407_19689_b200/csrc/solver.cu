@@ -663,7 +663,13 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     // single dense launch per pass wins, e.g. 1024^2)
     if (getenv("PDOT_K2_TRACE") && atoi(getenv("PDOT_K2_TRACE")) != 0) {
       unsigned long long* kd = nullptr;
-      if (cudaMalloc(&kd, (size_t)(h->CB + h->T) * 4 * sizeof(unsigned long long)) == cudaSuccess) c.kdbg = kd;
+      if (cudaMalloc(&kd, (size_t)((h->CB + h->T) * 4 + 16) * sizeof(unsigned long long)) == cudaSuccess) {
+        c.kdbg = kd;
+        c.ktl = kd + (h->CB + h->T) * 4;
+        unsigned long long init[16];
+        for (int k = 0; k < 16; ++k) init[k] = (k < 8 && (k & 1) == 0) ? ~0ull : 0ull;
+        cudaMemcpy(c.ktl, init, sizeof(init), cudaMemcpyHostToDevice);
+      }
     }
     const char* env = getenv("PDOT_SCREEN");
     h->screen_on = env ? atoi(env) != 0 : (double)m_total * (double)n >= (double)(1 << 22);
@@ -1408,7 +1414,7 @@ int pdot_debug_k2(pdot_solver* h, unsigned long long* out, int64_t cap) {
   if (!h || !h->host.kdbg) return 0;
   DeviceGuard dg(h->device);
   const int64_t nb = h->CB + h->T;
-  const int64_t k = std::min<int64_t>(cap, nb * 4);
+  const int64_t k = std::min<int64_t>(cap, nb * 4 + 16);
   if (cudaMemcpy(out, h->host.kdbg, k * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
   return (int)nb;
 }

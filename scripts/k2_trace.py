@@ -18,6 +18,11 @@ lib = _lib.load()
 lib.pdot_debug_k2.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int64]
 buf = (ctypes.c_ulonglong * 8192)()
 nb = lib.pdot_debug_k2(h.ptr, buf, 8192)
+tl = np.array(buf[nb * 4 + 8:nb * 4 + 16], dtype=np.float64)
+t00 = tl[0]
+names = ("K0", "K1", "K1b", "K2")
+print("pass timeline (us from K0 start): " + ", ".join(
+    f"{names[k]} {(tl[2 * k] - t00) / 1e3:.1f}..{(tl[2 * k + 1] - t00) / 1e3:.1f}" for k in range(4)))
 a = np.array(buf[:nb * 4], dtype=np.float64).reshape(nb, 4)
 t0 = a[:, 0].min()
 a[:, :3] -= t0
