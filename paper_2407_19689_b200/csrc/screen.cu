@@ -592,25 +592,30 @@ __device__ __forceinline__ void assemble_tile(const Ctl& c, int64_t tu, int64_t 
 #pragma unroll
     for (int q = 0; q < NQ; ++q) c.rowpart[(tu * NQ + q) * c.m + i] = acc[q];
   }
-  {  // scalars: thread (strip w, scalar s)
-    const int w = th >> 3, s = th & 7;
-    double ws = 0.0;
-    if (w < kWarps && s < NS) {
-      const int nb = (int)imin64(c.nbt, c.nbands - b0);
-      uint32_t nibs[32];
+  {  // scalars: thread (strip w, band bl) forms its strip-band values (one round
+     // trip for all of them), then the band-ordered and strip-ordered sums run
+     // on shared memory
+    const int nb = (int)imin64(c.nbt, c.nbands - b0);
+    const int w = th & 7, bl = th >> 3;
+    if (bl < nb) {
+      const unsigned nib = (__ldg(c.bcr + (b0 + bl) * c.U + tu) >> (4 * w)) & 0xfu;
+      const double* base = c.cscal + ((b0 + bl) * c.ncp + tu * 32 + 4 * w) * kMaxNS;
+      double v[4][NS];
 #pragma unroll
-      for (int bl = 0; bl < 32; ++bl) nibs[bl] = bl < nb ? (__ldg(c.bcr + (b0 + bl) * c.U + tu) >> (4 * w)) & 0xfu : 0u;
+      for (int x = 0; x < 4; ++x)
 #pragma unroll
-      for (int bl = 0; bl < 32; ++bl) {
-        const unsigned nib = nibs[bl];
-        if (!nib) continue;
-        const double* base = c.cscal + ((b0 + bl) * c.ncp + tu * 32 + 4 * w) * kMaxNS + s;
-        double v[4];
+        for (int s = 0; s < NS; ++s) v[x][s] = ((nib >> x) & 1u) ? __ldg(base + x * kMaxNS + s) : 0.0;
 #pragma unroll
-        for (int x = 0; x < 4; ++x) v[x] = ((nib >> x) & 1u) ? __ldg(base + x * kMaxNS) : 0.0;
-        ws += (v[0] + v[1]) + (v[2] + v[3]);
-      }
+      for (int s = 0; s < NS; ++s) sm[(bl * 8 + w) * 8 + s] = (v[0][s] + v[1][s]) + (v[2][s] + v[3][s]);
     }
+    __syncthreads();
+    double ws = 0.0;
+    if (th < 64) {  // thread (w, s): band-ordered sum
+      const int ww = th >> 3, s = th & 7;
+      if (s < NS)
+        for (int k = 0; k < nb; ++k) ws += sm[(k * 8 + ww) * 8 + s];
+    }
+    __syncthreads();
     if (th < 64) sm[th] = ws;
     __syncthreads();
     if (th < NS) {
@@ -624,7 +629,7 @@ __device__ __forceinline__ void assemble_tile(const Ctl& c, int64_t tu, int64_t 
 }
 
 __global__ void __launch_bounds__(kThreads) tile_kernel(const Ctl* __restrict__ ctlp, int force_op) {
-  __shared__ double sm[64];
+  __shared__ double sm[32 * 8 * 8];  // [band][strip][scalar] strip-band values
   const Ctl& c = *ctlp;
   if (c.done || !c.screen) return;
   const int op = force_op >= 0 ? force_op : c.op;
