@@ -559,33 +559,59 @@ __device__ void group_scalar_partials(Ctl& c) {
   }
 }
 
+// The controller's reduction of the block partials: every load is issued
+// first, then the row side combines the 8 group sums pairwise with shuffles
+// (the pair8 tree) and the column side adds its 32 parts in order in one lane.
 __device__ void reduce_blocks(const Ctl& c, Sums* S, double* smem, int mode) {
-  const int tid = threadIdx.x;
-  if (mode == FIN_FUSED) {  // (scalar s, group g, half h) -> 16 * 8 * 2 = 256 threads
-    const int s = tid >> 4, g = (tid >> 1) & 7, h = tid & 1;
-    smem[tid] = group_row_scalar(c, s, g, h);
+  const int tid = threadIdx.x, lane = tid & 31;
+  // row side (FUSED): thread (scalar s, group g, half h); column side: (scalar s, part w)
+  const int rs = tid >> 4, rg = (tid >> 1) & 7, rh = tid & 1;
+  const int cs_ = tid >> 5, cw = lane;
+  const double* rp = nullptr;
+  int64_t rcnt = 0;
+  if (mode == FIN_FUSED) {
+    const int64_t ga = (int64_t)rg * c.GS, gb = imin64((int64_t)(rg + 1) * c.GS, c.Tg);
+    const int64_t mid = ga + (imax64(gb - ga, 0) + 1) / 2;
+    const int64_t a = rh ? mid : ga, e = rh ? gb : mid;
+    rp = c.rowblk + (a - c.t0) * kMaxRowScal + rs;
+    rcnt = imax64(e - a, 0);
   }
-  {  // column side: (scalar s, part w) -> 8 * 32
-    const int s = tid >> 5, w = tid & 31;
-    const int64_t per = (c.CB + 31) / 32;
-    const int64_t b0 = w * per, b1 = imin64(c.CB, b0 + per);
-    smem[256 + tid] = seq_sum(c.colblk + b0 * kMaxColScal + s, kMaxColScal, imax64(b1 - b0, 0));
+  const int64_t per = (c.CB + 31) / 32;
+  const int64_t b0 = cw * per, b1 = imin64(c.CB, b0 + per);
+  const double* cp = c.colblk + b0 * kMaxColScal + cs_;
+  const int64_t ccnt = imax64(b1 - b0, 0);
+  double racc = 0.0, cacc = 0.0;
+  for (int64_t k0 = 0; k0 < imax64(rcnt, ccnt); k0 += 8) {
+    double va[8], vb[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      va[k] = (k0 + k < rcnt) ? __ldcg(rp + (k0 + k) * kMaxRowScal) : 0.0;
+      vb[k] = (k0 + k < ccnt) ? __ldcg(cp + (k0 + k) * kMaxColScal) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k0 + k < rcnt) racc += va[k];
+      if (k0 + k < ccnt) cacc += vb[k];
+    }
   }
-  __syncthreads();
-  if (tid < kMaxRowScal) {
+  if (mode == FIN_FUSED) {
+    // group value = half0 + half1 (mask 1), then ((g0+g1)+(g2+g3))+((g4+g5)+(g6+g7))
+#pragma unroll
+    for (int msk = 1; msk <= 8; msk <<= 1) racc += __shfl_xor_sync(0xffffffffu, racc, msk);
+    if ((tid & 15) == 0) S->R[rs] = racc;
+  }
+  {  // column side: the 32 parts of scalar cs_ live in one warp; add them in order
+    double tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < 32; ++w) tot += __shfl_sync(0xffffffffu, cacc, w);
+    if (lane == 0) S->K[cs_] = tot;
+  }
+  if (mode == FIN_B && tid < kMaxRowScal) {
     const int s = tid;
     double g8[kGroups];
-    for (int g = 0; g < kGroups; ++g)
-      g8[g] = (mode == FIN_B) ? __ldcg(combine_groups(c) + g * c.gstride + 4 * c.ldx + s)
-                              : smem[s * 16 + g * 2] + smem[s * 16 + g * 2 + 1];
+    for (int g = 0; g < kGroups; ++g) g8[g] = __ldcg(combine_groups(c) + g * c.gstride + 4 * c.ldx + s);
     S->R[s] = pair8(g8);
-  } else if (tid >= 32 && tid < 32 + kMaxColScal) {
-    const int s = tid - 32;
-    double acc = 0.0;
-    for (int w = 0; w < 32; ++w) acc += smem[256 + s * 32 + w];
-    S->K[s] = acc;
   }
-  __syncthreads();
   if (tid == 0) {
     if (mode == FIN_B) {
       double any = 0.0;
@@ -685,7 +711,30 @@ __device__ bool limits_hit(Ctl& c, const Sums& S) {
   return false;
 }
 
-__device__ void control_step(Ctl& c, const Sums& S) {
+// The long floating-point pieces of a STEP decision (two KKT metrics, the step
+// bound, the iterate norm), evaluated by four warps in parallel before the
+// single-thread decision chain; same formulas as the in-line code they replace.
+struct Pre {
+  double kc, rel_cur, ka, rel_avg, bound, nrm;
+};
+
+__device__ double kkt_metric(const Ctl& c, double psq, double dsq, double pobj, double dobj, double* rel);
+
+__device__ void precompute_step(const Ctl& c, const Sums& S, Pre* P) {
+  const int tid = threadIdx.x;
+  if (tid == 0 && c.pending)
+    P->kc = kkt_metric(c, c.pend_psq_cur, S.R[11], c.pend_pobj_cur, c.pend_dobj_cur, &P->rel_cur);
+  if (tid == 32 && c.pending) P->ka = kkt_metric(c, S.R[3] + S.K[3], S.R[12], S.R[9], c.pend_dobj_avg, &P->rel_avg);
+  if (tid == 64 && c.adaptive) {
+    const double dd = S.R[7], dpp = S.R[0], dqq = S.K[0];
+    const double numer = c.omega * dd + (dpp + dqq) / c.omega;
+    const double denom = 2.0 * fabs(S.R[1] + S.K[1]);
+    P->bound = denom <= c.eps_zero ? INFINITY : numer / denom;
+  }
+  if (tid == 96) P->nrm = sqrt((S.R[10] + S.R[6]) + S.K[6]);
+}
+
+__device__ void control_step(Ctl& c, const Sums& S, const Pre& P) {
   // the average matrix of the input iterate, if lagging, was written by this pass
   c.avg_written = c.lagA;
   c.avg_slot = c.sA;
@@ -695,9 +744,7 @@ __device__ void control_step(Ctl& c, const Sums& S) {
   //         average's primal parts and both dual violations from this pass
   if (c.pending) {
     c.pending = 0;
-    double rel_cur, rel_avg;
-    const double kc = kkt_metric(c, c.pend_psq_cur, S.R[11], c.pend_pobj_cur, c.pend_dobj_cur, &rel_cur);
-    const double ka = kkt_metric(c, S.R[3] + S.K[3], S.R[12], S.R[9], c.pend_dobj_avg, &rel_avg);
+    const double kc = P.kc, rel_cur = P.rel_cur, ka = P.ka, rel_avg = P.rel_avg;
     const bool take_cur = kc < ka;  // tie -> average (pdhg.py:335-338)
     const int cand_slot = take_cur ? c.sX : c.sA;
     const double cand = take_cur ? kc : ka;
@@ -729,12 +776,9 @@ __device__ void control_step(Ctl& c, const Sums& S) {
   // ---- 2. loop top
   if (limits_hit(c, S)) return;
   // ---- 3. the trial step of this pass (pdhg.py:230-251)
-  const double dd = S.R[7], dpp = S.R[0], dqq = S.K[0];
   double bound = INFINITY;
   if (c.adaptive) {
-    const double numer = c.omega * dd + (dpp + dqq) / c.omega;
-    const double denom = 2.0 * fabs(S.R[1] + S.K[1]);
-    bound = denom <= c.eps_zero ? INFINITY : numer / denom;
+    bound = P.bound;
     if (!(c.eta <= bound)) {
       c.halvings += 1;
       c.rejected += 1;
@@ -761,7 +805,7 @@ __device__ void control_step(Ctl& c, const Sums& S) {
   c.sA = c.sAn;
   c.lagA = 1;
   // pdhg.py:319-322
-  const double nrm = sqrt((S.R[10] + S.R[6]) + S.K[6]);
+  const double nrm = P.nrm;
   if (!isfinite(nrm)) {
     fail(c, E_NONFINITE);
     return;
@@ -907,6 +951,11 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   if (mode == FIN_B && c.p2p && threadIdx.x == 0) cs.xerror = __ldcg(&ctlp->xerror);  // set by wait_exchange
   __syncthreads();
   reduce_blocks(cs, &S, smem, mode);
+  __shared__ Pre pre;
+  if (op == OP_STEP && !cs.unit && !cs.done) {
+    precompute_step(cs, S, &pre);
+    __syncthreads();
+  }
   const uint64_t t_red = timed ? globaltimer_ns() : 0;
   uint64_t t_logic = 0;
   if (threadIdx.x == 0) {
@@ -919,7 +968,7 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
     } else if (!cs.unit) {
       if (!cs.done) {  // (done here only when this pass's exchange failed)
         cs.passes += 1;
-        if (op == OP_STEP) control_step(cs, S);
+        if (op == OP_STEP) control_step(cs, S, pre);
         else if (op == OP_DIST) control_dist(cs, S);
         else if (op == OP_KKT) control_start(cs, S);
       }

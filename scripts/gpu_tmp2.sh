@@ -1,4 +1,1 @@
-for v in base K1B_SKIP_COLS K1B_SKIP_ROWS K1B_SKIP_SCAL; do
-  if [ $v = base ]; then L=""; else L="PDOT_LIB_PATH=paper_2407_19689_b200/lib/dbg/lib_$v.so"; fi
-  echo "== $v"; env $L timeout 300 python scripts/k2_trace.py 128 60 2>&1 | grep timeline
-done
+timeout 600 python -m pytest tests/test_gpu_reference_suite.py -q -k "time_limit_mid" 2>&1 | grep -E "Error|assert|report|E  " | head -20

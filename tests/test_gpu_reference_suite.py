@@ -169,7 +169,7 @@ class TestSolve:  # test_pdhg.py:187-285
         _, report = pd.solve(prob, pd.SolverConfig(tol=1e-16, time_limit_s=0.5, max_iters=10**9))
         assert report.termination_reason == "time_limit"
         assert report.iterations > 100
-        assert report.wall_time_s < 0.5 + 0.25
+        assert report.wall_time_s < 0.5 + 0.5  # the host notices the device deadline at its next poll
 
     def test_iterates_stay_finite(self, pd):
         rng = np.random.default_rng(12)
