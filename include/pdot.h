@@ -114,6 +114,12 @@ int pdot_set_slot(pdot_solver* h, int slot, const double* X_any, int64_t ldX, co
 /* Copy slot `slot` out (any of the pointers may be NULL). */
 int pdot_get_slot(pdot_solver* h, int slot, double* X_any, int64_t ldX, double* p_any,
                   double* q_any);
+/* Copy slot `slot` out moving only its occupied 8 x 16 cells (screened handles,
+ * where every other cell is exactly +0.0 on the device): X_host must be
+ * zero-filled by the caller (e.g. calloc / np.zeros).  *cells_out = cells moved.
+ * PDOT_ESTATE when screening is off. */
+int pdot_get_slot_sparse(pdot_solver* h, int slot, double* X_host, int64_t ldX, double* p_any, double* q_any,
+                         int64_t* cells_out);
 /* Device pointers of a slot's buffers (X has leading dimension ldx). */
 int pdot_slot_ptrs(pdot_solver* h, int slot, double** X, double** p, double** q);
 

@@ -411,5 +411,9 @@ __host__ __device__ __forceinline__ bool unit_pass(const Ctl& c, int op) {
 // screening metadata: min C per cell, per-slot occupancy and dual bounds
 void launch_minc_build(const Ctl& ctl_host, double* minc, cudaStream_t s);
 void launch_slot_meta(const Ctl& ctl_host, int slot, bool scan_occ, cudaStream_t s);
+// sparse device->host copy of a slot matrix: occupied cells -> list, list -> staging (8 x 16 each)
+unsigned launch_occ_list(const Ctl& ctl_host, int slot, uint32_t* list, unsigned* count_dev, cudaStream_t s);
+void launch_cell_gather(const Ctl& ctl_host, int slot, const uint32_t* list, int64_t k0, int64_t k1, double* out,
+                        cudaStream_t s);
 
 }  // namespace pdot

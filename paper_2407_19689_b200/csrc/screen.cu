@@ -725,7 +725,69 @@ __global__ void bounds_kernel(const double* __restrict__ p, const double* __rest
   }
 }
 
+// sparse device -> host copy of a slot matrix (pdot_get_slot with screening
+// on): list the cells whose occupancy byte is set (the rest is +0.0 in memory),
+// then gather them, 8 rows x 16 columns each, into a staging buffer
+__global__ void occ_list_kernel(const uint8_t* __restrict__ occ_bytes, int64_t nbands, int64_t ncells,
+                                int64_t nstrips, uint32_t* __restrict__ list, unsigned* __restrict__ count) {
+  const int64_t total = nbands * nstrips * kCellsPerStrip;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t band = e / (nstrips * kCellsPerStrip), cell = e - band * nstrips * kCellsPerStrip;
+    const bool on = cell < ncells && occ_bytes[e] != 0;
+    const unsigned bal = __ballot_sync(__activemask(), on);
+    if (!on) continue;
+    // one atomic per warp
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(bal) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(count, (unsigned)__popc(bal));
+    base = __shfl_sync(bal, base, leader);
+    list[base + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)((band << 12) | cell);
+  }
+}
+
+__global__ void cell_gather_kernel(const double* __restrict__ X, int64_t ldx, int64_t m, int64_t n,
+                                   const uint32_t* __restrict__ list, int64_t k0, int64_t k1,
+                                   double* __restrict__ out) {
+  // one warp per cell: lane = (row rg, column pair cp) as in the cell kernel
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k = k0 + w; k < k1; k += nw) {
+    const uint32_t entry = list[k];
+    const int64_t band = entry >> 12, cell = entry & 0xfffu;
+    const int cp = lane & 7, rg = lane >> 3;
+    const int64_t j = cell * kCell + cp * 2;
+    double* o = out + (k - k0) * (kBand * kCell);
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int r = 2 * rg + rr;
+      const int64_t i = band * kBand + r;
+      double2 v = make_double2(0.0, 0.0);
+      if (i < m && j < n) v = *reinterpret_cast<const double2*>(X + i * ldx + j);
+      *reinterpret_cast<double2*>(o + r * kCell + cp * 2) = v;
+    }
+  }
+}
+
 }  // namespace
+
+unsigned launch_occ_list(const Ctl& h, int slot, uint32_t* list, unsigned* count_dev, cudaStream_t s) {
+  cudaMemsetAsync(count_dev, 0, sizeof(unsigned), s);
+  const uint8_t* ob = reinterpret_cast<const uint8_t*>(h.occ + (int64_t)slot * h.nbands * h.nstrips);
+  occ_list_kernel<<<148 * 8, 256, 0, s>>>(ob, h.nbands, h.ncells, h.nstrips, list, count_dev);
+  unsigned cnt = 0;
+  cudaMemcpyAsync(&cnt, count_dev, sizeof(unsigned), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  return cnt;
+}
+
+void launch_cell_gather(const Ctl& h, int slot, const uint32_t* list, int64_t k0, int64_t k1, double* out,
+                        cudaStream_t s) {
+  const int64_t warps = k1 - k0;
+  const unsigned blocks = (unsigned)imin64((warps * 32 + 255) / 256, 148 * 16);
+  if (blocks > 0) cell_gather_kernel<<<blocks, 256, 0, s>>>(h.slot[slot].X, h.ldx, h.m, h.n, list, k0, k1, out);
+}
 
 void prepare_sparse_kernel() {
   cudaFuncSetAttribute(generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);

@@ -766,6 +766,7 @@ int pdot_destroy(pdot_solver* h) {
   if (h->slot_mem) cudaFree(h->slot_mem);
   if (h->work) cudaFree(h->work);
   if (h->screen_mem) cudaFree(h->screen_mem);
+  if (h->d2h_count) cudaFree(h->d2h_count);
   if (h->counter) cudaFree(h->counter);
   if (h->status_h) cudaFreeHost(h->status_h);
   for (int i = 0; i < 2; ++i) {
@@ -878,6 +879,90 @@ int pdot_get_slot(pdot_solver* h, int slot, double* X_any, int64_t ldX, double* 
     if (int rc = copy_vec(p_any, s.p, h->m, h->stream)) return rc;
   if (q_any)
     if (int rc = copy_vec(q_any, s.q, h->n, h->stream)) return rc;
+  CK(cudaStreamSynchronize(h->stream));
+  return PDOT_OK;
+}
+
+// Sparse device -> host copy of a slot (screened handles): only the cells whose
+// occupancy byte is set are moved; every other cell is +0.0 in device memory
+// (the screening invariant), so X_host must come zero-filled (np.zeros).  The
+// occupied cells are gathered into device staging, DMA'd through the pinned
+// double buffer and scattered by host threads while the next chunk moves.
+int pdot_get_slot_sparse(pdot_solver* h, int slot, double* X_host, int64_t ldX, double* p_any, double* q_any,
+                         int64_t* cells_out) {
+  if (!h || slot < 0 || slot >= pdot::kNSlot || !X_host) return set_err(PDOT_EINVAL, "bad argument");
+  if (ldX < h->n) return set_err(PDOT_EINVAL, "X: leading dimension must be >= n");
+  if (!h->host.screen) return set_err(PDOT_ESTATE, "sparse copy needs a screened handle (occupancy maintained)");
+  DeviceGuard dg(h->device);
+  const Ctl& c = h->host;
+  if (!h->d2h_count) CK(cudaMalloc(&h->d2h_count, sizeof(unsigned)));
+  const unsigned cnt = pdot::launch_occ_list(c, slot, c.ulist, h->d2h_count, h->stream);
+  CK(cudaGetLastError());
+  if (cells_out) *cells_out = cnt;
+  constexpr int64_t kCellVals = pdot::kBand * pdot::kCell;  // 128 doubles per cell
+  if (cnt > 0) {
+    // chunk = what fits one pinned bounce buffer and the device staging area (the
+    // per-pass cell partial buffer, idle between solves)
+    if (!h->bounce[0]) {
+      const size_t want = std::min<size_t>((size_t)cnt * kCellVals * sizeof(double), (size_t)64 << 20);
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaHostAlloc(&h->bounce[i], want, cudaHostAllocDefault));
+        CK(cudaEventCreateWithFlags(&h->bounce_ev[i], cudaEventDisableTiming));
+      }
+      h->bounce_bytes = want;
+    }
+    const int64_t stage_cells = (c.nbands * pdot::kMaxNQ * c.ldx) / kCellVals;
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>((int64_t)(h->bounce_bytes / (kCellVals * 8)), stage_cells));
+    const int64_t nchunks = ((int64_t)cnt + chunk - 1) / chunk;
+    std::vector<uint32_t> list(cnt);
+    CK(cudaMemcpyAsync(list.data(), c.ulist, cnt * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
+    auto scatter = [&](int64_t k) {
+      const int64_t k0 = k * chunk, k1 = std::min<int64_t>((int64_t)cnt, k0 + chunk);
+      const double* b = h->bounce[k & 1];
+      // visit the chunk's cells in row order and give each host thread a
+      // contiguous row range: first touches of the zero-filled destination then
+      // fault pages in without threads contending for the same page tables
+      std::vector<int64_t> order((size_t)(k1 - k0));
+      for (int64_t t = k0; t < k1; ++t) order[t - k0] = t;
+      std::sort(order.begin(), order.end(), [&](int64_t a, int64_t e) { return list[a] < list[e]; });
+      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+      const unsigned nthreads = (k1 - k0) > 2048 ? std::min(hw, 32u) : 1;
+      auto work = [&, b, k0](int64_t a, int64_t e) {
+        for (int64_t u = a; u < e; ++u) {
+          const int64_t t = order[u];
+          const uint32_t entry = list[t];
+          const int64_t i0 = (int64_t)(entry >> 12) * pdot::kBand, j0 = (int64_t)(entry & 0xfffu) * pdot::kCell;
+          const int64_t rows = std::min<int64_t>(pdot::kBand, h->m - i0), cols = std::min<int64_t>(pdot::kCell, h->n - j0);
+          const double* src = b + (t - k0) * kCellVals;
+          for (int64_t r = 0; r < rows; ++r)
+            memcpy(X_host + (i0 + r) * ldX + j0, src + r * pdot::kCell, (size_t)cols * sizeof(double));
+        }
+      };
+      if (nthreads == 1) {
+        work(0, (int64_t)order.size());
+        return;
+      }
+      std::vector<std::thread> pool;
+      const int64_t nn = (int64_t)order.size();
+      for (unsigned t = 0; t < nthreads; ++t) pool.emplace_back(work, nn * t / nthreads, nn * (t + 1) / nthreads);
+      for (auto& th : pool) th.join();
+    };
+    for (int64_t k = 0; k < nchunks; ++k) {
+      const int64_t k0 = k * chunk, k1 = std::min<int64_t>((int64_t)cnt, k0 + chunk);
+      pdot::launch_cell_gather(c, slot, c.ulist, k0, k1, c.ccol, h->stream);
+      CK(cudaMemcpyAsync(h->bounce[k & 1], c.ccol, (size_t)(k1 - k0) * kCellVals * sizeof(double),
+                         cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaEventRecord(h->bounce_ev[k & 1], h->stream));
+      if (k == 0) CK(cudaStreamSynchronize(h->stream));  // the list is on the host now
+      if (k > 0) scatter(k - 1);  // overlaps with the DMA of chunk k
+      CK(cudaEventSynchronize(h->bounce_ev[k & 1]));
+    }
+    scatter(nchunks - 1);
+  }
+  if (p_any)
+    if (int rc = copy_vec(p_any, c.slot[slot].p, h->m, h->stream)) return rc;
+  if (q_any)
+    if (int rc = copy_vec(q_any, c.slot[slot].q, h->n, h->stream)) return rc;
   CK(cudaStreamSynchronize(h->stream));
   return PDOT_OK;
 }

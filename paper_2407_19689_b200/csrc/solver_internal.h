@@ -56,6 +56,7 @@ struct pdot_solver {
   // block screening (screen.cu): metadata allocation, min C of the bound problem
   char* screen_mem = nullptr;
   double* minc_buf = nullptr;
+  unsigned* d2h_count = nullptr;  // counter of the sparse device->host copy
   bool screen_on = true;        // screened passes (default from 2^22 entries; PDOT_SCREEN / pdot_set_screening)
   size_t bounce_bytes = 0;
   cudaEvent_t bounce_ev[2] = {nullptr, nullptr};

@@ -150,6 +150,21 @@ def as_device_problem(prob, device: int = 0) -> DeviceProblem:
     return DeviceProblem.from_host(prob, device)
 
 
+def zeros_plan(shape):
+    """A zero-filled float64 array whose untouched pages stay the shared zero
+    page: anonymous memory with 4 KB pages (numpy's own large allocations ask
+    for 2 MB pages, and every first touch of one zeroes 2 MB -- scattering a
+    sparse plan into np.zeros of a 16384^2 plan costs ~35 ms, into this ~5 ms)."""
+    import mmap
+    nbytes = int(np.prod(shape)) * 8
+    if nbytes < (1 << 22):
+        return np.zeros(shape)
+    mm = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    if hasattr(mmap, "MADV_NOHUGEPAGE"):
+        mm.madvise(mmap.MADV_NOHUGEPAGE)
+    return np.frombuffer(mm, dtype=np.float64).reshape(shape)
+
+
 class Handle:
     """Owns one pdot_solver* (one problem shape, or one row shard, on one GPU)."""
 
@@ -238,10 +253,22 @@ class Handle:
             torch.cuda.synchronize(self.device)
         _lib.check(self.lib.pdot_set_slot(self.ptr, slot, Xp, ld if Xp else self.n, pp, qp))
 
+    def screened(self) -> bool:
+        return self.screen_stats()["screen_on"] == 1
+
     def get_slot(self, slot: int, want_X=True, out=None):
-        X = (out if out is not None else np.empty((self.m, self.n))) if want_X else None
+        """Copy a slot to the host.  On a screened handle only the occupied 8x16
+        cells travel (every other cell is exactly +0.0 on the device) into a
+        zero-filled array; otherwise the dense plan is copied."""
         p = np.empty(self.m)
         q = np.empty(self.n)
+        if want_X and out is None and self.screened():
+            X = zeros_plan((self.m, self.n))
+            cells = ctypes.c_int64()
+            _lib.check(self.lib.pdot_get_slot_sparse(self.ptr, slot, X.ctypes.data, self.n, p.ctypes.data,
+                                                     q.ctypes.data, ctypes.byref(cells)))
+            return X, p, q
+        X = (out if out is not None else np.empty((self.m, self.n))) if want_X else None
         _lib.check(self.lib.pdot_get_slot(self.ptr, slot, X.ctypes.data if want_X else None, self.n,
                                           p.ctypes.data, q.ctypes.data))
         return X, p, q

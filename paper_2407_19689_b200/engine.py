@@ -165,7 +165,10 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
     phases["setup_s"] = time.perf_counter() - t_start - phases["h2d_problem_s"]
     stepwise = trace is not None
     cfg = config_struct(config, trace_level=1 if trace is not None else 0, poll_passes=poll_passes)
-    out = _Prefault((dp.m, dp.n)) if not return_device and dp.m * dp.n >= (1 << 22) else None
+    # dense output plans are pre-faulted during the solve; a screened handle copies
+    # only the occupied cells into a zero-filled array (Handle.get_slot)
+    out = _Prefault((dp.m, dp.n)) if (not return_device and dp.m * dp.n >= (1 << 22)
+                                      and not h.screened()) else None
     res = _lib.Result()
     lib = h.lib
     if not stepwise:

@@ -24,6 +24,25 @@ for rep in range(3):
     t1 = time.perf_counter()
     print(f"solve {t1 - t0:.4f}s iters {rep_.iterations} phases " +
           " ".join(f"{k}={v:.4f}" for k, v in rep_._phases.items()), flush=True)
+# pieces: the sparse copy of the final plan
+(slot, hh), rep2 = pd.solve_device(device.DeviceProblem.from_host(prob), cfg)
+import ctypes
+from paper_2407_19689_b200 import _lib
+import mmap
+def zeros_small_pages(shape):
+    nbytes = int(np.prod(shape)) * 8
+    mm = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    mm.madvise(mmap.MADV_NOHUGEPAGE)
+    return np.frombuffer(mm, dtype=np.float64).reshape(shape)
+for k in range(4):
+    X = np.zeros((prob.m, prob.n)) if k < 2 else zeros_small_pages((prob.m, prob.n))
+    p = np.empty(prob.m); q = np.empty(prob.n); cells = ctypes.c_int64()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _lib.check(hh.lib.pdot_get_slot_sparse(hh.ptr, slot, X.ctypes.data, prob.n, p.ctypes.data, q.ctypes.data,
+                                           ctypes.byref(cells)))
+    t1 = time.perf_counter()
+    print(f"sparse d2h {'np.zeros' if k < 2 else 'mmap 4K'} {t1 - t0:.4f}s cells {cells.value} ({cells.value * 1024 / 1e6:.1f} MB)")
 # pieces
 torch.cuda.synchronize()
 t0 = time.perf_counter()

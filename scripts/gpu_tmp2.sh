@@ -1,1 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_reference_suite.py -q -k "time_limit_mid" 2>&1 | grep -E "Error|assert|report|E  " | head -20
+cat /sys/kernel/mm/transparent_hugepage/enabled; timeout 600 python scripts/e2e_probe.py 128 2>&1 | tail -7
