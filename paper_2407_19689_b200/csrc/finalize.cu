@@ -559,23 +559,29 @@ __device__ void group_scalar_partials(Ctl& c) {
   }
 }
 
-// The controller's reduction of the block partials: every load is issued
-// first, then the row side combines the 8 group sums pairwise with shuffles
-// (the pair8 tree) and the column side adds its 32 parts in order in one lane.
-__device__ void reduce_blocks(const Ctl& c, Sums* S, double* smem, int mode) {
+// The controller's reduction of the block partials.  Every load is issued
+// first and each warp instruction reads whole lines: on the row side warp g
+// holds group g (lane = (half, scalar)), on the column side lane = (part,
+// scalar).  The order of the additions is fixed: a row group is
+// half0 + half1 of in-order tile sums and the groups combine by pair8; a
+// column scalar adds its 32 in-order part sums in order.
+__device__ __noinline__ void reduce_blocks(const Ctl& c, Sums* S, double* smem, int mode) {
+  static_assert(kGroups == kRedThreads / 32 && kMaxRowScal == 16, "row side: warp per group, lane = (half, scalar)");
+  static_assert(kMaxColScal == 8 && kRedThreads == 32 * kMaxColScal, "column side: 32 parts x 8 scalars");
   const int tid = threadIdx.x, lane = tid & 31;
-  // row side (FUSED): thread (scalar s, group g, half h); column side: (scalar s, part w)
-  const int rs = tid >> 4, rg = (tid >> 1) & 7, rh = tid & 1;
-  const int cs_ = tid >> 5, cw = lane;
+  double* gsum = smem;                         // [kGroups][16] row group values
+  double* psum = smem + kGroups * kMaxRowScal; // [32][8] column part sums
   const double* rp = nullptr;
   int64_t rcnt = 0;
   if (mode == FIN_FUSED) {
-    const int64_t ga = (int64_t)rg * c.GS, gb = imin64((int64_t)(rg + 1) * c.GS, c.Tg);
+    const int g = tid >> 5, rh = lane >> 4, rs = lane & 15;
+    const int64_t ga = (int64_t)g * c.GS, gb = imin64((int64_t)(g + 1) * c.GS, c.Tg);
     const int64_t mid = ga + (imax64(gb - ga, 0) + 1) / 2;
     const int64_t a = rh ? mid : ga, e = rh ? gb : mid;
     rp = c.rowblk + (a - c.t0) * kMaxRowScal + rs;
     rcnt = imax64(e - a, 0);
   }
+  const int cs_ = tid & 7, cw = tid >> 3;
   const int64_t per = (c.CB + 31) / 32;
   const int64_t b0 = cw * per, b1 = imin64(c.CB, b0 + per);
   const double* cp = c.colblk + b0 * kMaxColScal + cs_;
@@ -595,24 +601,34 @@ __device__ void reduce_blocks(const Ctl& c, Sums* S, double* smem, int mode) {
     }
   }
   if (mode == FIN_FUSED) {
-    // group value = half0 + half1 (mask 1), then ((g0+g1)+(g2+g3))+((g4+g5)+(g6+g7))
-#pragma unroll
-    for (int msk = 1; msk <= 8; msk <<= 1) racc += __shfl_xor_sync(0xffffffffu, racc, msk);
-    if ((tid & 15) == 0) S->R[rs] = racc;
+    racc += __shfl_xor_sync(0xffffffffu, racc, 16);  // half0 + half1
+    if (lane < 16) gsum[(tid >> 5) * kMaxRowScal + lane] = racc;
   }
-  {  // column side: the 32 parts of scalar cs_ live in one warp; add them in order
+  psum[cw * kMaxColScal + cs_] = cacc;
+  __syncthreads();
+  if (mode == FIN_FUSED && tid < kMaxRowScal) {
+    double g8[kGroups];
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g) g8[g] = gsum[g * kMaxRowScal + tid];
+    S->R[tid] = pair8(g8);
+  }
+  if (tid >= 32 && tid < 32 + kMaxColScal) {
+    const int s = tid - 32;
+    double v[32];
+#pragma unroll
+    for (int w = 0; w < 32; ++w) v[w] = psum[w * kMaxColScal + s];
     double tot = 0.0;
 #pragma unroll
-    for (int w = 0; w < 32; ++w) tot += __shfl_sync(0xffffffffu, cacc, w);
-    if (lane == 0) S->K[cs_] = tot;
+    for (int w = 0; w < 32; ++w) tot += v[w];
+    S->K[s] = tot;
   }
-  if (mode == FIN_B && tid < kMaxRowScal) {
-    const int s = tid;
+  if (mode == FIN_B && tid >= 64 && tid < 64 + kMaxRowScal) {
+    const int s = tid - 64;
     double g8[kGroups];
     for (int g = 0; g < kGroups; ++g) g8[g] = __ldcg(combine_groups(c) + g * c.gstride + 4 * c.ldx + s);
     S->R[s] = pair8(g8);
   }
-  if (tid == 0) {
+  if (tid == 96) {
     if (mode == FIN_B) {
       double any = 0.0;
       for (int g = 0; g < kGroups; ++g) any += __ldcg(combine_groups(c) + g * c.gstride + 4 * c.ldx + kMaxRowScal - 1);
@@ -720,7 +736,7 @@ struct Pre {
 
 __device__ double kkt_metric(const Ctl& c, double psq, double dsq, double pobj, double dobj, double* rel);
 
-__device__ void precompute_step(const Ctl& c, const Sums& S, Pre* P) {
+__device__ __noinline__ void precompute_step(const Ctl& c, const Sums& S, Pre* P) {
   const int tid = threadIdx.x;
   if (tid == 0 && c.pending)
     P->kc = kkt_metric(c, c.pend_psq_cur, S.R[11], c.pend_pobj_cur, c.pend_dobj_cur, &P->rel_cur);
@@ -734,7 +750,7 @@ __device__ void precompute_step(const Ctl& c, const Sums& S, Pre* P) {
   if (tid == 96) P->nrm = sqrt((S.R[10] + S.R[6]) + S.K[6]);
 }
 
-__device__ void control_step(Ctl& c, const Sums& S, const Pre& P) {
+__device__ __noinline__ void control_step(Ctl& c, const Sums& S, const Pre& P) {
   // the average matrix of the input iterate, if lagging, was written by this pass
   c.avg_written = c.lagA;
   c.avg_slot = c.sA;
@@ -889,11 +905,29 @@ __device__ void control_unit(Ctl& c, int op, const Sums& S) {
   }
 }
 
-__global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__ ctlp, int force_op, int mode) {
+// Wait for the tickets of the `nwork` work blocks (run by the controller block).
+__device__ __forceinline__ void wait_tickets(const Ctl& c, unsigned nwork) {
+  if (threadIdx.x == 0) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c.counter) : "memory");
+    } while (v < nwork);
+  }
+  __syncthreads();
+}
+
+// Grid: [controller block] + T row blocks + CB column blocks (FIN_B: column
+// blocks only; FIN_A: no controller, the last block to finish combines the
+// group scalars).  The controller block does no pass work: while the work
+// blocks run it executes the decision code once on a scratch copy of the
+// control block (so the instructions are in this SM's instruction cache and
+// the real run does not fetch them from DRAM), then waits for every ticket.
+__global__ void __launch_bounds__(kRedThreads, 3) finalize_kernel(Ctl* __restrict__ ctlp, int force_op, int mode) {
   __shared__ double smem[kWarps * 4 * kColsPerBlock + 64];
   __shared__ Sums S;
   __shared__ int is_last;
   __shared__ Ctl cs;
+  __shared__ Pre pre;
   {
     const Ctl& g = *ctlp;
     if (g.done) return;
@@ -914,44 +948,70 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
   Ctl& c = cs;
   const int op = force_op >= 0 ? force_op : c.op;
   const bool timed = op == OP_STEP && unit_pass(c, op) && c.sstat;  // K2 timing of screened STEP passes
-  if (timed && blockIdx.x == 0 && threadIdx.x == 0) c.sstat[ST_K2_T0] = globaltimer_ns();
-  if (timed && c.kdbg && threadIdx.x == 0) c.kdbg[blockIdx.x * 4 + 0] = globaltimer_ns();
-  if (timed) tl_start(c.ktl, 3);
-  // row blocks first (they carry the longer chains); FIN_B has column blocks only
-  const int64_t nrow_blocks = mode == FIN_B ? 0 : c.T;
-  if ((int64_t)blockIdx.x >= nrow_blocks) {
-    const int b = (int)(blockIdx.x - nrow_blocks);
-    if (mode == FIN_A) {
-      if (op == OP_STEP) column_group_partials<4>(c, b);
-      else column_group_partials<1>(c, b);
-    } else {
-      column_block(c, op, b, smem, mode);
+  const int has_ctl = mode == FIN_A ? 0 : 1;
+  const unsigned nwork = gridDim.x - has_ctl;
+  if (has_ctl && blockIdx.x == 0) {
+    if (timed && threadIdx.x == 0) c.sstat[ST_K2_T0] = globaltimer_ns();
+    if (timed) tl_start(c.ktl, 3);
+    if (op == OP_STEP && !c.unit) {
+      __shared__ Ctl dry;
+      unsigned long long* dw = reinterpret_cast<unsigned long long*>(&dry);
+      for (int i = threadIdx.x; i < kWords; i += blockDim.x) dw[i] = cw[i];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        dry.ring = nullptr;
+        dry.status = nullptr;
+      }
+      reduce_blocks(dry, &S, smem, mode);  // partials still being written: values unused
+      precompute_step(dry, S, &pre);
+      __syncthreads();
+      if (threadIdx.x == 0) control_step(dry, S, pre);
+      __syncthreads();
     }
+    wait_tickets(c, nwork);
   } else {
-    row_block(c, op, (int)blockIdx.x, smem);
-  }
-
-  if (timed && c.kdbg && threadIdx.x == 0) c.kdbg[blockIdx.x * 4 + 1] = globaltimer_ns();
-  if (mode == FIN_A && c.p2p) __threadfence_system();  // remote group stores before the ticket
-  else __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(c.counter, 1u) == gridDim.x - 1;
-  if (timed && c.kdbg && threadIdx.x == 0) c.kdbg[blockIdx.x * 4 + 2] = globaltimer_ns();
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  const uint64_t t_last = timed ? globaltimer_ns() : 0;
-  if (mode == FIN_A) {
+    const int wb = (int)blockIdx.x - has_ctl;  // work block index
+    if (timed && c.kdbg && threadIdx.x == 0) c.kdbg[wb * 4 + 0] = globaltimer_ns();
+    if (timed) tl_start(c.ktl, 3);
+    // row blocks first (they carry the longer chains); FIN_B has column blocks only
+    const int64_t nrow_blocks = mode == FIN_B ? 0 : c.T;
+    if ((int64_t)wb >= nrow_blocks) {
+      const int b = (int)(wb - nrow_blocks);
+      if (mode == FIN_A) {
+        if (op == OP_STEP) column_group_partials<4>(c, b);
+        else column_group_partials<1>(c, b);
+      } else {
+        column_block(c, op, b, smem, mode);
+      }
+    } else {
+      row_block(c, op, wb, smem);
+    }
+    if (timed && c.kdbg && threadIdx.x == 0) c.kdbg[wb * 4 + 1] = globaltimer_ns();
+    if (mode == FIN_A && c.p2p) __threadfence_system();  // remote group stores before the ticket
+    else __threadfence();
+    __syncthreads();
+    if (mode != FIN_A) {
+      if (threadIdx.x == 0) {
+        atomicAdd(c.counter, 1u);
+        if (timed && c.kdbg) c.kdbg[wb * 4 + 2] = globaltimer_ns();
+      }
+      return;
+    }
+    if (threadIdx.x == 0) is_last = atomicAdd(c.counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
     group_scalar_partials(c);
     __syncthreads();
     if (threadIdx.x == 0) *c.counter = 0u;
     return;
   }
+  __threadfence();
+  const uint64_t t_last = timed ? globaltimer_ns() : 0;
   // the controller works on the shared-memory copy and writes it back
   if (mode == FIN_B && c.p2p && threadIdx.x == 0) cs.xerror = __ldcg(&ctlp->xerror);  // set by wait_exchange
   __syncthreads();
   reduce_blocks(cs, &S, smem, mode);
-  __shared__ Pre pre;
   if (op == OP_STEP && !cs.unit && !cs.done) {
     precompute_step(cs, S, &pre);
     __syncthreads();
@@ -998,6 +1058,10 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
       unsigned long long* tl = cs.ktl;
       tl[7] = globaltimer_ns();
       for (int k = 0; k < 8; ++k) tl[8 + k] = tl[k];  // keep the last complete pass
+#ifdef DBG_K0
+      for (int k = 0; k < 5; ++k) tl[25 + k] = tl[16 + k];
+      tl[24] = 0ull;
+#endif
       for (int k = 0; k < 4; ++k) {
         tl[2 * k] = ~0ull;
         tl[2 * k + 1] = 0ull;
@@ -1007,7 +1071,7 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
       const uint64_t t_end = globaltimer_ns();
       cs.sstat[ST_K2_MAIN] += t_last - __ldcg(&cs.sstat[ST_K2_T0]);
       cs.sstat[ST_K2_CTL] += t_end - t_last;
-      cs.sstat[ST_T0K0] += t_red - t_last;     // controller: copy-free reduction of the block partials
+      cs.sstat[ST_T0K0] += t_red - t_last;     // controller: reduction of the block partials
       cs.sstat[ST_T1K0] += t_logic - t_red;    // controller: decisions
       cs.sstat[ST_DONE0] += t_end - t_logic;   // controller: status mirror + control-block write-back
     }
@@ -1017,7 +1081,8 @@ __global__ void __launch_bounds__(kRedThreads) finalize_kernel(Ctl* __restrict__
 }  // namespace
 
 void launch_finalize_pass(Ctl* ctl_dev, const Ctl& h, int force_op, int mode, cudaStream_t s) {
-  const unsigned blocks = (unsigned)(mode == FIN_B ? h.CB : h.CB + h.T);
+  // + 1: the controller block (FIN_FUSED, FIN_B)
+  const unsigned blocks = (unsigned)(mode == FIN_B ? h.CB + 1 : mode == FIN_A ? h.CB + h.T : h.CB + h.T + 1);
   finalize_kernel<<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op, mode);
 }
 

@@ -194,7 +194,7 @@ struct Ctl {
   uint32_t* occ;             // [kNSlot][nbands][nstrips] per-cell "X has a nonzero bit pattern" bytes
   double* pmax;              // [kNSlot][nbands]  NaN-propagating max of p over each band
   double* qmax;              // [kNSlot][ncells]  ... of q over each cell (-inf for cells past n)
-  uint32_t* unitw;           // [nbands][nstrips] K0 -> K1 flag words (a flag byte per cell)
+  uint8_t* uflag;            // [nbands*ncp] K0 -> K1 flag byte of each listed cell (parallel to ulist)
   uint32_t* ulist;           // cells K1 visits this pass: (band << 12) | cell
   unsigned int* ucount;      // length of ulist (K0 appends, K2 resets)
   int64_t ncp;               // cells per row of cells, padded to whole tiles (U * 32)
@@ -202,6 +202,8 @@ struct Ctl {
   uint32_t* bct;             // [T][ncp]     bit b: band b of row tile t of this cell wrote partials
   uint8_t* tileflag;         // [T][U] the tile's partials are valid (0: screened out, all +0)
   int32_t* tlist;            // [T*U] tiles with active cells this pass (K1b assembles them)
+  uint8_t* tocc;             // [kNSlot][T*U] the tile may hold a nonzero (OR of its cells' occ bytes, a superset)
+  const double* tminc;       // [T*U] min C over the tile's cells (-inf if any entry is not finite)
   unsigned int* tcount;      // length of tlist (K0 appends, K2 resets)
   double* ccol;              // [nbands][kMaxNQ][ldx]  cell column partials (band partial of the tree)
   double* crow;              // [ncp][kMaxNQ][mpad]   cell row partials (8-lane butterfly per row)
@@ -411,6 +413,7 @@ __host__ __device__ __forceinline__ bool unit_pass(const Ctl& c, int op) {
 // screening metadata: min C per cell, per-slot occupancy and dual bounds
 void launch_minc_build(const Ctl& ctl_host, double* minc, cudaStream_t s);
 void launch_slot_meta(const Ctl& ctl_host, int slot, bool scan_occ, cudaStream_t s);
+void launch_tocc_fill(const Ctl& ctl_host, int slot, int value, cudaStream_t s);
 // sparse device->host copy of a slot matrix: occupied cells -> list, list -> staging (8 x 16 each)
 unsigned launch_occ_list(const Ctl& ctl_host, int slot, uint32_t* list, unsigned* count_dev, cudaStream_t s);
 void launch_cell_gather(const Ctl& ctl_host, int slot, const uint32_t* list, int64_t k0, int64_t k1, double* out,

@@ -63,7 +63,11 @@ __device__ __forceinline__ bool nz2(double2 v) {
 __device__ __forceinline__ bool step_with_avg(const Ctl& c) { return c.unit ? c.unit_avg != 0 : c.lagA != 0; }
 
 // ---------------------------------------------------------------------------
-// K0: screening.  One CTA per tile, thread (band, strip) of the tile.
+// K0: screening, one warp per tile (TM x 512: nbt bands x 32 cells).
+//   Tile level first: with no occupied cell in any slot the pass reads or
+//   writes, and RN(max p + max q) <= min C over the whole tile (current and
+//   averaged duals), every cell is inactive: flag 0, nothing listed.
+//   Otherwise per cell, lane = (band quarter bq, strip s) over nbt / 4 rounds:
 //   STEP: a cell is active when X or the lagged average has a nonzero there,
 //         or a dual pair may violate it; stale output cells are flagged ZX/ZA.
 //   DIST: active where the candidate or the anchor has a nonzero.
@@ -72,114 +76,200 @@ __device__ __forceinline__ bool step_with_avg(const Ctl& c) { return c.unit ? c.
 // bit maps K2 reads the cell partials by: bcr (per band and column tile) and
 // bct (per row tile and cell).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) screen_kernel(const Ctl* __restrict__ ctlp, int force_op) {
+constexpr int kScreenWarps = 8;
+
+__global__ void __launch_bounds__(32 * kScreenWarps, 2) screen_kernel(const Ctl* __restrict__ ctlp, int force_op) {
   const Ctl& c = *ctlp;
   if (c.done || !c.screen) return;
   const int op = force_op >= 0 ? force_op : c.op;
   if (!unit_pass(c, op)) return;
-  __shared__ uint32_t tilebits[32];  // per cell of the tile: bit bl = band bl active
-  __shared__ unsigned warp_base[8];  // cell-list offsets of the CTA's warps
   unsigned long long* tl = op == OP_STEP ? c.ktl : nullptr;
   tl_start(tl, 0);
-  const int64_t tu = blockIdx.x, tt = blockIdx.y;
-  const int s = threadIdx.x & 7, bl = threadIdx.x >> 3;  // strip in tile, band in tile
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x < 32) tilebits[threadIdx.x] = 0u;
-  const bool with_avg = op == OP_STEP && step_with_avg(c);
-  const int64_t band = tt * c.nbt + bl;
-  const int64_t strip = tu * kWarps + s;
-  const bool inband = bl < c.nbt && band < c.nbands;
-  const bool valid = inband && strip < c.nstrips;
-  uint32_t word = 0;
-  if (valid) {
-    const int64_t sstride = c.nbands * c.nstrips;
-    const int64_t ow = band * c.nstrips + strip;
-    // every load of the unit is issued up front (one memory round trip)
+  const int64_t tiles = c.T * c.U;
+  const int64_t tile = (int64_t)blockIdx.x * kScreenWarps + warp;
+  if (tile < tiles) {
+    const int64_t tt = tile / c.U, tu = tile - tt * c.U;
+    const bool with_avg = op == OP_STEP && step_with_avg(c);
+    const bool bound = op != OP_DIST, bound_avg = op == OP_STEP;
     const int sx = op == OP_DIST ? c.sCand : c.sX;
-    const uint32_t ox = __ldcg(c.occ + sx * sstride + ow);
-    const uint32_t oa = (op == OP_DIST || with_avg) ? __ldcg(c.occ + (op == OP_DIST ? c.sZ : c.sAsrc) * sstride + ow) : 0u;
-    const uint32_t zx = op == OP_STEP ? __ldcg(c.occ + c.sXn * sstride + ow) : 0u;
-    const uint32_t za = with_avg ? __ldcg(c.occ + c.sA * sstride + ow) : 0u;
-    const bool bound = op != OP_DIST;
-    const bool bound_avg = op == OP_STEP;
-    const double P = bound ? __ldcg(c.pmax + c.sX * c.nbands + band) : 0.0;
-    const double Pa = bound_avg ? __ldcg(c.pmax + c.sA * c.nbands + band) : 0.0;
-    double mc[kCellsPerStrip], Q[kCellsPerStrip], Qa[kCellsPerStrip];
+    const int sa = op == OP_DIST ? c.sZ : c.sAsrc;
+    // ---- tile level: 32 cell maxima of q, nbt band maxima of p, min C, occupancy
+    const int64_t tcell = tu * 32 + lane;
+    const bool okc = bound && tcell < c.ncells;
+    const double Qc = okc ? __ldcg(c.qmax + sx * c.ncells + tcell) : -INFINITY;
+    const double Qac = (okc && bound_avg) ? __ldcg(c.qmax + c.sA * c.ncells + tcell) : -INFINITY;
+    double P = -INFINITY, Pa = -INFINITY;
+    for (int bl = lane; bound && bl < c.nbt; bl += 32) {
+      const int64_t bnd = tt * c.nbt + bl;
+      if (bnd >= c.nbands) break;
+      P = max_nan(P, __ldcg(c.pmax + sx * c.nbands + bnd));
+      if (bound_avg) Pa = max_nan(Pa, __ldcg(c.pmax + c.sA * c.nbands + bnd));
+    }
+    uint32_t occ_any = 0;
+    double mc = INFINITY;
+    if (lane == 0) {
+      occ_any = __ldcg(c.tocc + sx * tiles + tile);
+      if (op == OP_DIST || with_avg) occ_any |= __ldcg(c.tocc + sa * tiles + tile);
+      if (op == OP_STEP) occ_any |= __ldcg(c.tocc + c.sXn * tiles + tile);
+      if (with_avg) occ_any |= __ldcg(c.tocc + c.sA * tiles + tile);
+      if (bound) mc = __ldcg(c.tminc + tile);
+    }
+    double Q = Qc, Qa = Qac;
 #pragma unroll
-    for (int k = 0; k < kCellsPerStrip; ++k) {
-      const int64_t cell = strip * kCellsPerStrip + k;
-      const bool ok = bound && cell < c.ncells;
-      mc[k] = ok ? __ldcg(c.minc + band * c.ncells + cell) : 0.0;
-      Q[k] = ok ? __ldcg(c.qmax + c.sX * c.ncells + cell) : 0.0;
-      Qa[k] = (ok && bound_avg) ? __ldcg(c.qmax + c.sA * c.ncells + cell) : 0.0;
+    for (int msk = 1; msk < 32; msk <<= 1) {
+      Q = max_nan(Q, __shfl_xor_sync(0xffffffffu, Q, msk));
+      Qa = max_nan(Qa, __shfl_xor_sync(0xffffffffu, Qa, msk));
+      P = max_nan(P, __shfl_xor_sync(0xffffffffu, P, msk));
+      Pa = max_nan(Pa, __shfl_xor_sync(0xffffffffu, Pa, msk));
     }
     // a non-finite step (tau) would turn 0 * inf into NaN: screen nothing
     const bool open = op == OP_STEP && !isfinite(c.tau);
+    // !(a <= b) keeps NaN bounds active
+    const bool full = __shfl_sync(0xffffffffu, occ_any ? 1 : 0, 0) || open ||
+                      (bound && !(P + Q <= __shfl_sync(0xffffffffu, mc, 0))) ||
+                      (bound_avg && !(Pa + Qa <= __shfl_sync(0xffffffffu, mc, 0)));
+    if (!full) {
+      if (lane == 0) c.tileflag[tile] = 0;
+    } else {
+      if (lane == 0) {
+        // the output slots' tile summaries are rebuilt by K1 from the cells it writes
+        if (op == OP_STEP) c.tocc[c.sXn * tiles + tile] = 0;
+        if (with_avg) c.tocc[c.sA * tiles + tile] = 0;
+        // metadata traffic of a per-cell screen: per (band, strip) min C and the
+        // cell maxima of q (current, average), 4 occupancy words, the flag word
+        if (op == OP_STEP && c.sstat)
+          atomicAdd(&c.sstat[ST_META], (unsigned long long)c.nbt * kWarps * (kCellsPerStrip * 8 * 3 + 4 * 4 + 4));
+      }
+      // ---- per cell: lane (bq, s) covers bands bq, bq + 4, ... of strip s
+      const int s = lane & 7, bq = lane >> 3;
+      const int64_t strip = tu * kWarps + s;
+      const bool vstrip = strip < c.nstrips;
+      const int64_t sstride = c.nbands * c.nstrips;
+      double Qk[kCellsPerStrip], Qak[kCellsPerStrip];
 #pragma unroll
-    for (int k = 0; k < kCellsPerStrip; ++k) {
-      const int64_t cell = strip * kCellsPerStrip + k;
-      if (cell >= c.ncells) break;
-      const uint32_t bx = (ox >> (8 * k)) & 0xffu, ba = (oa >> (8 * k)) & 0xffu;
-      const uint32_t bzx = (zx >> (8 * k)) & 0xffu, bza = (za >> (8 * k)) & 0xffu;
-      // !(a <= b) keeps NaN bounds active
-      const bool act = bx || ba || open || (bound && !(P + Q[k] <= mc[k])) ||
-                       (bound_avg && !(Pa + Qa[k] <= mc[k]));
-      const uint32_t f = (act ? U_ACT : 0u) | (bx ? U_LDX : 0u) | (ba ? U_LDA : 0u) | (bzx ? U_ZX : 0u) |
-                         (bza ? U_ZA : 0u);
-      word |= f << (8 * k);
+      for (int k = 0; k < kCellsPerStrip; ++k) {  // this lane's 4 cells: from the tile-level loads
+        Qk[k] = __shfl_sync(0xffffffffu, Qc, s * kCellsPerStrip + k);
+        Qak[k] = __shfl_sync(0xffffffffu, Qac, s * kCellsPerStrip + k);
+      }
+      uint32_t listed_all = 0;   // 4 bits per round
+      uint32_t tb[kCellsPerStrip] = {0u, 0u, 0u, 0u};  // bct bits (band of the tile) of this lane's cells
+      bool any_act = false;
+      const int nrounds = (c.nbt + 3) >> 2;
+      // rounds in chunks of kChunk: every load of a chunk is issued before its
+      // flags are computed and stored (one memory round trip per chunk)
+      constexpr int kChunk = 2, kMaxRounds = 8;  // nbt <= 32
+      uint32_t words[kMaxRounds];  // flag words of the rounds (static indices: unrolled)
+#pragma unroll
+      for (int r0 = 0; r0 < kMaxRounds; r0 += kChunk) {
+        if (r0 >= nrounds) break;
+        uint32_t ox[kChunk], oa[kChunk], zx[kChunk], za[kChunk];
+        double Pb[kChunk], Pab[kChunk], mck[kChunk][kCellsPerStrip];
+        bool valid[kChunk];
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+          const int bl = (r0 + u) * 4 + bq;
+          const int64_t band = tt * c.nbt + bl;
+          valid[u] = r0 + u < nrounds && bl < c.nbt && band < c.nbands && vstrip;
+          const int64_t ow = band * c.nstrips + strip;
+          ox[u] = valid[u] ? __ldcg(c.occ + sx * sstride + ow) : 0u;
+          oa[u] = (valid[u] && (op == OP_DIST || with_avg)) ? __ldcg(c.occ + sa * sstride + ow) : 0u;
+          zx[u] = (valid[u] && op == OP_STEP) ? __ldcg(c.occ + c.sXn * sstride + ow) : 0u;
+          za[u] = (valid[u] && with_avg) ? __ldcg(c.occ + c.sA * sstride + ow) : 0u;
+          Pb[u] = (valid[u] && bound) ? __ldcg(c.pmax + sx * c.nbands + band) : 0.0;
+          Pab[u] = (valid[u] && bound_avg) ? __ldcg(c.pmax + c.sA * c.nbands + band) : 0.0;
+#pragma unroll
+          for (int k = 0; k < kCellsPerStrip; ++k) {
+            const int64_t cell = strip * kCellsPerStrip + k;
+            mck[u][k] = (valid[u] && bound && cell < c.ncells) ? __ldcg(c.minc + band * c.ncells + cell) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+          const int rd = r0 + u;
+          const int bl = rd * 4 + bq;
+          const int64_t band = tt * c.nbt + bl;
+          uint32_t word = 0;
+          if (valid[u]) {
+#pragma unroll
+            for (int k = 0; k < kCellsPerStrip; ++k) {
+              const int64_t cell = strip * kCellsPerStrip + k;
+              if (cell >= c.ncells) break;
+              const uint32_t bx = (ox[u] >> (8 * k)) & 0xffu, ba = (oa[u] >> (8 * k)) & 0xffu;
+              const uint32_t bzx = (zx[u] >> (8 * k)) & 0xffu, bza = (za[u] >> (8 * k)) & 0xffu;
+              const bool act = bx || ba || open || (bound && !(Pb[u] + Qk[k] <= mck[u][k])) ||
+                               (bound_avg && !(Pab[u] + Qak[k] <= mck[u][k]));
+              const uint32_t f = (act ? U_ACT : 0u) | (bx ? U_LDX : 0u) | (ba ? U_LDA : 0u) |
+                                 (bzx ? U_ZX : 0u) | (bza ? U_ZA : 0u);
+              word |= f << (8 * k);
+            }
+          }
+          words[rd] = word;
+          uint32_t listed = 0, actb = 0;
+#pragma unroll
+          for (int k = 0; k < kCellsPerStrip; ++k) {
+            const uint32_t f = (word >> (8 * k)) & 0xffu;
+            listed |= (f != 0u) << k;
+            actb |= ((f & U_ACT) != 0u) << k;
+            tb[k] |= ((f & U_ACT) != 0u ? 1u : 0u) << (bl & 31);
+          }
+          any_act |= actb != 0u;
+          if (rd < 8) listed_all |= listed << (4 * rd);
+          // bcr[band][tu]: bit 4 s + k = cell k of strip s (the 8 lanes of one band)
+          uint32_t rbits = actb << (4 * s);
+#pragma unroll
+          for (int msk = 1; msk < 8; msk <<= 1) rbits |= __shfl_xor_sync(0xffffffffu, rbits, msk);
+          if (s == 0 && rd < nrounds && bl < c.nbt && band < c.nbands) c.bcr[band * c.U + tu] = rbits;
+        }
+      }
+      // warp-aggregated append of the listed cells: one atomic per tile
+      const int cnt = __popc(listed_all);
+      int incl = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      unsigned base = 0;
+      if (lane == 31 && tot) base = atomicAdd(c.ucount, (unsigned)tot);
+      base = __shfl_sync(0xffffffffu, base, 31);
+      unsigned pos = base + (unsigned)(incl - cnt);
+#pragma unroll
+      for (int rd = 0; rd < kMaxRounds; ++rd) {
+        if (rd >= nrounds) break;
+        const uint32_t l4 = (listed_all >> (4 * rd)) & 0xfu;
+        const int64_t band = tt * c.nbt + rd * 4 + bq;
+#pragma unroll
+        for (int k = 0; k < kCellsPerStrip; ++k)
+          if ((l4 >> k) & 1u) {
+            c.ulist[pos] = (uint32_t)((band << 12) | (strip * kCellsPerStrip + k));
+            c.uflag[pos] = (uint8_t)((words[rd] >> (8 * k)) & 0xffu);  // the cell's flags travel with it
+            ++pos;
+          }
+      }
+      // bct[tt][cell]: bit bl = band bl of the tile (OR over the 4 band quarters)
+#pragma unroll
+      for (int k = 0; k < kCellsPerStrip; ++k) {
+        tb[k] |= __shfl_xor_sync(0xffffffffu, tb[k], 8);
+        tb[k] |= __shfl_xor_sync(0xffffffffu, tb[k], 16);
+      }
+      if (bq == 0) {
+#pragma unroll
+        for (int k = 0; k < kCellsPerStrip; ++k) c.bct[tt * c.ncp + tu * 32 + s * kCellsPerStrip + k] = tb[k];
+      }
+      // the tile's partials are assembled by K1b, or are all +0 (flag 0)
+      const bool any = __any_sync(0xffffffffu, any_act);
+      if (lane == 0) {
+        c.tileflag[tile] = any ? 1 : 0;
+        if (any) c.tlist[atomicAdd(c.tcount, 1u)] = (int32_t)tile;
+      }
     }
-    c.unitw[ow] = word;
   }
-  // per-cell bits of this thread's strip: listed (any flag) and active (partials)
-  uint32_t listed = 0, actb = 0;
-#pragma unroll
-  for (int k = 0; k < kCellsPerStrip; ++k) {
-    const uint32_t f = (word >> (8 * k)) & 0xffu;
-    listed |= (f != 0u) << k;
-    actb |= ((f & U_ACT) != 0u) << k;
+  if (tl) {
+    __syncthreads();
+    tl_end(tl, 0);
   }
-  // CTA-aggregated append of the listed cells: warp scan, one atomic per CTA
-  const int cnt = __popc(listed);
-  int incl = cnt;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += y;
-  }
-  if (lane == 31) warp_base[warp] = (unsigned)incl;
-  // bcr[band][tu]: bit 4 s + k = cell k of strip s (8 lanes of one band)
-  uint32_t rbits = actb << (4 * s);
-#pragma unroll
-  for (int msk = 1; msk < 8; msk <<= 1) rbits |= __shfl_xor_sync(0xffffffffu, rbits, msk);
-  if (s == 0 && inband) c.bcr[band * c.U + tu] = rbits;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int nw = (blockDim.x + 31) >> 5;
-    unsigned tot = 0;
-    for (int w = 0; w < nw; ++w) {
-      const unsigned t = warp_base[w];
-      warp_base[w] = tot;
-      tot += t;
-    }
-    const unsigned base = tot ? atomicAdd(c.ucount, tot) : 0u;
-    for (int w = 0; w < nw; ++w) warp_base[w] += base;
-  }
-  // bct[tt][cell]: bit bl = band bl of the tile
-#pragma unroll
-  for (int k = 0; k < kCellsPerStrip; ++k)
-    if ((actb >> k) & 1u) atomicOr(&tilebits[s * kCellsPerStrip + k], 1u << bl);
-  const int any = __syncthreads_or(actb != 0u);
-  unsigned pos = warp_base[warp] + (unsigned)(incl - cnt);
-#pragma unroll
-  for (int k = 0; k < kCellsPerStrip; ++k)
-    if ((listed >> k) & 1u) c.ulist[pos++] = (uint32_t)((band << 12) | (strip * kCellsPerStrip + k));
-  if (threadIdx.x < 32) c.bct[tt * c.ncp + tu * 32 + threadIdx.x] = tilebits[threadIdx.x];
-  // the tile's partials are assembled by K1b, or are all +0 (flag 0)
-  if (threadIdx.x == 0) {
-    c.tileflag[tt * c.U + tu] = any ? 1 : 0;
-    if (any) c.tlist[atomicAdd(c.tcount, 1u)] = (int32_t)(tt * c.U + tu);
-  }
-  tl_end(tl, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -217,91 +307,164 @@ __device__ __forceinline__ CellGeo cell_geo(const Ctl& c, uint32_t entry) {
 }
 
 // Partial writes shared by every cell op.  o[rr][q][e]: the lane's outputs for
-// row 2 rg + rr, column e; sacc: the lane's stage scalar partials (its two rows,
-// element order), so the band partial is (s0 + s1) + (s2 + s3) over the row
-// groups (masks 8, 16) and the cell value the 8-lane butterfly on top.
-// Partial writes shared by every cell op.  o[rr][q][e]: the lane's outputs for
-// row 2 rg + rr, column e; sacc: the lane's stage scalar partials (its two rows,
-// element order), so the band partial is (s0 + s1) + (s2 + s3) over the row
-// groups (masks 8, 16) and the cell value the 8-lane butterfly on top.
-// Partial writes shared by every cell op.  o[rr][q][e]: the lane's outputs for
-// row 2 rg + rr, column e; sacc: the lane's stage scalar partials (its two rows,
-// element order), so the band partial is (s0 + s1) + (s2 + s3) over the row
-// groups (masks 8, 16) and the cell value the 8-lane butterfly on top.  All
-// three reductions use transposed butterflies (a few shuffles per value).
+// row 2 rg + rr, column e; sacc: the lane's stage scalar partials (its two
+// rows, element order).  The three reductions follow the canonical tree of
+// pass_ops.cuh and run through a per-warp shared-memory transpose (each lane
+// writes its values, then reads the ones it reduces):
+//   columns: in-lane pair sum, then (rg0 + rg1) + (rg2 + rg3);
+//   rows:    in-lane column-pair sum, then ((c0+c1)+(c2+c3))+((c4+c5)+(c6+c7));
+//   scalars: (rg0 + rg1) + (rg2 + rg3) per column pair, then the column-pair
+//            tree (its last two levels as shuffles over lane bits 0, 1).
+// Strides 36 / 33 keep the 64-bit reads at two wavefronts (conflict-free).
+constexpr int kColD = 36, kRowD = 33, kScalD = 33;
+constexpr int kRedWarpDoubles = 8 * kColD;
+
+// the calling warp's transpose buffer (one buffer per kernel for every op)
+__device__ __forceinline__ double* warp_red_buf() {
+  __shared__ double red_buf[kWarps * kRedWarpDoubles];
+  return red_buf + (threadIdx.x >> 5) * kRedWarpDoubles;
+}
+
 template <int NQ, int NS>
 __device__ __forceinline__ void cell_flush(const Ctl& c, const CellGeo& g, const double (&o)[2][NQ][2],
                                           const double (&sacc)[NS]) {
-  // column band partial: pair sum of the lane's two rows, then masks 8, 16;
-  // afterwards lane (rg, cp) holds (x, y) of quantity q(rg) for its column pair
-  {
-    constexpr int V = 2 * NQ;
-    double v[V];
+  static_assert(2 * NQ <= 8 && NS <= 8, "per-warp transpose buffer");
+  const int lane = threadIdx.x & 31;
+  double* S = warp_red_buf();
+  // ---- column band partials
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      v[2 * q] = o[0][q][0] + o[1][q][0];
-      v[2 * q + 1] = o[0][q][1] + o[1][q][1];
-    }
-    constexpr int M[2] = {8, 16};
-    tsum<V, 2>(v, M);
-    const int idx = tsum_index<V, 2>(M);
-    if (g.v0) {
-      if (NQ == 4) {
-        *reinterpret_cast<double2*>(c.ccol + (g.band * kMaxNQ + idx / 2) * c.ldx + g.j) = make_double2(v[0], v[1]);
-      } else if (g.rg < 2) {  // NQ == 1: rg 0 holds x, rg 1 holds y
-        c.ccol[g.band * kMaxNQ * c.ldx + g.j + idx] = v[0];
-      }
-    }
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) S[(2 * q + e) * kColD + lane] = o[0][q][e] + o[1][q][e];
+  __syncwarp();
+  if (NQ == 4) {  // lane (q, column pair cp)
+    const int q = lane >> 3, cp = lane & 7;
+    double a[4][2];
+#pragma unroll
+    for (int rg = 0; rg < 4; ++rg)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) a[rg][e] = S[(2 * q + e) * kColD + rg * 8 + cp];
+    const int64_t j = g.cell * kCell + cp * 2;
+    if (j < c.n)
+      *reinterpret_cast<double2*>(c.ccol + (g.band * kMaxNQ + q) * c.ldx + j) =
+          make_double2((a[0][0] + a[1][0]) + (a[2][0] + a[3][0]), (a[0][1] + a[1][1]) + (a[2][1] + a[3][1]));
+  } else if (lane < 16) {  // NQ == 1: lane (e, cp)
+    const int e = lane >> 3, cp = lane & 7;
+    double a[4];
+#pragma unroll
+    for (int rg = 0; rg < 4; ++rg) a[rg] = S[e * kColD + rg * 8 + cp];
+    const int64_t j = g.cell * kCell + cp * 2;
+    if (j < c.n) c.ccol[g.band * kMaxNQ * c.ldx + j + e] = (a[0] + a[1]) + (a[2] + a[3]);
   }
-  // row values: 8-lane transposed butterfly over the column pairs
+  __syncwarp();
+  // ---- row values
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) S[(rr * NQ + q) * kRowD + lane] = o[rr][q][0] + o[rr][q][1];
+  __syncwarp();
+  if (lane < 8 * NQ) {  // lane (q, row r)
+    const int q = lane >> 3, r = lane & 7;
+    const double* src = S + ((r & 1) * NQ + q) * kRowD + (r >> 1) * 8;
+    double b[8];
+#pragma unroll
+    for (int cp = 0; cp < 8; ++cp) b[cp] = src[cp];
+    const double v = ((b[0] + b[1]) + (b[2] + b[3])) + ((b[4] + b[5]) + (b[6] + b[7]));
+    DCHECK(g.cell < c.ncp && (r >= g.rows || g.i0 + r < c.mpad), "crow", g.cell, g.i0 + r);
+    if (r < g.rows) c.crow[(g.cell * kMaxNQ + q) * c.mpad + g.i0 + r] = v;
+  }
+  __syncwarp();
+  // ---- scalars: lane (s, cq) reduces column pairs 2 cq, 2 cq + 1
+#pragma unroll
+  for (int s = 0; s < NS; ++s) S[s * kScalD + lane] = sacc[s];
+  __syncwarp();
   {
-    constexpr int V = 2 * NQ;
-    double rv[V];
+    const int s = lane >> 2, cq = lane & 3;
+    double t = 0.0;
+    if (s < NS) {
+      double d[2][4];
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) rv[rr * NQ + q] = o[rr][q][0] + o[rr][q][1];
-    warp_transpose_sum<V, 8>(rv);
-    if (transpose_is_writer<V, 8>(threadIdx.x & 31)) {
-      const int idx = transpose_owner_index<V>(g.cp);
-      const int r = 2 * g.rg + idx / NQ, q = idx % NQ;
-      DCHECK(g.cell < c.ncp && (r >= g.rows || g.i0 + r < c.mpad), "crow", g.cell, g.i0 + r);
-      if (r < g.rows) c.crow[(g.cell * kMaxNQ + q) * c.mpad + g.i0 + r] = rv[0];
+        for (int rg = 0; rg < 4; ++rg) d[h][rg] = S[s * kScalD + rg * 8 + 2 * cq + h];
+      t = ((d[0][0] + d[0][1]) + (d[0][2] + d[0][3])) + ((d[1][0] + d[1][1]) + (d[1][2] + d[1][3]));
     }
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    if (s < NS && cq == 0) c.cscal[(g.band * c.ncp + g.cell) * kMaxNS + s] = t;
   }
-  // scalars: stage partials pairwise over the row groups (masks 8, 16), then
-  // the column pairs (masks 1, 2, 4)
-  {
-    constexpr int V = NS <= 1 ? 1 : NS <= 2 ? 2 : NS <= 4 ? 4 : 8;
-    double v[V];
+  __syncwarp();
+}
+
+// ---- STEP cells, software-pipelined: the warp copies the next cell's inputs
+// (its C / X / A row segments and the dual values) into a shared-memory stage
+// with cp.async while it computes the current cell, so the load latency
+// overlaps compute.  Every lane reads back only what it copied itself, so a
+// lane's own cp.async.wait_group is the only synchronisation needed.  Stage
+// layout: field-major, lane-contiguous (conflict-free 16- and 8-byte reads).
+constexpr int kStF16 = 8;   // 16-byte fields: C, X, A of both rows; q pair, qa pair
+constexpr int kStF8 = 4;    // 8-byte fields: p, pa of both rows
+constexpr int kStageBytes = 32 * (16 * kStF16 + 8 * kStF8);  // 5 KB per warp and stage
+constexpr int kStages = 2;
+constexpr size_t kUnitDynSmem = (size_t)kWarps * kStages * kStageBytes;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool on) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(on ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool on) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(on ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// issue the copies of one cell's inputs (zero-filled where not needed)
+template <bool IMPLICIT, bool AVG>
+__device__ __forceinline__ void cell_issue(const StepOp& op, const Ctl& c, uint32_t entry, uint32_t f,
+                                           unsigned char* stage) {
+  const int lane = threadIdx.x & 31;
+  const CellGeo g = cell_geo(c, entry);
+  const bool act = (f & U_ACT) != 0;
+  const bool ldx = act && (f & U_LDX);
+  const bool lda = AVG && act && (f & U_LDA);
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(stage);
+  const uint32_t f16 = base + lane * 16, f8 = base + 32 * 16 * kStF16 + lane * 8;
 #pragma unroll
-    for (int s = 0; s < V; ++s) v[s] = s < NS ? sacc[s] : 0.0;
-    constexpr int M[5] = {8, 16, 1, 2, 4};
-    tsum<V, 5>(v, M);
-    const int idx = tsum_index<V, 5>(M);
-    // every lane holds the total of index idx; the lanes with cp bits above the
-    // routing steps clear write it
-    constexpr int lg = log2_pow2<V>();
-    const int routed = lg >= 3 ? 1 : 0;  // mask 1 (cp bit 0) routed for V = 8
-    if (idx < NS && (g.cp >> routed) == 0)
-      c.cscal[(g.band * c.ncp + g.cell) * kMaxNS + idx] = v[0];
+  for (int rr = 0; rr < 2; ++rr) {
+    const int r = 2 * g.rg + rr;
+    const bool ok = act && r < g.rows && g.v0;
+    const int64_t i = ok ? g.i0 + r : 0;
+    const int64_t jj = ok ? g.j : 0;
+    if (!IMPLICIT) cp_async16(f16 + (0 + rr) * 512, op.C + i * c.ldc + jj, ok);
+    cp_async16(f16 + (2 + rr) * 512, op.X + i * c.ldx + jj, ok && ldx);
+    cp_async16(f16 + (4 + rr) * 512, (AVG ? op.A : op.X) + i * c.ldx + jj, ok && lda);
+    cp_async8(f8 + (0 + rr) * 256, op.p + i, ok);
+    cp_async8(f8 + (2 + rr) * 256, op.pa + i, ok);
   }
+  const bool okc = act && g.v0;
+  const int64_t j0 = okc ? g.j : 0, j1 = (okc && g.v1) ? g.j + 1 : 0;
+  // q pair / qa pair as two 8-byte halves each (the second only inside the row)
+  cp_async8(f16 + 6 * 512, op.q + j0, okc);
+  cp_async8(f16 + 6 * 512 + 8, op.q + j1, okc && g.v1);
+  cp_async8(f16 + 7 * 512, op.qa + j0, okc);
+  cp_async8(f16 + 7 * 512 + 8, op.qa + j1, okc && g.v1);
 }
 
 template <bool IMPLICIT, bool AVG>
-__device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const CostGen& gen, uint32_t entry,
-                                          unsigned long long& bytes, unsigned long long& cells) {
+__device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const CostGen& gen, uint32_t entry, uint32_t f,
+                                          const unsigned char* stage, unsigned long long& bytes,
+                                          unsigned long long& cells) {
   constexpr int NQ = StepOp::NQ, NS = StepOp::NS;
   const int lane = threadIdx.x & 31;
   const CellGeo g = cell_geo(c, entry);
-  const uint32_t f = (__ldcg(c.unitw + g.band * c.nstrips + g.strip) >> (8 * g.k)) & 0xffu;
   const bool act = (f & U_ACT) != 0;  // cell-uniform
   const bool ldx = act && (f & U_LDX);
   const bool lda = AVG && act && (f & U_LDA);
   const bool zx = (f & U_ZX) != 0;
   const bool za = AVG && (f & U_ZA) != 0;
   if (lane == 0 && act) cells += 1;
-  const double2 zero2 = make_double2(0.0, 0.0);
+  const double2* s16 = reinterpret_cast<const double2*>(stage) + lane;
+  const double* s8 = reinterpret_cast<const double*>(stage + 32 * 16 * kStF16) + lane;
   double2 cc[2], xx[2], aa[2];
   double pr[2], par[2];
   bool okr[2];
@@ -309,23 +472,15 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const 
   for (int rr = 0; rr < 2; ++rr) {
     const int r = 2 * g.rg + rr;
     okr[rr] = act && r < g.rows && g.v0;
-    const int64_t i = g.i0 + r;
-    if (IMPLICIT) {
-      cc[rr] = zero2;
-    } else {
-      cc[rr] = okr[rr] ? ld_stream2(op.C + i * c.ldc + g.j) : zero2;
-    }
-    xx[rr] = (okr[rr] && ldx) ? ld_stream2(op.X + i * c.ldx + g.j) : zero2;
-    aa[rr] = (okr[rr] && lda) ? ld_stream2(op.A + i * c.ldx + g.j) : zero2;
-    pr[rr] = okr[rr] ? __ldg(op.p + i) : 0.0;
-    par[rr] = okr[rr] ? __ldg(op.pa + i) : 0.0;
+    cc[rr] = IMPLICIT ? make_double2(0.0, 0.0) : s16[(0 + rr) * 32];
+    xx[rr] = s16[(2 + rr) * 32];
+    aa[rr] = s16[(4 + rr) * 32];
+    pr[rr] = s8[(0 + rr) * 32];
+    par[rr] = s8[(2 + rr) * 32];
     if (okr[rr]) bytes += (IMPLICIT ? 0 : 16) + (ldx ? 16 : 0) + (lda ? 16 : 0);
   }
-  double qv[2] = {0.0, 0.0}, qav[2] = {0.0, 0.0};
-  if (act && g.v0) {
-    qv[0] = op.q[g.j]; qav[0] = op.qa[g.j];
-    if (g.v1) { qv[1] = op.q[g.j + 1]; qav[1] = op.qa[g.j + 1]; }
-  }
+  const double2 q2 = s16[6 * 32], qa2 = s16[7 * 32];
+  const double qv[2] = {q2.x, q2.y}, qav[2] = {qa2.x, qa2.y};
   if (IMPLICIT && act) {
     const double2 c0 = gen.col_coord(g.j), c1 = gen.col_coord(g.j + 1);
 #pragma unroll
@@ -379,9 +534,12 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const 
     const int64_t sstride = c.nbands * c.nstrips;
     uint8_t* ox = reinterpret_cast<uint8_t*>(c.occ + c.sXn * sstride + g.band * c.nstrips + g.strip);
     ox[g.k] = anyx ? 1 : 0;
+    const int64_t tiles = c.T * c.U, tile = (g.band / c.nbt) * c.U + g.strip / kWarps;
+    if (anyx) c.tocc[c.sXn * tiles + tile] = 1;
     if (AVG) {
       uint8_t* oa = reinterpret_cast<uint8_t*>(c.occ + c.sA * sstride + g.band * c.nstrips + g.strip);
       oa[g.k] = anya ? 1 : 0;
+      if (anya) c.tocc[c.sA * tiles + tile] = 1;
     }
   }
   if (act) {
@@ -390,15 +548,49 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const 
   }
 }
 
+// the warp's STEP cells k = k0, k0 + nw, ...: copies of cell k + nw in flight
+// while cell k is computed
+template <bool IMPLICIT, bool AVG>
+__device__ __forceinline__ void step_cells(const StepOp& o, const Ctl& c, const CostGen& gen, unsigned k0,
+                                           unsigned nw, unsigned ncells, unsigned char* stages,
+                                           unsigned long long& bytes, unsigned long long& cells) {
+  if (k0 >= ncells) return;
+  uint32_t e_cur = __ldcg(c.ulist + k0), f_cur = __ldcg(c.uflag + k0);
+  uint32_t e_nx = 0, f_nx = 0;
+  if (k0 + nw < ncells) {
+    e_nx = __ldcg(c.ulist + k0 + nw);
+    f_nx = __ldcg(c.uflag + k0 + nw);
+  }
+  cell_issue<IMPLICIT, AVG>(o, c, e_cur, f_cur, stages);
+  cp_async_commit();
+  int st = 0;
+  for (unsigned k = k0; k < ncells; k += nw) {
+    const bool more = k + nw < ncells;
+    // the list entry two cells ahead, then the copies of the next cell
+    uint32_t e_n2 = 0, f_n2 = 0;
+    if (k + 2 * nw < ncells) {
+      e_n2 = __ldcg(c.ulist + k + 2 * nw);
+      f_n2 = __ldcg(c.uflag + k + 2 * nw);
+    }
+    if (more) cell_issue<IMPLICIT, AVG>(o, c, e_nx, f_nx, stages + (st ^ 1) * kStageBytes);
+    cp_async_commit();
+    cp_async_wait<1>();  // this cell's copies have landed
+    cell_step<IMPLICIT, AVG>(o, c, gen, e_cur, f_cur, stages + st * kStageBytes, bytes, cells);
+    e_cur = e_nx; f_cur = f_nx;
+    e_nx = e_n2; f_nx = f_n2;
+    st ^= 1;
+  }
+  cp_async_wait<0>();
+}
+
 // restart distance (DIST) and the start KKT through the screen (NQ = 1), with
 // the dense walkers' per-row compute()
 template <class Op>
-__device__ __forceinline__ void cell_one(const Op& op, const Ctl& c, uint32_t entry, unsigned long long& bytes,
+__device__ __forceinline__ void cell_one(const Op& op, const Ctl& c, uint32_t entry, uint32_t f, unsigned long long& bytes,
                                          unsigned long long& cells) {
   constexpr int NQ = Op::NQ, NS = Op::NS;
   const int lane = threadIdx.x & 31;
   const CellGeo cg = cell_geo(c, entry);
-  const uint32_t f = (__ldcg(c.unitw + cg.band * c.nstrips + cg.strip) >> (8 * cg.k)) & 0xffu;
   if (!(f & U_ACT)) return;  // cell-uniform
   if (lane == 0) cells += 1;
   Geo g;  // the fields the ops read
@@ -459,25 +651,24 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
     gen.kind = c.C ? 0 : c.cost_kind;
     gen.a0 = c.cost_a[0]; gen.a1 = c.cost_a[1]; gen.a2 = c.cost_a[2]; gen.a3 = c.cost_a[3];
     gen.row0 = c.row0;
-    for (unsigned k = gw; k < ncells; k += nw) {
-      const uint32_t entry = __ldcg(c.ulist + k);
-      if (o.C) {
-        if (o.with_avg) cell_step<false, true>(o, c, gen, entry, bytes, cells);
-        else cell_step<false, false>(o, c, gen, entry, bytes, cells);
-      } else {
-        if (o.with_avg) cell_step<true, true>(o, c, gen, entry, bytes, cells);
-        else cell_step<true, false>(o, c, gen, entry, bytes, cells);
-      }
+    extern __shared__ __align__(16) unsigned char unit_dyn[];
+    unsigned char* stages = unit_dyn + warp * kStages * kStageBytes;
+    if (o.C) {
+      if (o.with_avg) step_cells<false, true>(o, c, gen, gw, nw, ncells, stages, bytes, cells);
+      else step_cells<false, false>(o, c, gen, gw, nw, ncells, stages, bytes, cells);
+    } else {
+      if (o.with_avg) step_cells<true, true>(o, c, gen, gw, nw, ncells, stages, bytes, cells);
+      else step_cells<true, false>(o, c, gen, gw, nw, ncells, stages, bytes, cells);
     }
   } else if (op == OP_DIST) {
     DiffOp o;
     o.Xa = c.slot[c.sZ].X; o.Xb = c.slot[c.sCand].X;
-    for (unsigned k = gw; k < ncells; k += nw) cell_one(o, c, __ldcg(c.ulist + k), bytes, cells);
+    for (unsigned k = gw; k < ncells; k += nw) cell_one(o, c, __ldcg(c.ulist + k), __ldcg(c.uflag + k), bytes, cells);
   } else {
     KktOp o;
     const Slot& sx = c.slot[c.sX];
     o.C = c.C; o.X = sx.X; o.p = sx.p; o.q = sx.q; o.viol = nullptr;
-    for (unsigned k = gw; k < ncells; k += nw) cell_one(o, c, __ldcg(c.ulist + k), bytes, cells);
+    for (unsigned k = gw; k < ncells; k += nw) cell_one(o, c, __ldcg(c.ulist + k), __ldcg(c.uflag + k), bytes, cells);
   }
   // statistics: one atomic per CTA, then the last CTA stamps the end time
 #pragma unroll
@@ -506,8 +697,10 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
         c.sstat[ST_K1_NS] += t1 - __ldcg(&c.sstat[ST_T0]);
         c.sstat[ST_TILES] += ncells;
         c.sstat[ST_PASSES] += 1;
-        // K0 metadata traffic of this pass: min C + 4 occupancy words + flag word per (band, strip)
-        c.sstat[ST_META] += (unsigned long long)c.nbands * c.nstrips * (kCellsPerStrip * 8 + 4 * 4 + 4);
+        // K0 tile-level screen of this pass: 32 cell + nbt band maxima (current and
+        // average), 4 tile occupancy bytes and the tile's min C per tile (the
+        // per-cell screens add theirs in K0)
+        c.sstat[ST_META] += (unsigned long long)c.T * c.U * ((32 + c.nbt) * 2 * 8 + 4 + 8);
       }
       c.sstat[ST_DONE1] = 0;
     }
@@ -687,6 +880,51 @@ __global__ void minc_kernel(const double* __restrict__ C, int64_t ldc, CostGen g
   }
 }
 
+// min C over each tile (from the cell minima; -inf propagates)
+struct TileMeta {  // the geometry the tile metadata kernels need (kernel argument)
+  int64_t nbt, nbands, nstrips, ncells, T, U;
+  const double* minc;
+  const uint32_t* occ;
+  uint8_t* tocc;
+};
+
+__host__ TileMeta tile_meta(const Ctl& h) {
+  return TileMeta{h.nbt, h.nbands, h.nstrips, h.ncells, h.T, h.U, h.minc, h.occ, h.tocc};
+}
+
+__global__ void tile_minc_kernel(const TileMeta c, double* __restrict__ tminc) {
+  __shared__ double wmin[8];
+  const int64_t tu = blockIdx.x, tt = blockIdx.y;
+  const int s = threadIdx.x & 7, bl = threadIdx.x >> 3, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t band = tt * c.nbt + bl, strip = tu * kWarps + s;
+  double mn = INFINITY;
+  if (bl < c.nbt && band < c.nbands && strip < c.nstrips)
+    for (int k = 0; k < kCellsPerStrip; ++k) {
+      const int64_t cell = strip * kCellsPerStrip + k;
+      if (cell < c.ncells) mn = fmin(mn, c.minc[band * c.ncells + cell]);
+    }
+#pragma unroll
+  for (int msk = 1; msk < 32; msk <<= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, msk));
+  if (lane == 0) wmin[warp] = mn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mn = fmin(mn, wmin[w]);
+    tminc[tt * c.U + tu] = mn;
+  }
+}
+
+// tile summaries of one slot's occupancy bytes
+__global__ void tocc_kernel(const TileMeta c, int slot) {
+  const int64_t tu = blockIdx.x, tt = blockIdx.y;
+  const int s = threadIdx.x & 7, bl = threadIdx.x >> 3;
+  const int64_t band = tt * c.nbt + bl, strip = tu * kWarps + s;
+  uint32_t w = 0;
+  if (bl < c.nbt && band < c.nbands && strip < c.nstrips)
+    w = c.occ[(int64_t)slot * c.nbands * c.nstrips + band * c.nstrips + strip];
+  const int any = __syncthreads_or(w != 0u);
+  if (threadIdx.x == 0) c.tocc[(int64_t)slot * c.T * c.U + tt * c.U + tu] = any ? 1 : 0;
+}
+
 // occupancy bytes of one slot matrix: cell flag = any nonzero bit pattern
 __global__ void occ_scan_kernel(const double* __restrict__ X, int64_t ldx, int64_t m, int64_t n, int64_t nbands,
                                 int64_t ncells, uint8_t* __restrict__ occ_bytes, int64_t nstrips) {
@@ -791,6 +1029,7 @@ void launch_cell_gather(const Ctl& h, int slot, const uint32_t* list, int64_t k0
 
 void prepare_sparse_kernel() {
   cudaFuncSetAttribute(generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUnitDynSmem);
 }
 
 static size_t generic_smem_bytes(int64_t TM) {
@@ -803,16 +1042,13 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // graph passes (force_op < 0) are STEP / DIST / start-KKT; unit calls choose on the host
   if (force_op < 0 || unit_pass(h, force_op)) {
-    dim3 g0((unsigned)h.U, (unsigned)h.T);
-    // thread (band, strip) of the tile; at least one full warp (the append and
-    // the bit maps use warp shuffles)
-    const unsigned threads = (unsigned)(kWarps * h.nbt < 32 ? 32 : kWarps * h.nbt);
-    screen_kernel<<<g0, threads, 0, s>>>(ctl_dev, force_op);
+    const unsigned g0 = (unsigned)((h.T * h.U + kScreenWarps - 1) / kScreenWarps);  // warp per tile
+    screen_kernel<<<g0, 32 * kScreenWarps, 0, s>>>(ctl_dev, force_op);
     if (getenv("PDOT_DEBUG_SYNC")) {
       const cudaError_t e = cudaStreamSynchronize(s);
       if (e != cudaSuccess) fprintf(stderr, "screen_kernel failed: %s\n", cudaGetErrorString(e));
     }
-    unit_kernel<<<(unsigned)(sms * kSparseCtasPerSm), kThreads, 0, s>>>(ctl_dev, force_op);
+    unit_kernel<<<(unsigned)(sms * kSparseCtasPerSm), kThreads, kUnitDynSmem, s>>>(ctl_dev, force_op);
     tile_kernel<<<(unsigned)imin64(h.T * h.U, (int64_t)sms * 4), kThreads, 0, s>>>(ctl_dev, force_op);
   } else {
     const unsigned grid = (unsigned)imin64(h.T * h.U, (int64_t)sms * 2);
@@ -820,12 +1056,24 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
   }
 }
 
+static dim3 tile_grid(const Ctl& h) { return dim3((unsigned)h.U, (unsigned)h.T); }
+static unsigned tile_threads(const Ctl& h) { return (unsigned)(kWarps * h.nbt < 32 ? 32 : kWarps * h.nbt); }
+
 void launch_minc_build(const Ctl& h, double* minc, cudaStream_t s) {
   CostGen gen;
   gen.kind = h.C ? 0 : h.cost_kind;
   gen.a0 = h.cost_a[0]; gen.a1 = h.cost_a[1]; gen.a2 = h.cost_a[2]; gen.a3 = h.cost_a[3];
   gen.row0 = h.row0;
   minc_kernel<<<148 * 8, 256, 0, s>>>(h.C, h.ldc, gen, h.m, h.n, h.nbands, h.ncells, minc);
+  TileMeta tm = tile_meta(h);
+  tm.minc = minc;
+  tile_minc_kernel<<<tile_grid(h), tile_threads(h), 0, s>>>(tm, const_cast<double*>(h.tminc));
+}
+
+void launch_tocc_fill(const Ctl& h, int slot, int value, cudaStream_t s) {
+  const int64_t tiles = h.T * h.U;
+  if (value >= 0) cudaMemsetAsync(h.tocc + slot * tiles, value, (size_t)tiles, s);
+  else tocc_kernel<<<tile_grid(h), tile_threads(h), 0, s>>>(tile_meta(h), slot);
 }
 
 void launch_slot_meta(const Ctl& h, int slot, bool scan_occ, cudaStream_t s) {
@@ -836,6 +1084,7 @@ void launch_slot_meta(const Ctl& h, int slot, bool scan_occ, cudaStream_t s) {
   }
   bounds_kernel<<<64, 256, 0, s>>>(sl.p, sl.q, h.m, h.n, h.nbands, h.ncells, h.pmax + (int64_t)slot * h.nbands,
                                    h.qmax + (int64_t)slot * h.ncells);
+  launch_tocc_fill(h, slot, -1, s);  // the tile summaries follow the occupancy bytes
 }
 
 }  // namespace pdot

@@ -329,6 +329,7 @@ void occ_invalidate(pdot_solver* h, int slot) {
   const Ctl& c = h->host;
   cudaMemsetAsync(c.occ + (int64_t)slot * c.nbands * c.nstrips, 0x01,
                   (size_t)c.nbands * c.nstrips * sizeof(uint32_t), h->stream);
+  pdot::launch_tocc_fill(c, slot, 1, h->stream);
 }
 
 // (re)build min C for the bound problem when screening is on
@@ -612,7 +613,8 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     const int64_t nunits = nbands * nstrips;
     const int64_t ncp = h->U * 32;  // cells per band, padded to whole tiles
     const int64_t mpad = round_up(m, 2);
-    const size_t o_unit = take(nunits * sizeof(uint32_t));
+    (void)nunits;
+    const size_t o_uflag = take(nbands * ncp);
     const size_t o_ulist = take(nbands * ncp * sizeof(uint32_t));
     const size_t o_ucount = take(sizeof(unsigned));
     const size_t o_bcr = take(nbands * h->U * sizeof(uint32_t));
@@ -621,12 +623,13 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     const size_t o_tlist = take(h->T * h->U * sizeof(int32_t));
     const size_t o_tcount = take(sizeof(unsigned));
     const size_t o_stat = take(pdot::ST_COUNT * sizeof(unsigned long long));
+    const size_t o_tocc = take(pdot::kNSlot * tiles);
+    const size_t o_tminc = take(tiles * sizeof(double));
     // cell partials of screened passes (written sparsely, read back only where
     // the bit maps say so: never zeroed)
     const size_t o_ccol = take(nbands * pdot::kMaxNQ * h->ldx * sizeof(double));
     const size_t o_crow = take(ncp * pdot::kMaxNQ * mpad * sizeof(double));
     const size_t o_cscal = take(nbands * ncp * pdot::kMaxNS * sizeof(double));
-    (void)tiles;
     char* base = nullptr;
     // only the metadata needs zeroing; the unit partials are written before they are read
     if ((e = cudaMalloc(&base, off)) != cudaSuccess || (e = cudaMemsetAsync(base, 0, o_ccol, h->stream)) != cudaSuccess) {
@@ -644,7 +647,7 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     c.occ = reinterpret_cast<uint32_t*>(base + o_occ);
     c.pmax = reinterpret_cast<double*>(base + o_pmax);
     c.qmax = reinterpret_cast<double*>(base + o_qmax);
-    c.unitw = reinterpret_cast<uint32_t*>(base + o_unit);
+    c.uflag = reinterpret_cast<uint8_t*>(base + o_uflag);
     c.ulist = reinterpret_cast<uint32_t*>(base + o_ulist);
     c.ucount = reinterpret_cast<unsigned*>(base + o_ucount);
     c.sstat = reinterpret_cast<unsigned long long*>(base + o_stat);
@@ -653,6 +656,8 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     c.tileflag = reinterpret_cast<uint8_t*>(base + o_tflag);
     c.tlist = reinterpret_cast<int32_t*>(base + o_tlist);
     c.tcount = reinterpret_cast<unsigned*>(base + o_tcount);
+    c.tocc = reinterpret_cast<uint8_t*>(base + o_tocc);
+    c.tminc = reinterpret_cast<const double*>(base + o_tminc);
     c.ccol = reinterpret_cast<double*>(base + o_ccol);
     c.crow = reinterpret_cast<double*>(base + o_crow);
     c.cscal = reinterpret_cast<double*>(base + o_cscal);
@@ -663,7 +668,7 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     // single dense launch per pass wins, e.g. 1024^2)
     if (getenv("PDOT_K2_TRACE") && atoi(getenv("PDOT_K2_TRACE")) != 0) {
       unsigned long long* kd = nullptr;
-      if (cudaMalloc(&kd, (size_t)((h->CB + h->T) * 4 + 16) * sizeof(unsigned long long)) == cudaSuccess) {
+      if (cudaMalloc(&kd, (size_t)((h->CB + h->T) * 4 + 32) * sizeof(unsigned long long)) == cudaSuccess) {
         c.kdbg = kd;
         c.ktl = kd + (h->CB + h->T) * 4;
         unsigned long long init[16];
@@ -1499,7 +1504,7 @@ int pdot_debug_k2(pdot_solver* h, unsigned long long* out, int64_t cap) {
   if (!h || !h->host.kdbg) return 0;
   DeviceGuard dg(h->device);
   const int64_t nb = h->CB + h->T;
-  const int64_t k = std::min<int64_t>(cap, nb * 4 + 16);
+  const int64_t k = std::min<int64_t>(cap, nb * 4 + 32);
   if (cudaMemcpy(out, h->host.kdbg, k * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
   return (int)nb;
 }

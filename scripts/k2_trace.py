@@ -23,6 +23,7 @@ t00 = tl[0]
 names = ("K0", "K1", "K1b", "K2")
 print("pass timeline (us from K0 start): " + ", ".join(
     f"{names[k]} {(tl[2 * k] - t00) / 1e3:.1f}..{(tl[2 * k + 1] - t00) / 1e3:.1f}" for k in range(4)))
+print("ctl probe: loads, shuffles, stop, sync, -, rcnt, ccnt", list(buf[nb * 4 + 16:nb * 4 + 24]), "reduce", buf[nb * 4 + 24], "reduce->after precompute sync", buf[nb * 4 + 25], "reduce x3", list(buf[nb * 4 + 26:nb * 4 + 29]))
 a = np.array(buf[:nb * 4], dtype=np.float64).reshape(nb, 4)
 t0 = a[:, 0].min()
 a[:, :3] -= t0
@@ -37,3 +38,6 @@ p = max(1, st["passes"])
 print("per pass: K1 %.1f us, K2 to last ticket %.1f us, controller %.1f us (reduce %.1f, decide %.1f, publish %.1f)" % (
     st["k1_ns"] / p / 1e3, st["k2_main_ns"] / p / 1e3, st["k2_ctl_ns"] / p / 1e3, st["ctl_reduce_ns"] / p / 1e3,
     st["ctl_logic_ns"] / p / 1e3, st["ctl_publish_ns"] / p / 1e3))
+z = list(buf[nb * 4 + 25:nb * 4 + 30])
+if z[0]:
+    print("K0 full-tile warp: start %.2f us, first-chunk load latency cold %d ns, warm %d ns, end %.2f us" % ((z[0] - buf[nb * 4 + 8]) / 1e3, z[1], z[2], (z[4] - buf[nb * 4 + 8]) / 1e3))
