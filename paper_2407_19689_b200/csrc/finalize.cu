@@ -136,18 +136,26 @@ __device__ __forceinline__ uint32_t flag_mask(const uint8_t* f, int64_t stride, 
   return m;
 }
 
+// the same mask, formed cooperatively: lane k loads flag k, one ballot (every
+// lane of the warp must be active and pass the same arguments)
+__device__ __forceinline__ uint32_t warp_flag_mask(const uint8_t* f, int64_t stride, int64_t count) {
+  const int lane = threadIdx.x & 31;
+  return __ballot_sync(0xffffffffu, lane < count && __ldg(f + lane * stride) != 0);
+}
+
 template <int NQ>
 __device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j, double2 (&acc)[NQ]) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = make_double2(0.0, 0.0);
   const int64_t ta = imax64((int64_t)g * c.GS, c.t0);
   const int64_t tb = imin64(imin64((int64_t)(g + 1) * c.GS, c.Tg), c.t0 + c.T);
-  if (j >= c.n) return;
   // tiles whose flag is 0 were screened out entirely: their partials are +0;
-  // the flags are read first, then the partials of the flagged tiles 4 at a time
-  const uint8_t* flags = c.tileflag + (j / kTileN);
+  // the flags are read first (one per lane, a ballot: the warp's 64 columns share
+  // their column tile), then the partials of the flagged tiles 4 at a time
+  const uint8_t* flags = c.tileflag + (imin64(j, c.n - 1) / kTileN);
   for (int64_t tc = ta; tc < tb; tc += 32) {
-    uint32_t m = flag_mask(flags + (tc - c.t0) * c.U, c.U, tb - tc);
+    uint32_t m = warp_flag_mask(flags + (tc - c.t0) * c.U, c.U, tb - tc);
+    if (j >= c.n) m = 0u;
     while (m) {
       int tk[4];
       int cnt = 0;
@@ -246,10 +254,13 @@ template <int NQ>
 __device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ]) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) row[q] = 0.0;
-  if (i >= c.m) return;
-  const uint8_t* flags = c.tileflag + (i / c.TM) * c.U;  // screened-out tiles: partials +0
+  // screened-out tiles: partials +0.  A full warp of rows of one row tile
+  // forms the flag mask with one ballot; otherwise each thread reads the flags.
+  const bool full = __activemask() == 0xffffffffu && c.TM % 32 == 0;
+  const uint8_t* flags = c.tileflag + (imin64(i, c.m - 1) / c.TM) * c.U;
   for (int64_t uc = 0; uc < c.U; uc += 32) {
-    uint32_t m = flag_mask(flags + uc, 1, c.U - uc);
+    uint32_t m = full ? warp_flag_mask(flags + uc, 1, c.U - uc) : (i < c.m ? flag_mask(flags + uc, 1, c.U - uc) : 0u);
+    if (i >= c.m) m = 0u;
     while (m) {
       int uk[4];
       int cnt = 0;
@@ -485,11 +496,12 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
     for (int s = 0; s < nr; ++s) c.rowblk[(int64_t)t * kMaxRowScal + s] = vals[s];
   }
   // tile scalars of this row tile (sum over column tiles, in order; screened-out tiles are +0)
-  if (threadIdx.x < ns) {
+  if (threadIdx.x < 32) {  // warp 0: the flag masks by ballot, then lanes < ns sum
     const uint8_t* flags = c.tileflag + (int64_t)t * c.U;
     double acc = 0.0;
     for (int64_t uc = 0; uc < c.U; uc += 32) {
-      uint32_t m = flag_mask(flags + uc, 1, c.U - uc);
+      uint32_t m = warp_flag_mask(flags + uc, 1, c.U - uc);
+      if (threadIdx.x >= ns) m = 0u;
       while (m) {
         int uk[8];
         int cnt = 0;
@@ -511,7 +523,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
           if (e < cnt) acc += v[e];
       }
     }
-    c.rowblk[(int64_t)t * kMaxRowScal + nr + threadIdx.x] = acc;
+    if (threadIdx.x < ns) c.rowblk[(int64_t)t * kMaxRowScal + nr + threadIdx.x] = acc;
   }
 }
 

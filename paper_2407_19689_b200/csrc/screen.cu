@@ -761,29 +761,51 @@ __device__ __forceinline__ void assemble_tile(const Ctl& c, int64_t tu, int64_t 
       for (int q = 0; q < NQ; ++q) *reinterpret_cast<double2*>(c.colpart + (tt * NQ + q) * c.ldx + j) = acc[q];
     }
   }
-  for (int r = th; r < c.TM; r += blockDim.x) {  // rows
-    const int64_t i = tt * c.TM + r;
-    if (i >= c.m) break;
-    uint32_t word = __ldg(c.bcr + (i / kBand) * c.U + tu);
-    double acc[NQ];
+  {  // rows: thread (row, quantity pair); active strips in order, two per round trip
+    constexpr int QP = NQ >= 2 ? 2 : 1;
+    constexpr int NSL = NQ / QP;
+    const int per = (int)blockDim.x / NSL;
+    const int qs = th / per;
+    for (int r = th - qs * per; r < c.TM; r += per) {
+      const int64_t i = tt * c.TM + r;
+      if (i >= c.m) break;
+      uint32_t word = __ldg(c.bcr + (i / kBand) * c.U + tu);
+      const double* rb = c.crow + (tu * 32 * kMaxNQ + qs * QP) * c.mpad + i;  // cell (tu, 0), q = qs * QP
+      const int64_t cstride = (int64_t)kMaxNQ * c.mpad;                       // next cell
+      double acc[QP];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-    while (word) {
-      const int w = (__ffs(word) - 1) >> 2;  // next active strip, in order
-      const unsigned nib = (word >> (4 * w)) & 0xfu;
-      word &= ~(0xfu << (4 * w));
-      const int64_t cb = tu * 32 + 4 * w;
-      double v[4][NQ];
+      for (int q = 0; q < QP; ++q) acc[q] = 0.0;
+      while (word) {
+        const int w0 = (__ffs(word) - 1) >> 2;
+        const unsigned nib0 = (word >> (4 * w0)) & 0xfu;
+        word &= ~(0xfu << (4 * w0));
+        int w1 = 0;
+        unsigned nib1 = 0u;
+        if (word) {
+          w1 = (__ffs(word) - 1) >> 2;
+          nib1 = (word >> (4 * w1)) & 0xfu;
+          word &= ~(0xfu << (4 * w1));
+        }
+        const double* p0 = rb + (int64_t)(4 * w0) * cstride;
+        const double* p1 = rb + (int64_t)(4 * w1) * cstride;
+        double v0[4][QP], v1[4][QP];
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+        for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int q = 0; q < NQ; ++q)
-          v[x][q] = ((nib >> x) & 1u) ? __ldg(c.crow + ((cb + x) * kMaxNQ + q) * c.mpad + i) : 0.0;
+          for (int q = 0; q < QP; ++q) {
+            v0[x][q] = ((nib0 >> x) & 1u) ? __ldg(p0 + x * cstride + q * c.mpad) : 0.0;
+            v1[x][q] = ((nib1 >> x) & 1u) ? __ldg(p1 + x * cstride + q * c.mpad) : 0.0;
+          }
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) acc[q] += (v[0][q] + v[1][q]) + (v[2][q] + v[3][q]);
+        for (int q = 0; q < QP; ++q) acc[q] += (v0[0][q] + v0[1][q]) + (v0[2][q] + v0[3][q]);
+        if (nib1) {
+#pragma unroll
+          for (int q = 0; q < QP; ++q) acc[q] += (v1[0][q] + v1[1][q]) + (v1[2][q] + v1[3][q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < QP; ++q) c.rowpart[(tu * NQ + qs * QP + q) * c.m + i] = acc[q];
     }
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) c.rowpart[(tu * NQ + q) * c.m + i] = acc[q];
   }
   {  // scalars: thread (strip w, band bl) forms its strip-band values (one round
      // trip for all of them), then the band-ordered and strip-ordered sums run

@@ -22,8 +22,8 @@ tl = np.array(buf[nb * 4 + 8:nb * 4 + 16], dtype=np.float64)
 t00 = tl[0]
 names = ("K0", "K1", "K1b", "K2")
 print("pass timeline (us from K0 start): " + ", ".join(
-    f"{names[k]} {(tl[2 * k] - t00) / 1e3:.1f}..{(tl[2 * k + 1] - t00) / 1e3:.1f}" for k in range(4)))
-print("ctl probe: loads, shuffles, stop, sync, -, rcnt, ccnt", list(buf[nb * 4 + 16:nb * 4 + 24]), "reduce", buf[nb * 4 + 24], "reduce->after precompute sync", buf[nb * 4 + 25], "reduce x3", list(buf[nb * 4 + 26:nb * 4 + 29]))
+    f"{names[k]} {(tl[2 * k] - t00) / 1e3:.1f}..{(tl[2 * k + 1] - t00) / 1e3:.1f}" for k in range(4)
+    if 0 < tl[2 * k + 1] and tl[2 * k] < 2 ** 63))
 a = np.array(buf[:nb * 4], dtype=np.float64).reshape(nb, 4)
 t0 = a[:, 0].min()
 a[:, :3] -= t0
@@ -41,3 +41,6 @@ print("per pass: K1 %.1f us, K2 to last ticket %.1f us, controller %.1f us (redu
 z = list(buf[nb * 4 + 25:nb * 4 + 30])
 if z[0]:
     print("K0 full-tile warp: start %.2f us, first-chunk load latency cold %d ns, warm %d ns, end %.2f us" % ((z[0] - buf[nb * 4 + 8]) / 1e3, z[1], z[2], (z[4] - buf[nb * 4 + 8]) / 1e3))
+kb = list(buf[nb * 4 + 25:nb * 4 + 29])
+if kb[0]:
+    print("K1b: tiles %d, slowest list read %.2f us, columns max %.2f, rows phase max %.2f us, scalars phase max %.2f us" % (kb[0], kb[1] / 1e3, buf[nb * 4 + 29] / 1e3, kb[2] / 1e3, kb[3] / 1e3))
