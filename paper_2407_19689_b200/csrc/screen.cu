@@ -87,8 +87,9 @@ __global__ void __launch_bounds__(32 * kScreenWarps, 2) screen_kernel(const Ctl*
   tl_start(tl, 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t tiles = c.T * c.U;
-  const int64_t tile = (int64_t)blockIdx.x * kScreenWarps + warp;
-  if (tile < tiles) {
+  // persistent: one wave of CTAs, each warp walks tiles warp, warp + nw, ...
+  for (int64_t tile = (int64_t)blockIdx.x * kScreenWarps + warp; tile < tiles;
+       tile += (int64_t)gridDim.x * kScreenWarps) {
     const int64_t tt = tile / c.U, tu = tile - tt * c.U;
     const bool with_avg = op == OP_STEP && step_with_avg(c);
     const bool bound = op != OP_DIST, bound_avg = op == OP_STEP;
@@ -231,6 +232,10 @@ __global__ void __launch_bounds__(32 * kScreenWarps, 2) screen_kernel(const Ctl*
         if (lane >= d) incl += y;
       }
       const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      // both list appends in flight together: the tile list (lane 0) and the cells (lane 31)
+      const bool any = __any_sync(0xffffffffu, any_act);
+      unsigned tslot = 0;
+      if (lane == 0 && any) tslot = atomicAdd(c.tcount, 1u);
       unsigned base = 0;
       if (lane == 31 && tot) base = atomicAdd(c.ucount, (unsigned)tot);
       base = __shfl_sync(0xffffffffu, base, 31);
@@ -259,10 +264,9 @@ __global__ void __launch_bounds__(32 * kScreenWarps, 2) screen_kernel(const Ctl*
         for (int k = 0; k < kCellsPerStrip; ++k) c.bct[tt * c.ncp + tu * 32 + s * kCellsPerStrip + k] = tb[k];
       }
       // the tile's partials are assembled by K1b, or are all +0 (flag 0)
-      const bool any = __any_sync(0xffffffffu, any_act);
       if (lane == 0) {
         c.tileflag[tile] = any ? 1 : 0;
-        if (any) c.tlist[atomicAdd(c.tcount, 1u)] = (int32_t)tile;
+        if (any) c.tlist[tslot] = (int32_t)tile;
       }
     }
   }
@@ -1064,8 +1068,8 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // graph passes (force_op < 0) are STEP / DIST / start-KKT; unit calls choose on the host
   if (force_op < 0 || unit_pass(h, force_op)) {
-    const unsigned g0 = (unsigned)((h.T * h.U + kScreenWarps - 1) / kScreenWarps);  // warp per tile
-    screen_kernel<<<g0, 32 * kScreenWarps, 0, s>>>(ctl_dev, force_op);
+    const unsigned g0 = (unsigned)imin64((h.T * h.U + kScreenWarps - 1) / kScreenWarps, (int64_t)sms * 2);
+    screen_kernel<<<g0, 32 * kScreenWarps, 0, s>>>(ctl_dev, force_op);  // warp per tile, persistent
     if (getenv("PDOT_DEBUG_SYNC")) {
       const cudaError_t e = cudaStreamSynchronize(s);
       if (e != cudaSuccess) fprintf(stderr, "screen_kernel failed: %s\n", cudaGetErrorString(e));
