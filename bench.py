@@ -358,7 +358,11 @@ def main():
     tp = ROOT / "profiles" / ("screened_kernel_traffic.json" if screened else "step_kernel_traffic.json")
     if tp.exists() and world == 1 and args.config == "c3":
         try:
-            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+            tj = json.loads(tp.read_text())
+            traffic = tj.get("dram_bytes_per_launch")
+            if traffic is None and tj.get("dram_to_algorithmic") is not None:
+                # warm-L2 DRAM bytes per algorithmic byte, measured by ncu over a whole solve
+                traffic = tj["dram_to_algorithmic"] * algo_bytes
         except (ValueError, OSError):
             traffic = None
 
