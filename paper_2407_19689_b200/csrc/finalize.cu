@@ -391,6 +391,39 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
 // ---------------------------------------------------------------------------
 // row blocks (one per row tile)
 // ---------------------------------------------------------------------------
+// Tile scalars of row tile t (sum over its column tiles, in order; screened-out
+// tiles are +0), by one warp: the flag masks by ballot, then lanes < ns sum.
+__device__ __forceinline__ void tile_scalars(Ctl& c, int t, int ns, int nr, int lane) {
+  const int tx = lane;
+  const uint8_t* flags = c.tileflag + (int64_t)t * c.U;
+  double acc = 0.0;
+  for (int64_t uc = 0; uc < c.U; uc += 32) {
+    uint32_t m = warp_flag_mask(flags + uc, 1, c.U - uc);
+    if (tx >= ns) m = 0u;
+    while (m) {
+      int uk[8];
+      int cnt = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        uk[e] = 0;
+        if (m) {
+          uk[e] = __ffs(m) - 1;
+          m &= m - 1;
+          cnt = e + 1;
+        }
+      }
+      double v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        v[e] = e < cnt ? __ldcg(c.tilescal + ((int64_t)t * c.U + uc + uk[e]) * kMaxNS + tx) : 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (e < cnt) acc += v[e];
+    }
+  }
+  if (tx < ns) c.rowblk[(int64_t)t * kMaxRowScal + nr + tx] = acc;
+}
+
 __device__ void row_block(Ctl& c, int op, int t, double* smem) {
   double vals[kMaxRowScal];
 #pragma unroll
@@ -400,6 +433,10 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
   // row-side scalars / tile scalars of this op
   const int nr = op == OP_STEP ? 7 : op == OP_KKT ? 3 : op == OP_ROUND ? 3 : 2;
   const int ns = op == OP_STEP ? 6 : op == OP_KKT ? 3 : 1;
+  // with rows for at most 7 warps, the last warp forms the tile scalars while the
+  // others work on the rows (otherwise warp 0 does after them)
+  const bool scal_early = c.TM <= kRedThreads - 32;
+  if (scal_early && threadIdx.x >= kRedThreads - 32) tile_scalars(c, t, ns, nr, threadIdx.x & 31);
   for (int r = threadIdx.x; r < c.TM; r += kRedThreads) {
     const int64_t i = i0 + r;
     const bool ok = r < rows;
@@ -495,36 +532,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < nr; ++s) c.rowblk[(int64_t)t * kMaxRowScal + s] = vals[s];
   }
-  // tile scalars of this row tile (sum over column tiles, in order; screened-out tiles are +0)
-  if (threadIdx.x < 32) {  // warp 0: the flag masks by ballot, then lanes < ns sum
-    const uint8_t* flags = c.tileflag + (int64_t)t * c.U;
-    double acc = 0.0;
-    for (int64_t uc = 0; uc < c.U; uc += 32) {
-      uint32_t m = warp_flag_mask(flags + uc, 1, c.U - uc);
-      if (threadIdx.x >= ns) m = 0u;
-      while (m) {
-        int uk[8];
-        int cnt = 0;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          uk[e] = 0;
-          if (m) {
-            uk[e] = __ffs(m) - 1;
-            m &= m - 1;
-            cnt = e + 1;
-          }
-        }
-        double v[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          v[e] = e < cnt ? __ldcg(c.tilescal + ((int64_t)t * c.U + uc + uk[e]) * kMaxNS + threadIdx.x) : 0.0;
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (e < cnt) acc += v[e];
-      }
-    }
-    if (threadIdx.x < ns) c.rowblk[(int64_t)t * kMaxRowScal + nr + threadIdx.x] = acc;
-  }
+  if (!scal_early && threadIdx.x < 32) tile_scalars(c, t, ns, nr, threadIdx.x);
 }
 
 // ---------------------------------------------------------------------------
