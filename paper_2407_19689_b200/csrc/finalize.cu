@@ -18,7 +18,7 @@
 namespace pdot {
 namespace {
 
-constexpr int kColsPerBlock = 64;
+constexpr int kColsPerBlock = 128;  // two 64-column halves per lane pair set
 
 // fixed-order block sum of K per-thread values; result valid in thread 0
 template <int K>
@@ -143,24 +143,31 @@ __device__ __forceinline__ uint32_t warp_flag_mask(const uint8_t* f, int64_t str
   return __ballot_sync(0xffffffffu, lane < count && __ldg(f + lane * stride) != 0);
 }
 
+// A lane owns two column pairs of the block: j and j + kColsPerBlock / 2.
+constexpr int kHalfCols = 64;
+constexpr int kColBatch = 2;  // flagged tiles per round trip (register budget: 2 x 2 x NQ double2)
+
 template <int NQ>
-__device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j, double2 (&acc)[NQ]) {
+__device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j, double2 (&acc)[2][NQ]) {
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) acc[q] = make_double2(0.0, 0.0);
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[h][q] = make_double2(0.0, 0.0);
   const int64_t ta = imax64((int64_t)g * c.GS, c.t0);
   const int64_t tb = imin64(imin64((int64_t)(g + 1) * c.GS, c.Tg), c.t0 + c.T);
   // tiles whose flag is 0 were screened out entirely: their partials are +0;
-  // the flags are read first (one per lane, a ballot: the warp's 64 columns share
-  // their column tile), then the partials of the flagged tiles 4 at a time
+  // the flags are read first (one per lane, a ballot: the block's columns share
+  // their column tile), then the partials of the flagged tiles kColBatch at a time
   const uint8_t* flags = c.tileflag + (imin64(j, c.n - 1) / kTileN);
+  const bool v0 = j < c.n, v1 = j + kHalfCols < c.n;
   for (int64_t tc = ta; tc < tb; tc += 32) {
     uint32_t m = warp_flag_mask(flags + (tc - c.t0) * c.U, c.U, tb - tc);
-    if (j >= c.n) m = 0u;
+    if (!v0) m = 0u;
     while (m) {
-      int tk[4];
+      int tk[kColBatch];
       int cnt = 0;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < kColBatch; ++e) {
         tk[e] = 0;
         if (m) {
           tk[e] = __ffs(m) - 1;
@@ -168,21 +175,25 @@ __device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j,
           cnt = e + 1;
         }
       }
-      double2 v[4][NQ];
+      double2 v[kColBatch][2][NQ];
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
+      for (int e = 0; e < kColBatch; ++e)
 #pragma unroll
-        for (int q = 0; q < NQ; ++q)
-          v[e][q] = e < cnt ? __ldcg(reinterpret_cast<const double2*>(c.colpart + ((tc + tk[e] - c.t0) * NQ + q) * c.ldx + j))
-                            : make_double2(0.0, 0.0);
+        for (int q = 0; q < NQ; ++q) {
+          const double* p = c.colpart + ((tc + tk[e] - c.t0) * NQ + q) * c.ldx + j;
+          v[e][0][q] = e < cnt ? __ldcg(reinterpret_cast<const double2*>(p)) : make_double2(0.0, 0.0);
+          v[e][1][q] = (e < cnt && v1) ? __ldcg(reinterpret_cast<const double2*>(p + kHalfCols)) : make_double2(0.0, 0.0);
+        }
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
+      for (int e = 0; e < kColBatch; ++e)
         if (e < cnt)
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) {
-            acc[q].x += v[e][q].x;
-            acc[q].y += v[e][q].y;
-          }
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              acc[h][q].x += v[e][h][q].x;
+              acc[h][q].y += v[e][h][q].y;
+            }
     }
   }
 }
@@ -194,12 +205,14 @@ __device__ void column_group_partials(const Ctl& c, int b) {
   const int g = c.g0 + warp;
   if (g < c.g1) {
     const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
-    double2 acc[NQ];
+    double2 acc[2][NQ];
     group_column_sum<NQ>(c, g, j, acc);
-    if (j < c.n) {
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) store_group2(c, g * c.gstride + q * c.ldx + j, acc[q]);
-    }
+    for (int h = 0; h < 2; ++h)
+      if (j + h * kHalfCols < c.n) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) store_group2(c, g * c.gstride + q * c.ldx + j + h * kHalfCols, acc[h][q]);
+      }
   }
 }
 
@@ -226,14 +239,16 @@ __device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_o
     return;
   }
   const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
-  double2 acc[NQ];
+  double2 acc[2][NQ];
   group_column_sum<NQ>(c, warp, j, acc);
-  // smem [group][q][64]
+  // smem [group][q][kColsPerBlock]
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    smem[(warp * NQ + q) * kColsPerBlock + lane * 2] = acc[q].x;
-    smem[(warp * NQ + q) * kColsPerBlock + lane * 2 + 1] = acc[q].y;
-  }
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      smem[(warp * NQ + q) * kColsPerBlock + h * kHalfCols + lane * 2] = acc[h][q].x;
+      smem[(warp * NQ + q) * kColsPerBlock + h * kHalfCols + lane * 2 + 1] = acc[h][q].y;
+    }
   __syncthreads();
   if (jj < kColsPerBlock) {
 #pragma unroll
@@ -381,10 +396,25 @@ __device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
       }
     }
   }
-  block_sum<kMaxColScal>(vals, smem);
-  if (threadIdx.x == 0) {
+  // one scalar partial per 64-column half (the unit of the column-side scalar
+  // order): half h = the in-order sum over the 8 warp slots of warps 2h, 2h + 1
+  // (the other slots +0), as a 64-column block formed it
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int s = 0; s < kMaxColScal; ++s) c.colblk[(int64_t)b * kMaxColScal + s] = vals[s];
+    for (int k = 0; k < kMaxColScal; ++k) {
+      double x = vals[k];
+#pragma unroll
+      for (int msk = 16; msk >= 1; msk >>= 1) x += __shfl_xor_sync(0xffffffffu, x, msk);
+      if (lane == 0) smem[warp * kMaxColScal + k] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * kMaxColScal) {
+      const int h = threadIdx.x / kMaxColScal, k = threadIdx.x % kMaxColScal;
+      double acc = smem[(2 * h) * kMaxColScal + k];
+      for (int w = 1; w < kWarps; ++w) acc += (w < 2) ? smem[(2 * h + w) * kMaxColScal + k] : 0.0;
+      if ((int64_t)b * 2 + h < c.ncolblk) c.colblk[((int64_t)b * 2 + h) * kMaxColScal + k] = acc;
+    }
   }
 }
 
@@ -602,8 +632,8 @@ __device__ __noinline__ void reduce_blocks(const Ctl& c, Sums* S, double* smem, 
     rcnt = imax64(e - a, 0);
   }
   const int cs_ = tid & 7, cw = tid >> 3;
-  const int64_t per = (c.CB + 31) / 32;
-  const int64_t b0 = cw * per, b1 = imin64(c.CB, b0 + per);
+  const int64_t per = (c.ncolblk + 31) / 32;
+  const int64_t b0 = cw * per, b1 = imin64(c.ncolblk, b0 + per);
   const double* cp = c.colblk + b0 * kMaxColScal + cs_;
   const int64_t ccnt = imax64(b1 - b0, 0);
   double racc = 0.0, cacc = 0.0;
@@ -942,7 +972,7 @@ __device__ __forceinline__ void wait_tickets(const Ctl& c, unsigned nwork) {
 // blocks run it executes the decision code once on a scratch copy of the
 // control block (so the instructions are in this SM's instruction cache and
 // the real run does not fetch them from DRAM), then waits for every ticket.
-__global__ void __launch_bounds__(kRedThreads, 3) finalize_kernel(Ctl* __restrict__ ctlp, int force_op, int mode) {
+__global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restrict__ ctlp, int force_op, int mode) {
   __shared__ double smem[kWarps * 4 * kColsPerBlock + 64];
   __shared__ Sums S;
   __shared__ int is_last;

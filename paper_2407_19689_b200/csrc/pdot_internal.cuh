@@ -116,7 +116,8 @@ struct Ctl {
   int64_t m, n, ldc, ldx;
   int64_t T, U;            // row tiles (local), column tiles
   int64_t TM;              // rows per tile
-  int64_t CB;              // finalize column blocks
+  int64_t CB;              // finalize column blocks (kColsPerBlock = 128 columns each)
+  int64_t ncolblk;         // column-side scalar partials: one per 64 columns
   // ---- row sharding; single GPU: m_total = m, Tg = T, t0 = 0, groups 0..8 ----
   int64_t m_total, row0;   // global rows, first local row
   int64_t Tg, t0, GS;      // global row tiles, first local tile, tiles per reduction group

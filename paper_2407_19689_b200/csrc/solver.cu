@@ -547,7 +547,7 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
   h->row0 = row0;
   h->gstride = round_up(4 * h->ldx + pdot::kMaxRowScal, 2);
   h->U = (n + pdot::kTileN - 1) / pdot::kTileN;
-  h->CB = (n + 63) / 64;
+  h->CB = (n + 127) / 128;  // finalize column blocks (kColsPerBlock)
 
   const int64_t mat = m * h->ldx;
   const int64_t per_slot = mat + round_up(m, 2) + h->ldx;
@@ -558,7 +558,7 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
   const int64_t w_rowpart = h->U * 4 * round_up(m, 2);
   const int64_t w_tiles = h->T * h->U * pdot::kMaxNS;
   const int64_t w_rowblk = h->T * pdot::kMaxRowScal;
-  const int64_t w_colblk = h->CB * pdot::kMaxColScal;
+  const int64_t w_colblk = 2 * h->CB * pdot::kMaxColScal;  // one per 64-column half
   const int64_t w_rows = 4 * round_up(m, 2), w_cols = 4 * h->ldx;
   const int64_t w_va = 2 * round_up(m, 2), w_vb = 2 * h->ldx;
   const int64_t w_gbuf = pdot::kGroups * h->gstride;
@@ -705,6 +705,7 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
   c.U = h->U;
   c.TM = TM;
   c.CB = h->CB;
+  c.ncolblk = (n + 63) / 64;
   for (int s = 0; s < pdot::kNSlot; ++s) {
     double* base = h->slot_mem + (size_t)s * per_slot;
     c.slot[s].X = base;
