@@ -44,3 +44,8 @@ if z[0]:
 kb = list(buf[nb * 4 + 25:nb * 4 + 29])
 if kb[0]:
     print("K1b: tiles %d, slowest list read %.2f us, columns max %.2f, rows phase max %.2f us, scalars phase max %.2f us" % (kb[0], kb[1] / 1e3, buf[nb * 4 + 29] / 1e3, kb[2] / 1e3, kb[3] / 1e3))
+if os.environ.get("K2_COLSPLIT"):
+    x = a[T:nb]
+    x3 = x[:, 3] - t0
+    print("column blocks: column sums done at median %.0f ns after entry (max %.0f), work end %.0f" % (
+        np.median(x3 - x[:, 0]), (x3 - x[:, 0]).max(), np.median(x[:, 1] - x[:, 0])))
