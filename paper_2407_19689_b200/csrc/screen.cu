@@ -538,7 +538,7 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const 
     const int64_t sstride = c.nbands * c.nstrips;
     uint8_t* ox = reinterpret_cast<uint8_t*>(c.occ + c.sXn * sstride + g.band * c.nstrips + g.strip);
     ox[g.k] = anyx ? 1 : 0;
-    const int64_t tiles = c.T * c.U, tile = (g.band / c.nbt) * c.U + g.strip / kWarps;
+    const int64_t tiles = c.T * c.U, tile = (g.band >> (__ffs(c.nbt) - 1)) * c.U + g.strip / kWarps;  // nbt: a power of two
     if (anyx) c.tocc[c.sXn * tiles + tile] = 1;
     if (AVG) {
       uint8_t* oa = reinterpret_cast<uint8_t*>(c.occ + c.sA * sstride + g.band * c.nstrips + g.strip);
