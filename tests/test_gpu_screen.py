@@ -147,3 +147,44 @@ def test_screening_engages(pd):
     frac = st["active_cells"] / (st["passes"] * st["cells_per_plan"])
     print("C1 active cell fraction", frac, st)
     assert frac < 0.3
+
+
+@pytest.mark.parametrize("bad", [np.inf, np.nan])
+def test_screened_non_finite_costs(pd, bad):
+    """Non-finite costs: their cells (and tiles) are never screened out (min C =
+    -inf), so whatever the dense walker does with inf * 0 or NaN -- a result or
+    the same exception -- the screened walker reproduces it."""
+    from paper_2407_19689_b200 import instances as inst
+    base = inst.sqeuclid_problem(32, 6)  # 1024 x 1024: many row and column tiles
+    C = np.array(base.C, dtype=np.float64)
+    C[700, 37] = bad
+    C[5, 1000] = bad
+    prob = _raw(C, np.asarray(base.f), np.asarray(base.g))
+    cfg = pd.SolverConfig(tol=1e-4, deterministic=True, max_iters=60)
+    out = []
+    from paper_2407_19689_b200 import device
+    for on in (False, True):
+        device.set_screening(on)
+        try:
+            it, rep = pd.solve(prob, cfg)
+            out.append(("ok", rep.to_json(), it))
+        except Exception as e:  # noqa: BLE001 - the same failure is the expectation
+            out.append(("err", type(e).__name__ + str(e), None))
+    assert out[0][0] == out[1][0] and out[0][1] == out[1][1]
+    if out[0][0] == "ok":
+        assert _same_iterate(out[0][2], out[1][2])
+
+
+def test_screened_far_violation(pd):
+    """A single cell far from the support whose cost is low enough to be
+    violated: the tile-level screen must keep its tile and the cell screen must
+    catch it."""
+    from paper_2407_19689_b200 import instances as inst
+    base = inst.sqeuclid_problem(32, 7)
+    C = np.array(base.C, dtype=np.float64)
+    C[900, 40] = -5.0  # far off the diagonal, strongly attractive
+    prob = _raw(C, np.asarray(base.f), np.asarray(base.g))
+    cfg = pd.SolverConfig(tol=1e-4, deterministic=True, max_iters=400)
+    (it0, r0, _), (it1, r1, _) = _solve_both(pd, prob, cfg)
+    assert r0.to_json() == r1.to_json()
+    assert _same_iterate(it0, it1)
