@@ -19,17 +19,19 @@
 // memory.  K1 therefore writes zeros into an output cell that it does not
 // compute only when that cell's old occ bit says it may hold stale data.
 //
-//   K0 screen_kernel  (one CTA per tile, one thread per (band, strip)):
-//       reads min C, dual bounds and occupancy; writes one unit word per
-//       (band, strip) (a flag byte per cell), the tile flag, and appends the
-//       tile to the visit list when any cell needs work.
-//   K1 sparse_kernel  (persistent, 8 warps per CTA, one warp per strip):
-//       walks the listed tiles; per band it loads C / X / A only for active
-//       cells, runs the same StepOp::elem as the dense walker, stores X+ / A'
-//       where nonzero (or stale), updates occupancy and flushes the tile's
-//       partials exactly like the dense walker.  Non-STEP ops (start KKT,
-//       restart distance, unit calls, rounding) take the generic walker over
-//       all tiles.
+//   K0 screen_kernel  (persistent, one warp per tile): a tile-level screen
+//       (tile min C, tile maxima of the duals, tile occupancy), then for the
+//       remaining tiles the per-cell screen: flag bytes, the list of cells K1
+//       visits (each with its flag byte), the bit maps K1b reads the cell
+//       partials by, the tile flag and the list of tiles with active cells.
+//   K1 unit_kernel    (persistent, one warp per listed cell): cp.async stages
+//       the next cell's C / X / A / duals while the current one runs the same
+//       StepOp::elem as the dense walker; stores X+ / A' where nonzero (or
+//       stale), updates cell and tile occupancy, writes the cell partials.
+//   K1b tile_kernel   (CTA per listed tile): reassembles the tile partials of
+//       the canonical tree from the cell partials.
+//   Non-STEP unit calls (KKT of a unit call, DIFF, ROUND) take generic_kernel
+//   over all tiles.
 // K2 (finalize.cu) skips tiles whose flag is 0: their partials are +0.
 #include <stdio.h>
 #include <stdlib.h>
