@@ -1,1 +1,2 @@
-timeout 900 python -m pytest -q tests/test_gpu_screen.py 2>&1 | tail -2
+nvidia-smi --query-gpu=memory.total,memory.used --format=csv
+timeout 1200 python scripts/big_check.py 181 120 2>&1 | tail -4
