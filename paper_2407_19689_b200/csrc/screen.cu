@@ -28,7 +28,7 @@
 //       the next cell's C / X / A / duals while the current one runs the same
 //       StepOp::elem as the dense walker; stores X+ / A' where nonzero (or
 //       stale), updates cell and tile occupancy, writes the cell partials.
-//   K1b tile_kernel   (CTA per listed tile): reassembles the tile partials of
+//   K1b tile_kernel   (CTA per listed tile and part): reassembles the tile partials of
 //       the canonical tree from the cell partials.
 //   Non-STEP unit calls (KKT of a unit call, DIFF, ROUND) take generic_kernel
 //   over all tiles.
@@ -717,7 +717,8 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
 // ---------------------------------------------------------------------------
 // K1b: assembles the per-tile partials of the canonical tree (the same layout
 // the dense walkers write: colpart / rowpart / tilescal) from the cell
-// partials, for every tile with an active cell.  One CTA per listed tile:
+// partials, for every tile with an active cell.  One CTA per listed tile and
+// part (part < 0: all three in one CTA):
 //   columns: thread = column pair, band-ordered sum of its cell column;
 //   rows:    thread = row, strip-ordered sum of the strip values
 //            ((c0 + c1) + (c2 + c3)) of the row segment's active cells;
@@ -725,10 +726,10 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
 //            then the strips in order.
 // ---------------------------------------------------------------------------
 template <int NQ, int NS>
-__device__ __forceinline__ void assemble_tile(const Ctl& c, int64_t tu, int64_t tt, double* sm) {
+__device__ __forceinline__ void assemble_tile(const Ctl& c, int64_t tu, int64_t tt, double* sm, int part) {
   const int th = threadIdx.x;
   const int64_t b0 = tt * c.nbt;
-  {  // columns
+  if (part < 0 || part == 0) {  // columns
     const int64_t j = tu * kTileN + th * 2;
     if (j < c.n) {
       uint32_t m = __ldg(c.bct + tt * c.ncp + j / kCell);
@@ -767,7 +768,7 @@ __device__ __forceinline__ void assemble_tile(const Ctl& c, int64_t tu, int64_t 
       for (int q = 0; q < NQ; ++q) *reinterpret_cast<double2*>(c.colpart + (tt * NQ + q) * c.ldx + j) = acc[q];
     }
   }
-  {  // rows: thread (row, quantity pair); active strips in order, two per round trip
+  if (part < 0 || part == 1) {  // rows: thread (row, quantity pair); active strips in order, two per round trip
     constexpr int QP = NQ >= 2 ? 2 : 1;
     constexpr int NSL = NQ / QP;
     const int per = (int)blockDim.x / NSL;
@@ -813,7 +814,7 @@ __device__ __forceinline__ void assemble_tile(const Ctl& c, int64_t tu, int64_t 
       for (int q = 0; q < QP; ++q) c.rowpart[(tu * NQ + qs * QP + q) * c.m + i] = acc[q];
     }
   }
-  {  // scalars: thread (strip w, band bl) forms its strip-band values (one round
+  if (part < 0 || part == 2) {  // scalars: thread (strip w, band bl) forms its strip-band values (one round
      // trip for all of them), then the band-ordered and strip-ordered sums run
      // on shared memory
     const int nb = (int)imin64(c.nbt, c.nbands - b0);
@@ -849,7 +850,7 @@ __device__ __forceinline__ void assemble_tile(const Ctl& c, int64_t tu, int64_t 
   }
 }
 
-__global__ void __launch_bounds__(kThreads) tile_kernel(const Ctl* __restrict__ ctlp, int force_op) {
+__global__ void __launch_bounds__(kThreads, 4) tile_kernel(const Ctl* __restrict__ ctlp, int force_op) {
   __shared__ double sm[32 * 8 * 8];  // [band][strip][scalar] strip-band values
   const Ctl& c = *ctlp;
   if (c.done || !c.screen) return;
@@ -858,12 +859,15 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Ctl* __restrict__ 
   const unsigned ntiles = __ldcg(c.tcount);
   unsigned long long* tl = op == OP_STEP ? c.ktl : nullptr;
   tl_start(tl, 2);
-  for (unsigned k = blockIdx.x; k < ntiles; k += gridDim.x) {
-    const int32_t tile = __ldcg(c.tlist + k);
+  // work item k = (listed tile k / 3, part k % 3): the column, row and scalar
+  // sums of one tile run in three CTAs side by side
+  for (unsigned k = blockIdx.x; k < ntiles * 3u; k += gridDim.x) {
+    const int32_t tile = __ldcg(c.tlist + k / 3u);
+    const int part = (int)(k % 3u);
     const int64_t tu = tile % c.U, tt = tile / c.U;
-    if (op == OP_STEP) assemble_tile<4, 6>(c, tu, tt, sm);
-    else if (op == OP_DIST) assemble_tile<1, 1>(c, tu, tt, sm);
-    else assemble_tile<1, 3>(c, tu, tt, sm);
+    if (op == OP_STEP) assemble_tile<4, 6>(c, tu, tt, sm, part);
+    else if (op == OP_DIST) assemble_tile<1, 1>(c, tu, tt, sm, part);
+    else assemble_tile<1, 3>(c, tu, tt, sm, part);
   }
   tl_end(tl, 2);
 }
@@ -1077,7 +1081,7 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
       if (e != cudaSuccess) fprintf(stderr, "screen_kernel failed: %s\n", cudaGetErrorString(e));
     }
     unit_kernel<<<(unsigned)(sms * kSparseCtasPerSm), kThreads, kUnitDynSmem, s>>>(ctl_dev, force_op);
-    tile_kernel<<<(unsigned)imin64(h.T * h.U, (int64_t)sms * 4), kThreads, 0, s>>>(ctl_dev, force_op);
+    tile_kernel<<<(unsigned)imin64(h.T * h.U * 3, (int64_t)sms * 4), kThreads, 0, s>>>(ctl_dev, force_op);
   } else {
     const unsigned grid = (unsigned)imin64(h.T * h.U, (int64_t)sms * 2);
     generic_kernel<<<grid, kThreads, generic_smem_bytes(h.TM), s>>>(ctl_dev, force_op);
