@@ -79,8 +79,9 @@ __device__ __forceinline__ bool step_with_avg(const Ctl& c) { return c.unit ? c.
 // bct (per row tile and cell).
 // ---------------------------------------------------------------------------
 constexpr int kScreenWarps = 8;
+constexpr int kScreenCtasPerSm = 2;  // 128 registers; 3 or 4 per SM spill and run slower (C3 11.4k -> 11.3k / 10.7k iter/s)
 
-__global__ void __launch_bounds__(32 * kScreenWarps, 2) screen_kernel(const Ctl* __restrict__ ctlp, int force_op) {
+__global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_kernel(const Ctl* __restrict__ ctlp, int force_op) {
   const Ctl& c = *ctlp;
   if (c.done || !c.screen) return;
   const int op = force_op >= 0 ? force_op : c.op;
@@ -1074,7 +1075,7 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // graph passes (force_op < 0) are STEP / DIST / start-KKT; unit calls choose on the host
   if (force_op < 0 || unit_pass(h, force_op)) {
-    const unsigned g0 = (unsigned)imin64((h.T * h.U + kScreenWarps - 1) / kScreenWarps, (int64_t)sms * 2);
+    const unsigned g0 = (unsigned)imin64((h.T * h.U + kScreenWarps - 1) / kScreenWarps, (int64_t)sms * kScreenCtasPerSm);
     screen_kernel<<<g0, 32 * kScreenWarps, 0, s>>>(ctl_dev, force_op);  // warp per tile, persistent
     if (getenv("PDOT_DEBUG_SYNC")) {
       const cudaError_t e = cudaStreamSynchronize(s);
