@@ -1075,7 +1075,10 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // graph passes (force_op < 0) are STEP / DIST / start-KKT; unit calls choose on the host
   if (force_op < 0 || unit_pass(h, force_op)) {
-    const unsigned g0 = (unsigned)imin64((h.T * h.U + kScreenWarps - 1) / kScreenWarps, (int64_t)sms * kScreenCtasPerSm);
+    unsigned g0 = (unsigned)imin64((h.T * h.U + kScreenWarps - 1) / kScreenWarps, (int64_t)sms * kScreenCtasPerSm);
+    // test hook: PDOT_K0_BLOCKS caps K0's grid (read per launch), so that small
+    // problems run the persistent tile walk with many tiles per warp
+    if (const char* e = getenv("PDOT_K0_BLOCKS")) g0 = (unsigned)imin64(g0, imax64(1, atoi(e)));
     screen_kernel<<<g0, 32 * kScreenWarps, 0, s>>>(ctl_dev, force_op);  // warp per tile, persistent
     if (getenv("PDOT_DEBUG_SYNC")) {
       const cudaError_t e = cudaStreamSynchronize(s);

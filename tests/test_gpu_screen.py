@@ -98,6 +98,26 @@ def test_screened_warm_start_and_trace(pd):
         assert _same_iterate(a, b)
 
 
+@pytest.mark.parametrize("blocks", [1, 3])
+def test_screened_k0_many_tiles_per_warp(pd, monkeypatch, blocks):
+    """K0 is persistent: each warp walks tiles warp, warp + nw, ...  Capping its
+    grid (PDOT_K0_BLOCKS) gives every warp 32 or 11 tiles of a 4096^2 warm start
+    from a dense plan (every tile occupied, so every tile takes the per-cell
+    screen): still bit-identical to the dense walker."""
+    from paper_2407_19689_b200 import instances as inst
+    monkeypatch.setenv("PDOT_K0_BLOCKS", str(blocks))
+    prob = inst.sqeuclid_problem(64, 2)  # 4096^2: 256 tiles of 128 x 512
+    n = prob.m
+    rng = np.random.default_rng(11)
+    X0 = rng.random((n, n)) * 1e-9
+    X0[rng.random((n, n)) < 0.5] = 0.0
+    init = pd.Iterate(X0, rng.standard_normal(n) * 1e-3, rng.standard_normal(n) * 1e-3)
+    cfg = pd.SolverConfig(tol=1e-9, max_iters=40, deterministic=True)
+    (it0, r0, _), (it1, r1, _) = _solve_both(pd, prob, cfg, initial=init)
+    assert r0.to_json() == r1.to_json()
+    assert _same_iterate(it0, it1)
+
+
 def test_screened_implicit_cost(pd):
     prob = pd.DeviceProblem.sqeuclid_grid(32, 2, implicit=True)
     cfg = pd.SolverConfig(tol=1e-4, deterministic=True)
