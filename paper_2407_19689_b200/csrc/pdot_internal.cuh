@@ -380,6 +380,18 @@ struct CostGen {
   }
 };
 
+// Copy the control block into shared memory (one round trip for all of its
+// fields, instead of a chain of dependent global loads at kernel entry); every
+// thread of the block must call it.  The kernels only write through the
+// pointers it holds, never its fields.
+__device__ __forceinline__ void ctl_to_shared(const Ctl* __restrict__ g, Ctl* s) {
+  constexpr int kW = (int)(sizeof(Ctl) / sizeof(unsigned long long));
+  const unsigned long long* gw = reinterpret_cast<const unsigned long long*>(g);
+  unsigned long long* sw = reinterpret_cast<unsigned long long*>(s);
+  for (int i = threadIdx.x; i < kW; i += blockDim.x) sw[i] = __ldcg(gw + i);
+  __syncthreads();
+}
+
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

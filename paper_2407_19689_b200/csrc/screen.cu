@@ -82,7 +82,9 @@ constexpr int kScreenWarps = 8;
 constexpr int kScreenCtasPerSm = 2;  // 128 registers; 3 or 4 per SM spill and run slower (C3 11.4k -> 11.3k / 10.7k iter/s)
 
 __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_kernel(const Ctl* __restrict__ ctlp, int force_op) {
-  const Ctl& c = *ctlp;
+  __shared__ Ctl ctl_s;  // the control block, one round trip for all fields
+  ctl_to_shared(ctlp, &ctl_s);
+  const Ctl& c = ctl_s;
   if (c.done || !c.screen) return;
   const int op = force_op >= 0 ? force_op : c.op;
   if (!unit_pass(c, op)) return;
@@ -93,7 +95,8 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
   // persistent: one wave of CTAs, each warp walks tiles warp, warp + nw, ...
   for (int64_t tile = (int64_t)blockIdx.x * kScreenWarps + warp; tile < tiles;
        tile += (int64_t)gridDim.x * kScreenWarps) {
-    const int64_t tt = tile / c.U, tu = tile - tt * c.U;
+    // 32-bit division: tile indices fit (T * U < 2^31), and the 64-bit one is a subroutine call
+    const int64_t tt = (uint32_t)tile / (uint32_t)c.U, tu = tile - tt * c.U;
     const bool with_avg = op == OP_STEP && step_with_avg(c);
     const bool bound = op != OP_DIST, bound_avg = op == OP_STEP;
     const int sx = op == OP_DIST ? c.sCand : c.sX;
@@ -865,7 +868,7 @@ __global__ void __launch_bounds__(kThreads, 4) tile_kernel(const Ctl* __restrict
   for (unsigned k = blockIdx.x; k < ntiles * 3u; k += gridDim.x) {
     const int32_t tile = __ldcg(c.tlist + k / 3u);
     const int part = (int)(k % 3u);
-    const int64_t tu = tile % c.U, tt = tile / c.U;
+    const int64_t tt = (uint32_t)tile / (uint32_t)c.U, tu = tile - tt * c.U;  // 32-bit division
     if (op == OP_STEP) assemble_tile<4, 6>(c, tu, tt, sm, part);
     else if (op == OP_DIST) assemble_tile<1, 1>(c, tu, tt, sm, part);
     else assemble_tile<1, 3>(c, tu, tt, sm, part);
