@@ -24,6 +24,8 @@ constexpr int kRedThreads = 256;          // finalize-kernel block size
 constexpr int kMaxRowScal = 16;           // per-row-tile scalar partials (finalize)
 constexpr int kMaxColScal = 8;            // per-column-block scalar partials (finalize)
 constexpr int kRingCap = 1 << 16;         // trace/event ring entries (host mapped)
+constexpr int kListPad = 1 << 14;         // extra cell-list entries: K1 reads every warp's first two
+                                          // entries before it knows the list length (<= 1024 SMs)
 
 // Block screening of the STEP pass (screen.cu).  The plan is cut
 // into cells of kBand rows x kCell columns; a warp strip is kStrip = 4 cells.

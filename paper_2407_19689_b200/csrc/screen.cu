@@ -562,15 +562,14 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const 
 // while cell k is computed
 template <bool IMPLICIT, bool AVG>
 __device__ __forceinline__ void step_cells(const StepOp& o, const Ctl& c, const CostGen& gen, unsigned k0,
-                                           unsigned nw, unsigned ncells, unsigned char* stages,
+                                           unsigned nw, const unsigned* ncells_p, unsigned char* stages,
                                            unsigned long long& bytes, unsigned long long& cells) {
-  if (k0 >= ncells) return;
+  // this warp's first two list entries are read before the list length is known
+  // (the list has kListPad spare entries; values past the length are not used)
   uint32_t e_cur = __ldcg(c.ulist + k0), f_cur = __ldcg(c.uflag + k0);
-  uint32_t e_nx = 0, f_nx = 0;
-  if (k0 + nw < ncells) {
-    e_nx = __ldcg(c.ulist + k0 + nw);
-    f_nx = __ldcg(c.uflag + k0 + nw);
-  }
+  uint32_t e_nx = __ldcg(c.ulist + k0 + nw), f_nx = __ldcg(c.uflag + k0 + nw);
+  const unsigned ncells = __ldcg(ncells_p);
+  if (k0 >= ncells) return;
   cell_issue<IMPLICIT, AVG>(o, c, e_cur, f_cur, stages);
   cp_async_commit();
   int st = 0;
@@ -664,11 +663,11 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
     extern __shared__ __align__(16) unsigned char unit_dyn[];
     unsigned char* stages = unit_dyn + warp * kStages * kStageBytes;
     if (o.C) {
-      if (o.with_avg) step_cells<false, true>(o, c, gen, gw, nw, ncells, stages, bytes, cells);
-      else step_cells<false, false>(o, c, gen, gw, nw, ncells, stages, bytes, cells);
+      if (o.with_avg) step_cells<false, true>(o, c, gen, gw, nw, c.ucount, stages, bytes, cells);
+      else step_cells<false, false>(o, c, gen, gw, nw, c.ucount, stages, bytes, cells);
     } else {
-      if (o.with_avg) step_cells<true, true>(o, c, gen, gw, nw, ncells, stages, bytes, cells);
-      else step_cells<true, false>(o, c, gen, gw, nw, ncells, stages, bytes, cells);
+      if (o.with_avg) step_cells<true, true>(o, c, gen, gw, nw, c.ucount, stages, bytes, cells);
+      else step_cells<true, false>(o, c, gen, gw, nw, c.ucount, stages, bytes, cells);
     }
   } else if (op == OP_DIST) {
     DiffOp o;
@@ -860,13 +859,17 @@ __global__ void __launch_bounds__(kThreads, 4) tile_kernel(const Ctl* __restrict
   if (c.done || !c.screen) return;
   const int op = force_op >= 0 ? force_op : c.op;
   if (!unit_pass(c, op)) return;
+  // the first item's tile is read before the list length is known (the grid
+  // has at most 3 T U blocks, so blockIdx.x / 3 is inside the list buffer)
+  int32_t tile_nx = __ldcg(c.tlist + blockIdx.x / 3u);
   const unsigned ntiles = __ldcg(c.tcount);
   unsigned long long* tl = op == OP_STEP ? c.ktl : nullptr;
   tl_start(tl, 2);
   // work item k = (listed tile k / 3, part k % 3): the column, row and scalar
   // sums of one tile run in three CTAs side by side
   for (unsigned k = blockIdx.x; k < ntiles * 3u; k += gridDim.x) {
-    const int32_t tile = __ldcg(c.tlist + k / 3u);
+    const int32_t tile = tile_nx;
+    if (k + gridDim.x < ntiles * 3u) tile_nx = __ldcg(c.tlist + (k + gridDim.x) / 3u);
     const int part = (int)(k % 3u);
     const int64_t tt = (uint32_t)tile / (uint32_t)c.U, tu = tile - tt * c.U;  // 32-bit division
     if (op == OP_STEP) assemble_tile<4, 6>(c, tu, tt, sm, part);

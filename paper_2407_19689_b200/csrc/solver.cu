@@ -614,8 +614,8 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     const int64_t ncp = h->U * 32;  // cells per band, padded to whole tiles
     const int64_t mpad = round_up(m, 2);
     (void)nunits;
-    const size_t o_uflag = take(nbands * ncp);
-    const size_t o_ulist = take(nbands * ncp * sizeof(uint32_t));
+    const size_t o_uflag = take(nbands * ncp + pdot::kListPad);
+    const size_t o_ulist = take((nbands * ncp + pdot::kListPad) * sizeof(uint32_t));
     const size_t o_ucount = take(sizeof(unsigned));
     const size_t o_bcr = take(nbands * h->U * sizeof(uint32_t));
     const size_t o_bct = take(h->T * ncp * sizeof(uint32_t));
