@@ -1090,7 +1090,9 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
       const cudaError_t e = cudaStreamSynchronize(s);
       if (e != cudaSuccess) fprintf(stderr, "screen_kernel failed: %s\n", cudaGetErrorString(e));
     }
-    unit_kernel<<<(unsigned)(sms * kSparseCtasPerSm), kThreads, kUnitDynSmem, s>>>(ctl_dev, force_op);
+    // every warp reads list entries gw and gw + nw up front: 2 nw <= kListPad
+    const unsigned g1 = (unsigned)imin64((int64_t)sms * kSparseCtasPerSm, kListPad / (2 * kWarps));
+    unit_kernel<<<g1, kThreads, kUnitDynSmem, s>>>(ctl_dev, force_op);
     tile_kernel<<<(unsigned)imin64(h.T * h.U * 3, (int64_t)sms * 4), kThreads, 0, s>>>(ctl_dev, force_op);
   } else {
     const unsigned grid = (unsigned)imin64(h.T * h.U, (int64_t)sms * 2);
