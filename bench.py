@@ -301,7 +301,7 @@ def main():
 
         def run(cfg):
             nonlocal h
-            (_, h), rep = pd.solve_device(dp, cfg, device=local)
+            (_, h), rep = pd.solve_device(dp, cfg, device=local, handle=h)
             return rep
     # warm-up: W iterations (graph build, caches, clocks)
     warm_rep = run(pd.SolverConfig(tol=1e-12, max_iters=args.warmup))

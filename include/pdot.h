@@ -43,7 +43,7 @@ extern "C" {
 /* trace event types (SolveTrace, pdhg.py:106-118) */
 #define PDOT_EV_START 1   /* x = initial metric, y = initial relative KKT */
 #define PDOT_EV_ACCEPT 2  /* x = eta, y = step bound  (trace.etas / trace.step_bounds) */
-#define PDOT_EV_CAND 3    /* x = candidate KKT      (trace.candidate_kkts) */
+#define PDOT_EV_CAND 3    /* x = candidate KKT (trace.candidate_kkts), y = current, z = average; ia = 1 if current won */
 #define PDOT_EV_RESTART 4 /* ia = inner length, x = candidate KKT, y = omega after update */
 #define PDOT_EV_REJECT 5  /* x = rejected eta, y = bound */
 

@@ -815,7 +815,8 @@ __device__ __noinline__ void control_step(Ctl& c, const Sums& S, const Pre& P) {
     const int cand_slot = take_cur ? c.sX : c.sA;
     const double cand = take_cur ? kc : ka;
     const double cand_rel = take_cur ? rel_cur : rel_avg;
-    if (c.trace_level > 0) ring_push(c, EV_CAND, 0, cand, 0.0, 0.0);
+    // both metrics travel with the candidate: the host can report decision margins
+    if (c.trace_level > 0) ring_push(c, EV_CAND, take_cur ? 1 : 0, cand, kc, ka);
     if (cand < c.best_kkt) {  // pdhg.py:342-344 (role alias instead of a copy)
       c.sB = cand_slot;
       c.best_kkt = cand;

@@ -89,7 +89,8 @@ enum EvType : int { EV_START = 1, EV_ACCEPT = 2, EV_CAND = 3, EV_RESTART = 4, EV
 struct Event {
   int32_t type;
   int32_t ia;      // restart length (EV_RESTART)
-  double x, y, z;  // ACCEPT: eta, bound ; CAND: cand_kkt ; RESTART: kkt, omega ; START: kkt
+  double x, y, z;  // ACCEPT: eta, bound ; CAND: cand_kkt, kkt_cur, kkt_avg (ia: current won) ;
+                   // RESTART: kkt, omega ; START: kkt ; REJECT: eta, bound
 };
 
 // Host-mapped status mirror: written by the controller every pass, read by the
@@ -198,9 +199,11 @@ struct Ctl {
   double* pmax;              // [kNSlot][nbands]  NaN-propagating max of p over each band
   double* qmax;              // [kNSlot][ncells]  ... of q over each cell (-inf for cells past n)
   uint8_t* uflag;            // [nbands*ncp] K0 -> K1 flag byte of each listed cell (parallel to ulist)
-  uint32_t* ulist;           // cells K1 visits this pass: (band << 12) | cell
+  uint32_t* ulist;           // cells K1 visits this pass: (band << cbits) | cell
   unsigned int* ucount;      // length of ulist (K0 appends, K2 resets)
   int64_t ncp;               // cells per row of cells, padded to whole tiles (U * 32)
+  int32_t cbits, cbits_pad_;  // cell-index bits of a ulist entry: smallest >= 12 with 2^cbits >= ncp
+                              // (pdot_create rejects screening when nbands does not fit the rest)
   uint32_t* bcr;             // [nbands][U]  bit k: cell k of column tile u wrote partials this pass
   uint32_t* bct;             // [T][ncp]     bit b: band b of row tile t of this cell wrote partials
   uint8_t* tileflag;         // [T][U] the tile's partials are valid (0: screened out, all +0)
@@ -219,6 +222,15 @@ struct Ctl {
   Event* ring;             // host mapped, kRingCap entries
 };
 static_assert(sizeof(Ctl) % 8 == 0, "the controller copies Ctl as 8-byte words");
+
+// cell-list entries: band in the high bits, cell index in the low cbits
+__host__ __device__ __forceinline__ uint32_t cell_entry(int64_t band, int64_t cell, int cbits) {
+  return (uint32_t)(((uint64_t)band << cbits) | (uint64_t)cell);
+}
+__host__ __device__ __forceinline__ int64_t entry_band(uint32_t e, int cbits) { return (int64_t)(e >> cbits); }
+__host__ __device__ __forceinline__ int64_t entry_cell(uint32_t e, int cbits) {
+  return (int64_t)(e & ((1u << cbits) - 1u));
+}
 
 // ---------------------------------------------------------------------------
 // small device helpers

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
 #pragma unroll
         for (int k = 0; k < kCellsPerStrip; ++k)
           if ((l4 >> k) & 1u) {
-            c.ulist[pos] = (uint32_t)((band << 12) | (strip * kCellsPerStrip + k));
+            c.ulist[pos] = cell_entry(band, strip * kCellsPerStrip + k, c.cbits);
             c.uflag[pos] = (uint8_t)((words[rd] >> (8 * k)) & 0xffu);  // the cell's flags travel with it
             ++pos;
           }
@@ -300,8 +300,8 @@ struct CellGeo {
 __device__ __forceinline__ CellGeo cell_geo(const Ctl& c, uint32_t entry) {
   const int lane = threadIdx.x & 31;
   CellGeo g;
-  g.band = entry >> 12;
-  g.cell = entry & 0xfffu;
+  g.band = entry_band(entry, c.cbits);
+  g.cell = entry_cell(entry, c.cbits);
   DCHECK(g.band < c.nbands, "band", g.band, c.nbands);
   DCHECK(g.cell < c.ncells, "cell", g.cell, c.ncells);
   g.strip = g.cell >> 2;
@@ -1006,7 +1006,7 @@ __global__ void bounds_kernel(const double* __restrict__ p, const double* __rest
 // on): list the cells whose occupancy byte is set (the rest is +0.0 in memory),
 // then gather them, 8 rows x 16 columns each, into a staging buffer
 __global__ void occ_list_kernel(const uint8_t* __restrict__ occ_bytes, int64_t nbands, int64_t ncells,
-                                int64_t nstrips, uint32_t* __restrict__ list, unsigned* __restrict__ count) {
+                                int64_t nstrips, int cbits, uint32_t* __restrict__ list, unsigned* __restrict__ count) {
   const int64_t total = nbands * nstrips * kCellsPerStrip;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t band = e / (nstrips * kCellsPerStrip), cell = e - band * nstrips * kCellsPerStrip;
@@ -1019,11 +1019,11 @@ __global__ void occ_list_kernel(const uint8_t* __restrict__ occ_bytes, int64_t n
     unsigned base = 0;
     if (lane == leader) base = atomicAdd(count, (unsigned)__popc(bal));
     base = __shfl_sync(bal, base, leader);
-    list[base + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)((band << 12) | cell);
+    list[base + __popc(bal & ((1u << lane) - 1u))] = cell_entry(band, cell, cbits);
   }
 }
 
-__global__ void cell_gather_kernel(const double* __restrict__ X, int64_t ldx, int64_t m, int64_t n,
+__global__ void cell_gather_kernel(const double* __restrict__ X, int64_t ldx, int64_t m, int64_t n, int cbits,
                                    const uint32_t* __restrict__ list, int64_t k0, int64_t k1,
                                    double* __restrict__ out) {
   // one warp per cell: lane = (row rg, column pair cp) as in the cell kernel
@@ -1032,7 +1032,7 @@ __global__ void cell_gather_kernel(const double* __restrict__ X, int64_t ldx, in
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t k = k0 + w; k < k1; k += nw) {
     const uint32_t entry = list[k];
-    const int64_t band = entry >> 12, cell = entry & 0xfffu;
+    const int64_t band = entry_band(entry, cbits), cell = entry_cell(entry, cbits);
     const int cp = lane & 7, rg = lane >> 3;
     const int64_t j = cell * kCell + cp * 2;
     double* o = out + (k - k0) * (kBand * kCell);
@@ -1052,7 +1052,7 @@ __global__ void cell_gather_kernel(const double* __restrict__ X, int64_t ldx, in
 unsigned launch_occ_list(const Ctl& h, int slot, uint32_t* list, unsigned* count_dev, cudaStream_t s) {
   cudaMemsetAsync(count_dev, 0, sizeof(unsigned), s);
   const uint8_t* ob = reinterpret_cast<const uint8_t*>(h.occ + (int64_t)slot * h.nbands * h.nstrips);
-  occ_list_kernel<<<148 * 8, 256, 0, s>>>(ob, h.nbands, h.ncells, h.nstrips, list, count_dev);
+  occ_list_kernel<<<148 * 8, 256, 0, s>>>(ob, h.nbands, h.ncells, h.nstrips, h.cbits, list, count_dev);
   unsigned cnt = 0;
   cudaMemcpyAsync(&cnt, count_dev, sizeof(unsigned), cudaMemcpyDeviceToHost, s);
   cudaStreamSynchronize(s);
@@ -1063,7 +1063,7 @@ void launch_cell_gather(const Ctl& h, int slot, const uint32_t* list, int64_t k0
                         cudaStream_t s) {
   const int64_t warps = k1 - k0;
   const unsigned blocks = (unsigned)imin64((warps * 32 + 255) / 256, 148 * 16);
-  if (blocks > 0) cell_gather_kernel<<<blocks, 256, 0, s>>>(h.slot[slot].X, h.ldx, h.m, h.n, list, k0, k1, out);
+  if (blocks > 0) cell_gather_kernel<<<blocks, 256, 0, s>>>(h.slot[slot].X, h.ldx, h.m, h.n, h.cbits, list, k0, k1, out);
 }
 
 void prepare_sparse_kernel() {

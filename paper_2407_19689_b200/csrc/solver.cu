@@ -350,7 +350,8 @@ int screen_setup(pdot_solver* h) {
 int d2h_matrix_bounced(pdot_solver* h, double* dst, int64_t ldd, const double* src, int64_t lds, int64_t m,
                        int64_t n) {
   const int64_t row_bytes = n * (int64_t)sizeof(double);
-  const int64_t rows_per = std::max<int64_t>(1, (int64_t)h->bounce_bytes / row_bytes);
+  if ((int64_t)h->bounce_bytes < row_bytes) return copy_matrix(dst, ldd, src, lds, m, n, h->stream);
+  const int64_t rows_per = (int64_t)h->bounce_bytes / row_bytes;
   const int64_t nchunks = (m + rows_per - 1) / rows_per;
   const unsigned nthreads = 8;
   auto copy_out = [&](int64_t k) {
@@ -663,6 +664,12 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     c.cscal = reinterpret_cast<double*>(base + o_cscal);
     c.ncp = ncp;
     c.mpad = mpad;
+    // a cell-list entry is one 32-bit word, (band << cbits) | cell: cbits grows with
+    // the row of cells (n > 65536 needs more than 12 bits), the band takes the rest
+    int cbits = 12;
+    while (((int64_t)1 << cbits) < ncp) ++cbits;
+    c.cbits = cbits;
+    h->screen_ok = cbits < 32 && nbands <= ((int64_t)1 << (32 - cbits));
     // PDOT_SCREEN=0/1 forces the walker; by default the screened pass is used
     // from 2^22 plan entries up (below that the plan is L2-resident and the
     // single dense launch per pass wins, e.g. 1024^2)
@@ -677,7 +684,7 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
       }
     }
     const char* env = getenv("PDOT_SCREEN");
-    h->screen_on = env ? atoi(env) != 0 : (double)m_total * (double)n >= (double)(1 << 22);
+    h->screen_on = h->screen_ok && (env ? atoi(env) != 0 : (double)m_total * (double)n >= (double)(1 << 22));
   }
   if (nranks > 1) {  // peer-memory exchange buffer (separate allocation: shareable by CUDA IPC)
     h->xbuf_bytes = (size_t)(2 * pdot::kGroups * h->gstride) * sizeof(double) +
@@ -910,7 +917,9 @@ int pdot_get_slot_sparse(pdot_solver* h, int slot, double* X_host, int64_t ldX, 
     // chunk = what fits one pinned bounce buffer and the device staging area (the
     // per-pass cell partial buffer, idle between solves)
     if (!h->bounce[0]) {
-      const size_t want = std::min<size_t>((size_t)cnt * kCellVals * sizeof(double), (size_t)64 << 20);
+      // the same 64 MB the dense path allocates for big plans: a later dense
+      // get_slot on this handle reuses the buffer (d2h_matrix_bounced)
+      const size_t want = (size_t)64 << 20;
       for (int i = 0; i < 2; ++i) {
         CK(cudaHostAlloc(&h->bounce[i], want, cudaHostAllocDefault));
         CK(cudaEventCreateWithFlags(&h->bounce_ev[i], cudaEventDisableTiming));
@@ -937,7 +946,8 @@ int pdot_get_slot_sparse(pdot_solver* h, int slot, double* X_host, int64_t ldX, 
         for (int64_t u = a; u < e; ++u) {
           const int64_t t = order[u];
           const uint32_t entry = list[t];
-          const int64_t i0 = (int64_t)(entry >> 12) * pdot::kBand, j0 = (int64_t)(entry & 0xfffu) * pdot::kCell;
+          const int64_t i0 = pdot::entry_band(entry, c.cbits) * pdot::kBand;
+          const int64_t j0 = pdot::entry_cell(entry, c.cbits) * pdot::kCell;
           const int64_t rows = std::min<int64_t>(pdot::kBand, h->m - i0), cols = std::min<int64_t>(pdot::kCell, h->n - j0);
           const double* src = b + (t - k0) * kCellVals;
           for (int64_t r = 0; r < rows; ++r)
@@ -1514,6 +1524,8 @@ int pdot_set_screening(pdot_solver* h, int on) {
   if (!h) return set_err(PDOT_EINVAL, "null handle");
   DeviceGuard dg(h->device);
   const bool was = h->host.screen != 0;
+  if (on && !h->screen_ok)
+    return set_err(PDOT_EINVAL, "block screening needs (bands x cells) of the plan to fit a 32-bit cell list entry");
   h->screen_on = on != 0;
   if (int rc = screen_setup(h)) return rc;
   if (h->host.screen && !was) {

@@ -57,6 +57,7 @@ struct pdot_solver {
   char* screen_mem = nullptr;
   double* minc_buf = nullptr;
   unsigned* d2h_count = nullptr;  // counter of the sparse device->host copy
+  bool screen_ok = true;        // the plan geometry fits the 32-bit cell list (solver.cu, pdot_create)
   bool screen_on = true;        // screened passes (default from 2^22 entries; PDOT_SCREEN / pdot_set_screening)
   size_t bounce_bytes = 0;
   cudaEvent_t bounce_ev[2] = {nullptr, nullptr};

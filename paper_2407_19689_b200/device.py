@@ -303,6 +303,15 @@ def get_handle(m: int, n: int, device: int = 0) -> Handle:
     return h
 
 
+def detach_handle(h: Handle) -> None:
+    """Take ``h`` out of the shared cache: its caller now owns it exclusively
+    (a device-resident result in one of its slots cannot be overwritten by a
+    later solve of the same shape, which gets a fresh handle)."""
+    for k, v in list(_HANDLES.items()):
+        if v is h:
+            del _HANDLES[k]
+
+
 def release_handles() -> None:
     """Drop the cache's references; a handle is destroyed once no caller holds
     it (a solve_device result keeps its handle alive)."""

@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib
 from .config import ADAPTIVE, RELATIVE, SolverConfig, SolveTrace
-from .device import DeviceProblem, as_device_problem, get_handle
+from .device import DeviceProblem, as_device_problem, detach_handle, get_handle
 from .records import Iterate, SolveReport
 
 
@@ -51,7 +51,7 @@ def _events(h) -> list:
     buf = (_lib.Event * 4096)()
     while True:
         k = h.lib.pdot_get_events(h.ptr, buf, 4096)
-        out.extend((buf[i].type, buf[i].ia, buf[i].x, buf[i].y) for i in range(k))
+        out.extend((buf[i].type, buf[i].ia, buf[i].x, buf[i].y, buf[i].z) for i in range(k))
         if k < 4096:
             return out
 
@@ -97,7 +97,10 @@ def assemble_report(h, res, config: SolverConfig, trace: SolveTrace | None, roun
     """Trace events + device result -> SolveReport (pdhg.py:380-399)."""
     lib = h.lib
     restart_lengths, restart_kkts = [], []
-    for typ, ia, x, y in _events(h):
+    events = _events(h)
+    if trace is not None:
+        trace._events = events  # noqa: SLF001 - raw device events (margins for parity reports)
+    for typ, ia, x, y, _z in events:
         if typ == _lib.EV_START:
             restart_kkts.append(x)
         elif typ == _lib.EV_RESTART:
@@ -139,7 +142,7 @@ def assemble_report(h, res, config: SolverConfig, trace: SolveTrace | None, roun
 
 def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = None,
           trace: SolveTrace | None = None, *, device: int = 0, return_device: bool = False,
-          poll_passes: int = 0):
+          poll_passes: int = 0, trace_snapshots: bool = True, handle=None):
     """Run restarted PDHG until the KKT tolerance, iteration or time limit.
 
     Same contract as the reference ``otsolve.solve`` (pdhg.py:254-265):
@@ -148,7 +151,13 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
     best evaluated candidate is returned.  ``prob`` may be a host problem
     (numpy ``C f g``) or a ``DeviceProblem`` already in HBM.  With
     ``return_device=True`` the iterate stays on the device (a ``(slot, handle)``
-    pair is returned in place of numpy arrays; see ``solve_device``).
+    pair is returned in place of numpy arrays; see ``solve_device``) and the
+    handle is taken out of the shared cache, so no later solve can overwrite
+    the returned slot.  ``trace_snapshots=False`` records only the scalar
+    trace lists (etas, step bounds, candidate KKTs, omegas, restart KKTs) and
+    runs the batched graph loop instead of stepping pass by pass.  ``handle``
+    runs the solve on a handle the caller owns (e.g. one returned by an
+    earlier ``return_device`` solve) instead of the shared cache.
     """
     t_start = time.perf_counter()
     phases = {}
@@ -156,15 +165,20 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
         config = SolverConfig()
     dp = as_device_problem(prob, device)
     phases["h2d_problem_s"] = time.perf_counter() - t_start
-    h = get_handle(dp.m, dp.n, dp.device)
+    if handle is not None:
+        if (handle.m, handle.n, handle.device) != (dp.m, dp.n, dp.device):
+            raise ValueError("handle shape / device does not match the problem")
+        h = handle
+    else:
+        h = get_handle(dp.m, dp.n, dp.device)
     h.bind(dp)
     if initial is not None:
         h.set_slot(0, initial.X, initial.p, initial.q)
     else:
         h.set_slot(0, None, None, None)
     phases["setup_s"] = time.perf_counter() - t_start - phases["h2d_problem_s"]
-    stepwise = trace is not None
-    cfg = config_struct(config, trace_level=1 if trace is not None else 0, poll_passes=poll_passes)
+    stepwise = trace is not None and (trace_snapshots or trace.record_inner)
+    cfg = config_struct(config, trace_level=2 if trace is not None else 0, poll_passes=poll_passes)
     # dense output plans are pre-faulted during the solve; a screened handle copies
     # only the occupied cells into a zero-filled array (Handle.get_slot)
     out = _Prefault((dp.m, dp.n)) if (not return_device and dp.m * dp.n >= (1 << 22)
@@ -207,6 +221,8 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
     report._e2e_s = elapsed  # noqa: SLF001
     report._phases = phases  # noqa: SLF001
     if return_device:
+        if handle is None:
+            detach_handle(h)
         return (int(res.final_slot), h), report
     t2 = time.perf_counter()
     X = None if out is None else out.result()

@@ -234,14 +234,34 @@ def whitenoise_images(r, seed):
 
 
 def whitenoise_marginals(r, seed):
+    """The two marginals of synth_instance("whitenoise", r, seed), normalised
+    ONCE from the raw pixels as marginal_from_image does (instance.py:153-158).
+    Callers that build a problem from these weights must not normalise them a
+    second time (w / sum(w) of an already-normalised w moves entries by an ulp):
+    pass them as ``Marginal`` objects, not arrays (see sqeuclid_problem)."""
     src, dst = whitenoise_images(r, seed)
     return Marginal(src.ravel()).weights, Marginal(dst.ravel()).weights
 
 
+def whitenoise_marginal_objects(r, seed):
+    """(Marginal, Marginal) built from the raw pixels: marginal_from_image."""
+    src, dst = whitenoise_images(r, seed)
+    return Marginal(src.ravel()), Marginal(dst.ravel())
+
+
 def sqeuclid_problem(r, seed):
-    """C1/C2/C3/C5 family: whitenoise marginals, exact sq-Euclidean cost."""
-    f, g = whitenoise_marginals(r, seed)
-    return OTProblem(CostMatrix(sqeuclid_grid_cost(r)), Marginal(f), Marginal(g))
+    """C1/C2/C3/C5 family: whitenoise marginals, exact sq-Euclidean cost.
+
+    Marginals are normalised once, from the raw pixels, exactly like the
+    reference's grid_problem / marginal_from_image (instance.py:153-158,
+    232-239), so f and g are bitwise the ones DeviceProblem.sqeuclid_grid
+    uploads."""
+    fm, gm = whitenoise_marginal_objects(r, seed)
+    prob = OTProblem(CostMatrix(sqeuclid_grid_cost(r)), fm, gm)
+    # the exact integer norm, as the device problem uses: equal to the reference's
+    # np.linalg.norm(C) up to r = 64 (tested) and free of BLAS rounding beyond
+    prob._fro = sqeuclid_fro_norm(r)
+    return prob
 
 
 RECT_SRC = (64, 128)   # C4 source grid (rows, cols)  -> m = 8192
@@ -269,22 +289,31 @@ def rect_l1_cost_rows(row0, row1, src_shape=RECT_SRC, dst_shape=RECT_DST):
     return (np.abs(a[:, None] - c[None, :]) + np.abs(b[:, None] - d[None, :])).astype(np.float64)
 
 
-def sparse_marginals(size, seed, density=0.1):
-    """C4 marginals: `density` of the cells carry U(0.1, 1.1) mass, the rest 0."""
+def sparse_weights(size, seed, density=0.1):
+    """Raw C4 weights: `density` of the cells carry U(0.1, 1.1) mass, the rest 0."""
     rng = np.random.default_rng(seed)
     k = max(1, int(round(density * size)))
     support = rng.choice(size, size=k, replace=False)
     w = np.zeros(size)
     w[support] = 0.1 + rng.random(k)
-    return Marginal(w).weights
+    return w
+
+
+def sparse_marginals(size, seed, density=0.1):
+    """C4 marginals: sparse_weights normalised once (Marginal)."""
+    return Marginal(sparse_weights(size, seed, density)).weights
 
 
 def rect_problem(seed, src_shape=RECT_SRC, dst_shape=RECT_DST):
+    """C4 family; marginals normalised once from the raw weights (the same f, g
+    as DeviceProblem.rect_l1)."""
     m = src_shape[0] * src_shape[1]
     n = dst_shape[0] * dst_shape[1]
-    f = sparse_marginals(m, 2 * seed)
-    g = sparse_marginals(n, 2 * seed + 1)
-    return OTProblem(CostMatrix(rect_l1_cost(src_shape, dst_shape)), Marginal(f), Marginal(g))
+    fm = Marginal(sparse_weights(m, 2 * seed))
+    gm = Marginal(sparse_weights(n, 2 * seed + 1))
+    prob = OTProblem(CostMatrix(rect_l1_cost(src_shape, dst_shape)), fm, gm)
+    prob._fro = rect_l1_fro_norm(src_shape, dst_shape)
+    return prob
 
 
 def grid_side(mn):

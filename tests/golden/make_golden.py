@@ -33,7 +33,24 @@ from paper_2407_19689_b200 import instances as inst  # noqa: E402
 
 
 def ref_problem(C, f, g):
+    """Reference problem from RAW weights: Marginal normalises them once."""
     return ot.OTProblem(ot.CostMatrix(C), ot.Marginal(f), ot.Marginal(g))
+
+
+def ref_sqeuclid(r, seed):
+    """The C1/C2/C3 family through the reference's own generators: whitenoise
+    images from synth_instance, marginals from marginal_from_image (normalised
+    once, instance.py:153-158), exact integer sq-Euclidean cost."""
+    src, dst = ot.synth_instance("whitenoise", r, seed)
+    return ot.OTProblem(ot.CostMatrix(inst.sqeuclid_grid_cost(r)), ot.marginal_from_image(src),
+                        ot.marginal_from_image(dst))
+
+
+def ref_rect(seed, src_shape, dst_shape):
+    """The C4 family (builder-defined): raw sparse weights, normalised once."""
+    m, n = src_shape[0] * src_shape[1], dst_shape[0] * dst_shape[1]
+    return ref_problem(inst.rect_l1_cost(src_shape, dst_shape), inst.sparse_weights(m, 2 * seed),
+                       inst.sparse_weights(n, 2 * seed + 1))
 
 
 def random_problem(rng, m, n, margin=0.05):
@@ -101,13 +118,8 @@ def solve_cases():
                       rng.standard_normal(6) * 0.1)
     cases.append(("warm5x6", p, dict(tol=1e-6), init))
     for r, seed, tol in ((4, 0, 1e-6), (8, 1, 1e-4), (16, 0, 1e-4)):
-        f, g = inst.whitenoise_marginals(r, seed)
-        cases.append((f"sqeuc_r{r}_s{seed}", ref_problem(inst.sqeuclid_grid_cost(r), f, g),
-                      dict(tol=tol), None))
-    f = inst.sparse_marginals(128, 0)
-    g = inst.sparse_marginals(512, 1)
-    C = inst.rect_l1_cost((8, 16), (16, 32))
-    cases.append(("rect_l1_128x512", ref_problem(C, f, g), dict(tol=1e-4), None))
+        cases.append((f"sqeuc_r{r}_s{seed}", ref_sqeuclid(r, seed), dict(tol=tol), None))
+    cases.append(("rect_l1_128x512", ref_rect(0, (8, 16), (16, 32)), dict(tol=1e-4), None))
     return cases
 
 
@@ -129,8 +141,8 @@ def sinkhorn_cases():
     cases = [("rand5x4", random_problem(rng, 5, 4), 0.05, 1e-8),
              ("grid8_l1", ot.grid_problem("cauchy_like", 8, "l1", seed=2), 0.05, 1e-6),
              ("shapes16_l2", ot.grid_problem("shapes", 16, "l2", seed=11), 0.01, 1e-4)]
-    f = inst.sparse_marginals(128, 3)
-    g = inst.sparse_marginals(256, 4)
+    f = inst.sparse_weights(128, 3)
+    g = inst.sparse_weights(256, 4)
     cases.append(("rect_sparse", ref_problem(inst.rect_l1_cost((8, 16), (16, 16)) / 10.0, f, g), 0.05, 1e-6))
     arrays, meta = {}, {}
     for name, prob, pen, tol in cases:
@@ -178,12 +190,16 @@ def main():
     # C1 (m = n = 1024, whitenoise, exact sq-Euclidean), tol 1e-4: report only
     c1 = {}
     for seed in (0,):
-        f, g = inst.whitenoise_marginals(32, seed)
-        prob = ref_problem(inst.sqeuclid_grid_cost(32), f, g)
-        it, rep = ot.solve(prob, ot.SolverConfig(tol=1e-4, deterministic=True))
+        prob = ref_sqeuclid(32, seed)
+        trace = ot.SolveTrace()
+        it, rep = ot.solve(prob, ot.SolverConfig(tol=1e-4, deterministic=True), trace=trace)
         c1[str(seed)] = dict(report=json.loads(rep.to_json()),
                              pre_rounding_objective=float(np.vdot(prob.C, it.X)),
-                             dual_objective=float(prob.f @ it.p + prob.g @ it.q))
+                             dual_objective=float(prob.f @ it.p + prob.g @ it.q),
+                             cost_fro_norm=prob.cost_fro_norm, marginal_norm=prob.marginal_norm,
+                             trace=dict(etas=trace.etas, step_bounds=trace.step_bounds,
+                                        candidate_kkts=trace.candidate_kkts, omegas=trace.omegas,
+                                        restart_kkts=trace.restart_kkts))
         print("C1 seed", seed, rep.iterations, rep.restarts)
     (HERE / "c1.json").write_text(json.dumps(c1, indent=1, sort_keys=True))
 
@@ -191,8 +207,7 @@ def main():
     # and C1 seeds 1-2 at tol 1e-4 (trajectory-sensitive; compared in the envelope)
     p4 = {}
     for r, seed, tol in ((16, 0, 1e-8), (16, 1, 1e-8), (16, 2, 1e-8), (32, 1, 1e-4), (32, 2, 1e-4)):
-        f, g = inst.whitenoise_marginals(r, seed)
-        prob = ref_problem(inst.sqeuclid_grid_cost(r), f, g)
+        prob = ref_sqeuclid(r, seed)
         it, rep = ot.solve(prob, ot.SolverConfig(tol=tol, deterministic=True))
         p4[f"r{r}_s{seed}_tol{tol:g}"] = dict(r=r, seed=seed, tol=tol, report=json.loads(rep.to_json()),
                                                pre_rounding_objective=float(np.vdot(prob.C, it.X)))

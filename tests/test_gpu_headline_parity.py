@@ -1,0 +1,188 @@
+"""Parity at the HEADLINE configurations, on the default (screened) walker.
+
+At >= 2^22 plan entries the solver runs the screened pass (K0 screen, K1 cell
+walker, K1b tile assembly, K2 reduction + controller) with
+128-row tiles.  These tests pin that exact path against the reference:
+
+* one mid-solve STEP at C2 (4096^2), C3 (16384^2) and C4 (8192 x 32768): a
+  sparse iterate with nonzero duals taken from a GPU solve, k > 1, through
+  the same fused STEP pass the loop runs (``units.step_and_average``),
+  against the oracle's ``primal_dual_step`` and running mean (pdhg.py:121-129,
+  314-317): X+ and the average matrix bit-identical, p+, q+ and the dual
+  averages within 1e-12 relative (they sit behind a reduction);
+* SURVEY P2 on reference-run traces (tests/golden/make_headline_golden.py,
+  committed fixtures): C2 tol 1e-6, the 512 x 2048 C4 analogue, C1 seed 0 and
+  the first iterations of C3.  Etas, step bounds, candidate KKTs, restart
+  positions and omegas agree to 1e-10 relative over at least the first 50
+  iterations; the agreement horizon and the first decision whose margin is
+  below 1e-12 are printed;
+* SURVEY P3 on the complete reference runs: same termination reason,
+  final relative KKT <= tol, iterations inside the reference's own drift
+  envelope (the C2 re-runs with apply_A summed in long double / reversed).
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from p2_util import first_tight_decision, horizon, margins
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def _fx(name):
+    p = GOLD / f"headline_{name}.json"
+    if not p.exists():
+        pytest.skip(f"fixture {p.name} not generated")
+    return json.loads(p.read_text())
+
+
+def _device_problem(pd, fx):
+    """The fixture's instance, built on the device, with the reference's norms."""
+    case = fx["case"]
+    if case["kind"] == "sqeuclid":
+        dp = pd.DeviceProblem.sqeuclid_grid(case["r"], case["seed"])
+    else:
+        dp = pd.DeviceProblem.rect_l1(case["seed"], src=tuple(case["src"]), dst=tuple(case["dst"]))
+    assert (dp.m, dp.n) == (fx["m"], fx["n"])
+    assert dp.cost_fro_norm == fx["cost_fro_norm"]  # exact integer norm on both sides
+    dp.marginal_norm = fx["marginal_norm"]  # BLAS-computed by the reference: take its value
+    return dp
+
+
+# ---------------------------------------------------------------------------
+# one screened STEP at production geometry against the oracle
+# ---------------------------------------------------------------------------
+STEP_CASES = {
+    "c2": dict(kind="sqeuclid", r=64, iters=(40, 33)),
+    "c3": dict(kind="sqeuclid", r=128, iters=(30, 24)),
+    "c4": dict(kind="rect", iters=(30, 24)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(STEP_CASES))
+def test_mid_solve_step_bitwise(name):
+    import paper_2407_19689_b200 as pd
+    from oracle import pdot_oracle as O
+    from paper_2407_19689_b200 import instances as inst
+    from paper_2407_19689_b200.device import release_handles
+
+    case = STEP_CASES[name]
+    if case["kind"] == "sqeuclid":
+        host = inst.sqeuclid_problem(case["r"], 0)
+    else:
+        host = inst.rect_problem(0)
+    dp = pd.DeviceProblem.from_host(host)
+    # a mid-solve iterate and an older one as the running average
+    tr = pd.SolveTrace()
+    it, rep = pd.solve(dp, pd.SolverConfig(tol=1e-12, max_iters=case["iters"][0]), trace=tr,
+                       trace_snapshots=False)
+    av, _ = pd.solve(dp, pd.SolverConfig(tol=1e-12, max_iters=case["iters"][1]))
+    assert rep.iterations == case["iters"][0]
+    nnz = int(np.count_nonzero(it.X))
+    assert 0 < nnz < it.X.size // 50, nnz  # sparse: the screened regime
+    assert np.count_nonzero(it.p) > 0 and np.count_nonzero(it.q) > 0
+    eta, omega = tr.etas[-1], tr.omegas[-1] if tr.omegas else 1.0
+    tau, sigma, k = eta / omega, eta * omega, 7
+    h = pd.device.get_handle(dp.m, dp.n)
+    assert h.screened(), "the headline geometry must run the screened walker"
+    nxt, avg = pd.units.step_and_average(dp, it, av, tau, sigma, k)
+    Xn, pn, qn = O.primal_dual_step(host.C, host.f, host.g, it.X, it.p, it.q, tau, sigma)
+    assert np.array_equal(nxt.X, Xn), f"X+ differs in {int(np.count_nonzero(nxt.X != Xn))} entries"
+    np.testing.assert_allclose(nxt.p, pn, rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(nxt.q, qn, rtol=1e-12, atol=1e-300)
+    # running mean (pdhg.py:315-317): matrix of the input iterate, duals of the trial
+    A_ref = av.X + (it.X - av.X) / k
+    assert np.array_equal(avg.X, A_ref)
+    np.testing.assert_allclose(avg.p, av.p + (nxt.p - av.p) / k, rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(avg.q, av.q + (nxt.q - av.q) / k, rtol=1e-12, atol=1e-300)
+    # the step bound and both KKT metrics of the new point against the oracle
+    b_gpu = pd.stepsize_bound(it, nxt, omega)
+    b_ref = O.step_bound(it.X, it.p, it.q, Xn, pn, qn, omega)
+    assert b_gpu == pytest.approx(b_ref, rel=1e-11)
+    k_gpu = pd.kkt_error(dp, nxt, 1.7)
+    k_ref = O.kkt_blocks(host.C, host.f, host.g, Xn, pn, qn, host.cost_fro_norm, host.marginal_norm, 1.7)
+    assert k_gpu.relative_composite == pytest.approx(k_ref["relative_composite"], rel=1e-11)
+    assert k_gpu.composite == pytest.approx(k_ref["composite"], rel=1e-11)
+    print(f"{name}: nnz(X) {nnz}, screened STEP bit-identical; bound rel "
+          f"{abs(b_gpu - b_ref) / b_ref:.1e}")
+    del dp
+    release_handles()
+
+
+# ---------------------------------------------------------------------------
+# P2: reference-run traces
+# ---------------------------------------------------------------------------
+P2_CASES = {  # fixture -> iterations that must agree to 1e-10
+    "c2": 50,
+    "c4a": 50,
+    "c3": 50,
+}
+
+
+def _p2(name, need):
+    import paper_2407_19689_b200 as pd
+    from paper_2407_19689_b200.device import release_handles
+
+    fx = _fx(name)
+    dp = _device_problem(pd, fx)
+    cfg = pd.SolverConfig(tol=fx["case"]["tol"], deterministic=True)
+    max_it = None
+    if not fx["complete"]:
+        max_it = fx["iterations_recorded"]
+        cfg = pd.SolverConfig(tol=fx["case"]["tol"], deterministic=True, max_iters=max_it)
+    tr = pd.SolveTrace()
+    it, rep = pd.solve(dp, cfg, trace=tr, trace_snapshots=False)
+    assert pd.device.get_handle(dp.m, dp.n).screened()
+    ref_len = fx["report"]["restart_lengths"] if fx["complete"] else fx["restart_lengths"]
+    h, why, worst = horizon(tr, rep.restart_lengths, fx["trace"], ref_len, rtol=1e-10)
+    mg = margins(tr._events, cfg)
+    ti, kind, mval = first_tight_decision(mg, 1e-12)
+    print(f"P2 {name}: agreement horizon {h} iterations ({why}); worst rel diff inside {worst:.2e}; "
+          f"first decision margin < 1e-12: {ti} ({kind} {mval}); gpu {rep.iterations} it / "
+          f"{rep.restarts} rs, ref {fx.get('report', {}).get('iterations', max_it)}")
+    assert h >= min(need, len(fx["trace"]["etas"])), (h, why)
+    release_handles()
+    return fx, rep, it, dp
+
+
+@pytest.mark.parametrize("name", sorted(P2_CASES))
+def test_p2_headline(name):
+    fx, rep, it, dp = _p2(name, P2_CASES[name])
+    if fx["complete"]:
+        ref = fx["report"]
+        # P3: same termination, tolerance met
+        assert rep.termination_reason == ref["termination_reason"]
+        assert rep.final_relative_kkt <= fx["case"]["tol"]
+
+
+def test_p3_c2_envelope():
+    """C2 tol 1e-6 full solve inside the reference's self-drift envelope:
+    the reference itself re-run with apply_A summed in long double and in
+    reversed order."""
+    import paper_2407_19689_b200 as pd
+    from paper_2407_19689_b200 import instances as inst
+
+    fx = _fx("c2")
+    if not fx["complete"]:
+        pytest.skip("C2 reference run not complete")
+    runs = [fx] + [json.loads((GOLD / f"headline_c2_{v}.json").read_text())
+                   for v in ("ld", "rev") if (GOLD / f"headline_c2_{v}.json").exists()]
+    runs = [r for r in runs if r["complete"]]
+    its = [r["report"]["iterations"] for r in runs]
+    pre = [r["pre_rounding_objective"] for r in runs]
+    dp = _device_problem(pd, fx)
+    it, rep = pd.solve(dp, pd.SolverConfig(tol=1e-6, deterministic=True))
+    gpu_pre = float(np.vdot(inst.sqeuclid_grid_cost(64), it.X))
+    lo, hi = min(its), max(its)
+    span = max(hi - lo, 1)
+    print(f"C2 tol 1e-6: gpu {rep.iterations} it, <C,X> {gpu_pre:.10f}; reference runs {its}, <C,X> {pre}")
+    assert rep.termination_reason == "tolerance" and rep.final_relative_kkt <= 1e-6
+    # inside the envelope widened by its own span on each side
+    assert lo - span <= rep.iterations <= hi + span
+    spread = max(pre) - min(pre)
+    assert abs(gpu_pre - fx["pre_rounding_objective"]) <= max(2 * spread, 1e-9 * abs(gpu_pre))

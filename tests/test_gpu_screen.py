@@ -208,3 +208,45 @@ def test_screened_far_violation(pd):
     (it0, r0, _), (it1, r1, _) = _solve_both(pd, prob, cfg)
     assert r0.to_json() == r1.to_json()
     assert _same_iterate(it0, it1)
+
+
+def test_screened_wide_rows_beyond_4096_cells(pd):
+    """n > 65536: a row of 8x16 cells has more than 4096 cells, so the cell
+    index of a 32-bit list entry needs more than 12 bits (the band takes the
+    remaining bits, csrc/pdot_internal.cuh cell_entry).  80 x 65552 is above
+    2^22 entries, so screening is the default: it must be on, and agree bit for
+    bit with the dense walker, including the sparse device->host copy of the
+    final plan."""
+    from paper_2407_19689_b200 import instances as inst
+    from paper_2407_19689_b200.device import get_handle
+    m, n = 80, 65552
+    rng = np.random.default_rng(3)
+    # a sparse-plan problem: L1-like cost between row and column coordinates
+    a = np.sort(rng.random(m)) * n
+    C = np.abs(a[:, None] - np.arange(n)[None, :]) / 100.0
+    f = rng.random(m) + 0.1
+    g = rng.random(n) + 0.1
+    prob = inst.make_problem(C, f, g)
+    cfg = pd.SolverConfig(tol=1e-9, deterministic=True, max_iters=80)
+    (it0, r0, _), (it1, r1, _) = _solve_both(pd, prob, cfg)
+    assert get_handle(m, n).screened()
+    assert r0.to_json() == r1.to_json()
+    assert _same_iterate(it0, it1)
+    assert np.count_nonzero(it1.X[:, 65536:]) > 0  # cells past index 4095 carry mass
+
+
+def test_c5_geometry_virtual_shards(pd):
+    """C5 geometry (n = 65536, the widest row of cells a 12-bit index held) on a
+    reduced row count: rows 0..1023 of the 65536^2 instance, generated on the
+    device, solved on one handle and as 8 virtual row shards (screened passes,
+    device-copy exchange): bit-identical."""
+    from paper_2407_19689_b200.shard import solve_virtual
+    dp = pd.DeviceProblem.sqeuclid_grid(256, 0, rows=(0, 1024))
+    cfg = pd.SolverConfig(tol=1e-9, deterministic=True, max_iters=40)
+    it1, rep1 = pd.solve(dp, cfg)
+    assert pd.device.get_handle(dp.m, dp.n).screened()
+    itv, repv = solve_virtual(dp, cfg, 8)
+    assert (repv.iterations, repv.restarts, repv.restart_lengths) == (rep1.iterations, rep1.restarts,
+                                                                       rep1.restart_lengths)
+    assert repv.final_relative_kkt == rep1.final_relative_kkt
+    assert np.array_equal(itv.X, it1.X) and np.array_equal(itv.p, it1.p) and np.array_equal(itv.q, it1.q)
