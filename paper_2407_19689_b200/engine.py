@@ -137,6 +137,7 @@ def assemble_report(h, res, config: SolverConfig, trace: SolveTrace | None, roun
         restart_kkts=[float(v) for v in restart_kkts],
     )
     report._passes = int(res.passes)  # noqa: SLF001 - diagnostics for bench/tests
+    report._device_s = float(res.device_s)  # noqa: SLF001 - CUDA-event time of the loop
     return report
 
 

@@ -105,13 +105,32 @@ def _apply_A_reversed(X):
     return Xr.sum(axis=1)[::-1].copy(), Xr.sum(axis=0)[::-1].copy()
 
 
+def _apply_A_permuted(seed):
+    """apply_A summed in a seeded random order: the rows of X are summed over a
+    permuted column order and the columns over a permuted row order."""
+    perms = {}
+
+    def fn(X):
+        m, n = X.shape
+        if (m, n) not in perms:
+            rng = np.random.default_rng(1000 + seed)
+            perms[(m, n)] = (rng.permutation(n), rng.permutation(m))
+        pc, pr = perms[(m, n)]
+        return X[:, pc].sum(axis=1), X[pr, :].sum(axis=0)
+    return fn
+
+
 def _perturb(variant):
     """SURVEY A.3/A.8 self-drift envelope: the reference re-run with apply_A
-    summed in long double ("ld") or in reversed order ("rev"), patched at both
-    import sites (pdhg_step / stepsize_bound and kkt_error)."""
+    summed in long double ("ld"), in reversed order ("rev") or in a seeded
+    random order ("rnd<k>"), patched at both import sites (pdhg_step /
+    stepsize_bound and kkt_error)."""
     import otsolve.kkt as K
     import otsolve.pdhg as P
-    fn = {"ld": _apply_A_longdouble, "rev": _apply_A_reversed}[variant]
+    if variant.startswith("rnd"):
+        fn = _apply_A_permuted(int(variant[3:]))
+    else:
+        fn = {"ld": _apply_A_longdouble, "rev": _apply_A_reversed}[variant]
     P.apply_A = K.apply_A = fn
 
 
@@ -164,6 +183,15 @@ def finalize(name):
             t_last = d["t"]
             if d["k"] == "restart_kkts":
                 restart_at.append(len(tr["etas"]))
+    # the last streamed iteration's restart decision may still be in flight (the
+    # restart is recorded after its candidate KKT): keep only iterations whose
+    # successor has started, i.e. whose decisions are complete
+    keep = max(0, min(len(tr["etas"]) - 1, len(tr["candidate_kkts"])))
+    restart_at = [t for t in restart_at if t <= keep]
+    nr = len(restart_at)
+    tr = {"etas": tr["etas"][:keep], "step_bounds": tr["step_bounds"][:keep],
+          "candidate_kkts": tr["candidate_kkts"][:keep], "omegas": tr["omegas"][:nr],
+          "restart_kkts": tr["restart_kkts"][:nr]}
     lengths = [b - a for a, b in zip([0] + restart_at[:-1], restart_at)]
     done = any(d["k"] == "done" for d in lines)
     path = HERE / f"headline_{name}.json"

@@ -34,40 +34,68 @@ def restart_iterations(lengths):
     return out
 
 
-def horizon(gpu_trace, gpu_lengths, ref_trace, ref_lengths, rtol=1e-10):
-    """First iteration index (0-based) where the trajectories part, and why.
+def diffs(gpu_trace, gpu_lengths, ref_trace, ref_lengths):
+    """Per-iteration comparison over the common prefix.
 
-    Returns (h, reason, worst): all iterations < h agree within rtol (etas,
-    step bounds, candidate KKTs, restart positions, omegas); ``worst`` is the
-    largest relative difference seen inside the horizon."""
+    Returns (d, split, why): d[i] = largest relative difference of iteration
+    i's traced scalars (eta, step bound, candidate KKT, and omega at a restart);
+    ``split`` = first iteration whose DISCRETE path differs -- a restart at a
+    different iteration, or an eta off by more than 1e-3 relative (a different
+    accept / reject sequence shows up as a factor-of-two eta) -- or the common
+    length when the paths never split."""
     ge, re_ = gpu_trace.etas, ref_trace["etas"]
     gb, rb = gpu_trace.step_bounds, ref_trace["step_bounds"]
     gc, rc = gpu_trace.candidate_kkts, ref_trace["candidate_kkts"]
     go, ro = gpu_trace.omegas, ref_trace["omegas"]
-    gr, rr = restart_iterations(gpu_lengths), restart_iterations(ref_lengths)
+    gr, rr = set(restart_iterations(gpu_lengths)), set(restart_iterations(ref_lengths))
     n = min(len(ge), len(re_))
-    worst = 0.0
-    ri = 0  # restarts passed so far
+    d = []
+    ri = 0
     for i in range(n):
-        for nm, a, b in (("eta", ge, re_), ("bound", gb, rb), ("cand", gc, rc)):
+        di = 0.0
+        for a, b in ((ge, re_), (gb, rb), (gc, rc)):
             if i < len(a) and i < len(b):
-                d = _rel(a[i], b[i])
-                if d > rtol:
-                    return i, f"{nm} differs by {d:.2e}", worst
-                worst = max(worst, d)
-        # restarts that fire after iteration i+1 (1-based count of iterations)
-        g_here = [k for k, t in enumerate(gr) if t == i + 1]
-        r_here = [k for k, t in enumerate(rr) if t == i + 1]
-        if bool(g_here) != bool(r_here):
-            return i, "restart decision differs", worst
-        if g_here:
+                di = max(di, _rel(a[i], b[i]))
+        if _rel(ge[i], re_[i]) > 1e-3:
+            return d, i, f"accept/reject path differs (eta rel diff {_rel(ge[i], re_[i]):.1e})"
+        if ((i + 1) in gr) != ((i + 1) in rr):
+            return d, i, "restart decision differs"
+        if (i + 1) in gr:
             if ri < len(go) and ri < len(ro):
-                d = _rel(go[ri], ro[ri])
-                if d > rtol:
-                    return i, f"omega differs by {d:.2e}", worst
-                worst = max(worst, d)
+                di = max(di, _rel(go[ri], ro[ri]))
             ri += 1
-    return n, "end of common trace", worst
+        d.append(di)
+    return d, n, "end of common trace"
+
+
+def horizon(gpu_trace, gpu_lengths, ref_trace, ref_lengths, rtol=1e-10):
+    """First iteration index (0-based) where the trajectories part by more
+    than rtol, and why; (h, reason, worst) with ``worst`` the largest relative
+    difference inside the horizon."""
+    d, split, why = diffs(gpu_trace, gpu_lengths, ref_trace, ref_lengths)
+    worst = 0.0
+    for i, di in enumerate(d):
+        if di > rtol:
+            return i, f"a traced scalar differs by {di:.2e}", worst
+        worst = max(worst, di)
+    return split, why, worst
+
+
+def decision_horizon(gpu_trace, gpu_lengths, ref_trace, ref_lengths):
+    """(split, why, drift): the first iteration whose discrete path differs
+    and the largest relative scalar difference accumulated before it."""
+    d, split, why = diffs(gpu_trace, gpu_lengths, ref_trace, ref_lengths)
+    return split, why, max(d) if d else 0.0
+
+
+def growth(d, points=(10, 25, 50, 100, 200, 400, 800, 1600, 3200)):
+    """Running maximum of the per-iteration difference at a few checkpoints."""
+    out, run = {}, 0.0
+    for i, di in enumerate(d):
+        run = max(run, di)
+        if i + 1 in points:
+            out[i + 1] = run
+    return out
 
 
 def margins(events, config):
@@ -104,8 +132,12 @@ def margins(events, config):
 
 
 def first_tight_decision(mg, below=1e-12):
-    """Index of the first iteration whose smallest decision margin is < below."""
+    """Index of the first iteration whose smallest decision margin is < below.
+    An exact candidate tie (current == average bit for bit, e.g. k = 1, where
+    the average IS the iterate) is resolved identically by both sides (tie ->
+    average) and is not a tight decision."""
     for i, d in enumerate(mg):
-        if min(d.values()) < below:
+        d = {k: v for k, v in d.items() if not (k == "cand_choice" and v == 0.0)}
+        if d and min(d.values()) < below:
             return i, min(d, key=d.get), min(d.values())
     return None, None, None

@@ -27,7 +27,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from p2_util import first_tight_decision, horizon, margins
+from p2_util import decision_horizon, diffs, first_tight_decision, growth, horizon, margins
 
 pytestmark = pytest.mark.gpu
 
@@ -64,6 +64,33 @@ STEP_CASES = {
 }
 
 
+def _current_iterates(pd, dp, at):
+    """Step a solve pass by pass (pdot_advance) and copy the CURRENT iterate
+    (role 0) when the accepted-iteration count reaches each value of ``at``
+    (descending); returns those iterates and (eta, omega) after the last."""
+    import ctypes
+
+    from paper_2407_19689_b200 import _lib
+    from paper_2407_19689_b200.engine import config_struct
+
+    h = pd.device.get_handle(dp.m, dp.n, dp.device)
+    h.bind(dp)
+    h.set_slot(0, None, None, None)
+    cfg = config_struct(pd.SolverConfig(tol=1e-12, max_iters=max(at) + 5), trace_level=0)
+    _lib.check(h.lib.pdot_begin(h.ptr, ctypes.byref(cfg), 0.0))
+    prog = _lib.Progress()
+    got = {}
+    while len(got) < len(at):
+        _lib.check(h.lib.pdot_advance(h.ptr, 1, ctypes.byref(prog)))
+        assert not prog.done
+        if prog.iterations in at and prog.iterations not in got:
+            X, p, q = h.get_slot(prog.roles[0])
+            got[prog.iterations] = pd.Iterate(X, p, q)
+    res = _lib.Result()
+    _lib.check(h.lib.pdot_finish(h.ptr, ctypes.byref(res)))
+    return tuple(got[a] for a in at), (res.eta, res.omega)
+
+
 @pytest.mark.parametrize("name", sorted(STEP_CASES))
 def test_mid_solve_step_bitwise(name):
     import paper_2407_19689_b200 as pd
@@ -77,16 +104,11 @@ def test_mid_solve_step_bitwise(name):
     else:
         host = inst.rect_problem(0)
     dp = pd.DeviceProblem.from_host(host)
-    # a mid-solve iterate and an older one as the running average
-    tr = pd.SolveTrace()
-    it, rep = pd.solve(dp, pd.SolverConfig(tol=1e-12, max_iters=case["iters"][0]), trace=tr,
-                       trace_snapshots=False)
-    av, _ = pd.solve(dp, pd.SolverConfig(tol=1e-12, max_iters=case["iters"][1]))
-    assert rep.iterations == case["iters"][0]
+    # the CURRENT iterate at two points of a solve (the average becomes the older one)
+    (it, av), (eta, omega) = _current_iterates(pd, dp, case["iters"])
     nnz = int(np.count_nonzero(it.X))
     assert 0 < nnz < it.X.size // 50, nnz  # sparse: the screened regime
     assert np.count_nonzero(it.p) > 0 and np.count_nonzero(it.q) > 0
-    eta, omega = tr.etas[-1], tr.omegas[-1] if tr.omegas else 1.0
     tau, sigma, k = eta / omega, eta * omega, 7
     h = pd.device.get_handle(dp.m, dp.n)
     assert h.screened(), "the headline geometry must run the screened walker"
@@ -128,24 +150,39 @@ def _p2(name, need):
     import paper_2407_19689_b200 as pd
     from paper_2407_19689_b200.device import release_handles
 
+    from paper_2407_19689_b200.device import set_screening
+
     fx = _fx(name)
     dp = _device_problem(pd, fx)
+    set_screening(True)  # the default at >= 2^22 entries; forced for the smaller C4 analogue
     cfg = pd.SolverConfig(tol=fx["case"]["tol"], deterministic=True)
     max_it = None
     if not fx["complete"]:
         max_it = fx["iterations_recorded"]
         cfg = pd.SolverConfig(tol=fx["case"]["tol"], deterministic=True, max_iters=max_it)
     tr = pd.SolveTrace()
-    it, rep = pd.solve(dp, cfg, trace=tr, trace_snapshots=False)
-    assert pd.device.get_handle(dp.m, dp.n).screened()
+    try:
+        it, rep = pd.solve(dp, cfg, trace=tr, trace_snapshots=False)
+        assert pd.device.get_handle(dp.m, dp.n).screened()
+    finally:
+        set_screening(None)
     ref_len = fx["report"]["restart_lengths"] if fx["complete"] else fx["restart_lengths"]
     h, why, worst = horizon(tr, rep.restart_lengths, fx["trace"], ref_len, rtol=1e-10)
-    mg = margins(tr._events, cfg)
-    ti, kind, mval = first_tight_decision(mg, 1e-12)
-    print(f"P2 {name}: agreement horizon {h} iterations ({why}); worst rel diff inside {worst:.2e}; "
-          f"first decision margin < 1e-12: {ti} ({kind} {mval}); gpu {rep.iterations} it / "
-          f"{rep.restarts} rs, ref {fx.get('report', {}).get('iterations', max_it)}")
-    assert h >= min(need, len(fx["trace"]["etas"])), (h, why)
+    dh, dwhy, drift = decision_horizon(tr, rep.restart_lengths, fx["trace"], ref_len)
+    d, _, _ = diffs(tr, rep.restart_lengths, fx["trace"], ref_len)
+    n_common = min(len(tr.etas), len(fx["trace"]["etas"]))
+    ti, kind, mval = first_tight_decision(margins(tr._events, cfg), 1e-12)
+    print(f"P2 {name}: 1e-10 horizon {h} iterations ({why}; worst rel diff inside {worst:.2e}); "
+          f"same discrete path for {dh} of {n_common} iterations ({dwhy}; scalar drift before it {drift:.1e}); "
+          f"drift growth {{{', '.join(f'{k}: {v:.0e}' for k, v in growth(d).items())}}}; first decision margin "
+          f"< 1e-12: {ti} ({kind} {mval}); gpu {rep.iterations} it / {rep.restarts} rs, "
+          f"ref {fx.get('report', {}).get('iterations', max_it)} / {len(ref_len)}")
+    assert h >= min(need, n_common), (h, why)
+    # Past the 1e-10 horizon the rounding differences keep growing (restarted PDHG
+    # amplifies them); the discrete paths may part only once that drift is
+    # well beyond rounding level, or at an exact near-tie.  A split while the traced
+    # scalars still agree to 1e-10 would be a logic difference, not drift.
+    assert dh == n_common or drift > 1e-10 or ti is not None, (dh, dwhy, drift)
     release_handles()
     return fx, rep, it, dp
 
