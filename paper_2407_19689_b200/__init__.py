@@ -11,10 +11,13 @@ from .config import (ABSOLUTE, ADAPTIVE, FIXED_BETA, RELATIVE, SolverConfig, Sol
 from .device import DeviceProblem, release_handles
 from .engine import solve, solve_device
 from .entropic import Potentials, SinkhornConfig, sinkhorn_report_gap, sinkhorn_solve
-from .instances import CostMatrix, InstanceError, Marginal, OTProblem, make_problem
+from .instance_io import load_instance, save_instance
+from .instances import CostMatrix, InstanceError, Marginal, OTProblem, grid_cost, grid_problem, make_problem
 from .records import Iterate, KKTReport, SolveReport
 from .units import (adaptive_stepsize, apply_A, apply_At, duality_gap, kkt_error, pdhg_step,
-                    restart_candidate, round_to_feasible, rounded_objective, stepsize_bound)
+                    restart_candidate, round_to_feasible, rounded_objective, rounding_bound_check,
+                    stepsize_bound)
+from .sweep import BenchSummary, geomean_gap, run_bench, sgm10
 
 __all__ = [
     "ABSOLUTE", "ADAPTIVE", "FIXED_BETA", "RELATIVE", "SolverConfig", "SolveTrace", "StepState",
@@ -23,6 +26,8 @@ __all__ = [
     "Iterate", "KKTReport", "SolveReport", "adaptive_stepsize", "apply_A", "apply_At", "duality_gap",
     "kkt_error", "pdhg_step", "restart_candidate", "round_to_feasible", "rounded_objective",
     "stepsize_bound", "Potentials", "SinkhornConfig", "sinkhorn_report_gap", "sinkhorn_solve",
+    "rounding_bound_check", "load_instance", "save_instance", "grid_cost", "grid_problem",
+    "BenchSummary", "geomean_gap", "run_bench", "sgm10",
 ]
 
 __version__ = "0.1.0"

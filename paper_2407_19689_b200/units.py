@@ -162,3 +162,18 @@ def rounded_objective(prob, X: np.ndarray) -> float:
     out = _out(3)
     _lib.check(h.lib.pdot_round(h.ptr, 0, None, 0, out))
     return float(out[0])
+
+
+def rounding_bound_check(prob, X: np.ndarray, X_feas: np.ndarray) -> bool:
+    """Lemma 2 of the paper: |X_feas - X|_1 <= 2 (|f - X 1|_1 + |g - X^T 1|_1)
+    (rounding.py:43-50, same slack 1e-12 (1 + rhs)).  The marginal residuals
+    come from the GPU row / column sums; the entrywise l1 distance is reduced
+    on the device."""
+    require_cuda()
+    f, g = _host_marginals(prob)
+    rows, cols = apply_A(X)
+    rhs = 2.0 * (float(np.abs(f - rows).sum()) + float(np.abs(g - cols).sum()))
+    a = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float64)).cuda()
+    b = torch.from_numpy(np.ascontiguousarray(X_feas, dtype=np.float64)).cuda()
+    lhs = float((b - a).abs().sum().item())
+    return lhs <= rhs + 1e-12 * (1.0 + rhs)
