@@ -197,6 +197,12 @@ int pdot_set_virtual(pdot_solver* h, int on);
 int pdot_ipc_handle(pdot_solver* h, void* out64);
 int pdot_p2p_open(pdot_solver* h, const void* handles64, int count);
 int pdot_p2p_link_local(pdot_solver** hs, int count);
+/* Test hook: the peer-exchange protocol (group stores into every rank's buffer,
+ * st.release of the sequence flags, ld.acquire spin, parity double buffering)
+ * with `count` linked ranks emulated as the blocks of ONE cooperative launch,
+ * so the ranks run concurrently and the spins really wait.  out3r[3r + 0..2] =
+ * rank r's value mismatches, longest wait in ns, exchange-timeout flag. */
+int pdot_p2p_selftest(pdot_solver** hs, int count, int rounds, double delay_us, unsigned long long* out3r);
 int pdot_shard_pass(pdot_solver* h, int phase, pdot_progress* prog);
 int pdot_exchange_local(pdot_solver** hs, int count);
 
@@ -223,6 +229,12 @@ int pdot_gen_cost(double* C_dev, int64_t m, int64_t n, int64_t ldc, int kind, co
 int pdot_gen_cost_rows(double* C_dev, int64_t row0, int64_t rows, int64_t n, int64_t ldc, int kind,
                        const int64_t* a);
 /* ||C||_F on the device (deterministic): used for OTProblem.cost_fro_norm of device-built C */
+/* Host -> device copy of an m x n row-major matrix (cost upload of
+ * solve(host problem), pdhg.py:254-259 takes plain arrays): one DMA from
+ * page-locked memory; pageable memory is staged through two pinned 64 MB
+ * buffers, host threads filling one while the other is DMA'd. */
+int pdot_h2d_matrix(double* dst_dev, int64_t ldd, const double* src_host, int64_t lds, int64_t m, int64_t n,
+                    int device);
 int pdot_fro_norm(const double* C_dev, int64_t m, int64_t n, int64_t ldc, double* out);
 
 /* ---- measurement helpers (bench.py) ---- */

@@ -37,7 +37,8 @@ EXPORTS = (
     "pdot_kernel_launches", "pdot_time_finalize", "pdot_shard_rows", "pdot_create_shard", "pdot_shard_info",
     "pdot_nccl_unique_id", "pdot_comm_init", "pdot_set_virtual", "pdot_shard_pass", "pdot_exchange_local",
     "pdot_sinkhorn_solve", "pdot_ipc_handle", "pdot_p2p_open", "pdot_p2p_link_local",
-    "pdot_set_screening", "pdot_screen_stats", "pdot_get_slot_sparse",
+    "pdot_set_screening", "pdot_screen_stats", "pdot_get_slot_sparse", "pdot_p2p_selftest",
+    "pdot_h2d_matrix",
 )
 
 
@@ -111,6 +112,7 @@ _SIGS = {
     "pdot_apply_At": ([_P, _P, _I64, _I64, _P, _I64], ctypes.c_int),
     "pdot_gen_cost": ([_P, _I64, _I64, _I64, ctypes.c_int, ctypes.POINTER(_I64)], ctypes.c_int),
     "pdot_fro_norm": ([_P, _I64, _I64, _I64, _DP], ctypes.c_int),
+    "pdot_h2d_matrix": ([_P, _I64, _P, _I64, _I64, _I64, ctypes.c_int], ctypes.c_int),
     "pdot_time_stream_kernel": ([_P, ctypes.c_int, _DP], ctypes.c_int),
     "pdot_kernel_launches": ([_P], _I64),
     "pdot_time_finalize": ([_P, ctypes.c_int, _DP], ctypes.c_int),
@@ -130,6 +132,8 @@ _SIGS = {
     "pdot_ipc_handle": ([_P, _P], ctypes.c_int),
     "pdot_p2p_open": ([_P, _P, ctypes.c_int], ctypes.c_int),
     "pdot_p2p_link_local": ([ctypes.POINTER(_P), ctypes.c_int], ctypes.c_int),
+    "pdot_p2p_selftest": ([ctypes.POINTER(_P), ctypes.c_int, ctypes.c_int, _D, ctypes.POINTER(ctypes.c_ulonglong)],
+                          ctypes.c_int),
     "pdot_set_screening": ([_P, ctypes.c_int], ctypes.c_int),
     "pdot_get_slot_sparse": ([_P, ctypes.c_int, _P, _I64, _P, _P, ctypes.POINTER(_I64)], ctypes.c_int),
     "pdot_screen_stats": ([_P, ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong)], ctypes.c_int),

@@ -102,6 +102,18 @@ __device__ __forceinline__ void store_group1(const Ctl& c, int64_t off, double v
     c.gbuf[off] = v;
   }
 }
+// K2a tail: after every group store of this rank (each block fenced at system
+// scope), release this exchange's sequence number into every rank's flag word
+// for this sender.  Called by one thread.
+__device__ __forceinline__ void publish_exchange(const Ctl& c) {
+  __threadfence_system();
+  const unsigned long long seq = (unsigned long long)xseq_next(c);
+  for (int r = 0; r < c.nranks; ++r)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(xflag(c, r, c.rank)), "l"(seq) : "memory");
+}
+// K2b tail: this exchange is consumed (the same count on every rank)
+__device__ __forceinline__ void consume_exchange(const Ctl& c) { *xcounter(c) += 1ull; }
+
 // K2b: wait until every rank has published this exchange (bounded spin)
 __device__ void wait_exchange(Ctl& c) {
   if (threadIdx.x == 0) {
@@ -600,12 +612,7 @@ __device__ void group_scalar_partials(Ctl& c) {
   }
   if (c.p2p) {  // publish after every block's stores (each fenced at system scope before its ticket)
     __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      const unsigned long long seq = (unsigned long long)xseq_next(c);
-      for (int r = 0; r < c.nranks; ++r)
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(xflag(c, r, c.rank)), "l"(seq) : "memory");
-    }
+    if (threadIdx.x == 0) publish_exchange(c);
   }
 }
 
@@ -1071,7 +1078,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
   uint64_t t_logic = 0;
   if (threadIdx.x == 0) {
     if (mode == FIN_B && cs.p2p) {
-      *xcounter(cs) += 1ull;  // this exchange is consumed (same count on every rank)
+      consume_exchange(cs);
       if (cs.xerror) fail(cs, E_EXCHANGE);
     }
     if (!cs.done && cs.unit) {
@@ -1129,7 +1136,70 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
   }
 }
 
+// Test hook for the peer-memory exchange protocol with R ranks emulated in ONE
+// cooperative launch (every block co-resident, so a spin can never wait on a
+// block that is not running; separate launches that wait on one another on one
+// GPU are not safe).  Block r plays rank r's pass sequence `rounds` times:
+// a rank-dependent delay, its group stores into EVERY rank's exchange buffer
+// (store_group1, the K2a path), publish_exchange, then wait_exchange on its
+// own flags (the K2b path), a check of all 8 groups' values in its own buffer,
+// and consume_exchange.  out[r] = {errors, max ns spent waiting, xerror}.
+__global__ void p2p_protocol_kernel(Ctl* ctls, int rounds, unsigned long long delay_ns,
+                                    unsigned long long* out) {
+  Ctl& c = ctls[blockIdx.x];
+  __shared__ unsigned long long waited_max;
+  __shared__ int errors;
+  if (threadIdx.x == 0) {
+    waited_max = 0ull;
+    errors = 0;
+  }
+  __syncthreads();
+  constexpr int kVals = 8;
+  for (int s = 0; s < rounds; ++s) {
+    const double seqv = (double)xseq_next(c);
+    // ranks reach their stores at different times: the others' waits really spin
+    if (threadIdx.x == 0) {
+      const unsigned long long t0 = globaltimer_ns();
+      const unsigned long long d = ((unsigned)(s + c.rank) % (unsigned)c.nranks) * delay_ns;
+      while (globaltimer_ns() - t0 < d) {
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < (c.g1 - c.g0) * kVals; e += blockDim.x) {
+      const int g = c.g0 + e / kVals, j = e % kVals;
+      store_group1(c, g * c.gstride + j, seqv * 1e6 + 1000.0 * g + j);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) publish_exchange(c);
+    const unsigned long long w0 = globaltimer_ns();
+    wait_exchange(c);  // ends with __syncthreads
+    if (threadIdx.x == 0) {
+      const unsigned long long w = globaltimer_ns() - w0;
+      if (w > waited_max) waited_max = w;
+    }
+    const double* buf = xgroups(c, c.rank);
+    for (int e = threadIdx.x; e < kGroups * kVals; e += blockDim.x) {
+      const int g = e / kVals, j = e % kVals;
+      if (__ldcv(buf + g * c.gstride + j) != seqv * 1e6 + 1000.0 * g + j) atomicAdd(&errors, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) consume_exchange(c);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[blockIdx.x * 3 + 0] = (unsigned long long)errors;
+    out[blockIdx.x * 3 + 1] = waited_max;
+    out[blockIdx.x * 3 + 2] = (unsigned long long)c.xerror;
+  }
+}
+
 }  // namespace
+
+int launch_p2p_protocol_test(Ctl* ctls_dev, int nranks, int rounds, unsigned long long delay_ns,
+                             unsigned long long* out_dev, cudaStream_t s) {
+  void* args[] = {&ctls_dev, &rounds, &delay_ns, &out_dev};
+  return (int)cudaLaunchCooperativeKernel((const void*)p2p_protocol_kernel, dim3(nranks), dim3(128), args, 0, s);
+}
 
 void launch_finalize_pass(Ctl* ctl_dev, const Ctl& h, int force_op, int mode, cudaStream_t s) {
   // + 1: the controller block (FIN_FUSED, FIN_B)

@@ -427,6 +427,9 @@ __device__ __forceinline__ void tl_end(unsigned long long* tl, int k) {
 void launch_stream_pass(const Ctl* ctl_dev, const Ctl& ctl_host, int force_op, cudaStream_t s);
 enum FinMode : int { FIN_FUSED = 0, FIN_A = 1, FIN_B = 2 };
 void launch_finalize_pass(Ctl* ctl_dev, const Ctl& ctl_host, int force_op, int mode, cudaStream_t s);
+// peer-exchange protocol self-test: nranks emulated ranks in one cooperative launch
+int launch_p2p_protocol_test(Ctl* ctls_dev, int nranks, int rounds, unsigned long long delay_ns,
+                             unsigned long long* out_dev, cudaStream_t s);
 size_t stream_smem_bytes(int64_t TM);
 void prepare_stream_kernel();
 // block-screened pass (screen.cu): K0 screen + K1 unit walker, or the generic

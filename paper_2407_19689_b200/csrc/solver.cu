@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <thread>
 #include <string>
 #include <vector>
@@ -1506,6 +1507,110 @@ int pdot_p2p_link_local(pdot_solver** hs, int count) {
     DeviceGuard dg(hs[i]->device);
     if (int rc = upload_ctl(hs[i])) return rc;
   }
+  return PDOT_OK;
+}
+
+// Peer-memory exchange protocol under genuinely concurrent ranks (test hook):
+// the linked handles' control blocks drive pdot::p2p_protocol_kernel, one block
+// per rank in a single cooperative launch.  out3r[3 r + {0,1,2}] = rank r's
+// value mismatches, longest wait (ns) and exchange-timeout flag.  Each
+// handle's exchange counter advances by `rounds`, as after that many passes.
+int pdot_p2p_selftest(pdot_solver** hs, int count, int rounds, double delay_us, unsigned long long* out3r) {
+  if (!hs || count < 2 || count > pdot::kMaxRanks || rounds < 1 || !out3r) return set_err(PDOT_EINVAL, "bad argument");
+  for (int i = 0; i < count; ++i)
+    if (!hs[i] || !hs[i]->host.p2p || hs[i]->nranks != count || hs[i]->rank != i || hs[i]->device != hs[0]->device)
+      return set_err(PDOT_EINVAL, "pdot_p2p_selftest: needs ranks 0..count-1 linked on one device");
+  DeviceGuard dg(hs[0]->device);
+  std::vector<Ctl> ctls(count);
+  for (int i = 0; i < count; ++i) ctls[i] = hs[i]->host;
+  Ctl* ctl_dev = nullptr;
+  unsigned long long* out_dev = nullptr;
+  CK(cudaMalloc(&ctl_dev, count * sizeof(Ctl)));
+  CK(cudaMalloc(&out_dev, 3 * count * sizeof(unsigned long long)));
+  cudaStream_t s = hs[0]->stream;
+  for (int i = 0; i < count; ++i) CK(cudaStreamSynchronize(hs[i]->stream));
+  CK(cudaMemcpyAsync(ctl_dev, ctls.data(), count * sizeof(Ctl), cudaMemcpyHostToDevice, s));
+  const cudaError_t le = (cudaError_t)pdot::launch_p2p_protocol_test(ctl_dev, count, rounds,
+                                                                     (unsigned long long)(delay_us * 1e3), out_dev, s);
+  if (le != cudaSuccess) {
+    cudaFree(ctl_dev);
+    cudaFree(out_dev);
+    return cuda_fail(le, "cooperative launch", __LINE__);
+  }
+  CK(cudaMemcpyAsync(out3r, out_dev, 3 * count * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cudaFree(ctl_dev);
+  cudaFree(out_dev);
+  return PDOT_OK;
+}
+
+// Host -> device copy of an m x n matrix into a device buffer (leading
+// dimension ldd).  Page-locked sources go by one direct DMA.  Pageable sources
+// (a plain numpy array, the reference's own input type) are staged through two
+// 64 MB pinned buffers: host threads copy chunk k+1 into one while the DMA of
+// chunk k drains the other, instead of the driver's single-threaded staging.
+int pdot_h2d_matrix(double* dst_dev, int64_t ldd, const double* src, int64_t lds, int64_t m, int64_t n,
+                    int device) {
+  if (!dst_dev || !src || m < 0 || n < 0 || ldd < n || lds < n) return set_err(PDOT_EINVAL, "bad argument");
+  if (m == 0 || n == 0) return PDOT_OK;
+  DeviceGuard dg(device);
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  static cudaStream_t st = nullptr;
+  static double* pin[2] = {nullptr, nullptr};
+  static cudaEvent_t ev[2] = {nullptr, nullptr};
+  static int st_device = -1;
+  constexpr size_t kChunk = (size_t)64 << 20;
+  if (st_device != device) {  // (re)create the staging resources on this device
+    if (st) {
+      for (int i = 0; i < 2; ++i) {
+        cudaFreeHost(pin[i]);
+        cudaEventDestroy(ev[i]);
+      }
+      cudaStreamDestroy(st);
+      st = nullptr;
+    }
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaHostAlloc(&pin[i], kChunk, cudaHostAllocDefault));
+      CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+    st_device = device;
+  }
+  if (!is_pageable_host(src)) {
+    CK(cudaMemcpy2DAsync(dst_dev, ldd * sizeof(double), src, lds * sizeof(double), n * sizeof(double), m,
+                         cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return PDOT_OK;
+  }
+  const int64_t row_bytes = n * (int64_t)sizeof(double);
+  if ((int64_t)kChunk < row_bytes) {  // rows wider than a staging buffer: the driver's path
+    CK(cudaMemcpy2DAsync(dst_dev, ldd * sizeof(double), src, lds * sizeof(double), n * sizeof(double), m,
+                         cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return PDOT_OK;
+  }
+  const int64_t rows_per = (int64_t)kChunk / row_bytes;
+  const int64_t nchunks = (m + rows_per - 1) / rows_per;
+  const unsigned nthreads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int b = (int)(k & 1);
+    const int64_t r0 = k * rows_per, rows = std::min(rows_per, m - r0);
+    if (k >= 2) CK(cudaEventSynchronize(ev[b]));  // the DMA that last read this buffer is done
+    char* dstb = reinterpret_cast<char*>(pin[b]);
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < nthreads; ++t) {
+      const int64_t a = rows * t / nthreads, e = rows * (t + 1) / nthreads;
+      pool.emplace_back([=]() {
+        for (int64_t r = a; r < e; ++r) memcpy(dstb + r * row_bytes, src + (r0 + r) * lds, (size_t)row_bytes);
+      });
+    }
+    for (auto& th : pool) th.join();
+    CK(cudaMemcpy2DAsync(dst_dev + r0 * ldd, ldd * sizeof(double), pin[b], (size_t)row_bytes, (size_t)row_bytes,
+                         (size_t)rows, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(ev[b], st));
+  }
+  CK(cudaStreamSynchronize(st));
   return PDOT_OK;
 }
 

@@ -30,18 +30,16 @@ def even(n: int) -> int:
 
 
 def _h2d_matrix(A: np.ndarray, device: int):
-    """Host -> HBM copy of the cost matrix.  non_blocking lets a page-locked
-    source go by direct DMA (~55 GB/s measured) instead of torch's staged path
-    (~11 GB/s); the stream is synchronised before the buffer is used."""
+    """Host -> HBM copy of the cost matrix through ``pdot_h2d_matrix``: one
+    direct DMA from page-locked memory, or, from pageable memory (a plain numpy
+    array), a pinned double buffer filled by host threads while the other half
+    is DMA'd (csrc/solver.cu).  Odd n gets a zero pad column (even ldc)."""
     A = np.ascontiguousarray(A, dtype=np.float64)
     m, n = A.shape
-    if n % 2 == 0:
-        t = torch.empty((m, n), dtype=torch.float64, device=f"cuda:{device}")
-        t.copy_(torch.from_numpy(A), non_blocking=True)
-    else:
-        t = torch.zeros((m, n + 1), dtype=torch.float64, device=f"cuda:{device}")
-        t[:, :n].copy_(torch.from_numpy(A), non_blocking=True)
-    torch.cuda.current_stream(device).synchronize()
+    t = (torch.empty((m, n), dtype=torch.float64, device=f"cuda:{device}") if n % 2 == 0
+         else torch.zeros((m, n + 1), dtype=torch.float64, device=f"cuda:{device}"))
+    torch.cuda.synchronize(device)
+    _lib.check(_lib.load().pdot_h2d_matrix(t.data_ptr(), t.stride(0), A.ctypes.data, n, m, n, device))
     return t
 
 

@@ -36,3 +36,32 @@ def test_virtual_shards_rectangular_limit():
     assert repv.iterations == rep1.iterations == 60
     assert np.array_equal(itv.X, it1.X)
     assert np.array_equal(itv.p, it1.p) and np.array_equal(itv.q, it1.q)
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+def test_p2p_protocol_concurrent_ranks(nranks):
+    """The peer-memory exchange with the ranks genuinely concurrent: R linked
+    shard handles' control blocks drive one COOPERATIVE launch, one block per
+    rank (co-residency guaranteed; separate launches that spin on each other on
+    one GPU are unsafe).  Each rank stores its groups into every rank's buffer,
+    releases its flag, acquire-spins on the others' flags, checks all 8 groups
+    and consumes the exchange, for 6 rounds (both parities) with rank-staggered
+    delays, so the spins really wait."""
+    import ctypes
+
+    from paper_2407_19689_b200 import _lib
+    from paper_2407_19689_b200.device import Handle
+    hs = [Handle(1024, 1024, 0, nranks, r) for r in range(nranks)]
+    arr = (ctypes.c_void_p * nranks)(*[h.ptr.value for h in hs])
+    _lib.check(hs[0].lib.pdot_p2p_link_local(arr, nranks))
+    out = (ctypes.c_ulonglong * (3 * nranks))()
+    delay_us = 200.0
+    _lib.check(hs[0].lib.pdot_p2p_selftest(arr, nranks, 6, delay_us, out))
+    errors = [out[3 * r] for r in range(nranks)]
+    waited = [out[3 * r + 1] / 1e3 for r in range(nranks)]
+    timeouts = [out[3 * r + 2] for r in range(nranks)]
+    print(f"R={nranks}: mismatches {errors}, longest wait per rank (us) {[round(w) for w in waited]}")
+    assert errors == [0] * nranks and timeouts == [0] * nranks
+    assert max(waited) >= 0.5 * delay_us  # a rank waited for a late peer
+    for h in hs:
+        h.close()
