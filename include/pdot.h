@@ -67,6 +67,11 @@ typedef struct {
   double omega0;
   int32_t trace_level; /* 0: restarts only, 1: + etas/bounds/candidates, 2: + rejections */
   int32_t poll_passes; /* passes per CUDA-graph batch (0: automatic) */
+  int32_t host_omega;  /* 1: the primal weight of an adaptive restart is evaluated on the host
+                          with libm exp/log, the functions math.exp / math.log call
+                          (pdhg.py:185): the device pauses at the restart, the host
+                          evaluates omega and the device resumes.  0: device exp/log. */
+  int32_t reserved;
 } pdot_config;
 
 typedef struct {

@@ -51,6 +51,7 @@ class Config(ctypes.Structure):
         ("adaptive", ctypes.c_int32), ("relative", ctypes.c_int32),
         ("eta0", ctypes.c_double), ("omega0", ctypes.c_double),
         ("trace_level", ctypes.c_int32), ("poll_passes", ctypes.c_int32),
+        ("host_omega", ctypes.c_int32), ("reserved", ctypes.c_int32),
     ]
 
 

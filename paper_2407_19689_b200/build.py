@@ -9,7 +9,8 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-OUT = PKG / "lib" / "libpdot.so"
+# PDOT_BUILD_OUT: build elsewhere (e.g. the PDOT_DEVICE_CHECKS variant next to the product library)
+OUT = Path(os.environ.get("PDOT_BUILD_OUT", PKG / "lib" / "libpdot.so"))
 SOURCES = ["stream.cu", "screen.cu", "finalize.cu", "solver.cu", "sinkhorn.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -34,7 +35,7 @@ def build_library(verbose: bool = False, force: bool = False) -> Path:
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libpdot.so")
-    log = PKG / "lib" / "ptxas.log"
+    log = OUT.parent / "ptxas.log"
     log.write_text(r.stdout + r.stderr)
     if verbose:
         sys.stdout.write(r.stderr)

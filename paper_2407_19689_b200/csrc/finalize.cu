@@ -900,8 +900,17 @@ __device__ void control_dist(Ctl& c, const Sums& S) {
   // pdhg.py:353-362 + primal_weight_update pdhg.py:174-186
   const double dX = sqrt(S.R[2]);
   const double dpq = sqrt(S.R[0] + S.K[0]);
-  if (dX > c.eps_zero && dpq > c.eps_zero)
+  if (dX > c.eps_zero && dpq > c.eps_zero) {
+    if (c.host_omega) {  // pause: the host evaluates omega with libm, then resume_restart
+      c.om_dX = dX;
+      c.om_dpq = dpq;
+      c.omega_wait = 1;
+      c.done = 1;
+      c.op = OP_NONE;
+      return;
+    }
     c.omega = exp(c.theta * log(dpq / dX) + (1.0 - c.theta) * log(c.omega));
+  }
   do_restart(c, c.sCand, c.cand_kkt);
   prepare_step(c);
 }
@@ -1102,6 +1111,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
         cs.status->reason = cs.reason;
         cs.status->error = cs.error;
         cs.status->done = cs.done;
+        cs.status->pause = cs.omega_wait;
       }
     }
   }
@@ -1193,7 +1203,27 @@ __global__ void p2p_protocol_kernel(Ctl* ctls, int rounds, unsigned long long de
   }
 }
 
+// The restart that control_dist paused for a host-evaluated omega: set omega,
+// then the same restart actions (one thread; the next graph batch continues).
+__global__ void resume_restart_kernel(Ctl* ctlp, double omega) {
+  Ctl& c = *ctlp;
+  c.omega = omega;
+  c.omega_wait = 0;
+  c.done = 0;
+  do_restart(c, c.sCand, c.cand_kkt);
+  prepare_step(c);
+  if (c.status) {
+    c.status->ring_head = c.ring_head;
+    c.status->pause = 0;
+    c.status->done = 0;
+  }
+}
+
 }  // namespace
+
+void launch_resume_restart(Ctl* ctl_dev, double omega, cudaStream_t s) {
+  resume_restart_kernel<<<1, 1, 0, s>>>(ctl_dev, omega);
+}
 
 int launch_p2p_protocol_test(Ctl* ctls_dev, int nranks, int rounds, unsigned long long delay_ns,
                              unsigned long long* out_dev, cudaStream_t s) {

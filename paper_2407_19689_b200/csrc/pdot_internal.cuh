@@ -104,6 +104,8 @@ struct Status {
   volatile int64_t outer;
   volatile int64_t passes;
   volatile int64_t ring_head;
+  volatile int32_t pause;   // the controller waits for the host (host-evaluated omega)
+  int32_t pad_;
 };
 
 struct Slot {
@@ -143,6 +145,9 @@ struct Ctl {
   int32_t unit_avg;        // unit STEP call that also updates a running average
   uint64_t deadline_ns;    // %globaltimer deadline (0 = none)
   int32_t stop_request;    // host may set to force a time-limit stop
+  int32_t host_omega;      // adaptive restarts pause for a host-evaluated omega (pdot_config.host_omega)
+  int32_t omega_wait;      // paused: om_dX / om_dpq hold the restart distances
+  double om_dX, om_dpq;
   // ---- step state ----
   double eta, omega, tau, sigma;
   double kd, rkd;            // lazy matrix average: k of the iterate being averaged, RN(1/k)
@@ -427,6 +432,8 @@ __device__ __forceinline__ void tl_end(unsigned long long* tl, int k) {
 void launch_stream_pass(const Ctl* ctl_dev, const Ctl& ctl_host, int force_op, cudaStream_t s);
 enum FinMode : int { FIN_FUSED = 0, FIN_A = 1, FIN_B = 2 };
 void launch_finalize_pass(Ctl* ctl_dev, const Ctl& ctl_host, int force_op, int mode, cudaStream_t s);
+// resume a restart paused for a host-evaluated primal weight
+void launch_resume_restart(Ctl* ctl_dev, double omega, cudaStream_t s);
 // peer-exchange protocol self-test: nranks emulated ranks in one cooperative launch
 int launch_p2p_protocol_test(Ctl* ctls_dev, int nranks, int rounds, unsigned long long delay_ns,
                              unsigned long long* out_dev, cudaStream_t s);

@@ -8,6 +8,8 @@
 // batches in flight), so no iteration waits on the host.
 #include <cuda_runtime.h>
 #include <math.h>
+
+#include <cmath>
 #include <stdio.h>
 #include <string.h>
 
@@ -436,6 +438,22 @@ int auto_batch(const pdot_solver* h) {
   return L;
 }
 
+// A restart paused for a host-evaluated primal weight (pdot_config.host_omega):
+// omega = exp(theta log(dpq / dX) + (1 - theta) log(omega)) with the host's libm,
+// the functions the reference's math.exp / math.log call (pdhg.py:185), same
+// operation order, no contraction; then the device applies the restart.
+int host_omega_resume(pdot_solver* h) {
+  CK(cudaStreamSynchronize(h->stream));
+  if (int rc = download_ctl(h)) return rc;
+  const Ctl& c = h->host;
+  const double omega = std::exp(c.theta * std::log(c.om_dpq / c.om_dX) + (1.0 - c.theta) * std::log(c.omega));
+  pdot::launch_resume_restart(h->dev, omega, h->stream);
+  h->launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(h->stream));
+  return download_ctl(h);
+}
+
 // replay the graph until the controller reports done
 int drive(pdot_solver* h, int L) {
   int rc = build_graph(h, L);
@@ -448,7 +466,13 @@ int drive(pdot_solver* h, int L) {
     if (i > 0) {
       CK(cudaEventSynchronize(h->ev[(i - 1) & 1]));
       drain_ring(h);
-      if (h->status_h->done) break;
+      if (h->status_h->done) {
+        if (!h->status_h->pause) break;
+        // the batch in flight exits at once (done); resume after the host's omega
+        if (int rc2 = host_omega_resume(h)) return rc2;
+        i = 0;
+        continue;
+      }
     }
     ++i;
   }
@@ -1022,6 +1046,8 @@ int pdot_begin(pdot_solver* h, const pdot_config* cfg, double elapsed_before_s) 
   c.adaptive = cfg->adaptive;
   c.relative = cfg->relative;
   c.trace_level = cfg->trace_level;
+  c.host_omega = cfg->host_omega;
+  c.omega_wait = 0;
   c.eta = cfg->eta0 > 0 ? cfg->eta0 : 1.0 / (2.0 * sqrt((double)(h->m_total + h->n)));  // pdhg.py:225-227
   c.omega = cfg->omega0;
   c.tau = c.sigma = c.kd = c.rkd = c.kd_dual = c.rkd_dual = 0.0;
@@ -1065,8 +1091,14 @@ int pdot_advance(pdot_solver* h, int64_t max_passes, pdot_progress* prog) {
   if (max_passes < 0) {
     if (int rc = drive(h, h->poll_L)) return rc;
   } else {
-    for (int64_t i = 0; i < max_passes; ++i)
+    for (int64_t i = 0; i < max_passes; ++i) {
       if (int rc = run_pass(h, -1)) return rc;
+      if (h->host.host_omega) {  // a pass may have paused for a host-evaluated omega
+        CK(cudaStreamSynchronize(h->stream));
+        if (h->status_h->pause)
+          if (int rc = host_omega_resume(h)) return rc;
+      }
+    }
     CK(cudaEventRecord(h->t1, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     drain_ring(h);

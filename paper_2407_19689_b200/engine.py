@@ -25,7 +25,8 @@ from .device import DeviceProblem, as_device_problem, detach_handle, get_handle
 from .records import Iterate, SolveReport
 
 
-def config_struct(config: SolverConfig, trace_level: int, poll_passes: int = 0) -> _lib.Config:
+def config_struct(config: SolverConfig, trace_level: int, poll_passes: int = 0,
+                  host_omega: bool = False) -> _lib.Config:
     c = _lib.Config()
     c.tol = config.tol
     c.time_limit_s = config.time_limit_s
@@ -43,6 +44,7 @@ def config_struct(config: SolverConfig, trace_level: int, poll_passes: int = 0) 
     c.omega0 = config.omega0
     c.trace_level = trace_level
     c.poll_passes = poll_passes
+    c.host_omega = 1 if host_omega else 0
     return c
 
 
@@ -143,7 +145,7 @@ def assemble_report(h, res, config: SolverConfig, trace: SolveTrace | None, roun
 
 def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = None,
           trace: SolveTrace | None = None, *, device: int = 0, return_device: bool = False,
-          poll_passes: int = 0, trace_snapshots: bool = True, handle=None):
+          poll_passes: int = 0, trace_snapshots: bool = True, handle=None, host_omega: bool = False):
     """Run restarted PDHG until the KKT tolerance, iteration or time limit.
 
     Same contract as the reference ``otsolve.solve`` (pdhg.py:254-265):
@@ -159,6 +161,11 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
     runs the batched graph loop instead of stepping pass by pass.  ``handle``
     runs the solve on a handle the caller owns (e.g. one returned by an
     earlier ``return_device`` solve) instead of the shared cache.
+    ``host_omega=True`` evaluates the primal weight of each adaptive restart on
+    the host with libm's exp / log -- the functions the reference's math.exp /
+    math.log call (pdhg.py:185) -- instead of CUDA's (which may differ by an
+    ulp); the device pauses at each such restart (one round trip).
+    GPU-only knobs stay out of SolverConfig so config_echo matches the reference.
     """
     t_start = time.perf_counter()
     phases = {}
@@ -179,7 +186,8 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
         h.set_slot(0, None, None, None)
     phases["setup_s"] = time.perf_counter() - t_start - phases["h2d_problem_s"]
     stepwise = trace is not None and (trace_snapshots or trace.record_inner)
-    cfg = config_struct(config, trace_level=2 if trace is not None else 0, poll_passes=poll_passes)
+    cfg = config_struct(config, trace_level=2 if trace is not None else 0, poll_passes=poll_passes,
+                        host_omega=host_omega)
     # dense output plans are pre-faulted during the solve; a screened handle copies
     # only the occupied cells into a zero-filled array (Handle.get_slot)
     out = _Prefault((dp.m, dp.n)) if (not return_device and dp.m * dp.n >= (1 << 22)

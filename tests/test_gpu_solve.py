@@ -79,14 +79,15 @@ def test_solve_deterministic_bitwise(pd):
     assert r1.to_json() == r2.to_json()
 
 
-@pytest.mark.parametrize("screen", [False, True])
-def test_c1_seed0_matches_reference_report(pd, screen):
+@pytest.mark.parametrize("screen,host_omega", [(False, False), (True, False), (False, True)])
+def test_c1_seed0_matches_reference_report(pd, screen, host_omega):
     """C1 (1024^2, tol 1e-4, seed 0): the reference's drift envelope is exact
     (334 iterations / 21 restarts under every summation order), and
     the GPU reproduces that trajectory: identical iteration and restart counts
     and restart lengths, the traced scalars agree to 1e-10 over the whole solve,
     and both objectives to 1e-12 relative.  Both walkers (the default dense
-    walker at this size, and the screened walker forced on)."""
+    walker at this size, and the screened walker forced on), and with the
+    primal weight of each restart evaluated by the host's libm (host_omega)."""
     from p2_util import decision_horizon, horizon
     from paper_2407_19689_b200 import instances as inst
     from paper_2407_19689_b200.device import set_screening
@@ -96,14 +97,16 @@ def test_c1_seed0_matches_reference_report(pd, screen):
     set_screening(screen)
     try:
         tr = pd.SolveTrace()
-        it, rep = pd.solve(prob, pd.SolverConfig(tol=1e-4, deterministic=True), trace=tr, trace_snapshots=False)
+        it, rep = pd.solve(prob, pd.SolverConfig(tol=1e-4, deterministic=True), trace=tr, trace_snapshots=False,
+                           host_omega=host_omega)
     finally:
         set_screening(None)
     ref = gold["report"]
     h, why, worst = horizon(tr, rep.restart_lengths, gold["trace"], ref["restart_lengths"], rtol=1e-10)
     dh, dwhy, dworst = decision_horizon(tr, rep.restart_lengths, gold["trace"], ref["restart_lengths"])
     pre = float(np.vdot(prob.C, it.X))
-    print(f"GPU C1 seed0 (screen={screen}): {rep.iterations} it / {rep.restarts} rs, ref {ref['iterations']} / "
+    om = max(abs(a - b) / b for a, b in zip(tr.omegas, gold["trace"]["omegas"]))
+    print(f"GPU C1 seed0 (screen={screen}, host_omega={host_omega}): omega max rel diff {om:.1e}; {rep.iterations} it / {rep.restarts} rs, ref {ref['iterations']} / "
           f"{ref['restarts']}; 1e-10 horizon {h} ({why}, worst {worst:.1e}); decisions identical for "
           f"{dh} iterations (worst scalar rel diff {dworst:.1e}); rounded rel "
           f"{abs(rep.rounded_objective - ref['rounded_objective']) / ref['rounded_objective']:.1e}, pre rel "
