@@ -202,6 +202,8 @@ int pdot_set_virtual(pdot_solver* h, int on);
 int pdot_ipc_handle(pdot_solver* h, void* out64);
 int pdot_p2p_open(pdot_solver* h, const void* handles64, int count);
 int pdot_p2p_link_local(pdot_solver** hs, int count);
+/* device time (ms) of the last pdot_shard_pass call of phase 0 (K0/K1/K1b/K2a) and 1 (K2b) */
+int pdot_shard_pass_ms(const pdot_solver* h, double* ms2);
 /* Test hook: the peer-exchange protocol (group stores into every rank's buffer,
  * st.release of the sequence flags, ld.acquire spin, parity double buffering)
  * with `count` linked ranks emulated as the blocks of ONE cooperative launch,

@@ -38,7 +38,7 @@ EXPORTS = (
     "pdot_nccl_unique_id", "pdot_comm_init", "pdot_set_virtual", "pdot_shard_pass", "pdot_exchange_local",
     "pdot_sinkhorn_solve", "pdot_ipc_handle", "pdot_p2p_open", "pdot_p2p_link_local",
     "pdot_set_screening", "pdot_screen_stats", "pdot_get_slot_sparse", "pdot_p2p_selftest",
-    "pdot_h2d_matrix",
+    "pdot_h2d_matrix", "pdot_shard_pass_ms",
 )
 
 
@@ -113,6 +113,7 @@ _SIGS = {
     "pdot_apply_At": ([_P, _P, _I64, _I64, _P, _I64], ctypes.c_int),
     "pdot_gen_cost": ([_P, _I64, _I64, _I64, ctypes.c_int, ctypes.POINTER(_I64)], ctypes.c_int),
     "pdot_fro_norm": ([_P, _I64, _I64, _I64, _DP], ctypes.c_int),
+    "pdot_shard_pass_ms": ([_P, _DP], ctypes.c_int),
     "pdot_h2d_matrix": ([_P, _I64, _P, _I64, _I64, _I64, ctypes.c_int], ctypes.c_int),
     "pdot_time_stream_kernel": ([_P, ctypes.c_int, _DP], ctypes.c_int),
     "pdot_kernel_launches": ([_P], _I64),

@@ -816,6 +816,7 @@ int pdot_destroy(pdot_solver* h) {
     if (e) cudaEventDestroy(e);
   if (h->t0) cudaEventDestroy(h->t0);
   if (h->t1) cudaEventDestroy(h->t1);
+  if (h->ph0) cudaEventDestroy(h->ph0);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return PDOT_OK;
@@ -1419,6 +1420,8 @@ int pdot_set_virtual(pdot_solver* h, int on) {
 int pdot_shard_pass(pdot_solver* h, int phase, pdot_progress* prog) {
   if (!h || h->nranks == 1) return set_err(PDOT_EINVAL, "pdot_shard_pass needs a sharded handle");
   DeviceGuard dg(h->device);
+  if (!h->ph0) CK(cudaEventCreate(&h->ph0));
+  CK(cudaEventRecord(h->ph0, h->stream));
   if (phase == 0) {
     h->launches += launch_k1(h, -1);
     pdot::launch_finalize_pass(h->dev, h->host, -1, pdot::FIN_A, h->stream);
@@ -1430,6 +1433,7 @@ int pdot_shard_pass(pdot_solver* h, int phase, pdot_progress* prog) {
   CK(cudaGetLastError());
   CK(cudaEventRecord(h->t1, h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  CK(cudaEventElapsedTime(&h->phase_ms[phase ? 1 : 0], h->ph0, h->t1));
   drain_ring(h);
   if (prog) {
     if (int rc = download_ctl(h)) return rc;
@@ -1446,6 +1450,16 @@ int pdot_shard_pass(pdot_solver* h, int phase, pdot_progress* prog) {
     prog->avg_written = c.avg_written;
     prog->avg_slot = c.avg_slot;
   }
+  return PDOT_OK;
+}
+
+// Device time (CUDA events) of the last pdot_shard_pass call of each phase:
+// phase 0 = this shard's K0 / K1 / K1b / K2a, phase 1 = its K2b (combine +
+// controller).  Per-shard latency model of a row-sharded pass.
+int pdot_shard_pass_ms(const pdot_solver* h, double* ms2) {
+  if (!h || !ms2) return set_err(PDOT_EINVAL, "null argument");
+  ms2[0] = h->phase_ms[0];
+  ms2[1] = h->phase_ms[1];
   return PDOT_OK;
 }
 

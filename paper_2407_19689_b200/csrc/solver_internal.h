@@ -31,6 +31,8 @@ struct pdot_solver {
   int graph_L = 0;
   cudaEvent_t ev[2] = {nullptr, nullptr};
   cudaEvent_t t0 = nullptr, t1 = nullptr;
+  cudaEvent_t ph0 = nullptr;              // start of the last pdot_shard_pass call (per-phase timing)
+  float phase_ms[2] = {0.f, 0.f};         // device time of the last pdot_shard_pass call of each phase
   int64_t launches = 0;
   bool problem_set = false;
   std::chrono::steady_clock::time_point wall0;
