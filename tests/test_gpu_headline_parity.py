@@ -210,6 +210,8 @@ def test_p3_c2_envelope():
     runs = [fx] + [json.loads((GOLD / f"headline_c2_{v}.json").read_text())
                    for v in ("ld", "rev") if (GOLD / f"headline_c2_{v}.json").exists()]
     runs = [r for r in runs if r["complete"]]
+    if len(runs) < 3:
+        pytest.skip("the C2 drift-envelope reference runs (long double / reversed apply_A) are not complete")
     its = [r["report"]["iterations"] for r in runs]
     pre = [r["pre_rounding_objective"] for r in runs]
     dp = _device_problem(pd, fx)
