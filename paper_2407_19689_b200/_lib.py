@@ -149,7 +149,7 @@ def load(path: Path | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path is not None else Path(os.environ.get("PDOT_LIB_PATH", LIB_PATH))
+    p = Path(path) if path is not None else Path(os.environ.get("PDOT_LIB_PATH") or LIB_PATH)
     if not p.exists():
         raise RuntimeError(
             f"libpdot.so not found at {p}: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

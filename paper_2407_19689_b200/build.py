@@ -30,6 +30,7 @@ def build_library(verbose: bool = False, force: bool = False) -> Path:
         return OUT
     OUT.parent.mkdir(parents=True, exist_ok=True)
     extra = ["-DPDOT_DEVICE_CHECKS"] if os.environ.get("PDOT_DEVICE_CHECKS") == "1" else []
+    extra += os.environ.get("PDOT_NVCC_EXTRA", "").split()  # A/B variants (measurement tooling)
     cmd = [NVCC, *FLAGS, *extra, *map(str, srcs), "-o", str(OUT)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -1020,6 +1020,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
   if (has_ctl && blockIdx.x == 0) {
     if (timed && threadIdx.x == 0) c.sstat[ST_K2_T0] = globaltimer_ns();
     if (timed) tl_start(c.ktl, 3);
+#ifndef PDOT_K2_NO_DRYRUN
     if (op == OP_STEP && !c.unit) {
       __shared__ Ctl dry;
       unsigned long long* dw = reinterpret_cast<unsigned long long*>(&dry);
@@ -1035,6 +1036,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
       if (threadIdx.x == 0) control_step(dry, S, pre);
       __syncthreads();
     }
+#endif
     wait_tickets(c, nwork);
   } else {
     const int wb = (int)blockIdx.x - has_ctl;  // work block index

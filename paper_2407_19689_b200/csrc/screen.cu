@@ -291,13 +291,44 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
 // the lane-sequential row chain (passed from row group to row group) and the
 // 8-lane butterfly.
 // ---------------------------------------------------------------------------
+// K1's fixed geometry (set once per handle) travels as a KERNEL PARAMETER: its
+// fields sit in the constant bank and feed instructions directly, instead of
+// being reloaded from the control block in global memory for every cell (the
+// 128-register budget does not keep them all live).  KGeo exposes the same
+// member names as Ctl, so the cell functions are templates over the context
+// type; the per-pass output slots come from the control block (dyn).  ldc is
+// fixed while the problem is bound: pdot_set_problem drops the captured graph
+// when it changes.
+struct KGeo {
+  int64_t m, n, ldx, ldc, mpad, nbands, nstrips, ncells, ncp, T, U;
+  int64_t occ_stride, tiles;  // nbands * nstrips, T * U
+  int32_t nbt, cbits, nbt_log2, pad_;
+  uint32_t* occ;
+  uint8_t* tocc;
+  double* ccol;
+  double* crow;
+  double* cscal;
+  uint32_t* ulist;
+  uint8_t* uflag;
+  unsigned int* ucount;
+  // K1b (tile_kernel): the bit maps, tile list and per-tile partials it writes
+  int64_t TM;
+  const uint32_t* bcr;
+  const uint32_t* bct;
+  const int32_t* tlist;
+  const unsigned int* tcount;
+  double* colpart;
+  double* rowpart;
+  double* tilescal;
+};
 struct CellGeo {
   int64_t band, cell, strip, i0, j;
   int rows, k, rg, cp;
   bool v0, v1;
 };
 
-__device__ __forceinline__ CellGeo cell_geo(const Ctl& c, uint32_t entry) {
+template <class Cx>
+__device__ __forceinline__ CellGeo cell_geo(const Cx& c, uint32_t entry) {
   const int lane = threadIdx.x & 31;
   CellGeo g;
   g.band = entry_band(entry, c.cbits);
@@ -335,8 +366,8 @@ __device__ __forceinline__ double* warp_red_buf() {
   return red_buf + (threadIdx.x >> 5) * kRedWarpDoubles;
 }
 
-template <int NQ, int NS>
-__device__ __forceinline__ void cell_flush(const Ctl& c, const CellGeo& g, const double (&o)[2][NQ][2],
+template <int NQ, int NS, class Cx>
+__device__ __forceinline__ void cell_flush(const Cx& c, const CellGeo& g, const double (&o)[2][NQ][2],
                                           const double (&sacc)[NS]) {
   static_assert(2 * NQ <= 8 && NS <= 8, "per-warp transpose buffer");
   const int lane = threadIdx.x & 31;
@@ -429,8 +460,8 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // issue the copies of one cell's inputs (zero-filled where not needed)
-template <bool IMPLICIT, bool AVG>
-__device__ __forceinline__ void cell_issue(const StepOp& op, const Ctl& c, uint32_t entry, uint32_t f,
+template <bool IMPLICIT, bool AVG, class Cx>
+__device__ __forceinline__ void cell_issue(const StepOp& op, const Cx& c, uint32_t entry, uint32_t f,
                                            unsigned char* stage) {
   const int lane = threadIdx.x & 31;
   const CellGeo g = cell_geo(c, entry);
@@ -460,8 +491,9 @@ __device__ __forceinline__ void cell_issue(const StepOp& op, const Ctl& c, uint3
   cp_async8(f16 + 7 * 512 + 8, op.qa + j1, okc && g.v1);
 }
 
-template <bool IMPLICIT, bool AVG>
-__device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const CostGen& gen, uint32_t entry, uint32_t f,
+template <bool IMPLICIT, bool AVG, class Cx>
+__device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const Ctl& dyn, const CostGen& gen,
+                                          uint32_t entry, uint32_t f,
                                           const unsigned char* stage, unsigned long long& bytes,
                                           unsigned long long& cells) {
   constexpr int NQ = StepOp::NQ, NS = StepOp::NS;
@@ -541,15 +573,15 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const 
   // occupancy bytes of the cell in the two output slots
   const bool anyx = __any_sync(0xffffffffu, nzx), anya = __any_sync(0xffffffffu, nza);
   if (lane == 0) {
-    const int64_t sstride = c.nbands * c.nstrips;
-    uint8_t* ox = reinterpret_cast<uint8_t*>(c.occ + c.sXn * sstride + g.band * c.nstrips + g.strip);
+    const int sXn = dyn.sXn, sA = dyn.sA;
+    uint8_t* ox = reinterpret_cast<uint8_t*>(c.occ + sXn * c.occ_stride + g.band * c.nstrips + g.strip);
     ox[g.k] = anyx ? 1 : 0;
-    const int64_t tiles = c.T * c.U, tile = (g.band >> (__ffs(c.nbt) - 1)) * c.U + g.strip / kWarps;  // nbt: a power of two
-    if (anyx) c.tocc[c.sXn * tiles + tile] = 1;
+    const int64_t tile = (g.band >> c.nbt_log2) * c.U + g.strip / kWarps;  // nbt: a power of two
+    if (anyx) c.tocc[sXn * c.tiles + tile] = 1;
     if (AVG) {
-      uint8_t* oa = reinterpret_cast<uint8_t*>(c.occ + c.sA * sstride + g.band * c.nstrips + g.strip);
+      uint8_t* oa = reinterpret_cast<uint8_t*>(c.occ + sA * c.occ_stride + g.band * c.nstrips + g.strip);
       oa[g.k] = anya ? 1 : 0;
-      if (anya) c.tocc[c.sA * tiles + tile] = 1;
+      if (anya) c.tocc[sA * c.tiles + tile] = 1;
     }
   }
   if (act) {
@@ -560,8 +592,8 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Ctl& c, const 
 
 // the warp's STEP cells k = k0, k0 + nw, ...: copies of cell k + nw in flight
 // while cell k is computed
-template <bool IMPLICIT, bool AVG>
-__device__ __forceinline__ void step_cells(const StepOp& o, const Ctl& c, const CostGen& gen, unsigned k0,
+template <bool IMPLICIT, bool AVG, class Cx>
+__device__ __forceinline__ void step_cells(const StepOp& o, const Cx& c, const Ctl& dyn, const CostGen& gen, unsigned k0,
                                            unsigned nw, const unsigned* ncells_p, unsigned char* stages,
                                            unsigned long long& bytes, unsigned long long& cells) {
   // this warp's first two list entries are read before the list length is known
@@ -584,7 +616,7 @@ __device__ __forceinline__ void step_cells(const StepOp& o, const Ctl& c, const 
     if (more) cell_issue<IMPLICIT, AVG>(o, c, e_nx, f_nx, stages + (st ^ 1) * kStageBytes);
     cp_async_commit();
     cp_async_wait<1>();  // this cell's copies have landed
-    cell_step<IMPLICIT, AVG>(o, c, gen, e_cur, f_cur, stages + st * kStageBytes, bytes, cells);
+    cell_step<IMPLICIT, AVG>(o, c, dyn, gen, e_cur, f_cur, stages + st * kStageBytes, bytes, cells);
     e_cur = e_nx; f_cur = f_nx;
     e_nx = e_n2; f_nx = f_n2;
     st ^= 1;
@@ -641,7 +673,8 @@ __device__ __forceinline__ void cell_one(const Op& op, const Ctl& c, uint32_t en
   cell_flush<NQ, NS>(c, cg, o, sacc);
 }
 
-__global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const Ctl* __restrict__ ctlp, int force_op) {
+__global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const Ctl* __restrict__ ctlp, int force_op,
+                                                                          const KGeo geo) {
   const Ctl& c = *ctlp;
   if (c.done || !c.screen) return;
   const int op = force_op >= 0 ? force_op : c.op;
@@ -663,11 +696,11 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
     extern __shared__ __align__(16) unsigned char unit_dyn[];
     unsigned char* stages = unit_dyn + warp * kStages * kStageBytes;
     if (o.C) {
-      if (o.with_avg) step_cells<false, true>(o, c, gen, gw, nw, c.ucount, stages, bytes, cells);
-      else step_cells<false, false>(o, c, gen, gw, nw, c.ucount, stages, bytes, cells);
+      if (o.with_avg) step_cells<false, true>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells);
+      else step_cells<false, false>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells);
     } else {
-      if (o.with_avg) step_cells<true, true>(o, c, gen, gw, nw, c.ucount, stages, bytes, cells);
-      else step_cells<true, false>(o, c, gen, gw, nw, c.ucount, stages, bytes, cells);
+      if (o.with_avg) step_cells<true, true>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells);
+      else step_cells<true, false>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells);
     }
   } else if (op == OP_DIST) {
     DiffOp o;
@@ -728,8 +761,8 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
 //   scalars: thread (strip, scalar), band-ordered sum of strip-band values,
 //            then the strips in order.
 // ---------------------------------------------------------------------------
-template <int NQ, int NS>
-__device__ __forceinline__ void assemble_tile(const Ctl& c, int64_t tu, int64_t tt, double* sm, int part) {
+template <int NQ, int NS, class Cx>
+__device__ __forceinline__ void assemble_tile(const Cx& c, int64_t tu, int64_t tt, double* sm, int part) {
   const int th = threadIdx.x;
   const int64_t b0 = tt * c.nbt;
   if (part < 0 || part == 0) {  // columns
@@ -853,17 +886,18 @@ __device__ __forceinline__ void assemble_tile(const Ctl& c, int64_t tu, int64_t 
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 4) tile_kernel(const Ctl* __restrict__ ctlp, int force_op) {
+__global__ void __launch_bounds__(kThreads, 4) tile_kernel(const Ctl* __restrict__ ctlp, int force_op,
+                                                            const KGeo c) {
   __shared__ double sm[32 * 8 * 8];  // [band][strip][scalar] strip-band values
-  const Ctl& c = *ctlp;
-  if (c.done || !c.screen) return;
-  const int op = force_op >= 0 ? force_op : c.op;
-  if (!unit_pass(c, op)) return;
+  const Ctl& dyn = *ctlp;
+  if (dyn.done || !dyn.screen) return;
+  const int op = force_op >= 0 ? force_op : dyn.op;
+  if (!unit_pass(dyn, op)) return;
   // the first item's tile is read before the list length is known (the grid
   // has at most 3 T U blocks, so blockIdx.x / 3 is inside the list buffer)
   int32_t tile_nx = __ldcg(c.tlist + blockIdx.x / 3u);
   const unsigned ntiles = __ldcg(c.tcount);
-  unsigned long long* tl = op == OP_STEP ? c.ktl : nullptr;
+  unsigned long long* tl = op == OP_STEP ? dyn.ktl : nullptr;
   tl_start(tl, 2);
   // work item k = (listed tile k / 3, part k % 3): the column, row and scalar
   // sums of one tile run in three CTAs side by side
@@ -1092,8 +1126,12 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
     }
     // every warp reads list entries gw and gw + nw up front: 2 nw <= kListPad
     const unsigned g1 = (unsigned)imin64((int64_t)sms * kSparseCtasPerSm, kListPad / (2 * kWarps));
-    unit_kernel<<<g1, kThreads, kUnitDynSmem, s>>>(ctl_dev, force_op);
-    tile_kernel<<<(unsigned)imin64(h.T * h.U * 3, (int64_t)sms * 4), kThreads, 0, s>>>(ctl_dev, force_op);
+    const KGeo geo{h.m, h.n, h.ldx, h.ldc, h.mpad, h.nbands, h.nstrips, h.ncells, h.ncp, h.T, h.U,
+                   h.nbands * h.nstrips, h.T * h.U, h.nbt, h.cbits, __builtin_ctz((unsigned)h.nbt), 0,
+                   h.occ, h.tocc, h.ccol, h.crow, h.cscal, h.ulist, h.uflag, h.ucount,
+                   h.TM, h.bcr, h.bct, h.tlist, h.tcount, h.colpart, h.rowpart, h.tilescal};
+    unit_kernel<<<g1, kThreads, kUnitDynSmem, s>>>(ctl_dev, force_op, geo);
+    tile_kernel<<<(unsigned)imin64(h.T * h.U * 3, (int64_t)sms * 4), kThreads, 0, s>>>(ctl_dev, force_op, geo);
   } else {
     const unsigned grid = (unsigned)imin64(h.T * h.U, (int64_t)sms * 2);
     generic_kernel<<<grid, kThreads, generic_smem_bytes(h.TM), s>>>(ctl_dev, force_op);

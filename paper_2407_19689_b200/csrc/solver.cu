@@ -837,6 +837,10 @@ int pdot_set_problem(pdot_solver* h, const double* C_dev, int64_t ldc, const dou
   if (!h || !C_dev || !f_dev || !g_dev) return set_err(PDOT_EINVAL, "null argument");
   if (int rc = check_ld(ldc, h->n, "C")) return rc;
   if (((uintptr_t)C_dev & 15) != 0) return set_err(PDOT_EINVAL, "C must be 16-byte aligned");
+  if (h->graph && h->host.ldc != ldc) {  // K1 takes ldc as a captured kernel parameter
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
   h->host.C = C_dev;
   h->host.ldc = ldc;
   h->host.cost_kind = pdot::COST_EXPLICIT;
@@ -859,6 +863,10 @@ int pdot_set_problem_implicit(pdot_solver* h, int kind, const int64_t* a, const 
     if (a[0] * a[1] != m_total || a[2] * a[3] != n) return set_err(PDOT_EINVAL, "rect cost shape mismatch");
   } else {
     return set_err(PDOT_EINVAL, "unknown cost kind");
+  }
+  if (h->graph && h->host.ldc != h->ldx) {  // K1 takes ldc as a captured kernel parameter
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
   }
   h->host.C = nullptr;
   h->host.ldc = h->ldx;

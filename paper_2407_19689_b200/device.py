@@ -29,15 +29,18 @@ def even(n: int) -> int:
     return n + (n & 1)
 
 
-def _h2d_matrix(A: np.ndarray, device: int):
+def _h2d_matrix(A: np.ndarray, device: int, out=None):
     """Host -> HBM copy of the cost matrix through ``pdot_h2d_matrix``: one
     direct DMA from page-locked memory, or, from pageable memory (a plain numpy
     array), a pinned double buffer filled by host threads while the other half
     is DMA'd (csrc/solver.cu).  Odd n gets a zero pad column (even ldc)."""
     A = np.ascontiguousarray(A, dtype=np.float64)
     m, n = A.shape
-    t = (torch.empty((m, n), dtype=torch.float64, device=f"cuda:{device}") if n % 2 == 0
-         else torch.zeros((m, n + 1), dtype=torch.float64, device=f"cuda:{device}"))
+    if out is not None and tuple(out.shape) == (m, even(n)):
+        t = out  # a buffer the caller owns (the handle's cost buffer): no 2 GB allocation per call
+    else:
+        t = (torch.empty((m, n), dtype=torch.float64, device=f"cuda:{device}") if n % 2 == 0
+             else torch.zeros((m, n + 1), dtype=torch.float64, device=f"cuda:{device}"))
     torch.cuda.synchronize(device)
     _lib.check(_lib.load().pdot_h2d_matrix(t.data_ptr(), t.stride(0), A.ctypes.data, n, m, n, device))
     return t
@@ -75,10 +78,12 @@ class DeviceProblem:
         return self.C_t is None
 
     @classmethod
-    def from_host(cls, prob, device: int = 0) -> "DeviceProblem":
+    def from_host(cls, prob, device: int = 0, out=None) -> "DeviceProblem":
+        """Upload a host problem; ``out`` (an (m, even n) float64 CUDA tensor) receives C
+        instead of a fresh allocation."""
         require_cuda(device)
         C = np.asarray(prob.C, dtype=np.float64)
-        return cls(_h2d_matrix(C, device), _h2d_vector(prob.f, device), _h2d_vector(prob.g, device),
+        return cls(_h2d_matrix(C, device, out), _h2d_vector(prob.f, device), _h2d_vector(prob.g, device),
                    C.shape[0], C.shape[1], prob.cost_fro_norm, prob.marginal_norm, device, host=prob)
 
     @classmethod
@@ -142,10 +147,13 @@ class DeviceProblem:
         return dp
 
 
-def as_device_problem(prob, device: int = 0) -> DeviceProblem:
+def as_device_problem(prob, device: int = 0, handle=None) -> DeviceProblem:
+    """A host problem goes to HBM; with a handle, into that handle's reusable cost
+    buffer (repeated solve() calls of one shape then allocate nothing)."""
     if isinstance(prob, DeviceProblem):
         return prob
-    return DeviceProblem.from_host(prob, device)
+    out = handle.cost_buffer() if handle is not None else None
+    return DeviceProblem.from_host(prob, device, out=out)
 
 
 def zeros_plan(shape):
@@ -250,6 +258,13 @@ class Handle:
         if keep and torch is not None:
             torch.cuda.synchronize(self.device)
         _lib.check(self.lib.pdot_set_slot(self.ptr, slot, Xp, ld if Xp else self.n, pp, qp))
+
+    def cost_buffer(self):
+        """The handle's own (m, even n) device buffer for uploaded cost matrices."""
+        if getattr(self, "_cbuf", None) is None:
+            z = torch.empty if self.n % 2 == 0 else torch.zeros
+            self._cbuf = z((self.m, even(self.n)), dtype=torch.float64, device=f"cuda:{self.device}")
+        return self._cbuf
 
     def screened(self) -> bool:
         return self.screen_stats()["screen_on"] == 1

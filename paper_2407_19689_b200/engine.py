@@ -171,14 +171,17 @@ def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = No
     phases = {}
     if config is None:
         config = SolverConfig()
-    dp = as_device_problem(prob, device)
-    phases["h2d_problem_s"] = time.perf_counter() - t_start
     if handle is not None:
-        if (handle.m, handle.n, handle.device) != (dp.m, dp.n, dp.device):
-            raise ValueError("handle shape / device does not match the problem")
         h = handle
+    elif isinstance(prob, DeviceProblem):
+        h = get_handle(prob.m, prob.n, prob.device)
     else:
-        h = get_handle(dp.m, dp.n, dp.device)
+        m, n = np.shape(prob.C)
+        h = get_handle(m, n, device)
+    dp = as_device_problem(prob, device, handle=h)
+    if (h.m, h.n, h.device) != (dp.m, dp.n, dp.device):
+        raise ValueError("handle shape / device does not match the problem")
+    phases["h2d_problem_s"] = time.perf_counter() - t_start
     h.bind(dp)
     if initial is not None:
         h.set_slot(0, initial.X, initial.p, initial.q)
