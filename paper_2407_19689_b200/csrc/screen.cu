@@ -915,14 +915,38 @@ __global__ void __launch_bounds__(kThreads, 4) tile_kernel(const Ctl* __restrict
 
 // the unit calls the screen does not cover (KKT of a unit call, DIFF, ROUND):
 // the generic walker over every tile, per-tile partials
+// A tile whose plan entries are all +0.0 in the slot being rounded: the
+// row / column sums of the rounding stages 0-2 (rs_i * X, (rs_i * X) * cs_j)
+// are exact +0 there, so its partials are written as the zeros the walker
+// would produce, without reading the 512 KB of X.  (Stage 3 adds the rank-one
+// correction err_r err_c^T / total, which is dense, and reads C: never skipped.)
+__device__ __forceinline__ void zero_round_tile(const Ctl& c, int64_t tu, int64_t tt) {
+  const int64_t i0 = tt * c.TM, rows = imin64(c.TM, c.m - i0);
+  const int64_t col0 = tu * kTileN, cols = imin64(kTileN, c.n - col0);
+  for (int64_t j = 2 * threadIdx.x; j < cols; j += 2 * blockDim.x)
+    *reinterpret_cast<double2*>(c.colpart + tt * c.ldx + col0 + j) = make_double2(0.0, 0.0);
+  for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) c.rowpart[tu * c.m + i0 + r] = 0.0;
+  if (threadIdx.x == 0) {
+    c.tilescal[(tt * c.U + tu) * kMaxNS] = 0.0;
+    if (c.tileflag) c.tileflag[tt * c.U + tu] = 1;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1) generic_kernel(const Ctl* __restrict__ ctlp, int force_op) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* smem = reinterpret_cast<double*>(smem_raw);
   const Ctl& c = *ctlp;
   if (c.done) return;
   const int op = force_op >= 0 ? force_op : c.op;
-  for (int64_t t = blockIdx.x; t < c.T * c.U; t += gridDim.x) {
-    generic_tile(op, c, smem, t % c.U, t / c.U);
+  // rounding stages 0-2 on a screened handle: tiles without occupied cells are +0
+  const bool skip_empty = op == OP_ROUND && c.round_stage <= 2 && c.screen && c.tocc != nullptr;
+  const int64_t tiles = c.T * c.U;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    if (skip_empty && __ldcg(c.tocc + (int64_t)c.sX * tiles + t) == 0) {
+      zero_round_tile(c, t % c.U, t / c.U);
+    } else {
+      generic_tile(op, c, smem, t % c.U, t / c.U);
+    }
     __syncthreads();
   }
 }

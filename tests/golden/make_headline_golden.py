@@ -152,13 +152,17 @@ def run(name):
         for k in TRACE_KEYS:
             setattr(trace, k, _Stream(k, fh, t0))
         trace.restart_points = _Discard()
-        it, rep = ot.solve(prob, ot.SolverConfig(tol=case["tol"], deterministic=True), trace=trace)
+        # no wall-clock limit: C3 takes ~17 s per iteration here (SolverConfig's default
+        # time_limit_s = 3600 would stop it after ~210 iterations)
+        it, rep = ot.solve(prob, ot.SolverConfig(tol=case["tol"], deterministic=True, time_limit_s=1e9),
+                           trace=trace)
         wall = time.perf_counter() - t0
         rows, cols = np.nonzero(it.X)
         np.savez_compressed(HERE / f"headline_{name}.npz", rows=rows.astype(np.int32),
                             cols=cols.astype(np.int32), vals=it.X[rows, cols], p=it.p, q=it.q)
         out = dict(case=case, m=prob.m, n=prob.n, cost_fro_norm=prob.cost_fro_norm,
-                   marginal_norm=prob.marginal_norm, complete=True,
+                   marginal_norm=prob.marginal_norm, complete=rep.termination_reason == "tolerance",
+                   iterations_recorded=rep.iterations, restart_lengths=list(rep.restart_lengths),
                    omp_num_threads=os.environ.get("OMP_NUM_THREADS"),
                    report=json.loads(rep.to_json()),
                    pre_rounding_objective=float(np.vdot(prob.C, it.X)),
