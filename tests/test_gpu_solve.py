@@ -121,3 +121,18 @@ def test_c1_seed0_matches_reference_report(pd, screen, host_omega):
     assert pre == pytest.approx(gold["pre_rounding_objective"], rel=1e-12)
     # 7.3e-13 on the default path; the host-omega variant runs a rounding-level different path (1.4e-12)
     assert rep.rounded_objective == pytest.approx(ref["rounded_objective"], rel=5e-12 if host_omega else 1e-12)
+
+
+def test_device_result_survives_a_later_solve(pd):
+    """A return_device result owns its handle: a later solve of the same
+    shape gets another handle and cannot overwrite the returned slot."""
+    from paper_2407_19689_b200 import instances as inst
+    prob = inst.sqeuclid_problem(8, 1)
+    (slot, h), rep = pd.solve_device(pd.DeviceProblem.from_host(prob), pd.SolverConfig(tol=1e-6))
+    X1, p1, q1 = h.get_slot(slot)
+    other = inst.sqeuclid_problem(8, 2)  # same shape, different instance
+    (slot2, h2), _ = pd.solve_device(pd.DeviceProblem.from_host(other), pd.SolverConfig(tol=1e-6))
+    _, _ = pd.solve(other, pd.SolverConfig(tol=1e-6))
+    assert h2 is not h
+    X1b, p1b, q1b = h.get_slot(slot)
+    assert np.array_equal(X1, X1b) and np.array_equal(p1, p1b) and np.array_equal(q1, q1b)
