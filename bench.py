@@ -83,7 +83,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-i", str(index),
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("PDOT_SMI_MS", "200")], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
         self.first = ""
@@ -379,6 +379,10 @@ def main():
             "k0_metadata_bytes_per_pass": st["k0_bytes"] / st["passes"],
             "k2_us_to_last_block": st["k2_main_ns"] / st["passes"] / 1e3,
             "k2_controller_us": st["k2_ctl_ns"] / st["passes"] / 1e3,
+            "k2_end_to_next_k0_us": st["gap_k2_k0_ns"] / st["passes"] / 1e3,
+            "k2_end_to_next_k0_entry_us": st["gap_k2_k0_entry_ns"] / st["passes"] / 1e3,
+            "k0_start_to_k1_start_us": st["k0_to_k1_ns"] / st["passes"] / 1e3,
+            "k1_end_to_k2_start_us": st["k1_to_k2_ns"] / st["passes"] / 1e3,
             "pass_us_mean": pass_us,
             "k1_share_of_pass": 1e3 * k1_ms / pass_us,
             "note": "8x16 cells of the plan whose every output and reduction term is provably +0 are skipped "

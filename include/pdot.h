@@ -264,7 +264,7 @@ int pdot_set_screening(pdot_solver* h, int on);
  * cells visited, bytes moved by K1, K0 metadata bytes, summed K1 ns
  * (%globaltimer), screening on, cells per plan, summed K2 ns up to the last
  * block, summed K2 controller-tail ns, controller reduce / decide / publish ns}. */
-int pdot_screen_stats(pdot_solver* h, int reset, unsigned long long* out16);
+int pdot_screen_stats(pdot_solver* h, int reset, unsigned long long* out20);
 
 #ifdef __cplusplus
 }

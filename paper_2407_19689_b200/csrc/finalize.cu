@@ -1018,7 +1018,11 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
   const int has_ctl = mode == FIN_A ? 0 : 1;
   const unsigned nwork = gridDim.x - has_ctl;
   if (has_ctl && blockIdx.x == 0) {
-    if (timed && threadIdx.x == 0) c.sstat[ST_K2_T0] = globaltimer_ns();
+    if (timed && threadIdx.x == 0) {
+      const unsigned long long t0 = globaltimer_ns(), k1e = c.sstat[ST_K1_END];
+      c.sstat[ST_K2_T0] = t0;
+      if (k1e != 0 && t0 > k1e) c.sstat[ST_K1K2] += t0 - k1e;
+    }
     if (timed) tl_start(c.ktl, 3);
 #ifndef PDOT_K2_NO_DRYRUN
     if (op == OP_STEP && !c.unit) {
@@ -1103,8 +1107,17 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
       }
       if (timed) t_logic = globaltimer_ns();
       // publish to the host mirror (read by the host only after the pass's
-      // completion event, which orders these mapped-memory writes)
-      if (cs.status) {
+      // completion event, which orders these mapped-memory writes).  Stores to
+      // host memory hold the kernel's completion for a PCIe round trip, so an
+      // untraced solve publishes only every 16th pass and whenever the host must
+      // act (done, a paused restart); the host polls at graph-batch boundaries and
+      // drains the event ring completely once done.
+#ifndef PDOT_STATUS_EVERY_PASS
+      const bool publish = cs.done || cs.omega_wait || cs.trace_level > 0 || (cs.passes & 15) == 0;
+#else
+      const bool publish = true;
+#endif
+      if (cs.status && publish) {
         cs.status->total = cs.total;
         cs.status->outer = cs.outer;
         cs.status->passes = cs.passes;
@@ -1144,6 +1157,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
       cs.sstat[ST_T0K0] += t_red - t_last;     // controller: reduction of the block partials
       cs.sstat[ST_T1K0] += t_logic - t_red;    // controller: decisions
       cs.sstat[ST_DONE0] += t_end - t_logic;   // controller: status mirror + control-block write-back
+      cs.sstat[ST_K2_END] = globaltimer_ns();
     }
   }
 }

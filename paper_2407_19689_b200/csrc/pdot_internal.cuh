@@ -57,7 +57,15 @@ enum ScreenStat : int {
   ST_K2_T0 = 13,    // K2 of screened STEP passes: start stamp (block 0),
   ST_K2_MAIN = 14,  // summed time from start to the last block's ticket,
   ST_K2_CTL = 15,   // summed time of the controller tail (last block)
-  ST_COUNT = 16,
+  ST_K0_START = 16, // scratch: K0 start (block 0) of the running screened STEP pass
+  ST_K1_END = 17,   // scratch: K1 end (last CTA) of the running pass
+  ST_K2_END = 18,   // scratch: end of the last K2 (controller write-back done)
+  ST_GAP_K2K0 = 19, // summed: previous K2 end -> K0 start (launch gap between passes)
+  ST_K0K1 = 20,     // summed: K0 start -> K1 start (K0 + one launch gap)
+  ST_K1K2 = 21,     // summed: K1 end -> K2 start (K1b + two launch gaps)
+  ST_K0_ENTRY = 22, // scratch: K0 block 0's first instruction (before it reads the control block)
+  ST_GAP_LAUNCH = 23,  // summed: previous K2 end -> K0 entry (the part of the gap before K0 runs)
+  ST_COUNT = 24,
 };
 
 enum Op : int {

@@ -81,7 +81,9 @@ __device__ __forceinline__ bool step_with_avg(const Ctl& c) { return c.unit ? c.
 constexpr int kScreenWarps = 8;
 constexpr int kScreenCtasPerSm = 2;  // 128 registers; 3 or 4 per SM spill and run slower (C3 11.4k -> 11.3k / 10.7k iter/s)
 
-__global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_kernel(const Ctl* __restrict__ ctlp, int force_op) {
+__global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_kernel(const Ctl* __restrict__ ctlp, int force_op,
+                                                                                     unsigned long long* sstat0) {
+  if (sstat0 && blockIdx.x == 0 && threadIdx.x == 0) sstat0[ST_K0_ENTRY] = globaltimer_ns();
   __shared__ Ctl ctl_s;  // the control block, one round trip for all fields
   ctl_to_shared(ctlp, &ctl_s);
   const Ctl& c = ctl_s;
@@ -90,6 +92,16 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
   if (!unit_pass(c, op)) return;
   unsigned long long* tl = op == OP_STEP ? c.ktl : nullptr;
   tl_start(tl, 0);
+  if (op == OP_STEP && !c.unit && c.sstat && blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer_ns(), k2e = c.sstat[ST_K2_END];
+    c.sstat[ST_K0_START] = t0;
+    if (k2e != 0 && t0 > k2e) {
+      c.sstat[ST_GAP_K2K0] += t0 - k2e;
+      const unsigned long long ke = c.sstat[ST_K0_ENTRY];
+      if (ke > k2e) c.sstat[ST_GAP_LAUNCH] += ke - k2e;
+    }
+    c.sstat[ST_K2_END] = 0;  // only a STEP pass right after a STEP pass counts a gap
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t tiles = c.T * c.U;
   // persistent: one wave of CTAs, each warp walks tiles warp, warp + nw, ...
@@ -680,7 +692,14 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
   const int op = force_op >= 0 ? force_op : c.op;
   if (!unit_pass(c, op)) return;
   __shared__ unsigned long long red[2][kWarps];
-  if (blockIdx.x == 0 && threadIdx.x == 0) c.sstat[ST_T0] = globaltimer_ns();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer_ns();
+    c.sstat[ST_T0] = t0;
+    if (op == OP_STEP && !c.unit) {
+      const unsigned long long k0s = c.sstat[ST_K0_START];
+      if (k0s != 0 && t0 > k0s) c.sstat[ST_K0K1] += t0 - k0s;
+    }
+  }
   unsigned long long* tl = op == OP_STEP ? c.ktl : nullptr;
   tl_start(tl, 1);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -737,6 +756,7 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
       const unsigned long long t1 = globaltimer_ns();
       if (op == OP_STEP) {
         c.sstat[ST_K1_NS] += t1 - __ldcg(&c.sstat[ST_T0]);
+        c.sstat[ST_K1_END] = t1;
         c.sstat[ST_TILES] += ncells;
         c.sstat[ST_PASSES] += 1;
         // K0 tile-level screen of this pass: 32 cell + nbt band maxima (current and
@@ -1143,7 +1163,7 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
     // test hook: PDOT_K0_BLOCKS caps K0's grid (read per launch), so that small
     // problems run the persistent tile walk with many tiles per warp
     if (const char* e = getenv("PDOT_K0_BLOCKS")) g0 = (unsigned)imin64(g0, imax64(1, atoi(e)));
-    screen_kernel<<<g0, 32 * kScreenWarps, 0, s>>>(ctl_dev, force_op);  // warp per tile, persistent
+    screen_kernel<<<g0, 32 * kScreenWarps, 0, s>>>(ctl_dev, force_op, h.sstat);  // warp per tile, persistent
     if (getenv("PDOT_DEBUG_SYNC")) {
       const cudaError_t e = cudaStreamSynchronize(s);
       if (e != cudaSuccess) fprintf(stderr, "screen_kernel failed: %s\n", cudaGetErrorString(e));

@@ -1084,6 +1084,8 @@ int pdot_begin(pdot_solver* h, const pdot_config* cfg, double elapsed_before_s) 
   h->ring_tail = 0;
   h->events.clear();
   if (int rc = upload_ctl(h)) return rc;
+  if (c.sstat)  // the pass-gap statistics start over: no gap across the host's work between solves
+    CK(cudaMemsetAsync(c.sstat + pdot::ST_K2_END, 0, sizeof(unsigned long long), h->stream));
   if (remaining > 0.0 && remaining < 1e9) {
     stamp_deadline_kernel<<<1, 1, 0, h->stream>>>(h->dev, (uint64_t)(remaining * 1e9));
     h->launches += 1;
@@ -1720,7 +1722,12 @@ int pdot_screen_stats(pdot_solver* h, int reset, unsigned long long* out12) {
   out12[10] = st[pdot::ST_T0K0];
   out12[11] = st[pdot::ST_T1K0];
   out12[12] = st[pdot::ST_DONE0];
+  out12[13] = st[pdot::ST_GAP_K2K0];
+  out12[14] = st[pdot::ST_K0K1];
+  out12[15] = st[pdot::ST_K1K2];
+  out12[16] = st[pdot::ST_GAP_LAUNCH];
   if (reset) {
+    CK(cudaMemset(h->host.sstat + pdot::ST_K0_START, 0, 8 * sizeof(unsigned long long)));
     CK(cudaMemset(h->host.sstat, 0, 7 * sizeof(unsigned long long)));
     CK(cudaMemset(h->host.sstat + pdot::ST_K2_MAIN, 0, 2 * sizeof(unsigned long long)));
     CK(cudaMemset(h->host.sstat + pdot::ST_T0K0, 0, 3 * sizeof(unsigned long long)));

@@ -226,10 +226,11 @@ class Handle:
         self.screen = bool(on)
 
     def screen_stats(self, reset: bool = False) -> dict:
-        out = (ctypes.c_ulonglong * 16)()
+        out = (ctypes.c_ulonglong * 20)()
         _lib.check(self.lib.pdot_screen_stats(self.ptr, 1 if reset else 0, out))
         keys = ("passes", "active_cells", "cells_visited", "k1_bytes", "k0_bytes", "k1_ns", "screen_on",
-                "cells_per_plan", "k2_main_ns", "k2_ctl_ns", "ctl_reduce_ns", "ctl_logic_ns", "ctl_publish_ns")
+                "cells_per_plan", "k2_main_ns", "k2_ctl_ns", "ctl_reduce_ns", "ctl_logic_ns", "ctl_publish_ns",
+                "gap_k2_k0_ns", "k0_to_k1_ns", "k1_to_k2_ns", "gap_k2_k0_entry_ns")
         return dict(zip(keys, (int(v) for v in out)))
 
     def set_slot(self, slot: int, X=None, p=None, q=None) -> None:
