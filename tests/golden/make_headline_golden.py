@@ -6,6 +6,7 @@ benchmark instances and records its full trajectory:
     c2    m=n=4096  (64x64 grid) sq-Euclidean whitenoise seed 0, tol 1e-6
     c3    m=n=16384 (128x128 grid), tol 1e-4            (~20 s / iteration here)
     c4a   512 x 2048 analogue of C4 (L1 rect, sparse marginals) seed 0, tol 1e-4
+    c4    C4 itself, 8192 x 32768 (~20 s / iteration here: the first iterations)
     c1s1, c1s2   C1 seeds 1 and 2 (1024^2, tol 1e-4) with traces
 
     OPENBLAS_NUM_THREADS=1 OMP_NUM_THREADS=1 python tests/golden/make_headline_golden.py c2
@@ -52,6 +53,7 @@ CASES = {
     "c2": dict(kind="sqeuclid", r=64, seed=0, tol=1e-6),
     "c3": dict(kind="sqeuclid", r=128, seed=0, tol=1e-4),
     "c4a": dict(kind="rect", src=(16, 32), dst=(32, 64), seed=0, tol=1e-4),
+    "c4": dict(kind="rect", src=(64, 128), dst=(128, 256), seed=0, tol=1e-4),
     "c1s1": dict(kind="sqeuclid", r=32, seed=1, tol=1e-4),
     "c1s2": dict(kind="sqeuclid", r=32, seed=2, tol=1e-4),
 }

@@ -143,6 +143,7 @@ P2_CASES = {  # fixture -> iterations that must agree to 1e-10
     "c2": 50,
     "c4a": 50,
     "c3": 50,
+    "c4": 50,
 }
 
 
