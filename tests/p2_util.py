@@ -107,15 +107,11 @@ def margins(events, config):
     out = []
     epoch = prev = None
     cur = {}
-    k = 0
-    total = 0
     for typ, ia, x, y, z in events:
         if typ == 1:  # START
             epoch = prev = x
         elif typ == 2:  # ACCEPT
             cur = {"accept": (y - x) / x if ia and math.isfinite(y) else math.inf}
-            total += 1
-            k += 1
         elif typ == 3:  # CAND: x cand, y current, z average
             cur["cand_choice"] = abs(y - z) / max(abs(y), abs(z), 1e-300)
             th = [abs(x - config.beta_sufficient * epoch) / x, abs(x - config.beta_necessary * epoch) / x]
@@ -127,7 +123,6 @@ def margins(events, config):
             out.append(cur)
         elif typ == 4:  # RESTART
             epoch = prev = x
-            k = 0
     return out
 
 
