@@ -8,6 +8,7 @@ benchmark instances and records its full trajectory:
     c4a   512 x 2048 analogue of C4 (L1 rect, sparse marginals) seed 0, tol 1e-4
     c4    C4 itself, 8192 x 32768 (~20 s / iteration here: the first iterations)
     c1s1, c1s2   C1 seeds 1 and 2 (1024^2, tol 1e-4) with traces
+    c1p4, c2p4   C1 / C2 to tol 1e-8 (the converged objective)
 
     OPENBLAS_NUM_THREADS=1 OMP_NUM_THREADS=1 python tests/golden/make_headline_golden.py c2
 
@@ -54,6 +55,8 @@ CASES = {
     "c3": dict(kind="sqeuclid", r=128, seed=0, tol=1e-4),
     "c4a": dict(kind="rect", src=(16, 32), dst=(32, 64), seed=0, tol=1e-4),
     "c4": dict(kind="rect", src=(64, 128), dst=(128, 256), seed=0, tol=1e-4),
+    "c1p4": dict(kind="sqeuclid", r=32, seed=0, tol=1e-8),
+    "c2p4": dict(kind="sqeuclid", r=64, seed=0, tol=1e-8),
     "c1s1": dict(kind="sqeuclid", r=32, seed=1, tol=1e-4),
     "c1s2": dict(kind="sqeuclid", r=32, seed=2, tol=1e-4),
 }
