@@ -22,6 +22,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges for Nsight Systems / ncu --nvtx
+
 #include "../../include/pdot.h"
 #include "pdot_internal.cuh"
 
@@ -454,8 +456,15 @@ int host_omega_resume(pdot_solver* h) {
   return download_ctl(h);
 }
 
+// NVTX range for the lifetime of a scope (no-op unless a tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 // replay the graph until the controller reports done
 int drive(pdot_solver* h, int L) {
+  NvtxRange nv("pdot: solve loop (graph replays)");
   int rc = build_graph(h, L);
   if (rc) return rc;
   int64_t i = 0;
@@ -937,6 +946,7 @@ int pdot_get_slot(pdot_solver* h, int slot, double* X_any, int64_t ldX, double* 
 // double buffer and scattered by host threads while the next chunk moves.
 int pdot_get_slot_sparse(pdot_solver* h, int slot, double* X_host, int64_t ldX, double* p_any, double* q_any,
                          int64_t* cells_out) {
+  NvtxRange nv("pdot: sparse device->host plan copy");
   if (!h || slot < 0 || slot >= pdot::kNSlot || !X_host) return set_err(PDOT_EINVAL, "bad argument");
   if (ldX < h->n) return set_err(PDOT_EINVAL, "X: leading dimension must be >= n");
   if (!h->host.screen) return set_err(PDOT_ESTATE, "sparse copy needs a screened handle (occupancy maintained)");
@@ -1026,6 +1036,7 @@ int pdot_slot_ptrs(pdot_solver* h, int slot, double** X, double** p, double** q)
 }
 
 int pdot_begin(pdot_solver* h, const pdot_config* cfg, double elapsed_before_s) {
+  NvtxRange nv("pdot: begin (start KKT setup)");
   if (!h || !cfg) return set_err(PDOT_EINVAL, "null argument");
   if (!h->problem_set) return set_err(PDOT_ESTATE, "pdot_set_problem was not called");
   // pdhg.py:61-75
@@ -1178,6 +1189,7 @@ int64_t pdot_get_events(pdot_solver* h, pdot_event* out, int64_t cap) {
 }
 
 int pdot_round(pdot_solver* h, int slot, double* Xf_any, int64_t ldX, double* out3) {
+  NvtxRange nv("pdot: rounding");
   if (!h || slot < 0 || slot >= pdot::kNSlot) return set_err(PDOT_EINVAL, "bad handle or slot");
   if (!h->problem_set) return set_err(PDOT_ESTATE, "pdot_set_problem was not called");
   DeviceGuard dg(h->device);
@@ -1607,6 +1619,7 @@ int pdot_p2p_selftest(pdot_solver** hs, int count, int rounds, double delay_us, 
 // chunk k drains the other, instead of the driver's single-threaded staging.
 int pdot_h2d_matrix(double* dst_dev, int64_t ldd, const double* src, int64_t lds, int64_t m, int64_t n,
                     int device) {
+  NvtxRange nv("pdot: host->device cost matrix");
   if (!dst_dev || !src || m < 0 || n < 0 || ldd < n || lds < n) return set_err(PDOT_EINVAL, "bad argument");
   if (m == 0 || n == 0) return PDOT_OK;
   DeviceGuard dg(device);

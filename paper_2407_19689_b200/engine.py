@@ -144,8 +144,25 @@ def assemble_report(h, res, config: SolverConfig, trace: SolveTrace | None, roun
 
 
 def solve(prob, config: SolverConfig | None = None, initial: Iterate | None = None,
-          trace: SolveTrace | None = None, *, device: int = 0, return_device: bool = False,
-          poll_passes: int = 0, trace_snapshots: bool = True, handle=None, host_omega: bool = False):
+          trace: SolveTrace | None = None, **kw):
+    """Restarted PDHG to the KKT tolerance, iteration or time limit (pdhg.py:254-399);
+    see ``_solve`` for the GPU-only keyword options.  The call is one NVTX range
+    ("pdot.solve"); libpdot adds ranges for the upload, the loop, rounding and the
+    plan copy, so an Nsight timeline shows the phases of every call."""
+    from .device import torch
+    nvtx = torch.cuda.nvtx if torch is not None else None
+    if nvtx is not None:
+        nvtx.range_push("pdot.solve")
+    try:
+        return _solve(prob, config, initial, trace, **kw)
+    finally:
+        if nvtx is not None:
+            nvtx.range_pop()
+
+
+def _solve(prob, config: SolverConfig | None = None, initial: Iterate | None = None,
+           trace: SolveTrace | None = None, *, device: int = 0, return_device: bool = False,
+           poll_passes: int = 0, trace_snapshots: bool = True, handle=None, host_omega: bool = False):
     """Run restarted PDHG until the KKT tolerance, iteration or time limit.
 
     Same contract as the reference ``otsolve.solve`` (pdhg.py:254-265):
