@@ -57,10 +57,12 @@ def test_struct_layouts_match_ctypes(tmp_path):
         '#include <stdio.h>\n#include <stddef.h>\n#include "pdot.h"\n'
         'int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(pdot_config), sizeof(pdot_result),'
         ' sizeof(pdot_event), sizeof(pdot_progress), offsetof(pdot_config, eta0), offsetof(pdot_result, device_s));'
+        'printf("%zu\n", offsetof(pdot_config, host_omega));'
         'return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
     got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()))
     want = [ctypes.sizeof(_lib.Config), ctypes.sizeof(_lib.Result), ctypes.sizeof(_lib.Event),
-            ctypes.sizeof(_lib.Progress), _lib.Config.eta0.offset, _lib.Result.device_s.offset]
+            ctypes.sizeof(_lib.Progress), _lib.Config.eta0.offset, _lib.Result.device_s.offset,
+            _lib.Config.host_omega.offset]
     assert got == want
