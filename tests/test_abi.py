@@ -57,7 +57,7 @@ def test_struct_layouts_match_ctypes(tmp_path):
         '#include <stdio.h>\n#include <stddef.h>\n#include "pdot.h"\n'
         'int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(pdot_config), sizeof(pdot_result),'
         ' sizeof(pdot_event), sizeof(pdot_progress), offsetof(pdot_config, eta0), offsetof(pdot_result, device_s));'
-        'printf("%zu\n", offsetof(pdot_config, host_omega));'
+        'printf("%zu\\n", offsetof(pdot_config, host_omega));'
         'return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
