@@ -12,6 +12,7 @@
 // groups, summed sequentially inside a group and pairwise across groups.  A
 // row-sharded multi-GPU run owning whole groups reproduces the same tree.
 #include <math.h>
+#include <stdio.h>
 
 #include "pdot_internal.cuh"
 
@@ -793,9 +794,11 @@ struct Pre {
 
 __device__ double kkt_metric(const Ctl& c, double psq, double dsq, double pobj, double dobj, double* rel);
 
-__device__ __noinline__ void precompute_step(const Ctl& c, const Sums& S, Pre* P) {
+// t_cur: the thread that evaluates the current iterate's metric (0; the dry
+// run moves it off thread 0, which runs the decision code meanwhile)
+__device__ __noinline__ void precompute_step(const Ctl& c, const Sums& S, Pre* P, int t_cur = 0) {
   const int tid = threadIdx.x;
-  if (tid == 0 && c.pending)
+  if (tid == t_cur && c.pending)
     P->kc = kkt_metric(c, c.pend_psq_cur, S.R[11], c.pend_pobj_cur, c.pend_dobj_cur, &P->rel_cur);
   if (tid == 32 && c.pending) P->ka = kkt_metric(c, S.R[3] + S.K[3], S.R[12], S.R[9], c.pend_dobj_avg, &P->rel_avg);
   if (tid == 64 && c.adaptive) {
@@ -989,7 +992,21 @@ __device__ __forceinline__ void wait_tickets(const Ctl& c, unsigned nwork) {
 // blocks run it executes the decision code once on a scratch copy of the
 // control block (so the instructions are in this SM's instruction cache and
 // the real run does not fetch them from DRAM), then waits for every ticket.
+// PDOT_K2_PROF (measurement builds only): K2 phase times of screened STEP
+// passes, summed over a solve and printed by the controller at pass 600.
+// [0..3] work blocks: entry -> Ctl copied, -> work done, -> ticket, count;
+// [4..8] controller: entry -> copied, -> dry run done, -> tickets seen, -> reduced, -> end;
+// [9] max work-block ticket time after the controller's entry
+#ifdef PDOT_K2_PROF
+__device__ unsigned long long g_k2prof[16];
+__device__ unsigned long long g_k2entry;  // controller entry of the running pass
+#endif
+
 __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restrict__ ctlp, int force_op, int mode) {
+#ifdef PDOT_K2_PROF
+  const unsigned long long tq0 = globaltimer_ns();
+  unsigned long long tq1 = 0, tq2 = 0, tq3 = 0;
+#endif
   __shared__ double smem[kWarps * 4 * kColsPerBlock + 64];
   __shared__ Sums S;
   __shared__ int is_last;
@@ -1017,13 +1034,20 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
   const bool timed = op == OP_STEP && unit_pass(c, op) && c.sstat;  // K2 timing of screened STEP passes
   const int has_ctl = mode == FIN_A ? 0 : 1;
   const unsigned nwork = gridDim.x - has_ctl;
+#ifdef PDOT_K2_PROF
+  tq1 = globaltimer_ns();
+  if (timed && has_ctl && blockIdx.x == 0 && threadIdx.x == 0) g_k2entry = tq0;
+#endif
   if (has_ctl && blockIdx.x == 0) {
-    if (timed && threadIdx.x == 0) {
-      const unsigned long long t0 = globaltimer_ns(), k1e = c.sstat[ST_K1_END];
-      c.sstat[ST_K2_T0] = t0;
-      if (k1e != 0 && t0 > k1e) c.sstat[ST_K1K2] += t0 - k1e;
+    // pass statistics by the last thread (its load of the K1 end stamp is used
+    // only after the dry run: thread 0 starts the dry run without waiting)
+    unsigned long long k2_t0 = 0, k1e = 0;
+    if (timed && threadIdx.x == kRedThreads - 1) {
+      k2_t0 = globaltimer_ns();
+      k1e = __ldcg(&c.sstat[ST_K1_END]);
+      c.sstat[ST_K2_T0] = k2_t0;
     }
-    if (timed) tl_start(c.ktl, 3);
+    if (timed && c.ktl && threadIdx.x == kRedThreads - 1) atomicMin(c.ktl + 6, k2_t0);
 #ifndef PDOT_K2_NO_DRYRUN
     if (op == OP_STEP && !c.unit) {
       __shared__ Ctl dry;
@@ -1034,14 +1058,51 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
         dry.ring = nullptr;
         dry.status = nullptr;
       }
+#ifdef PDOT_K2_PROF
+      const unsigned long long td0 = globaltimer_ns();
+#endif
+#ifndef PDOT_K2_DRY_NORED
       reduce_blocks(dry, &S, smem, mode);  // partials still being written: values unused
-      precompute_step(dry, S, &pre);
+#endif
+#ifdef PDOT_K2_PROF
+      const unsigned long long td1 = globaltimer_ns();
+#endif
+#ifdef PDOT_K2_PROF
+      const unsigned long long td2 = globaltimer_ns();
+#endif
+      // the decision code and the four metric pieces warm the instruction cache
+      // side by side (different warps); the decision runs on metrics that take
+      // the common path (candidate kept, no restart, step accepted and grown)
+      __shared__ Pre pre_dry;
+      if (threadIdx.x == 0) {
+        Pre pd;
+        pd.kc = pd.ka = dry.epoch_kkt;
+        pd.rel_cur = pd.rel_avg = dry.best_rel;
+        pd.bound = 2.0 * dry.eta;
+        pd.nrm = 1.0;
+        control_step(dry, S, pd);
+      } else {
+        precompute_step(dry, S, &pre_dry, 128);
+      }
       __syncthreads();
-      if (threadIdx.x == 0) control_step(dry, S, pre);
-      __syncthreads();
+#ifdef PDOT_K2_PROF
+      if (timed && threadIdx.x == 0) {
+        g_k2prof[12] += td1 - td0;
+        g_k2prof[13] += td2 - td1;
+        g_k2prof[14] += globaltimer_ns() - td2;
+        g_k2prof[15] += td0 - tq0;
+      }
+#endif
     }
 #endif
+#ifdef PDOT_K2_PROF
+    tq2 = globaltimer_ns();
+#endif
+    if (timed && threadIdx.x == kRedThreads - 1 && k1e != 0 && k2_t0 > k1e) c.sstat[ST_K1K2] += k2_t0 - k1e;
     wait_tickets(c, nwork);
+#ifdef PDOT_K2_PROF
+    tq3 = globaltimer_ns();
+#endif
   } else {
     const int wb = (int)blockIdx.x - has_ctl;  // work block index
     if (timed && c.kdbg && threadIdx.x == 0) c.kdbg[wb * 4 + 0] = globaltimer_ns();
@@ -1065,8 +1126,22 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
     __syncthreads();
     if (mode != FIN_A) {
       if (threadIdx.x == 0) {
+#ifdef PDOT_K2_PROF
+        const unsigned long long tw = globaltimer_ns();
+#endif
         atomicAdd(c.counter, 1u);
         if (timed && c.kdbg) c.kdbg[wb * 4 + 2] = globaltimer_ns();
+#ifdef PDOT_K2_PROF
+        if (timed) {
+          const unsigned long long tt = globaltimer_ns();
+          atomicAdd(&g_k2prof[0], tq1 - tq0);
+          atomicAdd(&g_k2prof[1], tw - tq0);
+          atomicAdd(&g_k2prof[2], tt - tq0);
+          atomicAdd(&g_k2prof[3], 1ull);
+          const unsigned long long ce = *(volatile unsigned long long*)&g_k2entry;
+          if (tt > ce) atomicMax(&g_k2prof[9], tt - ce);
+        }
+#endif
       }
       return;
     }
@@ -1150,6 +1225,29 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
         tl[2 * k + 1] = 0ull;
       }
     }
+#ifdef PDOT_K2_PROF
+    if (timed) {
+      const unsigned long long te = globaltimer_ns();
+      g_k2prof[4] += tq1 - tq0;
+      g_k2prof[5] += tq2 - tq0;
+      g_k2prof[6] += tq3 - tq0;
+      g_k2prof[7] += t_red - tq0;
+      g_k2prof[8] += te - tq0;
+      g_k2prof[10] += g_k2prof[9];
+      g_k2prof[11] += 1;
+      g_k2prof[9] = 0;
+      if (cs.passes == 600) {
+        const double n = (double)g_k2prof[11], w = (double)g_k2prof[3];
+        printf("K2PROF (ns): work blocks entry->copied %.0f, ->work done %.0f, ->ticket %.0f; last ticket after "
+               "controller entry %.0f; controller entry->copied %.0f, ->dry run done %.0f, ->tickets seen %.0f, "
+               "->reduced %.0f, ->end %.0f\n",
+               g_k2prof[0] / w, g_k2prof[1] / w, g_k2prof[2] / w, g_k2prof[10] / n, g_k2prof[4] / n, g_k2prof[5] / n,
+               g_k2prof[6] / n, g_k2prof[7] / n, g_k2prof[8] / n);
+        printf("K2PROF dry run (ns): entry->start %.0f, reduce %.0f, precompute %.0f, control_step %.0f\n",
+               g_k2prof[15] / n, g_k2prof[12] / n, g_k2prof[13] / n, g_k2prof[14] / n);
+      }
+    }
+#endif
     if (timed) {
       const uint64_t t_end = globaltimer_ns();
       cs.sstat[ST_K2_MAIN] += t_last - __ldcg(&cs.sstat[ST_K2_T0]);

@@ -602,18 +602,29 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const C
   }
 }
 
+// PDOT_K1_PROF (measurement builds only): per-warp K1 phase times, summed over
+// a solve and printed by the last CTA of pass 600
+#ifdef PDOT_K1_PROF
+__device__ unsigned long long g_k1prof[16];
+#endif
+
 // the warp's STEP cells k = k0, k0 + nw, ...: copies of cell k + nw in flight
 // while cell k is computed
 template <bool IMPLICIT, bool AVG, class Cx>
 __device__ __forceinline__ void step_cells(const StepOp& o, const Cx& c, const Ctl& dyn, const CostGen& gen, unsigned k0,
                                            unsigned nw, const unsigned* ncells_p, unsigned char* stages,
-                                           unsigned long long& bytes, unsigned long long& cells) {
+                                           unsigned long long& bytes, unsigned long long& cells,
+                                           unsigned long long tp_entry) {
   // this warp's first two list entries are read before the list length is known
   // (the list has kListPad spare entries; values past the length are not used)
   uint32_t e_cur = __ldcg(c.ulist + k0), f_cur = __ldcg(c.uflag + k0);
   uint32_t e_nx = __ldcg(c.ulist + k0 + nw), f_nx = __ldcg(c.uflag + k0 + nw);
   const unsigned ncells = __ldcg(ncells_p);
   if (k0 >= ncells) return;
+#ifdef PDOT_K1_PROF
+  const unsigned long long tp_list = globaltimer_ns();
+  unsigned long long tp_first = 0, np = 0;
+#endif
   cell_issue<IMPLICIT, AVG>(o, c, e_cur, f_cur, stages);
   cp_async_commit();
   int st = 0;
@@ -628,12 +639,28 @@ __device__ __forceinline__ void step_cells(const StepOp& o, const Cx& c, const C
     if (more) cell_issue<IMPLICIT, AVG>(o, c, e_nx, f_nx, stages + (st ^ 1) * kStageBytes);
     cp_async_commit();
     cp_async_wait<1>();  // this cell's copies have landed
+#ifdef PDOT_K1_PROF
+    if (tp_first == 0) tp_first = globaltimer_ns();
+    ++np;
+#endif
     cell_step<IMPLICIT, AVG>(o, c, dyn, gen, e_cur, f_cur, stages + st * kStageBytes, bytes, cells);
     e_cur = e_nx; f_cur = f_nx;
     e_nx = e_n2; f_nx = f_n2;
     st ^= 1;
   }
   cp_async_wait<0>();
+#ifdef PDOT_K1_PROF
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned long long t_end = globaltimer_ns();
+    atomicAdd(&g_k1prof[0], tp_list - tp_entry);   // entry -> list length known
+    atomicAdd(&g_k1prof[1], tp_first - tp_entry);  // entry -> first cell's copies landed
+    atomicAdd(&g_k1prof[2], t_end - tp_first);     // cells
+    atomicAdd(&g_k1prof[3], np);
+    atomicAdd(&g_k1prof[4], 1ull);
+    atomicMax(&g_k1prof[5], t_end - tp_entry);
+    atomicAdd(&g_k1prof[6], t_end - tp_entry);
+  }
+#endif
 }
 
 // restart distance (DIST) and the start KKT through the screen (NQ = 1), with
@@ -687,6 +714,11 @@ __device__ __forceinline__ void cell_one(const Op& op, const Ctl& c, uint32_t en
 
 __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const Ctl* __restrict__ ctlp, int force_op,
                                                                           const KGeo geo) {
+#ifdef PDOT_K1_PROF
+  const unsigned long long tp_entry = globaltimer_ns();
+#else
+  const unsigned long long tp_entry = 0;
+#endif
   const Ctl& c = *ctlp;
   if (c.done || !c.screen) return;
   const int op = force_op >= 0 ? force_op : c.op;
@@ -715,11 +747,11 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
     extern __shared__ __align__(16) unsigned char unit_dyn[];
     unsigned char* stages = unit_dyn + warp * kStages * kStageBytes;
     if (o.C) {
-      if (o.with_avg) step_cells<false, true>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells);
-      else step_cells<false, false>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells);
+      if (o.with_avg) step_cells<false, true>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells, tp_entry);
+      else step_cells<false, false>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells, tp_entry);
     } else {
-      if (o.with_avg) step_cells<true, true>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells);
-      else step_cells<true, false>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells);
+      if (o.with_avg) step_cells<true, true>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells, tp_entry);
+      else step_cells<true, false>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells, tp_entry);
     }
   } else if (op == OP_DIST) {
     DiffOp o;
@@ -763,6 +795,15 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
         // average), 4 tile occupancy bytes and the tile's min C per tile (the
         // per-cell screens add theirs in K0)
         c.sstat[ST_META] += (unsigned long long)c.T * c.U * ((32 + c.nbt) * 2 * 8 + 4 + 8);
+#ifdef PDOT_K1_PROF
+        if (c.passes == 600) {
+          const double w = (double)g_k1prof[4];
+          printf("K1PROF per warp (ns): entry->list %.0f, entry->first cell %.0f, cells %.0f (%.2f cells, %.0f per cell), "
+                 "entry->end mean %.0f max %llu; kernel %.0f\n",
+                 g_k1prof[0] / w, g_k1prof[1] / w, g_k1prof[2] / w, g_k1prof[3] / w, (double)g_k1prof[2] / g_k1prof[3],
+                 g_k1prof[6] / w, g_k1prof[5], (double)c.sstat[ST_K1_NS] / c.sstat[ST_PASSES]);
+        }
+#endif
       }
       c.sstat[ST_DONE1] = 0;
     }
