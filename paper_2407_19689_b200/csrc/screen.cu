@@ -602,6 +602,24 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const C
   }
 }
 
+// The list length and a warp's first two list entries, read at kernel entry
+// (independent of the control block; the list has kListPad spare entries, so
+// values past the length are read but not used)
+struct ListHead {
+  uint32_t e_cur, f_cur, e_nx, f_nx;
+  unsigned ncells;
+};
+template <class Cx>
+__device__ __forceinline__ ListHead list_head(const Cx& c, unsigned k0, unsigned nw) {
+  ListHead h;
+  h.e_cur = __ldcg(c.ulist + k0);
+  h.f_cur = __ldcg(c.uflag + k0);
+  h.e_nx = __ldcg(c.ulist + k0 + nw);
+  h.f_nx = __ldcg(c.uflag + k0 + nw);
+  h.ncells = __ldcg(c.ucount);
+  return h;
+}
+
 // PDOT_K1_PROF (measurement builds only): per-warp K1 phase times, summed over
 // a solve and printed by the last CTA of pass 600
 #ifdef PDOT_K1_PROF
@@ -612,14 +630,12 @@ __device__ unsigned long long g_k1prof[16];
 // while cell k is computed
 template <bool IMPLICIT, bool AVG, class Cx>
 __device__ __forceinline__ void step_cells(const StepOp& o, const Cx& c, const Ctl& dyn, const CostGen& gen, unsigned k0,
-                                           unsigned nw, const unsigned* ncells_p, unsigned char* stages,
+                                           unsigned nw, const ListHead& lh, unsigned char* stages,
                                            unsigned long long& bytes, unsigned long long& cells,
                                            unsigned long long tp_entry) {
-  // this warp's first two list entries are read before the list length is known
-  // (the list has kListPad spare entries; values past the length are not used)
-  uint32_t e_cur = __ldcg(c.ulist + k0), f_cur = __ldcg(c.uflag + k0);
-  uint32_t e_nx = __ldcg(c.ulist + k0 + nw), f_nx = __ldcg(c.uflag + k0 + nw);
-  const unsigned ncells = __ldcg(ncells_p);
+  uint32_t e_cur = lh.e_cur, f_cur = lh.f_cur;
+  uint32_t e_nx = lh.e_nx, f_nx = lh.f_nx;
+  const unsigned ncells = lh.ncells;
   if (k0 >= ncells) return;
 #ifdef PDOT_K1_PROF
   const unsigned long long tp_list = globaltimer_ns();
@@ -719,7 +735,15 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
 #else
   const unsigned long long tp_entry = 0;
 #endif
-  const Ctl& c = *ctlp;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+  // the list head and the control block travel together (one round trip); the
+  // control block is read from shared memory from then on, so values the
+  // register budget cannot keep live are re-read from there, not from HBM
+  const ListHead lh = list_head(geo, gw, nw);
+  __shared__ Ctl ctl_s;
+  ctl_to_shared(ctlp, &ctl_s);
+  const Ctl& c = ctl_s;
   if (c.done || !c.screen) return;
   const int op = force_op >= 0 ? force_op : c.op;
   if (!unit_pass(c, op)) return;
@@ -734,9 +758,7 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
   }
   unsigned long long* tl = op == OP_STEP ? c.ktl : nullptr;
   tl_start(tl, 1);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned ncells = __ldcg(c.ucount);
-  const unsigned gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+  const unsigned ncells = lh.ncells;
   unsigned long long bytes = 0, cells = 0;
   if (op == OP_STEP) {
     const StepOp o = make_step_op(c);
@@ -747,11 +769,11 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
     extern __shared__ __align__(16) unsigned char unit_dyn[];
     unsigned char* stages = unit_dyn + warp * kStages * kStageBytes;
     if (o.C) {
-      if (o.with_avg) step_cells<false, true>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells, tp_entry);
-      else step_cells<false, false>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells, tp_entry);
+      if (o.with_avg) step_cells<false, true>(o, geo, c, gen, gw, nw, lh, stages, bytes, cells, tp_entry);
+      else step_cells<false, false>(o, geo, c, gen, gw, nw, lh, stages, bytes, cells, tp_entry);
     } else {
-      if (o.with_avg) step_cells<true, true>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells, tp_entry);
-      else step_cells<true, false>(o, geo, c, gen, gw, nw, geo.ucount, stages, bytes, cells, tp_entry);
+      if (o.with_avg) step_cells<true, true>(o, geo, c, gen, gw, nw, lh, stages, bytes, cells, tp_entry);
+      else step_cells<true, false>(o, geo, c, gen, gw, nw, lh, stages, bytes, cells, tp_entry);
     }
   } else if (op == OP_DIST) {
     DiffOp o;
