@@ -455,10 +455,16 @@ __device__ __forceinline__ void cell_flush(const Cx& c, const CellGeo& g, const 
 // overlaps compute.  Every lane reads back only what it copied itself, so a
 // lane's own cp.async.wait_group is the only synchronisation needed.  Stage
 // layout: field-major, lane-contiguous (conflict-free 16- and 8-byte reads).
-constexpr int kStF16 = 8;   // 16-byte fields: C, X, A of both rows; q pair, qa pair
-constexpr int kStF8 = 4;    // 8-byte fields: p, pa of both rows
-constexpr int kStageBytes = 32 * (16 * kStF16 + 8 * kStF8);  // 5 KB per warp and stage
-constexpr int kStages = 2;
+// Stage layout: C, X, A as 16-byte fields (both rows of each lane), then the
+// cell's duals ONCE (p, pa of its 8 rows; q, qa of its 16 columns), each copied
+// by one lane and read back by the lanes that need it (16-byte broadcasts).
+constexpr int kStMat = 32 * 16;                    // one 16-byte field of the warp
+constexpr int kStP = 6 * kStMat;                   // p[8], then pa[8], q[16], qa[16]
+constexpr int kStPa = kStP + 8 * 8;
+constexpr int kStQ = kStPa + 8 * 8;
+constexpr int kStQa = kStQ + 16 * 8;
+constexpr int kStageBytes = kStQa + 16 * 8;        // 3.4 KB per warp and stage
+constexpr int kStages = 3;                         // copies run two cells ahead
 constexpr size_t kUnitDynSmem = (size_t)kWarps * kStages * kStageBytes;
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool on) {
@@ -471,7 +477,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// issue the copies of one cell's inputs (zero-filled where not needed)
+// issue the copies of one cell's inputs (zero-filled where not needed).  Lane
+// L copies its C / X / A row pairs, p[L] (L < 8) or pa[L - 8] (8 <= L < 16), and
+// q[L] (L < 16) or qa[L - 16] (L >= 16).
 template <bool IMPLICIT, bool AVG, class Cx>
 __device__ __forceinline__ void cell_issue(const StepOp& op, const Cx& c, uint32_t entry, uint32_t f,
                                            unsigned char* stage) {
@@ -481,26 +489,29 @@ __device__ __forceinline__ void cell_issue(const StepOp& op, const Cx& c, uint32
   const bool ldx = act && (f & U_LDX);
   const bool lda = AVG && act && (f & U_LDA);
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(stage);
-  const uint32_t f16 = base + lane * 16, f8 = base + 32 * 16 * kStF16 + lane * 8;
+  const uint32_t f16 = base + lane * 16;
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
     const int r = 2 * g.rg + rr;
     const bool ok = act && r < g.rows && g.v0;
     const int64_t i = ok ? g.i0 + r : 0;
     const int64_t jj = ok ? g.j : 0;
-    if (!IMPLICIT) cp_async16(f16 + (0 + rr) * 512, op.C + i * c.ldc + jj, ok);
-    cp_async16(f16 + (2 + rr) * 512, op.X + i * c.ldx + jj, ok && ldx);
-    cp_async16(f16 + (4 + rr) * 512, (AVG ? op.A : op.X) + i * c.ldx + jj, ok && lda);
-    cp_async8(f8 + (0 + rr) * 256, op.p + i, ok);
-    cp_async8(f8 + (2 + rr) * 256, op.pa + i, ok);
+    if (!IMPLICIT) cp_async16(f16 + (0 + rr) * kStMat, op.C + i * c.ldc + jj, ok);
+    cp_async16(f16 + (2 + rr) * kStMat, op.X + i * c.ldx + jj, ok && ldx);
+    cp_async16(f16 + (4 + rr) * kStMat, (AVG ? op.A : op.X) + i * c.ldx + jj, ok && lda);
   }
-  const bool okc = act && g.v0;
-  const int64_t j0 = okc ? g.j : 0, j1 = (okc && g.v1) ? g.j + 1 : 0;
-  // q pair / qa pair as two 8-byte halves each (the second only inside the row)
-  cp_async8(f16 + 6 * 512, op.q + j0, okc);
-  cp_async8(f16 + 6 * 512 + 8, op.q + j1, okc && g.v1);
-  cp_async8(f16 + 7 * 512, op.qa + j0, okc);
-  cp_async8(f16 + 7 * 512 + 8, op.qa + j1, okc && g.v1);
+  if (lane < 16) {  // p / pa of row lane & 7
+    const int r = lane & 7;
+    const bool ok = act && r < g.rows;
+    const double* src = (lane < 8 ? op.p : op.pa) + (ok ? g.i0 + r : 0);
+    cp_async8(base + kStP + lane * 8, src, ok);
+  }
+  {  // q / qa of column lane & 15 of the cell
+    const int64_t jc = g.cell * kCell + (lane & 15);
+    const bool ok = act && jc < c.n;
+    const double* src = (lane < 16 ? op.q : op.qa) + (ok ? jc : 0);
+    cp_async8(base + kStQ + lane * 8, src, ok);
+  }
 }
 
 template <bool IMPLICIT, bool AVG, class Cx>
@@ -518,9 +529,11 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const C
   const bool za = AVG && (f & U_ZA) != 0;
   if (lane == 0 && act) cells += 1;
   const double2* s16 = reinterpret_cast<const double2*>(stage) + lane;
-  const double* s8 = reinterpret_cast<const double*>(stage + 32 * 16 * kStF16) + lane;
+  // the lane's two rows of p / pa and its column pair of q / qa (broadcast reads)
+  const double2 p2 = *reinterpret_cast<const double2*>(stage + kStP + 16 * g.rg);
+  const double2 pa2 = *reinterpret_cast<const double2*>(stage + kStPa + 16 * g.rg);
   double2 cc[2], xx[2], aa[2];
-  double pr[2], par[2];
+  const double pr[2] = {p2.x, p2.y}, par[2] = {pa2.x, pa2.y};
   bool okr[2];
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
@@ -529,11 +542,10 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const C
     cc[rr] = IMPLICIT ? make_double2(0.0, 0.0) : s16[(0 + rr) * 32];
     xx[rr] = s16[(2 + rr) * 32];
     aa[rr] = s16[(4 + rr) * 32];
-    pr[rr] = s8[(0 + rr) * 32];
-    par[rr] = s8[(2 + rr) * 32];
     if (okr[rr]) bytes += (IMPLICIT ? 0 : 16) + (ldx ? 16 : 0) + (lda ? 16 : 0);
   }
-  const double2 q2 = s16[6 * 32], qa2 = s16[7 * 32];
+  const double2 q2 = *reinterpret_cast<const double2*>(stage + kStQ + 16 * g.cp);
+  const double2 qa2 = *reinterpret_cast<const double2*>(stage + kStQa + 16 * g.cp);
   const double qv[2] = {q2.x, q2.y}, qav[2] = {qa2.x, qa2.y};
   if (IMPLICIT && act) {
     const double2 c0 = gen.col_coord(g.j), c1 = gen.col_coord(g.j + 1);
@@ -606,7 +618,7 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const C
 // (independent of the control block; the list has kListPad spare entries, so
 // values past the length are read but not used)
 struct ListHead {
-  uint32_t e_cur, f_cur, e_nx, f_nx;
+  uint32_t e_cur, f_cur, e_nx, f_nx, e_n2, f_n2;
   unsigned ncells;
 };
 template <class Cx>
@@ -616,6 +628,8 @@ __device__ __forceinline__ ListHead list_head(const Cx& c, unsigned k0, unsigned
   h.f_cur = __ldcg(c.uflag + k0);
   h.e_nx = __ldcg(c.ulist + k0 + nw);
   h.f_nx = __ldcg(c.uflag + k0 + nw);
+  h.e_n2 = __ldcg(c.ulist + k0 + 2 * nw);
+  h.f_n2 = __ldcg(c.uflag + k0 + 2 * nw);
   h.ncells = __ldcg(c.ucount);
   return h;
 }
@@ -633,36 +647,39 @@ __device__ __forceinline__ void step_cells(const StepOp& o, const Cx& c, const C
                                            unsigned nw, const ListHead& lh, unsigned char* stages,
                                            unsigned long long& bytes, unsigned long long& cells,
                                            unsigned long long tp_entry) {
-  uint32_t e_cur = lh.e_cur, f_cur = lh.f_cur;
-  uint32_t e_nx = lh.e_nx, f_nx = lh.f_nx;
+  // the warp's cells k0, k0 + nw, ...: cell i's copies are issued two cells
+  // ahead (stage i % 3) and its list entry three cells ahead
+  uint32_t e0 = lh.e_cur, f0 = lh.f_cur, e1 = lh.e_nx, f1 = lh.f_nx, e2 = lh.e_n2, f2 = lh.f_n2;
   const unsigned ncells = lh.ncells;
   if (k0 >= ncells) return;
 #ifdef PDOT_K1_PROF
   const unsigned long long tp_list = globaltimer_ns();
   unsigned long long tp_first = 0, np = 0;
 #endif
-  cell_issue<IMPLICIT, AVG>(o, c, e_cur, f_cur, stages);
+  cell_issue<IMPLICIT, AVG>(o, c, e0, f0, stages);
+  cp_async_commit();
+  if (k0 + nw < ncells) cell_issue<IMPLICIT, AVG>(o, c, e1, f1, stages + kStageBytes);
   cp_async_commit();
   int st = 0;
   for (unsigned k = k0; k < ncells; k += nw) {
-    const bool more = k + nw < ncells;
-    // the list entry two cells ahead, then the copies of the next cell
-    uint32_t e_n2 = 0, f_n2 = 0;
-    if (k + 2 * nw < ncells) {
-      e_n2 = __ldcg(c.ulist + k + 2 * nw);
-      f_n2 = __ldcg(c.uflag + k + 2 * nw);
+    uint32_t e3 = 0, f3 = 0;
+    if (k + 3 * nw < ncells) {
+      e3 = __ldcg(c.ulist + k + 3 * nw);
+      f3 = __ldcg(c.uflag + k + 3 * nw);
     }
-    if (more) cell_issue<IMPLICIT, AVG>(o, c, e_nx, f_nx, stages + (st ^ 1) * kStageBytes);
+    const int st2 = st == 0 ? 2 : st - 1;  // (st + 2) % 3
+    if (k + 2 * nw < ncells) cell_issue<IMPLICIT, AVG>(o, c, e2, f2, stages + st2 * kStageBytes);
     cp_async_commit();
-    cp_async_wait<1>();  // this cell's copies have landed
+    cp_async_wait<2>();  // this cell's copies have landed
 #ifdef PDOT_K1_PROF
     if (tp_first == 0) tp_first = globaltimer_ns();
     ++np;
 #endif
-    cell_step<IMPLICIT, AVG>(o, c, dyn, gen, e_cur, f_cur, stages + st * kStageBytes, bytes, cells);
-    e_cur = e_nx; f_cur = f_nx;
-    e_nx = e_n2; f_nx = f_n2;
-    st ^= 1;
+    cell_step<IMPLICIT, AVG>(o, c, dyn, gen, e0, f0, stages + st * kStageBytes, bytes, cells);
+    e0 = e1; f0 = f1;
+    e1 = e2; f1 = f2;
+    e2 = e3; f2 = f3;
+    st = st == 2 ? 0 : st + 1;
   }
   cp_async_wait<0>();
 #ifdef PDOT_K1_PROF
@@ -1231,8 +1248,8 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
       const cudaError_t e = cudaStreamSynchronize(s);
       if (e != cudaSuccess) fprintf(stderr, "screen_kernel failed: %s\n", cudaGetErrorString(e));
     }
-    // every warp reads list entries gw and gw + nw up front: 2 nw <= kListPad
-    const unsigned g1 = (unsigned)imin64((int64_t)sms * kSparseCtasPerSm, kListPad / (2 * kWarps));
+    // every warp reads list entries gw, gw + nw and gw + 2 nw up front: 3 nw <= kListPad
+    const unsigned g1 = (unsigned)imin64((int64_t)sms * kSparseCtasPerSm, kListPad / (3 * kWarps));
     const KGeo geo{h.m, h.n, h.ldx, h.ldc, h.mpad, h.nbands, h.nstrips, h.ncells, h.ncp, h.T, h.U,
                    h.nbands * h.nstrips, h.T * h.U, h.nbt, h.cbits, __builtin_ctz((unsigned)h.nbt), 0,
                    h.occ, h.tocc, h.ccol, h.crow, h.cscal, h.ulist, h.uflag, h.ucount,
