@@ -315,12 +315,15 @@ __device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ]) {
   }
 }
 
-__device__ void column_block(Ctl& c, int op, int b, double* smem, int mode) {
+// STEP: the hot path of every screened pass, compiled on its own (the rare ops
+// sit out of line in column_block_rare) so that its code is compact
+template <bool STEP>
+__device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* smem, int mode) {
   double vals[kMaxColScal];
 #pragma unroll
   for (int s = 0; s < kMaxColScal; ++s) vals[s] = 0.0;
   int64_t j;
-  if (op == OP_STEP) {
+  if constexpr (STEP) {
     // the vectors of this thread's column, loaded before the (long) column sums
     const int64_t jp = (int64_t)b * kColsPerBlock + threadIdx.x;
     const bool own = threadIdx.x < kColsPerBlock && jp < c.n;
@@ -467,7 +470,8 @@ __device__ __forceinline__ void tile_scalars(Ctl& c, int t, int ns, int nr, int 
   if (tx < ns) c.rowblk[(int64_t)t * kMaxRowScal + nr + tx] = acc;
 }
 
-__device__ void row_block(Ctl& c, int op, int t, double* smem) {
+template <bool STEP>
+__device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem) {
   double vals[kMaxRowScal];
 #pragma unroll
   for (int s = 0; s < kMaxRowScal; ++s) vals[s] = 0.0;
@@ -483,7 +487,7 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
   for (int r = threadIdx.x; r < c.TM; r += kRedThreads) {
     const int64_t i = i0 + r;
     const bool ok = r < rows;
-    if (op == OP_STEP) {
+    if constexpr (STEP) {
       // the vectors of this row, loaded before the (long) row sums
       const double pi = ok ? __ldcg(c.slot[c.sX].p + i) : 0.0;
       const double fi = ok ? __ldg(c.f + i) : 0.0;
@@ -577,6 +581,11 @@ __device__ void row_block(Ctl& c, int op, int t, double* smem) {
   }
   if (!scal_early && threadIdx.x < 32) tile_scalars(c, t, ns, nr, threadIdx.x);
 }
+
+__device__ __noinline__ void column_block_rare(Ctl& c, int op, int b, double* smem, int mode) {
+  column_block_t<false>(c, op, b, smem, mode);
+}
+__device__ __noinline__ void row_block_rare(Ctl& c, int op, int t, double* smem) { row_block_t<false>(c, op, t, smem); }
 
 // ---------------------------------------------------------------------------
 // controller
@@ -898,7 +907,7 @@ __device__ __noinline__ void control_step(Ctl& c, const Sums& S, const Pre& P) {
   prepare_step(c);
 }
 
-__device__ void control_dist(Ctl& c, const Sums& S) {
+__device__ __noinline__ void control_dist(Ctl& c, const Sums& S) {
   c.avg_written = 0;
   // pdhg.py:353-362 + primal_weight_update pdhg.py:174-186
   const double dX = sqrt(S.R[2]);
@@ -918,7 +927,7 @@ __device__ void control_dist(Ctl& c, const Sums& S) {
   prepare_step(c);
 }
 
-__device__ void control_start(Ctl& c, const Sums& S) {
+__device__ __noinline__ void control_start(Ctl& c, const Sums& S) {
   c.avg_written = 0;
   // pdhg.py:278-296
   const double nrm = sqrt((S.R[5] + S.R[2]) + S.K[2]);
@@ -941,7 +950,7 @@ __device__ void control_start(Ctl& c, const Sums& S) {
   prepare_step(c);
 }
 
-__device__ void control_unit(Ctl& c, int op, const Sums& S) {
+__device__ __noinline__ void control_unit(Ctl& c, int op, const Sums& S) {
   if (op == OP_KKT) {
     const double psq = S.R[0] + S.K[0];
     const double pobj = S.R[3], dsq = S.R[4];
@@ -1002,7 +1011,8 @@ __device__ unsigned long long g_k2prof[16];
 __device__ unsigned long long g_k2entry;  // controller entry of the running pass
 #endif
 
-__global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restrict__ ctlp, int force_op, int mode) {
+template <int mode>
+__global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restrict__ ctlp, int force_op) {
 #ifdef PDOT_K2_PROF
   const unsigned long long tq0 = globaltimer_ns();
   unsigned long long tq1 = 0, tq2 = 0, tq3 = 0;
@@ -1038,13 +1048,17 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
   tq1 = globaltimer_ns();
   if (timed && has_ctl && blockIdx.x == 0 && threadIdx.x == 0) g_k2entry = tq0;
 #endif
+  // screened-STEP statistics of this pass, read at entry by the controller
+  // block's last thread (K1 has completed) and accounted after the write-back
+  unsigned long long k2_t0 = 0, k1e = 0, k1s = 0, ncl = 0;
   if (has_ctl && blockIdx.x == 0) {
     // pass statistics by the last thread (its load of the K1 end stamp is used
     // only after the dry run: thread 0 starts the dry run without waiting)
-    unsigned long long k2_t0 = 0, k1e = 0;
     if (timed && threadIdx.x == kRedThreads - 1) {
       k2_t0 = globaltimer_ns();
       k1e = __ldcg(&c.sstat[ST_K1_END]);
+      k1s = __ldcg(&c.sstat[ST_T0]);
+      ncl = __ldcg(c.ucount);
       c.sstat[ST_K2_T0] = k2_t0;
     }
     if (timed && c.ktl && threadIdx.x == kRedThreads - 1) atomicMin(c.ktl + 6, k2_t0);
@@ -1098,7 +1112,6 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
 #ifdef PDOT_K2_PROF
     tq2 = globaltimer_ns();
 #endif
-    if (timed && threadIdx.x == kRedThreads - 1 && k1e != 0 && k2_t0 > k1e) c.sstat[ST_K1K2] += k2_t0 - k1e;
     wait_tickets(c, nwork);
 #ifdef PDOT_K2_PROF
     tq3 = globaltimer_ns();
@@ -1115,10 +1128,12 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
         if (op == OP_STEP) column_group_partials<4>(c, b);
         else column_group_partials<1>(c, b);
       } else {
-        column_block(c, op, b, smem, mode);
+        if (op == OP_STEP) column_block_t<true>(c, op, b, smem, mode);
+        else column_block_rare(c, op, b, smem, mode);
       }
     } else {
-      row_block(c, op, wb, smem);
+      if (op == OP_STEP) row_block_t<true>(c, op, wb, smem);
+      else row_block_rare(c, op, wb, smem);
     }
     if (timed && c.kdbg && threadIdx.x == 0) c.kdbg[wb * 4 + 1] = globaltimer_ns();
     if (mode == FIN_A && c.p2p) __threadfence_system();  // remote group stores before the ticket
@@ -1208,6 +1223,18 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
   __syncthreads();
   unsigned long long* gwo = reinterpret_cast<unsigned long long*>(ctlp);
   for (int i = threadIdx.x; i < kWords; i += blockDim.x) gwo[i] = cw[i];
+  if (timed && threadIdx.x == kRedThreads - 1) {
+    // K1 of this pass: first CTA start (ST_T0) -> latest CTA end (ST_K1_END)
+    if (k1e > k1s) cs.sstat[ST_K1_NS] += k1e - k1s;
+    cs.sstat[ST_K1_END] = 0;
+    cs.sstat[ST_TILES] += ncl;
+    cs.sstat[ST_PASSES] += 1;
+    // K0 tile-level screen of this pass: 32 cell + nbt band maxima (current and
+    // average), 4 tile occupancy bytes and the tile's min C per tile (the
+    // per-cell screens add theirs in K0)
+    cs.sstat[ST_META] += (unsigned long long)cs.T * cs.U * ((32 + cs.nbt) * 2 * 8 + 4 + 8);
+    if (k1e != 0 && k2_t0 > k1e) cs.sstat[ST_K1K2] += k2_t0 - k1e;
+  }
   if (threadIdx.x == 0) {
     *cs.counter = 0u;
     if (cs.ucount) *cs.ucount = 0u;  // the screened cell and tile lists of this pass are consumed
@@ -1348,7 +1375,9 @@ int launch_p2p_protocol_test(Ctl* ctls_dev, int nranks, int rounds, unsigned lon
 void launch_finalize_pass(Ctl* ctl_dev, const Ctl& h, int force_op, int mode, cudaStream_t s) {
   // + 1: the controller block (FIN_FUSED, FIN_B)
   const unsigned blocks = (unsigned)(mode == FIN_B ? h.CB + 1 : mode == FIN_A ? h.CB + h.T : h.CB + h.T + 1);
-  finalize_kernel<<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op, mode);
+  if (mode == FIN_FUSED) finalize_kernel<FIN_FUSED><<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op);
+  else if (mode == FIN_A) finalize_kernel<FIN_A><<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op);
+  else finalize_kernel<FIN_B><<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op);
 }
 
 }  // namespace pdot

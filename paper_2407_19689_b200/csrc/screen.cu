@@ -802,7 +802,9 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
     o.C = c.C; o.X = sx.X; o.p = sx.p; o.q = sx.q; o.viol = nullptr;
     for (unsigned k = gw; k < ncells; k += nw) cell_one(o, c, __ldcg(c.ulist + k), __ldcg(c.uflag + k), bytes, cells);
   }
-  // statistics: one atomic per CTA, then the last CTA stamps the end time
+  // statistics: fire-and-forget reductions per CTA (no fence, no done counter:
+  // the last CTA is not waited for); K2's controller turns the latest end stamp
+  // into the pass's K1 time
 #pragma unroll
   for (int msk = 16; msk >= 1; msk >>= 1) {
     bytes += __shfl_xor_sync(0xffffffffu, bytes, msk);
@@ -821,31 +823,16 @@ __global__ void __launch_bounds__(kThreads, kSparseCtasPerSm) unit_kernel(const 
     }
     atomicAdd(&c.sstat[ST_BYTES], tb);
     atomicAdd(&c.sstat[ST_CELLS], tc);
-    __threadfence();
-    const unsigned long long done = atomicAdd(&c.sstat[ST_DONE1], 1ull);
-    if (done == gridDim.x - 1) {
-      const unsigned long long t1 = globaltimer_ns();
-      if (op == OP_STEP) {
-        c.sstat[ST_K1_NS] += t1 - __ldcg(&c.sstat[ST_T0]);
-        c.sstat[ST_K1_END] = t1;
-        c.sstat[ST_TILES] += ncells;
-        c.sstat[ST_PASSES] += 1;
-        // K0 tile-level screen of this pass: 32 cell + nbt band maxima (current and
-        // average), 4 tile occupancy bytes and the tile's min C per tile (the
-        // per-cell screens add theirs in K0)
-        c.sstat[ST_META] += (unsigned long long)c.T * c.U * ((32 + c.nbt) * 2 * 8 + 4 + 8);
+    if (op == OP_STEP) atomicMax(&c.sstat[ST_K1_END], (unsigned long long)globaltimer_ns());
 #ifdef PDOT_K1_PROF
-        if (c.passes == 600) {
-          const double w = (double)g_k1prof[4];
-          printf("K1PROF per warp (ns): entry->list %.0f, entry->first cell %.0f, cells %.0f (%.2f cells, %.0f per cell), "
-                 "entry->end mean %.0f max %llu; kernel %.0f\n",
-                 g_k1prof[0] / w, g_k1prof[1] / w, g_k1prof[2] / w, g_k1prof[3] / w, (double)g_k1prof[2] / g_k1prof[3],
-                 g_k1prof[6] / w, g_k1prof[5], (double)c.sstat[ST_K1_NS] / c.sstat[ST_PASSES]);
-        }
-#endif
-      }
-      c.sstat[ST_DONE1] = 0;
+    if (blockIdx.x == 0 && c.passes == 600) {
+      const double w = (double)g_k1prof[4];
+      printf("K1PROF per warp (ns): entry->list %.0f, entry->first cell %.0f, cells %.0f (%.2f cells, %.0f per cell), "
+             "entry->end mean %.0f max %llu\n",
+             g_k1prof[0] / w, g_k1prof[1] / w, g_k1prof[2] / w, g_k1prof[3] / w, (double)g_k1prof[2] / g_k1prof[3],
+             g_k1prof[6] / w, g_k1prof[5]);
     }
+#endif
   }
   tl_end(tl, 1);
 }
@@ -997,13 +984,14 @@ __global__ void __launch_bounds__(kThreads, 4) tile_kernel(const Ctl* __restrict
   // has at most 3 T U blocks, so blockIdx.x / 3 is inside the list buffer)
   int32_t tile_nx = __ldcg(c.tlist + blockIdx.x / 3u);
   const unsigned ntiles = __ldcg(c.tcount);
+  const unsigned nitems = ntiles * 3u;
   unsigned long long* tl = op == OP_STEP ? dyn.ktl : nullptr;
   tl_start(tl, 2);
   // work item k = (listed tile k / 3, part k % 3): the column, row and scalar
   // sums of one tile run in three CTAs side by side
-  for (unsigned k = blockIdx.x; k < ntiles * 3u; k += gridDim.x) {
+  for (unsigned k = blockIdx.x; k < nitems; k += gridDim.x) {
     const int32_t tile = tile_nx;
-    if (k + gridDim.x < ntiles * 3u) tile_nx = __ldcg(c.tlist + (k + gridDim.x) / 3u);
+    if (k + gridDim.x < nitems) tile_nx = __ldcg(c.tlist + (k + gridDim.x) / 3u);
     const int part = (int)(k % 3u);
     const int64_t tt = (uint32_t)tile / (uint32_t)c.U, tu = tile - tt * c.U;  // 32-bit division
     if (op == OP_STEP) assemble_tile<4, 6>(c, tu, tt, sm, part);
