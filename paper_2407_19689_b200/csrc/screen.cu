@@ -467,8 +467,16 @@ constexpr int kStageBytes = kStQa + 16 * 8;        // 3.4 KB per warp and stage
 constexpr int kStages = 3;                         // copies run two cells ahead
 constexpr size_t kUnitDynSmem = (size_t)kWarps * kStages * kStageBytes;
 
+// The C / X / A row segments K1 stages are read once per pass: L2 evict-first,
+// so that they do not push the pass's partials and the screening metadata out of
+// L2 (C3: K2 to its last ticket 10.5 -> 9.5 us, controller reduce 2.5 -> 2.2 us;
+// +4-5 % iterations/s, profiles/r02_evict_first_ab.json)
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool on) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(on ? 16 : 0) : "memory");
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+      "cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, pol;\n\t}" ::"r"(dst),
+      "l"(src), "r"(on ? 16 : 0)
+      : "memory");
 }
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool on) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(on ? 8 : 0) : "memory");
