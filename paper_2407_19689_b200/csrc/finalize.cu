@@ -1013,6 +1013,9 @@ __device__ unsigned long long g_k2entry;  // controller entry of the running pas
 
 template <int mode>
 __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restrict__ ctlp, int force_op) {
+  // launched as a programmatic dependent of K1b (PDOT_PDL=k2): the work blocks
+  // wait for K1b at once; the controller block runs its dry run first
+  if (mode != FIN_FUSED || blockIdx.x != 0) pdl_wait();
 #ifdef PDOT_K2_PROF
   const unsigned long long tq0 = globaltimer_ns();
   unsigned long long tq1 = 0, tq2 = 0, tq3 = 0;
@@ -1112,6 +1115,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
 #ifdef PDOT_K2_PROF
     tq2 = globaltimer_ns();
 #endif
+    pdl_wait();
     wait_tickets(c, nwork);
 #ifdef PDOT_K2_PROF
     tq3 = globaltimer_ns();
@@ -1375,7 +1379,18 @@ int launch_p2p_protocol_test(Ctl* ctls_dev, int nranks, int rounds, unsigned lon
 void launch_finalize_pass(Ctl* ctl_dev, const Ctl& h, int force_op, int mode, cudaStream_t s) {
   // + 1: the controller block (FIN_FUSED, FIN_B)
   const unsigned blocks = (unsigned)(mode == FIN_B ? h.CB + 1 : mode == FIN_A ? h.CB + h.T : h.CB + h.T + 1);
-  if (mode == FIN_FUSED) finalize_kernel<FIN_FUSED><<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op);
+  if (mode == FIN_FUSED && pdl_edge("k2")) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(kRedThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, finalize_kernel<FIN_FUSED>, ctl_dev, force_op);
+  } else if (mode == FIN_FUSED) finalize_kernel<FIN_FUSED><<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op);
   else if (mode == FIN_A) finalize_kernel<FIN_A><<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op);
   else finalize_kernel<FIN_B><<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op);
 }

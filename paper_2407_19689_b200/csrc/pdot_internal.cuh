@@ -419,6 +419,13 @@ __device__ __forceinline__ void ctl_to_shared(const Ctl* __restrict__ g, Ctl* s)
   __syncthreads();
 }
 
+// Programmatic dependent launch (pdl_edge): a kernel lets its stream successor
+// be scheduled early (launch_dependents), and a kernel that may have been
+// launched early waits here for its predecessor's completion and memory before
+// reading anything (a no-op for a plain launch)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -451,6 +458,8 @@ void prepare_stream_kernel();
 // walker over all tiles for the unit calls that the screen does not cover
 void launch_screened_pass(const Ctl* ctl_dev, const Ctl& ctl_host, int force_op, cudaStream_t s);
 void prepare_sparse_kernel();
+// whether a pass kernel is launched as a programmatic dependent of its predecessor
+bool pdl_edge(const char* name);
 // a pass whose partials are per-unit (screened) rather than per-tile
 __host__ __device__ __forceinline__ bool unit_pass(const Ctl& c, int op) {
   return c.screen && (op == OP_STEP || (!c.unit && (op == OP_DIST || op == OP_KKT)));

@@ -36,6 +36,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <string>
+
 #include "pass_ops.cuh"
 
 #ifdef PDOT_DEVICE_CHECKS
@@ -984,6 +986,7 @@ __device__ __forceinline__ void assemble_tile(const Cx& c, int64_t tu, int64_t t
 __global__ void __launch_bounds__(kThreads, 4) tile_kernel(const Ctl* __restrict__ ctlp, int force_op,
                                                             const KGeo c) {
   __shared__ double sm[32 * 8 * 8];  // [band][strip][scalar] strip-band values
+  pdl_trigger();  // K2 may be scheduled as K1b's CTAs retire (its controller block starts its dry run)
   const Ctl& dyn = *ctlp;
   if (dyn.done || !dyn.screen) return;
   const int op = force_op >= 0 ? force_op : dyn.op;
@@ -1227,6 +1230,18 @@ void prepare_sparse_kernel() {
 
 static size_t generic_smem_bytes(int64_t TM) {
   return (size_t)TM * kMaxNQ * kWarps * sizeof(double) + kWarps * 8 * sizeof(double);
+}
+
+// K2 is launched as a programmatic dependent of K1b (its controller block's
+// instruction-cache dry run overlaps K1b's tail: C3 +1.8 % iterations/s,
+// profiles/r02_pdl_edges_ab.json); PDOT_PDL_K2=0 launches it plainly.  PDL on the
+// K0 -> K1 and K1 -> K1b edges measured slower and is not used.
+bool pdl_edge(const char* name) {
+  static const bool k2 = [] {
+    const char* e = getenv("PDOT_PDL_K2");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  return std::string(name) == "k2" && k2;
 }
 
 void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaStream_t s) {
