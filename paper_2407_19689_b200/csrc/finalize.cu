@@ -1140,14 +1140,20 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
       else row_block_rare(c, op, wb, smem);
     }
     if (timed && c.kdbg && threadIdx.x == 0) c.kdbg[wb * 4 + 1] = globaltimer_ns();
-    if (mode == FIN_A && c.p2p) __threadfence_system();  // remote group stores before the ticket
-    else __threadfence();
+    if (mode == FIN_A) {
+      if (c.p2p) __threadfence_system();  // remote group stores before the ticket
+      else __threadfence();
+    }
     __syncthreads();
     if (mode != FIN_A) {
       if (threadIdx.x == 0) {
 #ifdef PDOT_K2_PROF
         const unsigned long long tw = globaltimer_ns();
 #endif
+        // the block's partial stores (ordered before this thread by the barrier)
+        // are released with the ticket: one acq_rel fence instead of a
+        // sequentially consistent fence by every thread
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
         atomicAdd(c.counter, 1u);
         if (timed && c.kdbg) c.kdbg[wb * 4 + 2] = globaltimer_ns();
 #ifdef PDOT_K2_PROF
@@ -1173,7 +1179,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
     if (threadIdx.x == 0) *c.counter = 0u;
     return;
   }
-  __threadfence();
+  // (wait_tickets: the acquire load of the ticket count, then a barrier)
   const uint64_t t_last = timed ? globaltimer_ns() : 0;
   // the controller works on the shared-memory copy and writes it back
   if (mode == FIN_B && c.p2p && threadIdx.x == 0) cs.xerror = __ldcg(&ctlp->xerror);  // set by wait_exchange
