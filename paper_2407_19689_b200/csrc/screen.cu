@@ -473,12 +473,16 @@ constexpr size_t kUnitDynSmem = (size_t)kWarps * kStages * kStageBytes;
 // so that they do not push the pass's partials and the screening metadata out of
 // L2 (C3: K2 to its last ticket 10.5 -> 9.5 us, controller reduce 2.5 -> 2.2 us;
 // +4-5 % iterations/s, profiles/r02_evict_first_ab.json)
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool on) {
-  asm volatile(
-      "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
-      "cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, pol;\n\t}" ::"r"(dst),
-      "l"(src), "r"(on ? 16 : 0)
-      : "memory");
+// (the policy is made once per kernel: a plain asm, so the compiler hoists it)
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool on, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src),
+               "r"(on ? 16 : 0), "l"(pol)
+               : "memory");
 }
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool on) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(on ? 8 : 0) : "memory");
@@ -500,15 +504,16 @@ __device__ __forceinline__ void cell_issue(const StepOp& op, const Cx& c, uint32
   const bool lda = AVG && act && (f & U_LDA);
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(stage);
   const uint32_t f16 = base + lane * 16;
+  const uint64_t pol = l2_evict_first();
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
     const int r = 2 * g.rg + rr;
     const bool ok = act && r < g.rows && g.v0;
     const int64_t i = ok ? g.i0 + r : 0;
     const int64_t jj = ok ? g.j : 0;
-    if (!IMPLICIT) cp_async16(f16 + (0 + rr) * kStMat, op.C + i * c.ldc + jj, ok);
-    cp_async16(f16 + (2 + rr) * kStMat, op.X + i * c.ldx + jj, ok && ldx);
-    cp_async16(f16 + (4 + rr) * kStMat, (AVG ? op.A : op.X) + i * c.ldx + jj, ok && lda);
+    if (!IMPLICIT) cp_async16(f16 + (0 + rr) * kStMat, op.C + i * c.ldc + jj, ok, pol);
+    cp_async16(f16 + (2 + rr) * kStMat, op.X + i * c.ldx + jj, ok && ldx, pol);
+    cp_async16(f16 + (4 + rr) * kStMat, (AVG ? op.A : op.X) + i * c.ldx + jj, ok && lda, pol);
   }
   if (lane < 16) {  // p / pa of row lane & 7
     const int r = lane & 7;
@@ -527,7 +532,7 @@ __device__ __forceinline__ void cell_issue(const StepOp& op, const Cx& c, uint32
 template <bool IMPLICIT, bool AVG, class Cx>
 __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const Ctl& dyn, const CostGen& gen,
                                           uint32_t entry, uint32_t f,
-                                          const unsigned char* stage, unsigned long long& bytes,
+                                          const unsigned char* stage, unsigned& bytes,
                                           unsigned long long& cells) {
   constexpr int NQ = StepOp::NQ, NS = StepOp::NS;
   const int lane = threadIdx.x & 31;
@@ -620,7 +625,7 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const C
   }
   if (act) {
     cell_flush<NQ, NS>(c, g, o, sacc);
-    if (lane == 0) bytes += (unsigned long long)(NQ * kCell + NQ * kBand + NS) * 8 * 2;
+    if (lane == 0) bytes += (unsigned)(NQ * kCell + NQ * kBand + NS) * 8 * 2;
   }
 }
 
@@ -666,6 +671,7 @@ __device__ __forceinline__ void step_cells(const StepOp& o, const Cx& c, const C
   const unsigned long long tp_list = globaltimer_ns();
   unsigned long long tp_first = 0, np = 0;
 #endif
+  unsigned bytes32 = 0;  // this warp-lane's bytes (32-bit: a few hundred per cell)
   cell_issue<IMPLICIT, AVG>(o, c, e0, f0, stages);
   cp_async_commit();
   if (k0 + nw < ncells) cell_issue<IMPLICIT, AVG>(o, c, e1, f1, stages + kStageBytes);
@@ -685,13 +691,14 @@ __device__ __forceinline__ void step_cells(const StepOp& o, const Cx& c, const C
     if (tp_first == 0) tp_first = globaltimer_ns();
     ++np;
 #endif
-    cell_step<IMPLICIT, AVG>(o, c, dyn, gen, e0, f0, stages + st * kStageBytes, bytes, cells);
+    cell_step<IMPLICIT, AVG>(o, c, dyn, gen, e0, f0, stages + st * kStageBytes, bytes32, cells);
     e0 = e1; f0 = f1;
     e1 = e2; f1 = f2;
     e2 = e3; f2 = f3;
     st = st == 2 ? 0 : st + 1;
   }
   cp_async_wait<0>();
+  bytes += bytes32;
 #ifdef PDOT_K1_PROF
   if ((threadIdx.x & 31) == 0) {
     const unsigned long long t_end = globaltimer_ns();
