@@ -1013,9 +1013,10 @@ __device__ unsigned long long g_k2entry;  // controller entry of the running pas
 
 template <int mode>
 __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restrict__ ctlp, int force_op) {
-  // launched as a programmatic dependent of K1b (PDOT_PDL=k2): the work blocks
-  // wait for K1b at once; the controller block runs its dry run first
-  if (mode != FIN_FUSED || blockIdx.x != 0) pdl_wait();
+  // launched as a programmatic dependent of K1b (pdl_edge("k2")): every block
+  // copies the control block (K1b does not write it) before it waits for K1b,
+  // and the controller block also runs its dry run first
+  if (mode != FIN_FUSED) pdl_wait();
 #ifdef PDOT_K2_PROF
   const unsigned long long tq0 = globaltimer_ns();
   unsigned long long tq1 = 0, tq2 = 0, tq3 = 0;
@@ -1042,6 +1043,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
     for (int i = threadIdx.x; i < kWords; i += blockDim.x) cw[i] = __ldcg(gw + i);
   }
   __syncthreads();
+  if (mode == FIN_FUSED && blockIdx.x != 0) pdl_wait();  // the work blocks: K1b's partials from here on
   Ctl& c = cs;
   const int op = force_op >= 0 ? force_op : c.op;
   const bool timed = op == OP_STEP && unit_pass(c, op) && c.sstat;  // K2 timing of screened STEP passes
