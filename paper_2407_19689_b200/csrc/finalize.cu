@@ -330,6 +330,7 @@ __device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* sm
     const double qj = own ? __ldcg(c.slot[c.sX].q + jp) : 0.0;
     const double gj = own ? __ldg(c.g + jp) : 0.0;
     const double qaj = own ? __ldcg(c.slot[c.sA].q + jp) : 0.0;
+    pdl_wait();  // (a programmatic dependent of K1b: its partials from here on; a no-op otherwise)
     double col[4];
     column_sums<4>(c, b, col, j, smem, mode);
     double qb = -INFINITY, qab = -INFINITY;  // screening bounds of q+ and the dual average
@@ -483,7 +484,10 @@ __device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem)
   // with rows for at most 7 warps, the last warp forms the tile scalars while the
   // others work on the rows (otherwise warp 0 does after them)
   const bool scal_early = c.TM <= kRedThreads - 32;
-  if (scal_early && threadIdx.x >= kRedThreads - 32) tile_scalars(c, t, ns, nr, threadIdx.x & 31);
+  if (scal_early && threadIdx.x >= kRedThreads - 32) {
+    pdl_wait();
+    tile_scalars(c, t, ns, nr, threadIdx.x & 31);
+  }
   for (int r = threadIdx.x; r < c.TM; r += kRedThreads) {
     const int64_t i = i0 + r;
     const bool ok = r < rows;
@@ -492,6 +496,7 @@ __device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem)
       const double pi = ok ? __ldcg(c.slot[c.sX].p + i) : 0.0;
       const double fi = ok ? __ldg(c.f + i) : 0.0;
       const double pai = ok ? __ldcg(c.slot[c.sA].p + i) : 0.0;
+      pdl_wait();
       double row[4];
       row_sums<4>(c, ok ? i : c.m, row);
       double pb = -INFINITY, pab = -INFINITY;  // screening bounds of p+ and the dual average
@@ -579,7 +584,10 @@ __device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem)
   if (threadIdx.x == 0) {
     for (int s = 0; s < nr; ++s) c.rowblk[(int64_t)t * kMaxRowScal + s] = vals[s];
   }
-  if (!scal_early && threadIdx.x < 32) tile_scalars(c, t, ns, nr, threadIdx.x);
+  if (!scal_early && threadIdx.x < 32) {
+    pdl_wait();
+    tile_scalars(c, t, ns, nr, threadIdx.x);
+  }
 }
 
 __device__ __noinline__ void column_block_rare(Ctl& c, int op, int b, double* smem, int mode) {
@@ -1043,7 +1051,9 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
     for (int i = threadIdx.x; i < kWords; i += blockDim.x) cw[i] = __ldcg(gw + i);
   }
   __syncthreads();
-  if (mode == FIN_FUSED && blockIdx.x != 0) pdl_wait();  // the work blocks: K1b's partials from here on
+  // the work blocks of a STEP pass wait inside column_block_t / row_block_t, after
+  // issuing their vector loads (written by the previous pass); the rest wait here
+  if (mode == FIN_FUSED && blockIdx.x != 0 && !((force_op >= 0 ? force_op : cs.op) == OP_STEP)) pdl_wait();
   Ctl& c = cs;
   const int op = force_op >= 0 ? force_op : c.op;
   const bool timed = op == OP_STEP && unit_pass(c, op) && c.sstat;  // K2 timing of screened STEP passes
