@@ -161,7 +161,8 @@ constexpr int kHalfCols = 64;
 constexpr int kColBatch = 2;  // flagged tiles per round trip (register budget: 2 x 2 x NQ double2)
 
 template <int NQ>
-__device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j, double2 (&acc)[2][NQ]) {
+__device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j, double2 (&acc)[2][NQ],
+                                                 uint32_t m0 = 0u, bool has_m0 = false) {
 #pragma unroll
   for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -174,7 +175,8 @@ __device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j,
   const uint8_t* flags = c.tileflag + (imin64(j, c.n - 1) / kTileN);
   const bool v0 = j < c.n, v1 = j + kHalfCols < c.n;
   for (int64_t tc = ta; tc < tb; tc += 32) {
-    uint32_t m = warp_flag_mask(flags + (tc - c.t0) * c.U, c.U, tb - tc);
+    // (m0: the first 32 flags, read by the caller before waiting for K1b)
+    uint32_t m = (has_m0 && tc == ta) ? m0 : warp_flag_mask(flags + (tc - c.t0) * c.U, c.U, tb - tc);
     if (!v0) m = 0u;
     while (m) {
       int tk[kColBatch];
@@ -232,7 +234,8 @@ __device__ void column_group_partials(const Ctl& c, int b) {
 // Full column sums = pairwise combination of the 8 group sums (FIN_FUSED: the
 // groups are computed here; FIN_B: they come from the exchange buffer).
 template <int NQ>
-__device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_out, double* smem, int mode) {
+__device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_out, double* smem, int mode,
+                            uint32_t m0 = 0u, bool has_m0 = false) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int jj = threadIdx.x;
   j_out = (int64_t)b * kColsPerBlock + jj;
@@ -253,7 +256,7 @@ __device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_o
   }
   const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
   double2 acc[2][NQ];
-  group_column_sum<NQ>(c, warp, j, acc);
+  group_column_sum<NQ>(c, warp, j, acc, m0, has_m0);
   // smem [group][q][kColsPerBlock]
 #pragma unroll
   for (int h = 0; h < 2; ++h)
@@ -279,7 +282,7 @@ __device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_o
 }
 
 template <int NQ>
-__device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ]) {
+__device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ], uint32_t m0 = 0u, bool has_m0 = false) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) row[q] = 0.0;
   // screened-out tiles: partials +0.  A full warp of rows of one row tile
@@ -287,7 +290,9 @@ __device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ]) {
   const bool full = __activemask() == 0xffffffffu && c.TM % 32 == 0;
   const uint8_t* flags = c.tileflag + (imin64(i, c.m - 1) / c.TM) * c.U;
   for (int64_t uc = 0; uc < c.U; uc += 32) {
-    uint32_t m = full ? warp_flag_mask(flags + uc, 1, c.U - uc) : (i < c.m ? flag_mask(flags + uc, 1, c.U - uc) : 0u);
+    uint32_t m = (has_m0 && uc == 0) ? m0
+                 : full ? warp_flag_mask(flags + uc, 1, c.U - uc)
+                        : (i < c.m ? flag_mask(flags + uc, 1, c.U - uc) : 0u);
     if (i >= c.m) m = 0u;
     while (m) {
       int uk[4];
@@ -330,9 +335,19 @@ __device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* sm
     const double qj = own ? __ldcg(c.slot[c.sX].q + jp) : 0.0;
     const double gj = own ? __ldg(c.g + jp) : 0.0;
     const double qaj = own ? __ldcg(c.slot[c.sA].q + jp) : 0.0;
+    // this warp's group's tile flags: K0 wrote them, so they are read before the wait too
+    uint32_t m0 = 0u;
+    const bool has_m0 = mode == FIN_FUSED;
+    if (has_m0) {
+      const int g = threadIdx.x >> 5;
+      const int64_t ta = imax64((int64_t)g * c.GS, c.t0);
+      const int64_t tb = imin64(imin64((int64_t)(g + 1) * c.GS, c.Tg), c.t0 + c.T);
+      const int64_t jl = (int64_t)b * kColsPerBlock + (threadIdx.x & 31) * 2;
+      m0 = warp_flag_mask(c.tileflag + (imin64(jl, c.n - 1) / kTileN) + (ta - c.t0) * c.U, c.U, tb - ta);
+    }
     pdl_wait();  // (a programmatic dependent of K1b: its partials from here on; a no-op otherwise)
     double col[4];
-    column_sums<4>(c, b, col, j, smem, mode);
+    column_sums<4>(c, b, col, j, smem, mode, m0, has_m0);
     double qb = -INFINITY, qab = -INFINITY;  // screening bounds of q+ and the dual average
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       const double qn = qj + c.sigma * (gj - col[0]);        // pdhg.py:128
@@ -440,12 +455,13 @@ __device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* sm
 // ---------------------------------------------------------------------------
 // Tile scalars of row tile t (sum over its column tiles, in order; screened-out
 // tiles are +0), by one warp: the flag masks by ballot, then lanes < ns sum.
-__device__ __forceinline__ void tile_scalars(Ctl& c, int t, int ns, int nr, int lane) {
+__device__ __forceinline__ void tile_scalars(Ctl& c, int t, int ns, int nr, int lane, uint32_t m0 = 0u,
+                                             bool has_m0 = false) {
   const int tx = lane;
   const uint8_t* flags = c.tileflag + (int64_t)t * c.U;
   double acc = 0.0;
   for (int64_t uc = 0; uc < c.U; uc += 32) {
-    uint32_t m = warp_flag_mask(flags + uc, 1, c.U - uc);
+    uint32_t m = (has_m0 && uc == 0) ? m0 : warp_flag_mask(flags + uc, 1, c.U - uc);
     if (tx >= ns) m = 0u;
     while (m) {
       int uk[8];
@@ -485,8 +501,9 @@ __device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem)
   // others work on the rows (otherwise warp 0 does after them)
   const bool scal_early = c.TM <= kRedThreads - 32;
   if (scal_early && threadIdx.x >= kRedThreads - 32) {
+    const uint32_t m0 = warp_flag_mask(c.tileflag + (int64_t)t * c.U, 1, c.U);  // K0's flags, before the wait
     pdl_wait();
-    tile_scalars(c, t, ns, nr, threadIdx.x & 31);
+    tile_scalars(c, t, ns, nr, threadIdx.x & 31, m0, true);
   }
   for (int r = threadIdx.x; r < c.TM; r += kRedThreads) {
     const int64_t i = i0 + r;
@@ -496,9 +513,14 @@ __device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem)
       const double pi = ok ? __ldcg(c.slot[c.sX].p + i) : 0.0;
       const double fi = ok ? __ldg(c.f + i) : 0.0;
       const double pai = ok ? __ldcg(c.slot[c.sA].p + i) : 0.0;
+      // the row tile's first 32 flags (K0's) before the wait, as row_sums forms them
+      const int64_t ir = ok ? i : c.m;
+      const bool fullw = __activemask() == 0xffffffffu && c.TM % 32 == 0;
+      const uint8_t* fl = c.tileflag + (imin64(ir, c.m - 1) / c.TM) * c.U;
+      const uint32_t m0 = fullw ? warp_flag_mask(fl, 1, c.U) : (ir < c.m ? flag_mask(fl, 1, c.U) : 0u);
       pdl_wait();
       double row[4];
-      row_sums<4>(c, ok ? i : c.m, row);
+      row_sums<4>(c, ir, row, m0, true);
       double pb = -INFINITY, pab = -INFINITY;  // screening bounds of p+ and the dual average
       if (ok) {
         const double pn = pi + c.sigma * (fi - row[0]);       // pdhg.py:127
