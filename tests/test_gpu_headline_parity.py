@@ -196,6 +196,13 @@ def test_p2_headline(name):
         # P3: same termination, tolerance met
         assert rep.termination_reason == ref["termination_reason"]
         assert rep.final_relative_kkt <= fx["case"]["tol"]
+        if "pre_rounding_objective" in fx and fx["case"]["kind"] == "sqeuclid":
+            from paper_2407_19689_b200 import instances as inst
+
+            gpu_pre = float(np.vdot(inst.sqeuclid_grid_cost(fx["case"]["r"]), it.X))
+            ref_pre = fx["pre_rounding_objective"]
+            print(f"P3 {name}: gpu {rep.iterations} it, <C,X> {gpu_pre:.12f}; reference {ref['iterations']} it, "
+                  f"<C,X> {ref_pre:.12f}; rel {abs(gpu_pre - ref_pre) / abs(ref_pre):.2e}")
 
 
 def test_p3_c2_envelope():
