@@ -335,6 +335,8 @@ __device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* sm
     const double qj = own ? __ldcg(c.slot[c.sX].q + jp) : 0.0;
     const double gj = own ? __ldg(c.g + jp) : 0.0;
     const double qaj = own ? __ldcg(c.slot[c.sA].q + jp) : 0.0;
+    const bool srec = c.sr_on && !c.unit;  // slack certificates: this cell's drift counter
+    const double dq_old = (srec && own && (threadIdx.x & (kCell - 1)) == 0) ? __ldcg(c.sdq + jp / kCell) : 0.0;
     // this warp's group's tile flags: K0 wrote them, so they are read before the wait too
     uint32_t m0 = 0u;
     const bool has_m0 = mode == FIN_FUSED;
@@ -349,11 +351,13 @@ __device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* sm
     double col[4];
     column_sums<4>(c, b, col, j, smem, mode, m0, has_m0);
     double qb = -INFINITY, qab = -INFINITY;  // screening bounds of q+ and the dual average
+    double qdr = 0.0;                           // their drift (rounded up)
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       const double qn = qj + c.sigma * (gj - col[0]);        // pdhg.py:128
       const double dq = qn - qj;                              // pdhg.py:141
       c.slot[c.sXn].q[j] = qn;
       qb = qn;
+      if (srec) qdr = absdiff_ru(qn, qj);
       vals[0] = dq * dq;
       vals[1] = dq * col[1];
       const double pcx = col[2] - gj;                         // kkt.py:69
@@ -364,6 +368,7 @@ __device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* sm
         const double qan = qaj + div_by_count(qn - qaj, c.kd_dual, c.rkd_dual);  // pdhg.py:317
         c.slot[c.sAn].q[j] = qan;
         qab = qan;
+        if (srec) qdr = max_nan(qdr, absdiff_ru(qan, qaj));
         const double pca = col[3] - gj;
         vals[3] = pca * pca;
         vals[5] = gj * qan;
@@ -378,11 +383,13 @@ __device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* sm
       for (int msk = 1; msk < kCell; msk <<= 1) {
         qb = max_nan(qb, __shfl_xor_sync(gm, qb, msk));
         qab = max_nan(qab, __shfl_xor_sync(gm, qab, msk));
+        if (srec) qdr = max_nan(qdr, __shfl_xor_sync(gm, qdr, msk));
       }
       const int64_t cell = ((int64_t)b * kColsPerBlock + threadIdx.x) / kCell;
       if ((threadIdx.x & (kCell - 1)) == 0 && cell < c.ncells) {
         c.qmax[c.sXn * c.ncells + cell] = qb;
         if (!c.unit || c.unit_avg) c.qmax[c.sAn * c.ncells + cell] = qab;
+        if (srec) c.sdq[cell] = __dadd_ru(dq_old, qdr);
       }
     }
   } else if (op == OP_KKT) {
@@ -513,6 +520,8 @@ __device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem)
       const double pi = ok ? __ldcg(c.slot[c.sX].p + i) : 0.0;
       const double fi = ok ? __ldg(c.f + i) : 0.0;
       const double pai = ok ? __ldcg(c.slot[c.sA].p + i) : 0.0;
+      const bool srec = c.sr_on && !c.unit;  // slack certificates: this band's drift counter
+      const double dp_old = (srec && ok && (r & (kBand - 1)) == 0) ? __ldcg(c.sdp + i / kBand) : 0.0;
       // the row tile's first 32 flags (K0's) before the wait, as row_sums forms them
       const int64_t ir = ok ? i : c.m;
       const bool fullw = __activemask() == 0xffffffffu && c.TM % 32 == 0;
@@ -522,11 +531,13 @@ __device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem)
       double row[4];
       row_sums<4>(c, ir, row, m0, true);
       double pb = -INFINITY, pab = -INFINITY;  // screening bounds of p+ and the dual average
+      double pdr = 0.0;                           // their drift (rounded up)
       if (ok) {
         const double pn = pi + c.sigma * (fi - row[0]);       // pdhg.py:127
         const double dp = pn - pi;                             // pdhg.py:140
         c.slot[c.sXn].p[i] = pn;
         pb = pn;
+        if (srec) pdr = absdiff_ru(pn, pi);
         vals[0] += dp * dp;
         vals[1] += dp * row[1];
         const double prx = row[2] - fi;                        // kkt.py:68
@@ -537,6 +548,7 @@ __device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem)
           const double pan = pai + div_by_count(pn - pai, c.kd_dual, c.rkd_dual);  // pdhg.py:316
           c.slot[c.sAn].p[i] = pan;
           pab = pan;
+          if (srec) pdr = max_nan(pdr, absdiff_ru(pan, pai));
           const double pra = row[3] - fi;
           vals[3] += pra * pra;
           vals[5] += fi * pan;
@@ -551,11 +563,13 @@ __device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem)
         for (int msk = 1; msk < kBand; msk <<= 1) {
           pb = max_nan(pb, __shfl_xor_sync(gm, pb, msk));
           pab = max_nan(pab, __shfl_xor_sync(gm, pab, msk));
+          if (srec) pdr = max_nan(pdr, __shfl_xor_sync(gm, pdr, msk));
         }
         const int64_t band = i / kBand;
         if ((r & (kBand - 1)) == 0 && band < c.nbands) {
           c.pmax[c.sXn * c.nbands + band] = pb;
           if (!c.unit || c.unit_avg) c.pmax[c.sAn * c.nbands + band] = pab;
+          if (srec) c.sdp[band] = __dadd_ru(dp_old, pdr);
         }
       }
     } else if (op == OP_KKT) {
@@ -797,6 +811,8 @@ __device__ void do_restart(Ctl& c, int cand_slot, double cand_kkt) {
   c.outer += 1;
   c.inner = 0;
   c.sX = c.sA = c.sZ = c.sAsrc = cand_slot;
+  // new duals: every slack record written so far falls below the drift (record <= cap)
+  if (c.sr_on) c.sr_base = __dadd_ru(c.sr_base, 2.0 * c.sr_cap);
   c.lagA = 0;
   c.epoch_kkt = cand_kkt;
   c.prev_cand = cand_kkt;

@@ -227,6 +227,18 @@ struct Ctl {
   double* ccol;              // [nbands][kMaxNQ][ldx]  cell column partials (band partial of the tree)
   double* crow;              // [ncp][kMaxNQ][mpad]   cell row partials (8-lane butterfly per row)
   double* cscal;             // [nbands][ncp][kMaxNS] cell scalars
+  // Slack certificates (STEP passes of a solve): K1 records for every cell it
+  // computes a lower bound on min_ij (C_ij - p_i - q_j) over both dual pairs,
+  // shifted by the band / cell drift counters and the epoch base at that pass;
+  // K2 adds each pass's largest dual change per band / cell to the counters
+  // (rounded up), a restart adds 2 sr_cap to the base.  K0 drops a cell with
+  // no mass whose record still exceeds the drift since it was written, so
+  // p_i + q_j <= C_ij holds there exactly as the coarse bound would show.
+  double* srec;              // [nbands][ncells] record (NaN: none)
+  double* sdp;               // [nbands] cumulative band drift of p / p-average
+  double* sdq;               // [ncells] cumulative cell drift of q / q-average
+  double sr_base, sr_cap;    // epoch base; records are capped at sr_cap
+  int32_t sr_on, sr_pad_;
   unsigned long long* sstat; // [ST_COUNT]
   unsigned long long* kdbg;  // PDOT_K2_TRACE=1: per-block K2 timestamps of the last screened STEP pass
   unsigned long long* ktl;   // PDOT_K2_TRACE=1: pass timeline {K0, K1, K1b, K2} x {first start, last end}
@@ -358,6 +370,8 @@ __device__ __forceinline__ double mul_acc(double acc, double x, double y) { retu
 
 // max that propagates NaN (screening bounds: a NaN dual must keep its cells active)
 __device__ __forceinline__ double max_nan(double a, double b) { return (a > b || a != a) ? a : b; }
+// an upper bound on |a - b| (rounded up; NaN if either is NaN)
+__device__ __forceinline__ double absdiff_ru(double a, double b) { return max_nan(__dsub_ru(a, b), __dsub_ru(b, a)); }
 
 // numpy np.maximum(x, 0.0) for a scalar: NaN propagates, -0.0 stays -0.0
 __device__ __forceinline__ double relu_np(double x) { return x < 0.0 ? 0.0 : x; }

@@ -120,6 +120,9 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
     const bool okc = bound && tcell < c.ncells;
     const double Qc = okc ? __ldcg(c.qmax + sx * c.ncells + tcell) : -INFINITY;
     const double Qac = (okc && bound_avg) ? __ldcg(c.qmax + c.sA * c.ncells + tcell) : -INFINITY;
+    // slack certificates (STEP passes of a solve): the cells' drift counters
+    const bool use_rec = op == OP_STEP && !c.unit && c.sr_on;
+    const double dQc = (okc && use_rec) ? __ldcg(c.sdq + tcell) : 0.0;
     double P = -INFINITY, Pa = -INFINITY;
     for (int bl = lane; bound && bl < c.nbt; bl += 32) {
       const int64_t bnd = tt * c.nbt + bl;
@@ -167,12 +170,15 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
       const int64_t strip = tu * kWarps + s;
       const bool vstrip = strip < c.nstrips;
       const int64_t sstride = c.nbands * c.nstrips;
-      double Qk[kCellsPerStrip], Qak[kCellsPerStrip];
-#pragma unroll
-      for (int k = 0; k < kCellsPerStrip; ++k) {  // this lane's 4 cells: from the tile-level loads
-        Qk[k] = __shfl_sync(0xffffffffu, Qc, s * kCellsPerStrip + k);
-        Qak[k] = __shfl_sync(0xffffffffu, Qac, s * kCellsPerStrip + k);
-      }
+      // this lane's 4 cells' q bounds and drift counters: the tile-level loads,
+      // through shared memory (read where used, so they hold no registers)
+      __shared__ double qsh[kScreenWarps][3][32];
+      double(&qw)[3][32] = qsh[warp];
+      __syncwarp();  // the previous tile's reads are done
+      qw[0][lane] = Qc;
+      qw[1][lane] = Qac;
+      qw[2][lane] = dQc;
+      __syncwarp();
       uint32_t listed_all = 0;   // 4 bits per round
       uint32_t tb[kCellsPerStrip] = {0u, 0u, 0u, 0u};  // bct bits (band of the tile) of this lane's cells
       bool any_act = false;
@@ -185,7 +191,7 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
       for (int r0 = 0; r0 < kMaxRounds; r0 += kChunk) {
         if (r0 >= nrounds) break;
         uint32_t ox[kChunk], oa[kChunk], zx[kChunk], za[kChunk];
-        double Pb[kChunk], Pab[kChunk], mck[kChunk][kCellsPerStrip];
+        double Pb[kChunk], Pab[kChunk], mck[kChunk][kCellsPerStrip], dPb[kChunk], rk[kChunk][kCellsPerStrip];
         bool valid[kChunk];
 #pragma unroll
         for (int u = 0; u < kChunk; ++u) {
@@ -199,10 +205,12 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
           za[u] = (valid[u] && with_avg) ? __ldcg(c.occ + c.sA * sstride + ow) : 0u;
           Pb[u] = (valid[u] && bound) ? __ldcg(c.pmax + sx * c.nbands + band) : 0.0;
           Pab[u] = (valid[u] && bound_avg) ? __ldcg(c.pmax + c.sA * c.nbands + band) : 0.0;
+          dPb[u] = (valid[u] && use_rec) ? __ldcg(c.sdp + band) : 0.0;
 #pragma unroll
           for (int k = 0; k < kCellsPerStrip; ++k) {
             const int64_t cell = strip * kCellsPerStrip + k;
             mck[u][k] = (valid[u] && bound && cell < c.ncells) ? __ldcg(c.minc + band * c.ncells + cell) : 0.0;
+            rk[u][k] = (valid[u] && use_rec && cell < c.ncells) ? __ldcg(c.srec + band * c.ncells + cell) : 0.0;
           }
         }
 #pragma unroll
@@ -218,8 +226,15 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
               if (cell >= c.ncells) break;
               const uint32_t bx = (ox[u] >> (8 * k)) & 0xffu, ba = (oa[u] >> (8 * k)) & 0xffu;
               const uint32_t bzx = (zx[u] >> (8 * k)) & 0xffu, bza = (za[u] >> (8 * k)) & 0xffu;
-              const bool act = bx || ba || open || (bound && !(Pb[u] + Qk[k] <= mck[u][k])) ||
-                               (bound_avg && !(Pab[u] + Qak[k] <= mck[u][k]));
+              // a cell the coarse bound keeps is dropped when its slack record, less the
+              // drift since (all rounded down), is still positive: then p_i + q_j <= C_ij
+              // for both pairs (no certificate for a cell with a non-finite cost)
+              const int kc = s * kCellsPerStrip + k;
+              const bool coarse = (bound && !(Pb[u] + qw[0][kc] <= mck[u][k])) ||
+                                  (bound_avg && !(Pab[u] + qw[1][kc] <= mck[u][k]));
+              const bool cert = use_rec && mck[u][k] != -INFINITY &&
+                                __dsub_rd(__dsub_rd(__dsub_rd(rk[u][k], c.sr_base), dPb[u]), qw[2][kc]) > 0.0;
+              const bool act = bx || ba || open || (coarse && !cert);
               const uint32_t f = (act ? U_ACT : 0u) | (bx ? U_LDX : 0u) | (ba ? U_LDA : 0u) |
                                  (bzx ? U_ZX : 0u) | (bza ? U_ZA : 0u);
               word |= f << (8 * k);
@@ -334,6 +349,10 @@ struct KGeo {
   double* colpart;
   double* rowpart;
   double* tilescal;
+  // slack certificates (STEP cells of a solve when the control block's sr_on)
+  double* srec;
+  const double* sdp;
+  const double* sdq;
 };
 struct CellGeo {
   int64_t band, cell, strip, i0, j;
@@ -465,7 +484,8 @@ constexpr int kStP = 6 * kStMat;                   // p[8], then pa[8], q[16], q
 constexpr int kStPa = kStP + 8 * 8;
 constexpr int kStQ = kStPa + 8 * 8;
 constexpr int kStQa = kStQ + 16 * 8;
-constexpr int kStageBytes = kStQa + 16 * 8;        // 3.4 KB per warp and stage
+constexpr int kStD = kStQa + 16 * 8;               // the band's and the cell's drift counters
+constexpr int kStageBytes = kStD + 16;             // 3.4 KB per warp and stage
 constexpr int kStages = 3;                         // copies run two cells ahead
 constexpr size_t kUnitDynSmem = (size_t)kWarps * kStages * kStageBytes;
 
@@ -496,7 +516,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // q[L] (L < 16) or qa[L - 16] (L >= 16).
 template <bool IMPLICIT, bool AVG, class Cx>
 __device__ __forceinline__ void cell_issue(const StepOp& op, const Cx& c, uint32_t entry, uint32_t f,
-                                           unsigned char* stage) {
+                                           unsigned char* stage, bool sr) {
   const int lane = threadIdx.x & 31;
   const CellGeo g = cell_geo(c, entry);
   const bool act = (f & U_ACT) != 0;
@@ -527,13 +547,18 @@ __device__ __forceinline__ void cell_issue(const StepOp& op, const Cx& c, uint32
     const double* src = (lane < 16 ? op.q : op.qa) + (ok ? jc : 0);
     cp_async8(base + kStQ + lane * 8, src, ok);
   }
+  if (sr && lane < 2) {  // slack certificates: the drift counters the cell's record is shifted by
+    const bool ok = act;
+    const double* src = lane == 0 ? c.sdp + (ok ? g.band : 0) : c.sdq + (ok ? g.cell : 0);
+    cp_async8(base + kStD + lane * 8, src, ok);
+  }
 }
 
 template <bool IMPLICIT, bool AVG, class Cx>
 __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const Ctl& dyn, const CostGen& gen,
                                           uint32_t entry, uint32_t f,
                                           const unsigned char* stage, unsigned& bytes,
-                                          unsigned long long& cells) {
+                                          unsigned long long& cells, bool sr) {
   constexpr int NQ = StepOp::NQ, NS = StepOp::NS;
   const int lane = threadIdx.x & 31;
   const CellGeo g = cell_geo(c, entry);
@@ -575,6 +600,7 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const C
 #pragma unroll
   for (int s = 0; s < NS; ++s) sacc[s] = 0.0;
   bool nzx = false, nza = false;
+  double smin = INFINITY;  // slack certificate: min over the lane's entries, rounded down
 #pragma unroll
   for (int rr = 0; rr < 2; ++rr) {
     const int r = 2 * g.rg + rr;
@@ -586,6 +612,13 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const C
     if (okr[rr]) {  // StepOp::elem in the dense walkers' element order
       op.template elem<AVG>(cc[rr].x, xx[rr].x, aa[rr].x, pr[rr], qv[0], par[rr], qav[0], o0, sacc);
       if (g.v1) op.template elem<AVG>(cc[rr].y, xx[rr].y, aa[rr].y, pr[rr], qv[1], par[rr], qav[1], o1, sacc);
+      if (sr) {  // C - (p + q) and C - (pa + qa), each a lower bound of the exact value
+        smin = fmin(smin, fmin(__dsub_rd(cc[rr].x, __dadd_ru(pr[rr], qv[0])),
+                               __dsub_rd(cc[rr].x, __dadd_ru(par[rr], qav[0]))));
+        if (g.v1)
+          smin = fmin(smin, fmin(__dsub_rd(cc[rr].y, __dadd_ru(pr[rr], qv[1])),
+                                 __dsub_rd(cc[rr].y, __dadd_ru(par[rr], qav[1]))));
+      }
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -626,6 +659,15 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const C
   if (act) {
     cell_flush<NQ, NS>(c, g, o, sacc);
     if (lane == 0) bytes += (unsigned)(NQ * kCell + NQ * kBand + NS) * 8 * 2;
+    if (sr) {  // the cell's record: capped, shifted by the drift counters and the epoch base (rounded down)
+#pragma unroll
+      for (int msk = 16; msk >= 1; msk >>= 1) smin = fmin(smin, __shfl_xor_sync(0xffffffffu, smin, msk));
+      if (lane == 0) {
+        const double2 dd = *reinterpret_cast<const double2*>(stage + kStD);
+        const double rec = __dadd_rd(__dadd_rd(__dadd_rd(fmin(smin, dyn.sr_cap), dd.x), dd.y), dyn.sr_base);
+        c.srec[g.band * c.ncells + g.cell] = rec;
+      }
+    }
   }
 }
 
@@ -672,9 +714,10 @@ __device__ __forceinline__ void step_cells(const StepOp& o, const Cx& c, const C
   unsigned long long tp_first = 0, np = 0;
 #endif
   unsigned bytes32 = 0;  // this warp-lane's bytes (32-bit: a few hundred per cell)
-  cell_issue<IMPLICIT, AVG>(o, c, e0, f0, stages);
+  const bool sr = dyn.sr_on && !dyn.unit;  // slack certificates of this pass's cells
+  cell_issue<IMPLICIT, AVG>(o, c, e0, f0, stages, sr);
   cp_async_commit();
-  if (k0 + nw < ncells) cell_issue<IMPLICIT, AVG>(o, c, e1, f1, stages + kStageBytes);
+  if (k0 + nw < ncells) cell_issue<IMPLICIT, AVG>(o, c, e1, f1, stages + kStageBytes, sr);
   cp_async_commit();
   int st = 0;
   for (unsigned k = k0; k < ncells; k += nw) {
@@ -684,14 +727,14 @@ __device__ __forceinline__ void step_cells(const StepOp& o, const Cx& c, const C
       f3 = __ldcg(c.uflag + k + 3 * nw);
     }
     const int st2 = st == 0 ? 2 : st - 1;  // (st + 2) % 3
-    if (k + 2 * nw < ncells) cell_issue<IMPLICIT, AVG>(o, c, e2, f2, stages + st2 * kStageBytes);
+    if (k + 2 * nw < ncells) cell_issue<IMPLICIT, AVG>(o, c, e2, f2, stages + st2 * kStageBytes, sr);
     cp_async_commit();
     cp_async_wait<2>();  // this cell's copies have landed
 #ifdef PDOT_K1_PROF
     if (tp_first == 0) tp_first = globaltimer_ns();
     ++np;
 #endif
-    cell_step<IMPLICIT, AVG>(o, c, dyn, gen, e0, f0, stages + st * kStageBytes, bytes32, cells);
+    cell_step<IMPLICIT, AVG>(o, c, dyn, gen, e0, f0, stages + st * kStageBytes, bytes32, cells, sr);
     e0 = e1; f0 = f1;
     e1 = e2; f1 = f2;
     e2 = e3; f2 = f3;
@@ -1271,7 +1314,8 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
     const KGeo geo{h.m, h.n, h.ldx, h.ldc, h.mpad, h.nbands, h.nstrips, h.ncells, h.ncp, h.T, h.U,
                    h.nbands * h.nstrips, h.T * h.U, h.nbt, h.cbits, __builtin_ctz((unsigned)h.nbt), 0,
                    h.occ, h.tocc, h.ccol, h.crow, h.cscal, h.ulist, h.uflag, h.ucount,
-                   h.TM, h.bcr, h.bct, h.tlist, h.tcount, h.colpart, h.rowpart, h.tilescal};
+                   h.TM, h.bcr, h.bct, h.tlist, h.tcount, h.colpart, h.rowpart, h.tilescal,
+                   h.srec, h.sdp, h.sdq};
     unit_kernel<<<g1, kThreads, kUnitDynSmem, s>>>(ctl_dev, force_op, geo);
     tile_kernel<<<(unsigned)imin64(h.T * h.U * 3, (int64_t)sms * 4), kThreads, 0, s>>>(ctl_dev, force_op, geo);
   } else {

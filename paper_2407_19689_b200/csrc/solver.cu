@@ -337,6 +337,22 @@ void occ_invalidate(pdot_solver* h, int slot) {
   pdot::launch_tocc_fill(c, slot, 1, h->stream);
 }
 
+// Slack certificates start over with every solve (and resume): no records
+// (NaN), zero drift, base 0.  They need a finite positive cap (||C||_F >= every
+// |C_ij|); PDOT_SREC=0 turns them off.
+int srec_reset(pdot_solver* h) {
+  Ctl& c = h->host;
+  static const int env_on = getenv("PDOT_SREC") ? atoi(getenv("PDOT_SREC")) : 1;
+  c.sr_on = c.screen && c.srec && env_on && std::isfinite(c.cost_fro) && c.cost_fro > 0.0;
+  c.sr_cap = c.sr_on ? c.cost_fro : 0.0;
+  c.sr_base = 0.0;
+  if (!c.sr_on) return PDOT_OK;
+  CK(cudaMemsetAsync(c.srec, 0xff, (size_t)c.nbands * c.ncells * sizeof(double), h->stream));
+  CK(cudaMemsetAsync(c.sdp, 0, (size_t)c.nbands * sizeof(double), h->stream));
+  CK(cudaMemsetAsync(c.sdq, 0, (size_t)c.ncells * sizeof(double), h->stream));
+  return PDOT_OK;
+}
+
 // (re)build min C for the bound problem when screening is on
 int screen_setup(pdot_solver* h) {
   Ctl& c = h->host;
@@ -660,6 +676,9 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     const size_t o_stat = take(pdot::ST_COUNT * sizeof(unsigned long long));
     const size_t o_tocc = take(pdot::kNSlot * tiles);
     const size_t o_tminc = take(tiles * sizeof(double));
+    const size_t o_srec = take(nbands * ncells * sizeof(double));
+    const size_t o_sdp = take(nbands * sizeof(double));
+    const size_t o_sdq = take(ncells * sizeof(double));
     // cell partials of screened passes (written sparsely, read back only where
     // the bit maps say so: never zeroed)
     const size_t o_ccol = take(nbands * pdot::kMaxNQ * h->ldx * sizeof(double));
@@ -693,6 +712,9 @@ int pdot_create_shard(int64_t m_total, int64_t n, int nranks, int rank, int devi
     c.tcount = reinterpret_cast<unsigned*>(base + o_tcount);
     c.tocc = reinterpret_cast<uint8_t*>(base + o_tocc);
     c.tminc = reinterpret_cast<const double*>(base + o_tminc);
+    c.srec = reinterpret_cast<double*>(base + o_srec);
+    c.sdp = reinterpret_cast<double*>(base + o_sdp);
+    c.sdq = reinterpret_cast<double*>(base + o_sdq);
     c.ccol = reinterpret_cast<double*>(base + o_ccol);
     c.crow = reinterpret_cast<double*>(base + o_crow);
     c.cscal = reinterpret_cast<double*>(base + o_cscal);
@@ -1094,6 +1116,7 @@ int pdot_begin(pdot_solver* h, const pdot_config* cfg, double elapsed_before_s) 
   memset((void*)h->status_h, 0, sizeof(pdot::Status));
   h->ring_tail = 0;
   h->events.clear();
+  if (int rc = srec_reset(h)) return rc;
   if (int rc = upload_ctl(h)) return rc;
   if (c.sstat)  // the pass-gap statistics start over: no gap across the host's work between solves
     CK(cudaMemsetAsync(c.sstat + pdot::ST_K2_END, 0, sizeof(unsigned long long), h->stream));
@@ -1172,6 +1195,7 @@ int pdot_resume(pdot_solver* h, int64_t max_iters, pdot_result* res) {
   c.stop_request = 0;
   memset((void*)h->status_h, 0, sizeof(pdot::Status));
   h->status_h->ring_head = c.ring_head;
+  if (int rc = srec_reset(h)) return rc;
   if (int rc = upload_ctl(h)) return rc;
   CK(cudaEventRecord(h->t0, h->stream));
   const auto wall0 = std::chrono::steady_clock::now();
