@@ -158,7 +158,8 @@ __device__ __forceinline__ uint32_t warp_flag_mask(const uint8_t* f, int64_t str
 
 // A lane owns two column pairs of the block: j and j + kColsPerBlock / 2.
 constexpr int kHalfCols = 64;
-constexpr int kColBatch = 2;  // flagged tiles per round trip (register budget: 2 x 2 x NQ double2)
+constexpr int kColBatch = 2;  // flagged tiles per round trip (register budget: 2 x 2 x NQ double2;
+                              // 3 per round trip: no gain, 4: K2 +2.3 us, spills)
 
 template <int NQ>
 __device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j, double2 (&acc)[2][NQ],

@@ -80,6 +80,11 @@ __device__ __forceinline__ bool step_with_avg(const Ctl& c) { return c.unit ? c.
 // bit maps K2 reads the cell partials by: bcr (per band and column tile) and
 // bct (per row tile and cell).
 // ---------------------------------------------------------------------------
+// PDOT_K0_PROF (measurement builds only): phase times of the cell-by-cell tiles,
+// summed over a solve, printed by K0 at pass 600
+#ifdef PDOT_K0_PROF
+__device__ unsigned long long g_k0prof[8];
+#endif
 constexpr int kScreenWarps = 8;
 constexpr int kScreenCtasPerSm = 2;  // 128 registers; 3 or 4 per SM spill and run slower (C3 11.4k -> 11.3k / 10.7k iter/s)
 
@@ -106,11 +111,29 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t tiles = c.T * c.U;
+#ifdef PDOT_K0_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0 && c.passes == 600 && op == OP_STEP) {
+    const double n = (double)g_k0prof[0];
+    printf("K0PROF cell-by-cell tiles %.0f per pass; per tile (ns): tile start->flags decided %.0f, ->chunks done %.0f, "
+           "->list slots %.0f, ->end %.0f; kernel entry->first tile %.0f\n",
+           n / 600.0, g_k0prof[1] / n, g_k0prof[2] / n, g_k0prof[3] / n, g_k0prof[4] / n, g_k0prof[5] / (double)g_k0prof[6]);
+  }
+  const unsigned long long tk_entry = globaltimer_ns();
+  bool first_tile = true;
+#endif
   // persistent: one wave of CTAs, each warp walks tiles warp, warp + nw, ...
   for (int64_t tile = (int64_t)blockIdx.x * kScreenWarps + warp; tile < tiles;
        tile += (int64_t)gridDim.x * kScreenWarps) {
     // 32-bit division: tile indices fit (T * U < 2^31), and the 64-bit one is a subroutine call
     const int64_t tt = (uint32_t)tile / (uint32_t)c.U, tu = tile - tt * c.U;
+#ifdef PDOT_K0_PROF
+    const unsigned long long tp0 = globaltimer_ns();
+    if (first_tile && lane == 0 && op == OP_STEP) {
+      atomicAdd(&g_k0prof[5], tp0 - tk_entry);
+      atomicAdd(&g_k0prof[6], 1ull);
+    }
+    first_tile = false;
+#endif
     const bool with_avg = op == OP_STEP && step_with_avg(c);
     const bool bound = op != OP_DIST, bound_avg = op == OP_STEP;
     const int sx = op == OP_DIST ? c.sCand : c.sX;
@@ -156,6 +179,9 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
     if (!full) {
       if (lane == 0) c.tileflag[tile] = 0;
     } else {
+#ifdef PDOT_K0_PROF
+      const unsigned long long tp1 = globaltimer_ns();
+#endif
       if (lane == 0) {
         // the output slots' tile summaries are rebuilt by K1 from the cells it writes
         if (op == OP_STEP) c.tocc[c.sXn * tiles + tile] = 0;
@@ -259,6 +285,9 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
         }
       }
       // warp-aggregated append of the listed cells: one atomic per tile
+#ifdef PDOT_K0_PROF
+      const unsigned long long tp2 = globaltimer_ns();
+#endif
       const int cnt = __popc(listed_all);
       int incl = cnt;
 #pragma unroll
@@ -274,6 +303,9 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
       unsigned base = 0;
       if (lane == 31 && tot) base = atomicAdd(c.ucount, (unsigned)tot);
       base = __shfl_sync(0xffffffffu, base, 31);
+#ifdef PDOT_K0_PROF
+      const unsigned long long tp3 = globaltimer_ns();
+#endif
       unsigned pos = base + (unsigned)(incl - cnt);
 #pragma unroll
       for (int rd = 0; rd < kMaxRounds; ++rd) {
@@ -303,6 +335,16 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
         c.tileflag[tile] = any ? 1 : 0;
         if (any) c.tlist[tslot] = (int32_t)tile;
       }
+#ifdef PDOT_K0_PROF
+      if (lane == 0 && op == OP_STEP) {
+        const unsigned long long tp4 = globaltimer_ns();
+        atomicAdd(&g_k0prof[0], 1ull);
+        atomicAdd(&g_k0prof[1], tp1 - tp0);
+        atomicAdd(&g_k0prof[2], tp2 - tp0);
+        atomicAdd(&g_k0prof[3], tp3 - tp0);
+        atomicAdd(&g_k0prof[4], tp4 - tp0);
+      }
+#endif
     }
   }
   if (tl) {
