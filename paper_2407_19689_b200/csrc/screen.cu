@@ -146,13 +146,13 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
     // slack certificates (STEP passes of a solve): the cells' drift counters
     const bool use_rec = op == OP_STEP && !c.unit && c.sr_on;
     const double dQc = (okc && use_rec) ? __ldcg(c.sdq + tcell) : 0.0;
-    double P = -INFINITY, Pa = -INFINITY;
-    for (int bl = lane; bound && bl < c.nbt; bl += 32) {
-      const int64_t bnd = tt * c.nbt + bl;
-      if (bnd >= c.nbands) break;
-      P = max_nan(P, __ldcg(c.pmax + sx * c.nbands + bnd));
-      if (bound_avg) Pa = max_nan(Pa, __ldcg(c.pmax + c.sA * c.nbands + bnd));
-    }
+    // lane bl < nbt (<= 32): band bl's maxima of p (current, average) and drift counter
+    const int64_t lbnd = tt * c.nbt + lane;
+    const bool okb = bound && lane < c.nbt && lbnd < c.nbands;
+    const double Pl = okb ? __ldcg(c.pmax + sx * c.nbands + lbnd) : -INFINITY;
+    const double Pal = (okb && bound_avg) ? __ldcg(c.pmax + c.sA * c.nbands + lbnd) : -INFINITY;
+    const double dPl = (okb && use_rec) ? __ldcg(c.sdp + lbnd) : 0.0;
+    double P = Pl, Pa = Pal;
     uint32_t occ_any = 0;
     double mc = INFINITY;
     if (lane == 0) {
@@ -198,12 +198,15 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
       const int64_t sstride = c.nbands * c.nstrips;
       // this lane's 4 cells' q bounds and drift counters: the tile-level loads,
       // through shared memory (read where used, so they hold no registers)
-      __shared__ double qsh[kScreenWarps][3][32];
-      double(&qw)[3][32] = qsh[warp];
+      __shared__ double qsh[kScreenWarps][6][32];
+      double(&qw)[6][32] = qsh[warp];
       __syncwarp();  // the previous tile's reads are done
       qw[0][lane] = Qc;
       qw[1][lane] = Qac;
       qw[2][lane] = dQc;
+      qw[3][lane] = Pl;  // ... and the bands' (lane = band of the tile)
+      qw[4][lane] = Pal;
+      qw[5][lane] = dPl;
       __syncwarp();
       uint32_t listed_all = 0;   // 4 bits per round
       uint32_t tb[kCellsPerStrip] = {0u, 0u, 0u, 0u};  // bct bits (band of the tile) of this lane's cells
@@ -211,13 +214,16 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
       const int nrounds = (c.nbt + 3) >> 2;
       // rounds in chunks of kChunk: every load of a chunk is issued before its
       // flags are computed and stored (one memory round trip per chunk)
-      constexpr int kChunk = 2, kMaxRounds = 8;  // nbt <= 32
+#ifndef PDOT_K0_CHUNK
+#define PDOT_K0_CHUNK 2
+#endif
+      constexpr int kChunk = PDOT_K0_CHUNK, kMaxRounds = 8;  // nbt <= 32
       uint32_t words[kMaxRounds];  // flag words of the rounds (static indices: unrolled)
 #pragma unroll
       for (int r0 = 0; r0 < kMaxRounds; r0 += kChunk) {
         if (r0 >= nrounds) break;
         uint32_t ox[kChunk], oa[kChunk], zx[kChunk], za[kChunk];
-        double Pb[kChunk], Pab[kChunk], mck[kChunk][kCellsPerStrip], dPb[kChunk], rk[kChunk][kCellsPerStrip];
+        double mck[kChunk][kCellsPerStrip], rk[kChunk][kCellsPerStrip];
         bool valid[kChunk];
 #pragma unroll
         for (int u = 0; u < kChunk; ++u) {
@@ -229,9 +235,6 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
           oa[u] = (valid[u] && (op == OP_DIST || with_avg)) ? __ldcg(c.occ + sa * sstride + ow) : 0u;
           zx[u] = (valid[u] && op == OP_STEP) ? __ldcg(c.occ + c.sXn * sstride + ow) : 0u;
           za[u] = (valid[u] && with_avg) ? __ldcg(c.occ + c.sA * sstride + ow) : 0u;
-          Pb[u] = (valid[u] && bound) ? __ldcg(c.pmax + sx * c.nbands + band) : 0.0;
-          Pab[u] = (valid[u] && bound_avg) ? __ldcg(c.pmax + c.sA * c.nbands + band) : 0.0;
-          dPb[u] = (valid[u] && use_rec) ? __ldcg(c.sdp + band) : 0.0;
 #pragma unroll
           for (int k = 0; k < kCellsPerStrip; ++k) {
             const int64_t cell = strip * kCellsPerStrip + k;
@@ -256,10 +259,10 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
               // drift since (all rounded down), is still positive: then p_i + q_j <= C_ij
               // for both pairs (no certificate for a cell with a non-finite cost)
               const int kc = s * kCellsPerStrip + k;
-              const bool coarse = (bound && !(Pb[u] + qw[0][kc] <= mck[u][k])) ||
-                                  (bound_avg && !(Pab[u] + qw[1][kc] <= mck[u][k]));
+              const bool coarse = (bound && !(qw[3][bl] + qw[0][kc] <= mck[u][k])) ||
+                                  (bound_avg && !(qw[4][bl] + qw[1][kc] <= mck[u][k]));
               const bool cert = use_rec && mck[u][k] != -INFINITY &&
-                                __dsub_rd(__dsub_rd(__dsub_rd(rk[u][k], c.sr_base), dPb[u]), qw[2][kc]) > 0.0;
+                                __dsub_rd(__dsub_rd(__dsub_rd(rk[u][k], c.sr_base), qw[5][bl]), qw[2][kc]) > 0.0;
               const bool act = bx || ba || open || (coarse && !cert);
               const uint32_t f = (act ? U_ACT : 0u) | (bx ? U_LDX : 0u) | (ba ? U_LDA : 0u) |
                                  (bzx ? U_ZX : 0u) | (bza ? U_ZA : 0u);
