@@ -34,6 +34,7 @@
 //   over all tiles.
 // K2 (finalize.cu) skips tiles whose flag is 0: their partials are +0.
 #include <stdio.h>
+#include <limits.h>
 #include <stdlib.h>
 
 #include <string>
@@ -705,11 +706,16 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const C
     cell_flush<NQ, NS>(c, g, o, sacc);
     if (lane == 0) bytes += (unsigned)(NQ * kCell + NQ * kBand + NS) * 8 * 2;
     if (sr) {  // the cell's record: capped, shifted by the drift counters and the epoch base (rounded down)
-#pragma unroll
-      for (int msk = 16; msk >= 1; msk >>= 1) smin = fmin(smin, __shfl_xor_sync(0xffffffffu, smin, msk));
+      // warp minimum in one REDUX: the high word of a positive double orders like
+      // the double and, with the low word cleared, rounds it down; a slack <= 0
+      // (or NaN) in any lane means no certificate
+      const int key = smin > 0.0 ? __double2hiint(smin) : INT_MIN;
+      const int kmin = __reduce_min_sync(0xffffffffu, key);
       if (lane == 0) {
         const double2 dd = *reinterpret_cast<const double2*>(stage + kStD);
-        const double rec = __dadd_rd(__dadd_rd(__dadd_rd(fmin(smin, dyn.sr_cap), dd.x), dd.y), dyn.sr_base);
+        const double rec = kmin > 0 ? __dadd_rd(__dadd_rd(__dadd_rd(fmin(__hiloint2double(kmin, 0), dyn.sr_cap),
+                                                                    dd.x), dd.y), dyn.sr_base)
+                                    : -INFINITY;
         c.srec[g.band * c.ncells + g.cell] = rec;
       }
     }
