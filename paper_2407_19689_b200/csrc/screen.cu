@@ -81,6 +81,46 @@ __device__ __forceinline__ bool step_with_avg(const Ctl& c) { return c.unit ? c.
 // bit maps K2 reads the cell partials by: bcr (per band and column tile) and
 // bct (per row tile and cell).
 // ---------------------------------------------------------------------------
+// K1's fixed geometry (set once per handle) travels as a KERNEL PARAMETER: its
+// fields sit in the constant bank and feed instructions directly, instead of
+// being reloaded from the control block in global memory for every cell (the
+// 128-register budget does not keep them all live).  KGeo exposes the same
+// member names as Ctl, so the cell functions are templates over the context
+// type; the per-pass output slots come from the control block (dyn).  ldc is
+// fixed while the problem is bound: pdot_set_problem drops the captured graph
+// when it changes.
+struct KGeo {
+  int64_t m, n, ldx, ldc, mpad, nbands, nstrips, ncells, ncp, T, U;
+  int64_t occ_stride, tiles;  // nbands * nstrips, T * U
+  int32_t nbt, cbits, nbt_log2, pad_;
+  uint32_t* occ;
+  uint8_t* tocc;
+  double* ccol;
+  double* crow;
+  double* cscal;
+  uint32_t* ulist;
+  uint8_t* uflag;
+  unsigned int* ucount;
+  // K1b (tile_kernel): the bit maps, tile list and per-tile partials it writes
+  int64_t TM;
+  uint32_t* bcr;
+  uint32_t* bct;
+  int32_t* tlist;
+  unsigned int* tcount;
+  double* colpart;
+  double* rowpart;
+  double* tilescal;
+  // slack certificates (STEP cells of a solve when the control block's sr_on)
+  double* srec;
+  const double* sdp;
+  const double* sdq;
+  // K0 (screen_kernel): the bounds it reads and the flags it writes
+  const double* qmax;
+  const double* pmax;
+  const double* minc;
+  const double* tminc;
+  uint8_t* tileflag;
+};
 // PDOT_K0_PROF (measurement builds only): phase times of the cell-by-cell tiles,
 // summed over a solve, printed by K0 at pass 600
 #ifdef PDOT_K0_PROF
@@ -90,7 +130,8 @@ constexpr int kScreenWarps = 8;
 constexpr int kScreenCtasPerSm = 2;  // 128 registers; 3 or 4 per SM spill and run slower (C3 11.4k -> 11.3k / 10.7k iter/s)
 
 __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_kernel(const Ctl* __restrict__ ctlp, int force_op,
-                                                                                     unsigned long long* sstat0) {
+                                                                                     unsigned long long* sstat0,
+                                                                                     const KGeo g) {
   if (sstat0 && blockIdx.x == 0 && threadIdx.x == 0) sstat0[ST_K0_ENTRY] = globaltimer_ns();
   __shared__ Ctl ctl_s;  // the control block, one round trip for all fields
   ctl_to_shared(ctlp, &ctl_s);
@@ -111,7 +152,7 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
     c.sstat[ST_K2_END] = 0;  // only a STEP pass right after a STEP pass counts a gap
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t tiles = c.T * c.U;
+  const int64_t tiles = g.tiles;
 #ifdef PDOT_K0_PROF
   if (blockIdx.x == 0 && threadIdx.x == 0 && c.passes == 600 && op == OP_STEP) {
     const double n = (double)g_k0prof[0];
@@ -126,7 +167,7 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
   for (int64_t tile = (int64_t)blockIdx.x * kScreenWarps + warp; tile < tiles;
        tile += (int64_t)gridDim.x * kScreenWarps) {
     // 32-bit division: tile indices fit (T * U < 2^31), and the 64-bit one is a subroutine call
-    const int64_t tt = (uint32_t)tile / (uint32_t)c.U, tu = tile - tt * c.U;
+    const int64_t tt = (uint32_t)tile / (uint32_t)g.U, tu = tile - tt * g.U;
 #ifdef PDOT_K0_PROF
     const unsigned long long tp0 = globaltimer_ns();
     if (first_tile && lane == 0 && op == OP_STEP) {
@@ -141,27 +182,27 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
     const int sa = op == OP_DIST ? c.sZ : c.sAsrc;
     // ---- tile level: 32 cell maxima of q, nbt band maxima of p, min C, occupancy
     const int64_t tcell = tu * 32 + lane;
-    const bool okc = bound && tcell < c.ncells;
-    const double Qc = okc ? __ldcg(c.qmax + sx * c.ncells + tcell) : -INFINITY;
-    const double Qac = (okc && bound_avg) ? __ldcg(c.qmax + c.sA * c.ncells + tcell) : -INFINITY;
+    const bool okc = bound && tcell < g.ncells;
+    const double Qc = okc ? __ldcg(g.qmax + sx * g.ncells + tcell) : -INFINITY;
+    const double Qac = (okc && bound_avg) ? __ldcg(g.qmax + c.sA * g.ncells + tcell) : -INFINITY;
     // slack certificates (STEP passes of a solve): the cells' drift counters
     const bool use_rec = op == OP_STEP && !c.unit && c.sr_on;
-    const double dQc = (okc && use_rec) ? __ldcg(c.sdq + tcell) : 0.0;
+    const double dQc = (okc && use_rec) ? __ldcg(g.sdq + tcell) : 0.0;
     // lane bl < nbt (<= 32): band bl's maxima of p (current, average) and drift counter
-    const int64_t lbnd = tt * c.nbt + lane;
-    const bool okb = bound && lane < c.nbt && lbnd < c.nbands;
-    const double Pl = okb ? __ldcg(c.pmax + sx * c.nbands + lbnd) : -INFINITY;
-    const double Pal = (okb && bound_avg) ? __ldcg(c.pmax + c.sA * c.nbands + lbnd) : -INFINITY;
-    const double dPl = (okb && use_rec) ? __ldcg(c.sdp + lbnd) : 0.0;
+    const int64_t lbnd = tt * g.nbt + lane;
+    const bool okb = bound && lane < g.nbt && lbnd < g.nbands;
+    const double Pl = okb ? __ldcg(g.pmax + sx * g.nbands + lbnd) : -INFINITY;
+    const double Pal = (okb && bound_avg) ? __ldcg(g.pmax + c.sA * g.nbands + lbnd) : -INFINITY;
+    const double dPl = (okb && use_rec) ? __ldcg(g.sdp + lbnd) : 0.0;
     double P = Pl, Pa = Pal;
     uint32_t occ_any = 0;
     double mc = INFINITY;
     if (lane == 0) {
-      occ_any = __ldcg(c.tocc + sx * tiles + tile);
-      if (op == OP_DIST || with_avg) occ_any |= __ldcg(c.tocc + sa * tiles + tile);
-      if (op == OP_STEP) occ_any |= __ldcg(c.tocc + c.sXn * tiles + tile);
-      if (with_avg) occ_any |= __ldcg(c.tocc + c.sA * tiles + tile);
-      if (bound) mc = __ldcg(c.tminc + tile);
+      occ_any = __ldcg(g.tocc + sx * tiles + tile);
+      if (op == OP_DIST || with_avg) occ_any |= __ldcg(g.tocc + sa * tiles + tile);
+      if (op == OP_STEP) occ_any |= __ldcg(g.tocc + c.sXn * tiles + tile);
+      if (with_avg) occ_any |= __ldcg(g.tocc + c.sA * tiles + tile);
+      if (bound) mc = __ldcg(g.tminc + tile);
     }
     double Q = Qc, Qa = Qac;
 #pragma unroll
@@ -178,25 +219,25 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
                       (bound && !(P + Q <= __shfl_sync(0xffffffffu, mc, 0))) ||
                       (bound_avg && !(Pa + Qa <= __shfl_sync(0xffffffffu, mc, 0)));
     if (!full) {
-      if (lane == 0) c.tileflag[tile] = 0;
+      if (lane == 0) g.tileflag[tile] = 0;
     } else {
 #ifdef PDOT_K0_PROF
       const unsigned long long tp1 = globaltimer_ns();
 #endif
       if (lane == 0) {
         // the output slots' tile summaries are rebuilt by K1 from the cells it writes
-        if (op == OP_STEP) c.tocc[c.sXn * tiles + tile] = 0;
-        if (with_avg) c.tocc[c.sA * tiles + tile] = 0;
+        if (op == OP_STEP) g.tocc[c.sXn * tiles + tile] = 0;
+        if (with_avg) g.tocc[c.sA * tiles + tile] = 0;
         // metadata traffic of a per-cell screen: per (band, strip) min C and the
         // cell maxima of q (current, average), 4 occupancy words, the flag word
         if (op == OP_STEP && c.sstat)
-          atomicAdd(&c.sstat[ST_META], (unsigned long long)c.nbt * kWarps * (kCellsPerStrip * 8 * 3 + 4 * 4 + 4));
+          atomicAdd(&c.sstat[ST_META], (unsigned long long)g.nbt * kWarps * (kCellsPerStrip * 8 * 3 + 4 * 4 + 4));
       }
       // ---- per cell: lane (bq, s) covers bands bq, bq + 4, ... of strip s
       const int s = lane & 7, bq = lane >> 3;
       const int64_t strip = tu * kWarps + s;
-      const bool vstrip = strip < c.nstrips;
-      const int64_t sstride = c.nbands * c.nstrips;
+      const bool vstrip = strip < g.nstrips;
+      const int64_t sstride = g.occ_stride;
       // this lane's 4 cells' q bounds and drift counters: the tile-level loads,
       // through shared memory (read where used, so they hold no registers)
       __shared__ double qsh[kScreenWarps][6][32];
@@ -212,7 +253,7 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
       uint32_t listed_all = 0;   // 4 bits per round
       uint32_t tb[kCellsPerStrip] = {0u, 0u, 0u, 0u};  // bct bits (band of the tile) of this lane's cells
       bool any_act = false;
-      const int nrounds = (c.nbt + 3) >> 2;
+      const int nrounds = (g.nbt + 3) >> 2;
       // rounds in chunks of kChunk: every load of a chunk is issued before its
       // flags are computed and stored (one memory round trip per chunk)
 #ifndef PDOT_K0_CHUNK
@@ -229,31 +270,31 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
 #pragma unroll
         for (int u = 0; u < kChunk; ++u) {
           const int bl = (r0 + u) * 4 + bq;
-          const int64_t band = tt * c.nbt + bl;
-          valid[u] = r0 + u < nrounds && bl < c.nbt && band < c.nbands && vstrip;
-          const int64_t ow = band * c.nstrips + strip;
-          ox[u] = valid[u] ? __ldcg(c.occ + sx * sstride + ow) : 0u;
-          oa[u] = (valid[u] && (op == OP_DIST || with_avg)) ? __ldcg(c.occ + sa * sstride + ow) : 0u;
-          zx[u] = (valid[u] && op == OP_STEP) ? __ldcg(c.occ + c.sXn * sstride + ow) : 0u;
-          za[u] = (valid[u] && with_avg) ? __ldcg(c.occ + c.sA * sstride + ow) : 0u;
+          const int64_t band = tt * g.nbt + bl;
+          valid[u] = r0 + u < nrounds && bl < g.nbt && band < g.nbands && vstrip;
+          const int64_t ow = band * g.nstrips + strip;
+          ox[u] = valid[u] ? __ldcg(g.occ + sx * sstride + ow) : 0u;
+          oa[u] = (valid[u] && (op == OP_DIST || with_avg)) ? __ldcg(g.occ + sa * sstride + ow) : 0u;
+          zx[u] = (valid[u] && op == OP_STEP) ? __ldcg(g.occ + c.sXn * sstride + ow) : 0u;
+          za[u] = (valid[u] && with_avg) ? __ldcg(g.occ + c.sA * sstride + ow) : 0u;
 #pragma unroll
           for (int k = 0; k < kCellsPerStrip; ++k) {
             const int64_t cell = strip * kCellsPerStrip + k;
-            mck[u][k] = (valid[u] && bound && cell < c.ncells) ? __ldcg(c.minc + band * c.ncells + cell) : 0.0;
-            rk[u][k] = (valid[u] && use_rec && cell < c.ncells) ? __ldcg(c.srec + band * c.ncells + cell) : 0.0;
+            mck[u][k] = (valid[u] && bound && cell < g.ncells) ? __ldcg(g.minc + band * g.ncells + cell) : 0.0;
+            rk[u][k] = (valid[u] && use_rec && cell < g.ncells) ? __ldcg(g.srec + band * g.ncells + cell) : 0.0;
           }
         }
 #pragma unroll
         for (int u = 0; u < kChunk; ++u) {
           const int rd = r0 + u;
           const int bl = rd * 4 + bq;
-          const int64_t band = tt * c.nbt + bl;
+          const int64_t band = tt * g.nbt + bl;
           uint32_t word = 0;
           if (valid[u]) {
 #pragma unroll
             for (int k = 0; k < kCellsPerStrip; ++k) {
               const int64_t cell = strip * kCellsPerStrip + k;
-              if (cell >= c.ncells) break;
+              if (cell >= g.ncells) break;
               const uint32_t bx = (ox[u] >> (8 * k)) & 0xffu, ba = (oa[u] >> (8 * k)) & 0xffu;
               const uint32_t bzx = (zx[u] >> (8 * k)) & 0xffu, bza = (za[u] >> (8 * k)) & 0xffu;
               // a cell the coarse bound keeps is dropped when its slack record, less the
@@ -285,7 +326,7 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
           uint32_t rbits = actb << (4 * s);
 #pragma unroll
           for (int msk = 1; msk < 8; msk <<= 1) rbits |= __shfl_xor_sync(0xffffffffu, rbits, msk);
-          if (s == 0 && rd < nrounds && bl < c.nbt && band < c.nbands) c.bcr[band * c.U + tu] = rbits;
+          if (s == 0 && rd < nrounds && bl < g.nbt && band < g.nbands) g.bcr[band * g.U + tu] = rbits;
         }
       }
       // warp-aggregated append of the listed cells: one atomic per tile
@@ -303,9 +344,9 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
       // both list appends in flight together: the tile list (lane 0) and the cells (lane 31)
       const bool any = __any_sync(0xffffffffu, any_act);
       unsigned tslot = 0;
-      if (lane == 0 && any) tslot = atomicAdd(c.tcount, 1u);
+      if (lane == 0 && any) tslot = atomicAdd(g.tcount, 1u);
       unsigned base = 0;
-      if (lane == 31 && tot) base = atomicAdd(c.ucount, (unsigned)tot);
+      if (lane == 31 && tot) base = atomicAdd(g.ucount, (unsigned)tot);
       base = __shfl_sync(0xffffffffu, base, 31);
 #ifdef PDOT_K0_PROF
       const unsigned long long tp3 = globaltimer_ns();
@@ -315,12 +356,12 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
       for (int rd = 0; rd < kMaxRounds; ++rd) {
         if (rd >= nrounds) break;
         const uint32_t l4 = (listed_all >> (4 * rd)) & 0xfu;
-        const int64_t band = tt * c.nbt + rd * 4 + bq;
+        const int64_t band = tt * g.nbt + rd * 4 + bq;
 #pragma unroll
         for (int k = 0; k < kCellsPerStrip; ++k)
           if ((l4 >> k) & 1u) {
-            c.ulist[pos] = cell_entry(band, strip * kCellsPerStrip + k, c.cbits);
-            c.uflag[pos] = (uint8_t)((words[rd] >> (8 * k)) & 0xffu);  // the cell's flags travel with it
+            g.ulist[pos] = cell_entry(band, strip * kCellsPerStrip + k, g.cbits);
+            g.uflag[pos] = (uint8_t)((words[rd] >> (8 * k)) & 0xffu);  // the cell's flags travel with it
             ++pos;
           }
       }
@@ -332,12 +373,12 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
       }
       if (bq == 0) {
 #pragma unroll
-        for (int k = 0; k < kCellsPerStrip; ++k) c.bct[tt * c.ncp + tu * 32 + s * kCellsPerStrip + k] = tb[k];
+        for (int k = 0; k < kCellsPerStrip; ++k) g.bct[tt * g.ncp + tu * 32 + s * kCellsPerStrip + k] = tb[k];
       }
       // the tile's partials are assembled by K1b, or are all +0 (flag 0)
       if (lane == 0) {
-        c.tileflag[tile] = any ? 1 : 0;
-        if (any) c.tlist[tslot] = (int32_t)tile;
+        g.tileflag[tile] = any ? 1 : 0;
+        if (any) g.tlist[tslot] = (int32_t)tile;
       }
 #ifdef PDOT_K0_PROF
       if (lane == 0 && op == OP_STEP) {
@@ -366,40 +407,6 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
 // the lane-sequential row chain (passed from row group to row group) and the
 // 8-lane butterfly.
 // ---------------------------------------------------------------------------
-// K1's fixed geometry (set once per handle) travels as a KERNEL PARAMETER: its
-// fields sit in the constant bank and feed instructions directly, instead of
-// being reloaded from the control block in global memory for every cell (the
-// 128-register budget does not keep them all live).  KGeo exposes the same
-// member names as Ctl, so the cell functions are templates over the context
-// type; the per-pass output slots come from the control block (dyn).  ldc is
-// fixed while the problem is bound: pdot_set_problem drops the captured graph
-// when it changes.
-struct KGeo {
-  int64_t m, n, ldx, ldc, mpad, nbands, nstrips, ncells, ncp, T, U;
-  int64_t occ_stride, tiles;  // nbands * nstrips, T * U
-  int32_t nbt, cbits, nbt_log2, pad_;
-  uint32_t* occ;
-  uint8_t* tocc;
-  double* ccol;
-  double* crow;
-  double* cscal;
-  uint32_t* ulist;
-  uint8_t* uflag;
-  unsigned int* ucount;
-  // K1b (tile_kernel): the bit maps, tile list and per-tile partials it writes
-  int64_t TM;
-  const uint32_t* bcr;
-  const uint32_t* bct;
-  const int32_t* tlist;
-  const unsigned int* tcount;
-  double* colpart;
-  double* rowpart;
-  double* tilescal;
-  // slack certificates (STEP cells of a solve when the control block's sr_on)
-  double* srec;
-  const double* sdp;
-  const double* sdq;
-};
 struct CellGeo {
   int64_t band, cell, strip, i0, j;
   int rows, k, rg, cp;
@@ -1355,18 +1362,19 @@ void launch_screened_pass(const Ctl* ctl_dev, const Ctl& h, int force_op, cudaSt
     // test hook: PDOT_K0_BLOCKS caps K0's grid (read per launch), so that small
     // problems run the persistent tile walk with many tiles per warp
     if (const char* e = getenv("PDOT_K0_BLOCKS")) g0 = (unsigned)imin64(g0, imax64(1, atoi(e)));
-    screen_kernel<<<g0, 32 * kScreenWarps, 0, s>>>(ctl_dev, force_op, h.sstat);  // warp per tile, persistent
+    const KGeo geo{h.m, h.n, h.ldx, h.ldc, h.mpad, h.nbands, h.nstrips, h.ncells, h.ncp, h.T, h.U,
+                   h.nbands * h.nstrips, h.T * h.U, h.nbt, h.cbits, __builtin_ctz((unsigned)h.nbt), 0,
+                   h.occ, h.tocc, h.ccol, h.crow, h.cscal, h.ulist, h.uflag, h.ucount,
+                   h.TM, h.bcr, h.bct, h.tlist, h.tcount, h.colpart, h.rowpart, h.tilescal,
+                   h.srec, h.sdp, h.sdq, h.qmax, h.pmax, h.minc, h.tminc, h.tileflag};
+    screen_kernel<<<g0, 32 * kScreenWarps, 0, s>>>(ctl_dev, force_op, h.sstat, geo);  // warp per tile, persistent
     if (getenv("PDOT_DEBUG_SYNC")) {
       const cudaError_t e = cudaStreamSynchronize(s);
       if (e != cudaSuccess) fprintf(stderr, "screen_kernel failed: %s\n", cudaGetErrorString(e));
     }
     // every warp reads list entries gw, gw + nw and gw + 2 nw up front: 3 nw <= kListPad
     const unsigned g1 = (unsigned)imin64((int64_t)sms * kSparseCtasPerSm, kListPad / (3 * kWarps));
-    const KGeo geo{h.m, h.n, h.ldx, h.ldc, h.mpad, h.nbands, h.nstrips, h.ncells, h.ncp, h.T, h.U,
-                   h.nbands * h.nstrips, h.T * h.U, h.nbt, h.cbits, __builtin_ctz((unsigned)h.nbt), 0,
-                   h.occ, h.tocc, h.ccol, h.crow, h.cscal, h.ulist, h.uflag, h.ucount,
-                   h.TM, h.bcr, h.bct, h.tlist, h.tcount, h.colpart, h.rowpart, h.tilescal,
-                   h.srec, h.sdp, h.sdq};
+
     unit_kernel<<<g1, kThreads, kUnitDynSmem, s>>>(ctl_dev, force_op, geo);
     tile_kernel<<<(unsigned)imin64(h.T * h.U * 3, (int64_t)sms * 4), kThreads, 0, s>>>(ctl_dev, force_op, geo);
   } else {
