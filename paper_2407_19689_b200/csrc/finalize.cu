@@ -811,9 +811,9 @@ __device__ void do_restart(Ctl& c, int cand_slot, double cand_kkt) {
   ring_push(c, EV_RESTART, (int)c.inner, cand_kkt, c.omega, 0.0);
   c.outer += 1;
   c.inner = 0;
+  // (the slack records stay valid: both new dual pairs are the candidate's, which
+  // was one of this pass's two input pairs, and the records bound both of them)
   c.sX = c.sA = c.sZ = c.sAsrc = cand_slot;
-  // new duals: every slack record written so far falls below the drift (record <= cap)
-  if (c.sr_on) c.sr_base = __dadd_ru(c.sr_base, 2.0 * c.sr_cap);
   c.lagA = 0;
   c.epoch_kkt = cand_kkt;
   c.prev_cand = cand_kkt;

@@ -229,15 +229,15 @@ struct Ctl {
   double* cscal;             // [nbands][ncp][kMaxNS] cell scalars
   // Slack certificates (STEP passes of a solve): K1 records for every cell it
   // computes a lower bound on min_ij (C_ij - p_i - q_j) over both dual pairs,
-  // shifted by the band / cell drift counters and the epoch base at that pass;
-  // K2 adds each pass's largest dual change per band / cell to the counters
-  // (rounded up), a restart adds 2 sr_cap to the base.  K0 drops a cell with
-  // no mass whose record still exceeds the drift since it was written, so
-  // p_i + q_j <= C_ij holds there exactly as the coarse bound would show.
-  double* srec;              // [nbands][ncells] record (NaN: none)
+  // shifted by the band / cell drift counters at that pass; K2 adds each pass's
+  // largest dual change per band / cell to the counters (rounded up).  K0 drops
+  // a cell with no mass whose record still exceeds the drift since it was
+  // written, so p_i + q_j <= C_ij holds there exactly as the coarse bound would
+  // show.  A restart keeps them: both new pairs are the candidate's, one of the
+  // two pairs the records bound.
+  double* srec;              // [nbands][ncells] record (NaN / -inf: none)
   double* sdp;               // [nbands] cumulative band drift of p / p-average
   double* sdq;               // [ncells] cumulative cell drift of q / q-average
-  double sr_base, sr_cap;    // epoch base; records are capped at sr_cap
   int32_t sr_on, sr_pad_;
   unsigned long long* sstat; // [ST_COUNT]
   unsigned long long* kdbg;  // PDOT_K2_TRACE=1: per-block K2 timestamps of the last screened STEP pass

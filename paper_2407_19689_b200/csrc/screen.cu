@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
               const bool coarse = (bound && !(qw[3][bl] + qw[0][kc] <= mck[u][k])) ||
                                   (bound_avg && !(qw[4][bl] + qw[1][kc] <= mck[u][k]));
               const bool cert = use_rec && mck[u][k] != -INFINITY &&
-                                __dsub_rd(__dsub_rd(__dsub_rd(rk[u][k], c.sr_base), qw[5][bl]), qw[2][kc]) > 0.0;
+                                __dsub_rd(__dsub_rd(rk[u][k], qw[5][bl]), qw[2][kc]) > 0.0;
               const bool act = bx || ba || open || (coarse && !cert);
               const uint32_t f = (act ? U_ACT : 0u) | (bx ? U_LDX : 0u) | (ba ? U_LDA : 0u) |
                                  (bzx ? U_ZX : 0u) | (bza ? U_ZA : 0u);
@@ -712,7 +712,7 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const C
   if (act) {
     cell_flush<NQ, NS>(c, g, o, sacc);
     if (lane == 0) bytes += (unsigned)(NQ * kCell + NQ * kBand + NS) * 8 * 2;
-    if (sr) {  // the cell's record: capped, shifted by the drift counters and the epoch base (rounded down)
+    if (sr) {  // the cell's record: shifted by the drift counters (rounded down)
       // warp minimum in one REDUX: the high word of a positive double orders like
       // the double and, with the low word cleared, rounds it down; a slack <= 0
       // (or NaN) in any lane means no certificate
@@ -720,9 +720,7 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const C
       const int kmin = __reduce_min_sync(0xffffffffu, key);
       if (lane == 0) {
         const double2 dd = *reinterpret_cast<const double2*>(stage + kStD);
-        const double rec = kmin > 0 ? __dadd_rd(__dadd_rd(__dadd_rd(fmin(__hiloint2double(kmin, 0), dyn.sr_cap),
-                                                                    dd.x), dd.y), dyn.sr_base)
-                                    : -INFINITY;
+        const double rec = kmin > 0 ? __dadd_rd(__dadd_rd(__hiloint2double(kmin, 0), dd.x), dd.y) : -INFINITY;
         c.srec[g.band * c.ncells + g.cell] = rec;
       }
     }

@@ -338,14 +338,11 @@ void occ_invalidate(pdot_solver* h, int slot) {
 }
 
 // Slack certificates start over with every solve (and resume): no records
-// (NaN), zero drift, base 0.  They need a finite positive cap (||C||_F >= every
-// |C_ij|); PDOT_SREC=0 turns them off.
+// (NaN), zero drift.  PDOT_SREC=0 turns them off.
 int srec_reset(pdot_solver* h) {
   Ctl& c = h->host;
   static const int env_on = getenv("PDOT_SREC") ? atoi(getenv("PDOT_SREC")) : 1;
-  c.sr_on = c.screen && c.srec && env_on && std::isfinite(c.cost_fro) && c.cost_fro > 0.0;
-  c.sr_cap = c.sr_on ? c.cost_fro : 0.0;
-  c.sr_base = 0.0;
+  c.sr_on = c.screen && c.srec && env_on;
   if (!c.sr_on) return PDOT_OK;
   CK(cudaMemsetAsync(c.srec, 0xff, (size_t)c.nbands * c.ncells * sizeof(double), h->stream));
   CK(cudaMemsetAsync(c.sdp, 0, (size_t)c.nbands * sizeof(double), h->stream));
