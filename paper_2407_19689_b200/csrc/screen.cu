@@ -665,7 +665,8 @@ __device__ __forceinline__ void cell_step(const StepOp& op, const Cx& c, const C
     if (okr[rr]) {  // StepOp::elem in the dense walkers' element order
       op.template elem<AVG>(cc[rr].x, xx[rr].x, aa[rr].x, pr[rr], qv[0], par[rr], qav[0], o0, sacc);
       if (g.v1) op.template elem<AVG>(cc[rr].y, xx[rr].y, aa[rr].y, pr[rr], qv[1], par[rr], qav[1], o1, sacc);
-      if (sr) {  // C - (p + q) and C - (pa + qa), each a lower bound of the exact value
+      if (sr) {
+        // C - (p + q) and C - (pa + qa), each a lower bound of the exact value
         smin = fmin(smin, fmin(__dsub_rd(cc[rr].x, __dadd_ru(pr[rr], qv[0])),
                                __dsub_rd(cc[rr].x, __dadd_ru(par[rr], qav[0]))));
         if (g.v1)
