@@ -363,22 +363,6 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
             g.ulist[pos] = cell_entry(band, strip * kCellsPerStrip + k, g.cbits);
             g.uflag[pos] = (uint8_t)((words[rd] >> (8 * k)) & 0xffu);  // the cell's flags travel with it
             ++pos;
-#ifdef PDOT_K0_PREFETCH
-            // the cell's C rows (and X rows where loaded) into L2 ahead of K1's copies
-            const uint32_t fl = (words[rd] >> (8 * k)) & 0xffu;
-            if ((fl & U_ACT) && op == OP_STEP) {
-              const int64_t j0 = (strip * kCellsPerStrip + k) * kCell;
-              const double* Xs = (fl & U_LDX) ? c.slot[c.sX].X : nullptr;
-#pragma unroll
-              for (int r = 0; r < kBand; ++r) {
-                const int64_t i = band * kBand + r;
-                if (i < g.m) {
-                  if (c.C) asm volatile("prefetch.global.L2 [%0];" ::"l"(c.C + i * g.ldc + j0));
-                  if (Xs) asm volatile("prefetch.global.L2 [%0];" ::"l"(Xs + i * g.ldx + j0));
-                }
-              }
-            }
-#endif
           }
       }
       // bct[tt][cell]: bit bl = band bl of the tile (OR over the 4 band quarters)
