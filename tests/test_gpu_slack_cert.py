@@ -2,8 +2,8 @@
 exceeds the dual drift since it was recorded) against the plain cell screen
 (PDOT_SREC=0): the same screened solves, bit for bit, with fewer cells visited.
 The switch is read once per process, so each arm runs in its own interpreter.
-Cases: the sq-Euclidean grid (many restarts), the rectangular L1 cost, and the
-matrix-free cost."""
+Cases: the sq-Euclidean grid (many restarts), the rectangular L1 cost, the
+matrix-free cost, and restarts through the host-evaluated primal weight."""
 
 import json
 import os
@@ -27,9 +27,12 @@ if case == "grid":
     dp, tol = pd.DeviceProblem.sqeuclid_grid(32, 3), 1e-6          # 1024^2
 elif case == "rect":
     dp, tol = pd.DeviceProblem.rect_l1(1, src=(16, 32), dst=(32, 64)), 1e-5  # 512 x 2048
-else:
+elif case == "implicit":
     dp, tol = pd.DeviceProblem.sqeuclid_grid(24, 5, implicit=True), 1e-6   # 576^2, C generated in-kernel
-(slot, h), rep = pd.solve_device(dp, pd.SolverConfig(tol=tol, deterministic=True))
+else:  # host-evaluated primal weight: every adaptive restart pauses and resumes
+    dp, tol = pd.DeviceProblem.sqeuclid_grid(32, 4), 1e-5
+kw = {"host_omega": True} if case == "host_omega" else {}
+(slot, h), rep = pd.solve_device(dp, pd.SolverConfig(tol=tol, deterministic=True), **kw)
 X, p, q = h.get_slot(slot)
 st = h.screen_stats()
 hx = hashlib.sha256(np.ascontiguousarray(X).tobytes() + p.tobytes() + q.tobytes()).hexdigest()
@@ -47,7 +50,7 @@ def _run(case: str, srec: str) -> dict:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["grid", "rect", "implicit"])
+@pytest.mark.parametrize("case", ["grid", "rect", "implicit", "host_omega"])
 def test_slack_certificates_bit_identical(case):
     on, off = _run(case, "1"), _run(case, "0")
     assert on["screen_on"] == 1 and off["screen_on"] == 1
