@@ -374,8 +374,6 @@ __device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* sm
         vals[3] = pca * pca;
         vals[5] = gj * qan;
       }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) c.cols_out[q * c.ldx + j] = col[q];
     }
     if (threadIdx.x < kColsPerBlock) {  // NaN-propagating maxima over each 16-column cell
       const int lane = threadIdx.x & 31;
@@ -554,8 +552,6 @@ __device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem)
           vals[3] += pra * pra;
           vals[5] += fi * pan;
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) c.rows_out[q * c.m + i] = row[q];
       }
       {  // NaN-propagating maxima over each 8-row band (TM is a multiple of 8)
         const int lane = threadIdx.x & 31;

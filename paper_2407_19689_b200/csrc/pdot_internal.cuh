@@ -198,8 +198,8 @@ struct Ctl {
   double* tilescal;   // [T][U][kMaxNS]
   double* rowblk;     // [T][kMaxRowScal]
   double* colblk;     // [CB][kMaxColScal]
-  double* rows_out;   // [NQ][m] full row sums of the last pass (finalize writes)
-  double* cols_out;   // [NQ][ldx] full column sums of the last pass
+  double* rows_out;   // [NQ][m] full row sums of the last unit pass (finalize writes; STEP
+  double* cols_out;   // [NQ][ldx] ... column sums      passes skip them: nothing reads them)
   double* vec_a;      // scratch m (rounding row scale / error)
   double* vec_b;      // scratch n (rounding col scale / error)
   double* viol_out;   // unit kkt: dual-violation matrix (ldx) or null
