@@ -3,7 +3,8 @@ exceeds the dual drift since it was recorded) against the plain cell screen
 (PDOT_SREC=0): the same screened solves, bit for bit, with fewer cells visited.
 The switch is read once per process, so each arm runs in its own interpreter.
 Cases: the sq-Euclidean grid (many restarts), the rectangular L1 cost, the
-matrix-free cost, and restarts through the host-evaluated primal weight."""
+matrix-free cost, restarts through the host-evaluated primal weight, and C2
+(4096^2 to tol 1e-6: ~3.7k iterations, ~30 restarts)."""
 
 import json
 import os
@@ -27,6 +28,8 @@ if case == "grid":
     dp, tol = pd.DeviceProblem.sqeuclid_grid(32, 3), 1e-6          # 1024^2
 elif case == "rect":
     dp, tol = pd.DeviceProblem.rect_l1(1, src=(16, 32), dst=(32, 64)), 1e-5  # 512 x 2048
+elif case == "c2":
+    dp, tol = pd.DeviceProblem.sqeuclid_grid(64, 0), 1e-6          # C2: 4096^2, the headline's smaller sibling
 elif case == "implicit":
     dp, tol = pd.DeviceProblem.sqeuclid_grid(24, 5, implicit=True), 1e-6   # 576^2, C generated in-kernel
 else:  # host-evaluated primal weight: every adaptive restart pauses and resumes
@@ -50,7 +53,7 @@ def _run(case: str, srec: str) -> dict:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["grid", "rect", "implicit", "host_omega"])
+@pytest.mark.parametrize("case", ["grid", "rect", "implicit", "host_omega", "c2"])
 def test_slack_certificates_bit_identical(case):
     on, off = _run(case, "1"), _run(case, "0")
     assert on["screen_on"] == 1 and off["screen_on"] == 1
