@@ -13,6 +13,13 @@
 // because rounding is monotone.  Skipped cells add +0 to sums that started at
 // +0, so every partial, and hence every result, is bit-identical to the dense
 // TMA walker (stream.cu); tests/test_gpu_screen.py checks exactly that.
+// The same condition is also certified, for cells the bound above keeps, by a
+// slack record: K1 stores a rounded-down lower bound on the cell's exact
+// min (C_ij - p_i - q_j) over both dual pairs, shifted by per-band / per-cell
+// drift counters that K2 raises by each pass's largest dual change (rounded
+// up); K0 drops the cell while the record still exceeds the drift since
+// (pdot_internal.cuh, Ctl::srec; tests/test_gpu_slack_cert.py and
+// tests/test_slack_cert_soundness.py).
 //
 // Invariant: slot memory always holds the dense values.  occ[slot] marks cells
 // whose bits may be nonzero (a superset); a cell with occ = 0 is all +0.0 in
