@@ -201,7 +201,6 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
     const double Pl = okb ? __ldcg(g.pmax + sx * g.nbands + lbnd) : -INFINITY;
     const double Pal = (okb && bound_avg) ? __ldcg(g.pmax + c.sA * g.nbands + lbnd) : -INFINITY;
     const double dPl = (okb && use_rec) ? __ldcg(g.sdp + lbnd) : 0.0;
-    double P = Pl, Pa = Pal;
     uint32_t occ_any = 0;
     double mc = INFINITY;
     if (lane == 0) {
@@ -216,15 +215,14 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
     for (int msk = 1; msk < 32; msk <<= 1) {
       Q = max_nan(Q, __shfl_xor_sync(0xffffffffu, Q, msk));
       Qa = max_nan(Qa, __shfl_xor_sync(0xffffffffu, Qa, msk));
-      P = max_nan(P, __shfl_xor_sync(0xffffffffu, P, msk));
-      Pa = max_nan(Pa, __shfl_xor_sync(0xffffffffu, Pa, msk));
     }
     // a non-finite step (tau) would turn 0 * inf into NaN: screen nothing
     const bool open = op == OP_STEP && !isfinite(c.tau);
-    // !(a <= b) keeps NaN bounds active
-    const bool full = __shfl_sync(0xffffffffu, occ_any ? 1 : 0, 0) || open ||
-                      (bound && !(P + Q <= __shfl_sync(0xffffffffu, mc, 0))) ||
-                      (bound_avg && !(Pa + Qa <= __shfl_sync(0xffffffffu, mc, 0)));
+    // RN(max p + max q) <= min C, tested band by band with a vote (rounding is
+    // monotone: the same decision); !(a <= b) keeps NaN bounds active
+    const double mcb = __shfl_sync(0xffffffffu, mc, 0);
+    const bool bad = okb && (!(Pl + Q <= mcb) || (bound_avg && !(Pal + Qa <= mcb)));
+    const bool full = __shfl_sync(0xffffffffu, occ_any ? 1 : 0, 0) || open || __any_sync(0xffffffffu, bad);
     if (!full) {
       if (lane == 0) g.tileflag[tile] = 0;
     } else {
