@@ -161,8 +161,21 @@ constexpr int kHalfCols = 64;
 constexpr int kColBatch = 2;  // flagged tiles per round trip (register budget: 2 x 2 x NQ double2;
                               // 3 per round trip: no gain, 4: K2 +2.3 us, spills)
 
-template <int NQ>
-__device__ __forceinline__ void group_column_sum(const Ctl& c, int g, int64_t j, double2 (&acc)[2][NQ],
+// The work blocks' fixed geometry (set once per handle) as a KERNEL PARAMETER:
+// constant-bank operands in the tile-partial loops instead of shared-memory
+// loads of the control block.  The same member names as Ctl, so the loops are
+// templates over the view (the rare ops pass the control block itself).
+struct FGeo {
+  int64_t m, n, ldx, T, U, TM, GS, t0, Tg;
+  const uint8_t* tileflag;
+  const double* colpart;
+  const double* rowpart;
+  const double* tilescal;
+  double* rowblk;
+};
+
+template <int NQ, class Cx>
+__device__ __forceinline__ void group_column_sum(const Cx& c, int g, int64_t j, double2 (&acc)[2][NQ],
                                                  uint32_t m0 = 0u, bool has_m0 = false) {
 #pragma unroll
   for (int h = 0; h < 2; ++h)
@@ -234,9 +247,9 @@ __device__ void column_group_partials(const Ctl& c, int b) {
 
 // Full column sums = pairwise combination of the 8 group sums (FIN_FUSED: the
 // groups are computed here; FIN_B: they come from the exchange buffer).
-template <int NQ>
-__device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_out, double* smem, int mode,
-                            uint32_t m0 = 0u, bool has_m0 = false) {
+template <int NQ, class Cx>
+__device__ void column_sums(const Ctl& c, const Cx& gx, int b, double (&col)[NQ], int64_t& j_out, double* smem,
+                            int mode, uint32_t m0 = 0u, bool has_m0 = false) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int jj = threadIdx.x;
   j_out = (int64_t)b * kColsPerBlock + jj;
@@ -257,7 +270,7 @@ __device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_o
   }
   const int64_t j = (int64_t)b * kColsPerBlock + lane * 2;
   double2 acc[2][NQ];
-  group_column_sum<NQ>(c, warp, j, acc, m0, has_m0);
+  group_column_sum<NQ>(gx, warp, j, acc, m0, has_m0);
   // smem [group][q][kColsPerBlock]
 #pragma unroll
   for (int h = 0; h < 2; ++h)
@@ -282,8 +295,8 @@ __device__ void column_sums(const Ctl& c, int b, double (&col)[NQ], int64_t& j_o
   __syncthreads();
 }
 
-template <int NQ>
-__device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ], uint32_t m0 = 0u, bool has_m0 = false) {
+template <int NQ, class Cx>
+__device__ void row_sums(const Cx& c, int64_t i, double (&row)[NQ], uint32_t m0 = 0u, bool has_m0 = false) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) row[q] = 0.0;
   // screened-out tiles: partials +0.  A full warp of rows of one row tile
@@ -323,8 +336,8 @@ __device__ void row_sums(const Ctl& c, int64_t i, double (&row)[NQ], uint32_t m0
 
 // STEP: the hot path of every screened pass, compiled on its own (the rare ops
 // sit out of line in column_block_rare) so that its code is compact
-template <bool STEP>
-__device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* smem, int mode) {
+template <bool STEP, class Gx>
+__device__ __forceinline__ void column_block_t(Ctl& c, const Gx& gx, int op, int b, double* smem, int mode) {
   double vals[kMaxColScal];
 #pragma unroll
   for (int s = 0; s < kMaxColScal; ++s) vals[s] = 0.0;
@@ -350,7 +363,7 @@ __device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* sm
     }
     pdl_wait();  // (a programmatic dependent of K1b: its partials from here on; a no-op otherwise)
     double col[4];
-    column_sums<4>(c, b, col, j, smem, mode, m0, has_m0);
+    column_sums<4>(c, gx, b, col, j, smem, mode, m0, has_m0);
     double qb = -INFINITY, qab = -INFINITY;  // screening bounds of q+ and the dual average
     double qdr = 0.0;                           // their drift (rounded up)
     if (threadIdx.x < kColsPerBlock && j < c.n) {
@@ -393,7 +406,7 @@ __device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* sm
     }
   } else if (op == OP_KKT) {
     double col[1];
-    column_sums<1>(c, b, col, j, smem, mode);
+    column_sums<1>(c, gx, b, col, j, smem, mode);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       c.cols_out[j] = col[0];
       if (c.C || c.cost_kind > 0) {
@@ -407,7 +420,7 @@ __device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* sm
     }
   } else if (op == OP_DIFF || op == OP_DIST) {
     double col[1];
-    column_sums<1>(c, b, col, j, smem, mode);
+    column_sums<1>(c, gx, b, col, j, smem, mode);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       c.cols_out[j] = col[0];
       const double* qa = (op == OP_DIFF) ? c.slot[c.sX].q : c.slot[c.sZ].q;
@@ -418,7 +431,7 @@ __device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* sm
     }
   } else if (op == OP_ROUND) {
     double col[1];
-    column_sums<1>(c, b, col, j, smem, mode);
+    column_sums<1>(c, gx, b, col, j, smem, mode);
     if (threadIdx.x < kColsPerBlock && j < c.n) {
       c.cols_out[j] = col[0];
       const double gj = c.g[j];
@@ -461,7 +474,8 @@ __device__ __forceinline__ void column_block_t(Ctl& c, int op, int b, double* sm
 // ---------------------------------------------------------------------------
 // Tile scalars of row tile t (sum over its column tiles, in order; screened-out
 // tiles are +0), by one warp: the flag masks by ballot, then lanes < ns sum.
-__device__ __forceinline__ void tile_scalars(Ctl& c, int t, int ns, int nr, int lane, uint32_t m0 = 0u,
+template <class Cx>
+__device__ __forceinline__ void tile_scalars(const Cx& c, int t, int ns, int nr, int lane, uint32_t m0 = 0u,
                                              bool has_m0 = false) {
   const int tx = lane;
   const uint8_t* flags = c.tileflag + (int64_t)t * c.U;
@@ -493,8 +507,8 @@ __device__ __forceinline__ void tile_scalars(Ctl& c, int t, int ns, int nr, int 
   if (tx < ns) c.rowblk[(int64_t)t * kMaxRowScal + nr + tx] = acc;
 }
 
-template <bool STEP>
-__device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem) {
+template <bool STEP, class Gx>
+__device__ __forceinline__ void row_block_t(Ctl& c, const Gx& gx, int op, int t, double* smem) {
   double vals[kMaxRowScal];
 #pragma unroll
   for (int s = 0; s < kMaxRowScal; ++s) vals[s] = 0.0;
@@ -509,7 +523,7 @@ __device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem)
   if (scal_early && threadIdx.x >= kRedThreads - 32) {
     const uint32_t m0 = warp_flag_mask(c.tileflag + (int64_t)t * c.U, 1, c.U);  // K0's flags, before the wait
     pdl_wait();
-    tile_scalars(c, t, ns, nr, threadIdx.x & 31, m0, true);
+    tile_scalars(gx, t, ns, nr, threadIdx.x & 31, m0, true);
   }
   for (int r = threadIdx.x; r < c.TM; r += kRedThreads) {
     const int64_t i = i0 + r;
@@ -528,7 +542,7 @@ __device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem)
       const uint32_t m0 = fullw ? warp_flag_mask(fl, 1, c.U) : (ir < c.m ? flag_mask(fl, 1, c.U) : 0u);
       pdl_wait();
       double row[4];
-      row_sums<4>(c, ir, row, m0, true);
+      row_sums<4>(gx, ir, row, m0, true);
       double pb = -INFINITY, pab = -INFINITY;  // screening bounds of p+ and the dual average
       double pdr = 0.0;                           // their drift (rounded up)
       if (ok) {
@@ -619,14 +633,14 @@ __device__ __forceinline__ void row_block_t(Ctl& c, int op, int t, double* smem)
   }
   if (!scal_early && threadIdx.x < 32) {
     pdl_wait();
-    tile_scalars(c, t, ns, nr, threadIdx.x);
+    tile_scalars(gx, t, ns, nr, threadIdx.x);
   }
 }
 
 __device__ __noinline__ void column_block_rare(Ctl& c, int op, int b, double* smem, int mode) {
-  column_block_t<false>(c, op, b, smem, mode);
+  column_block_t<false>(c, c, op, b, smem, mode);
 }
-__device__ __noinline__ void row_block_rare(Ctl& c, int op, int t, double* smem) { row_block_t<false>(c, op, t, smem); }
+__device__ __noinline__ void row_block_rare(Ctl& c, int op, int t, double* smem) { row_block_t<false>(c, c, op, t, smem); }
 
 // ---------------------------------------------------------------------------
 // controller
@@ -1055,7 +1069,7 @@ __device__ unsigned long long g_k2entry;  // controller entry of the running pas
 #endif
 
 template <int mode>
-__global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restrict__ ctlp, int force_op) {
+__global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restrict__ ctlp, int force_op, const FGeo geo) {
   // launched as a programmatic dependent of K1b (pdl_edge("k2")): every block
   // copies the control block (K1b does not write it) before it waits for K1b,
   // and the controller block also runs its dry run first
@@ -1179,11 +1193,11 @@ __global__ void __launch_bounds__(kRedThreads, 2) finalize_kernel(Ctl* __restric
         if (op == OP_STEP) column_group_partials<4>(c, b);
         else column_group_partials<1>(c, b);
       } else {
-        if (op == OP_STEP) column_block_t<true>(c, op, b, smem, mode);
+        if (op == OP_STEP) column_block_t<true>(c, geo, op, b, smem, mode);
         else column_block_rare(c, op, b, smem, mode);
       }
     } else {
-      if (op == OP_STEP) row_block_t<true>(c, op, wb, smem);
+      if (op == OP_STEP) row_block_t<true>(c, geo, op, wb, smem);
       else row_block_rare(c, op, wb, smem);
     }
     if (timed && c.kdbg && threadIdx.x == 0) c.kdbg[wb * 4 + 1] = globaltimer_ns();
@@ -1430,6 +1444,7 @@ int launch_p2p_protocol_test(Ctl* ctls_dev, int nranks, int rounds, unsigned lon
 }
 
 void launch_finalize_pass(Ctl* ctl_dev, const Ctl& h, int force_op, int mode, cudaStream_t s) {
+  const FGeo geo{h.m, h.n, h.ldx, h.T, h.U, h.TM, h.GS, h.t0, h.Tg, h.tileflag, h.colpart, h.rowpart, h.tilescal, h.rowblk};
   // + 1: the controller block (FIN_FUSED, FIN_B)
   const unsigned blocks = (unsigned)(mode == FIN_B ? h.CB + 1 : mode == FIN_A ? h.CB + h.T : h.CB + h.T + 1);
   if (mode == FIN_FUSED && pdl_edge("k2")) {
@@ -1442,10 +1457,10 @@ void launch_finalize_pass(Ctl* ctl_dev, const Ctl& h, int force_op, int mode, cu
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, finalize_kernel<FIN_FUSED>, ctl_dev, force_op);
-  } else if (mode == FIN_FUSED) finalize_kernel<FIN_FUSED><<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op);
-  else if (mode == FIN_A) finalize_kernel<FIN_A><<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op);
-  else finalize_kernel<FIN_B><<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op);
+    cudaLaunchKernelEx(&cfg, finalize_kernel<FIN_FUSED>, ctl_dev, force_op, geo);
+  } else if (mode == FIN_FUSED) finalize_kernel<FIN_FUSED><<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op, geo);
+  else if (mode == FIN_A) finalize_kernel<FIN_A><<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op, geo);
+  else finalize_kernel<FIN_B><<<blocks, kRedThreads, 0, s>>>(ctl_dev, force_op, geo);
 }
 
 }  // namespace pdot
