@@ -166,12 +166,17 @@ constexpr int kColBatch = 2;  // flagged tiles per round trip (register budget: 
 // loads of the control block.  The same member names as Ctl, so the loops are
 // templates over the view (the rare ops pass the control block itself).
 struct FGeo {
-  int64_t m, n, ldx, T, U, TM, GS, t0, Tg;
+  int64_t m, n, ldx, T, U, TM, GS, t0, Tg, ncells, nbands, ncolblk;
   const uint8_t* tileflag;
   const double* colpart;
   const double* rowpart;
   const double* tilescal;
   double* rowblk;
+  double* colblk;
+  double* qmax;
+  double* pmax;
+  double* sdq;
+  double* sdp;
 };
 
 template <int NQ, class Cx>
@@ -345,28 +350,28 @@ __device__ __forceinline__ void column_block_t(Ctl& c, const Gx& gx, int op, int
   if constexpr (STEP) {
     // the vectors of this thread's column, loaded before the (long) column sums
     const int64_t jp = (int64_t)b * kColsPerBlock + threadIdx.x;
-    const bool own = threadIdx.x < kColsPerBlock && jp < c.n;
+    const bool own = threadIdx.x < kColsPerBlock && jp < gx.n;
     const double qj = own ? __ldcg(c.slot[c.sX].q + jp) : 0.0;
     const double gj = own ? __ldg(c.g + jp) : 0.0;
     const double qaj = own ? __ldcg(c.slot[c.sA].q + jp) : 0.0;
     const bool srec = c.sr_on && !c.unit;  // slack certificates: this cell's drift counter
-    const double dq_old = (srec && own && (threadIdx.x & (kCell - 1)) == 0) ? __ldcg(c.sdq + jp / kCell) : 0.0;
+    const double dq_old = (srec && own && (threadIdx.x & (kCell - 1)) == 0) ? __ldcg(gx.sdq + jp / kCell) : 0.0;
     // this warp's group's tile flags: K0 wrote them, so they are read before the wait too
     uint32_t m0 = 0u;
     const bool has_m0 = mode == FIN_FUSED;
     if (has_m0) {
       const int g = threadIdx.x >> 5;
-      const int64_t ta = imax64((int64_t)g * c.GS, c.t0);
-      const int64_t tb = imin64(imin64((int64_t)(g + 1) * c.GS, c.Tg), c.t0 + c.T);
+      const int64_t ta = imax64((int64_t)g * gx.GS, gx.t0);
+      const int64_t tb = imin64(imin64((int64_t)(g + 1) * gx.GS, gx.Tg), gx.t0 + gx.T);
       const int64_t jl = (int64_t)b * kColsPerBlock + (threadIdx.x & 31) * 2;
-      m0 = warp_flag_mask(c.tileflag + (imin64(jl, c.n - 1) / kTileN) + (ta - c.t0) * c.U, c.U, tb - ta);
+      m0 = warp_flag_mask(gx.tileflag + (imin64(jl, gx.n - 1) / kTileN) + (ta - gx.t0) * gx.U, gx.U, tb - ta);
     }
     pdl_wait();  // (a programmatic dependent of K1b: its partials from here on; a no-op otherwise)
     double col[4];
     column_sums<4>(c, gx, b, col, j, smem, mode, m0, has_m0);
     double qb = -INFINITY, qab = -INFINITY;  // screening bounds of q+ and the dual average
     double qdr = 0.0;                           // their drift (rounded up)
-    if (threadIdx.x < kColsPerBlock && j < c.n) {
+    if (threadIdx.x < kColsPerBlock && j < gx.n) {
       const double qn = qj + c.sigma * (gj - col[0]);        // pdhg.py:128
       const double dq = qn - qj;                              // pdhg.py:141
       c.slot[c.sXn].q[j] = qn;
@@ -398,16 +403,16 @@ __device__ __forceinline__ void column_block_t(Ctl& c, const Gx& gx, int op, int
         if (srec) qdr = max_nan(qdr, __shfl_xor_sync(gm, qdr, msk));
       }
       const int64_t cell = ((int64_t)b * kColsPerBlock + threadIdx.x) / kCell;
-      if ((threadIdx.x & (kCell - 1)) == 0 && cell < c.ncells) {
-        c.qmax[c.sXn * c.ncells + cell] = qb;
-        if (!c.unit || c.unit_avg) c.qmax[c.sAn * c.ncells + cell] = qab;
-        if (srec) c.sdq[cell] = __dadd_ru(dq_old, qdr);
+      if ((threadIdx.x & (kCell - 1)) == 0 && cell < gx.ncells) {
+        gx.qmax[c.sXn * gx.ncells + cell] = qb;
+        if (!c.unit || c.unit_avg) gx.qmax[c.sAn * gx.ncells + cell] = qab;
+        if (srec) gx.sdq[cell] = __dadd_ru(dq_old, qdr);
       }
     }
   } else if (op == OP_KKT) {
     double col[1];
     column_sums<1>(c, gx, b, col, j, smem, mode);
-    if (threadIdx.x < kColsPerBlock && j < c.n) {
+    if (threadIdx.x < kColsPerBlock && j < gx.n) {
       c.cols_out[j] = col[0];
       if (c.C || c.cost_kind > 0) {
         const Slot& sx = c.slot[c.sX];
@@ -421,7 +426,7 @@ __device__ __forceinline__ void column_block_t(Ctl& c, const Gx& gx, int op, int
   } else if (op == OP_DIFF || op == OP_DIST) {
     double col[1];
     column_sums<1>(c, gx, b, col, j, smem, mode);
-    if (threadIdx.x < kColsPerBlock && j < c.n) {
+    if (threadIdx.x < kColsPerBlock && j < gx.n) {
       c.cols_out[j] = col[0];
       const double* qa = (op == OP_DIFF) ? c.slot[c.sX].q : c.slot[c.sZ].q;
       const double* qb = (op == OP_DIFF) ? c.slot[c.sXn].q : c.slot[c.sCand].q;
@@ -432,14 +437,14 @@ __device__ __forceinline__ void column_block_t(Ctl& c, const Gx& gx, int op, int
   } else if (op == OP_ROUND) {
     double col[1];
     column_sums<1>(c, gx, b, col, j, smem, mode);
-    if (threadIdx.x < kColsPerBlock && j < c.n) {
+    if (threadIdx.x < kColsPerBlock && j < gx.n) {
       c.cols_out[j] = col[0];
       const double gj = c.g[j];
       if (c.round_stage == 1) {                       // rounding.py:26-28
         c.vec_b[j] = col[0] > 0.0 ? fmin(gj / col[0], 1.0) : 1.0;
       } else if (c.round_stage == 2) {                // rounding.py:34
         const double e = gj - col[0];
-        c.vec_b[c.ldx + j] = e < 0.0 ? 0.0 : e;
+        c.vec_b[gx.ldx + j] = e < 0.0 ? 0.0 : e;
       } else if (c.round_stage == 3) {
         vals[0] = gj * c.slot[c.sX].q[j];             // dual objective, pdhg.py:384
         const double pc = col[0] - gj;
@@ -464,7 +469,7 @@ __device__ __forceinline__ void column_block_t(Ctl& c, const Gx& gx, int op, int
       const int h = threadIdx.x / kMaxColScal, k = threadIdx.x % kMaxColScal;
       double acc = smem[(2 * h) * kMaxColScal + k];
       for (int w = 1; w < kWarps; ++w) acc += (w < 2) ? smem[(2 * h + w) * kMaxColScal + k] : 0.0;
-      if ((int64_t)b * 2 + h < c.ncolblk) c.colblk[((int64_t)b * 2 + h) * kMaxColScal + k] = acc;
+      if ((int64_t)b * 2 + h < gx.ncolblk) gx.colblk[((int64_t)b * 2 + h) * kMaxColScal + k] = acc;
     }
   }
 }
@@ -512,20 +517,20 @@ __device__ __forceinline__ void row_block_t(Ctl& c, const Gx& gx, int op, int t,
   double vals[kMaxRowScal];
 #pragma unroll
   for (int s = 0; s < kMaxRowScal; ++s) vals[s] = 0.0;
-  const int64_t i0 = (int64_t)t * c.TM;
-  const int rows = (int)imin64(c.TM, c.m - i0);
+  const int64_t i0 = (int64_t)t * gx.TM;
+  const int rows = (int)imin64(gx.TM, gx.m - i0);
   // row-side scalars / tile scalars of this op
   const int nr = op == OP_STEP ? 7 : op == OP_KKT ? 3 : op == OP_ROUND ? 3 : 2;
   const int ns = op == OP_STEP ? 6 : op == OP_KKT ? 3 : 1;
   // with rows for at most 7 warps, the last warp forms the tile scalars while the
   // others work on the rows (otherwise warp 0 does after them)
-  const bool scal_early = c.TM <= kRedThreads - 32;
+  const bool scal_early = gx.TM <= kRedThreads - 32;
   if (scal_early && threadIdx.x >= kRedThreads - 32) {
-    const uint32_t m0 = warp_flag_mask(c.tileflag + (int64_t)t * c.U, 1, c.U);  // K0's flags, before the wait
+    const uint32_t m0 = warp_flag_mask(gx.tileflag + (int64_t)t * gx.U, 1, gx.U);  // K0's flags, before the wait
     pdl_wait();
     tile_scalars(gx, t, ns, nr, threadIdx.x & 31, m0, true);
   }
-  for (int r = threadIdx.x; r < c.TM; r += kRedThreads) {
+  for (int r = threadIdx.x; r < gx.TM; r += kRedThreads) {
     const int64_t i = i0 + r;
     const bool ok = r < rows;
     if constexpr (STEP) {
@@ -534,12 +539,12 @@ __device__ __forceinline__ void row_block_t(Ctl& c, const Gx& gx, int op, int t,
       const double fi = ok ? __ldg(c.f + i) : 0.0;
       const double pai = ok ? __ldcg(c.slot[c.sA].p + i) : 0.0;
       const bool srec = c.sr_on && !c.unit;  // slack certificates: this band's drift counter
-      const double dp_old = (srec && ok && (r & (kBand - 1)) == 0) ? __ldcg(c.sdp + i / kBand) : 0.0;
+      const double dp_old = (srec && ok && (r & (kBand - 1)) == 0) ? __ldcg(gx.sdp + i / kBand) : 0.0;
       // the row tile's first 32 flags (K0's) before the wait, as row_sums forms them
-      const int64_t ir = ok ? i : c.m;
-      const bool fullw = __activemask() == 0xffffffffu && c.TM % 32 == 0;
-      const uint8_t* fl = c.tileflag + (imin64(ir, c.m - 1) / c.TM) * c.U;
-      const uint32_t m0 = fullw ? warp_flag_mask(fl, 1, c.U) : (ir < c.m ? flag_mask(fl, 1, c.U) : 0u);
+      const int64_t ir = ok ? i : gx.m;
+      const bool fullw = __activemask() == 0xffffffffu && gx.TM % 32 == 0;
+      const uint8_t* fl = gx.tileflag + (imin64(ir, gx.m - 1) / gx.TM) * gx.U;
+      const uint32_t m0 = fullw ? warp_flag_mask(fl, 1, gx.U) : (ir < gx.m ? flag_mask(fl, 1, gx.U) : 0u);
       pdl_wait();
       double row[4];
       row_sums<4>(gx, ir, row, m0, true);
@@ -577,15 +582,15 @@ __device__ __forceinline__ void row_block_t(Ctl& c, const Gx& gx, int op, int t,
           if (srec) pdr = max_nan(pdr, __shfl_xor_sync(gm, pdr, msk));
         }
         const int64_t band = i / kBand;
-        if ((r & (kBand - 1)) == 0 && band < c.nbands) {
-          c.pmax[c.sXn * c.nbands + band] = pb;
-          if (!c.unit || c.unit_avg) c.pmax[c.sAn * c.nbands + band] = pab;
-          if (srec) c.sdp[band] = __dadd_ru(dp_old, pdr);
+        if ((r & (kBand - 1)) == 0 && band < gx.nbands) {
+          gx.pmax[c.sXn * gx.nbands + band] = pb;
+          if (!c.unit || c.unit_avg) gx.pmax[c.sAn * gx.nbands + band] = pab;
+          if (srec) gx.sdp[band] = __dadd_ru(dp_old, pdr);
         }
       }
     } else if (op == OP_KKT) {
       double row[1];
-      row_sums<1>(c, ok ? i : c.m, row);
+      row_sums<1>(c, ok ? i : gx.m, row);
       if (ok) {
         c.rows_out[i] = row[0];
         if (c.C || c.cost_kind > 0) {
@@ -598,7 +603,7 @@ __device__ __forceinline__ void row_block_t(Ctl& c, const Gx& gx, int op, int t,
       }
     } else if (op == OP_DIFF || op == OP_DIST) {
       double row[1];
-      row_sums<1>(c, ok ? i : c.m, row);
+      row_sums<1>(c, ok ? i : gx.m, row);
       if (ok) {
         c.rows_out[i] = row[0];
         const double* pa = (op == OP_DIFF) ? c.slot[c.sX].p : c.slot[c.sZ].p;
@@ -609,7 +614,7 @@ __device__ __forceinline__ void row_block_t(Ctl& c, const Gx& gx, int op, int t,
       }
     } else if (op == OP_ROUND) {
       double row[1];
-      row_sums<1>(c, ok ? i : c.m, row);
+      row_sums<1>(c, ok ? i : gx.m, row);
       if (ok) {
         c.rows_out[i] = row[0];
         const double fi = c.f[i];
@@ -618,7 +623,7 @@ __device__ __forceinline__ void row_block_t(Ctl& c, const Gx& gx, int op, int t,
         } else if (c.round_stage == 2) {                           // rounding.py:33-35
           const double e = fi - row[0];
           const double er = e < 0.0 ? 0.0 : e;
-          c.vec_a[c.m + i] = er;
+          c.vec_a[gx.m + i] = er;
           vals[0] += er;
         } else if (c.round_stage == 3) {
           vals[1] += fi * c.slot[c.sX].p[i];
@@ -629,7 +634,7 @@ __device__ __forceinline__ void row_block_t(Ctl& c, const Gx& gx, int op, int t,
   }
   block_sum<kMaxRowScal>(vals, smem);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < nr; ++s) c.rowblk[(int64_t)t * kMaxRowScal + s] = vals[s];
+    for (int s = 0; s < nr; ++s) gx.rowblk[(int64_t)t * kMaxRowScal + s] = vals[s];
   }
   if (!scal_early && threadIdx.x < 32) {
     pdl_wait();
@@ -1444,7 +1449,9 @@ int launch_p2p_protocol_test(Ctl* ctls_dev, int nranks, int rounds, unsigned lon
 }
 
 void launch_finalize_pass(Ctl* ctl_dev, const Ctl& h, int force_op, int mode, cudaStream_t s) {
-  const FGeo geo{h.m, h.n, h.ldx, h.T, h.U, h.TM, h.GS, h.t0, h.Tg, h.tileflag, h.colpart, h.rowpart, h.tilescal, h.rowblk};
+  const FGeo geo{h.m,        h.n,       h.ldx,       h.T,        h.U,        h.TM,       h.GS,   h.t0,
+                 h.Tg,       h.ncells,  h.nbands,    h.ncolblk,  h.tileflag, h.colpart,  h.rowpart,
+                 h.tilescal, h.rowblk,  h.colblk,    h.qmax,     h.pmax,     h.sdq,      h.sdp};
   // + 1: the controller block (FIN_FUSED, FIN_B)
   const unsigned blocks = (unsigned)(mode == FIN_B ? h.CB + 1 : mode == FIN_A ? h.CB + h.T : h.CB + h.T + 1);
   if (mode == FIN_FUSED && pdl_edge("k2")) {
