@@ -170,6 +170,16 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
   const unsigned long long tk_entry = globaltimer_ns();
   bool first_tile = true;
 #endif
+  // the pass's slots and switches, once (registers: the loop's global stores
+  // would otherwise force reloads of the shared control block)
+  const bool with_avg = op == OP_STEP && step_with_avg(c);
+  const int sx = op == OP_DIST ? c.sCand : c.sX;
+  const int sa = op == OP_DIST ? c.sZ : c.sAsrc;
+  const int sA = c.sA, sXn = c.sXn;
+  const bool use_rec = op == OP_STEP && !c.unit && c.sr_on;
+  // a non-finite step (tau) would turn 0 * inf into NaN: screen nothing
+  const bool open = op == OP_STEP && !isfinite(c.tau);
+  unsigned long long* const sstat = c.sstat;
   // persistent: one wave of CTAs, each warp walks tiles warp, warp + nw, ...
   for (int64_t tile = (int64_t)blockIdx.x * kScreenWarps + warp; tile < tiles;
        tile += (int64_t)gridDim.x * kScreenWarps) {
@@ -183,31 +193,27 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
     }
     first_tile = false;
 #endif
-    const bool with_avg = op == OP_STEP && step_with_avg(c);
     const bool bound = op != OP_DIST, bound_avg = op == OP_STEP;
-    const int sx = op == OP_DIST ? c.sCand : c.sX;
-    const int sa = op == OP_DIST ? c.sZ : c.sAsrc;
     // ---- tile level: 32 cell maxima of q, nbt band maxima of p, min C, occupancy
     const int64_t tcell = tu * 32 + lane;
     const bool okc = bound && tcell < g.ncells;
     const double Qc = okc ? __ldcg(g.qmax + sx * g.ncells + tcell) : -INFINITY;
-    const double Qac = (okc && bound_avg) ? __ldcg(g.qmax + c.sA * g.ncells + tcell) : -INFINITY;
+    const double Qac = (okc && bound_avg) ? __ldcg(g.qmax + sA * g.ncells + tcell) : -INFINITY;
     // slack certificates (STEP passes of a solve): the cells' drift counters
-    const bool use_rec = op == OP_STEP && !c.unit && c.sr_on;
     const double dQc = (okc && use_rec) ? __ldcg(g.sdq + tcell) : 0.0;
     // lane bl < nbt (<= 32): band bl's maxima of p (current, average) and drift counter
     const int64_t lbnd = tt * g.nbt + lane;
     const bool okb = bound && lane < g.nbt && lbnd < g.nbands;
     const double Pl = okb ? __ldcg(g.pmax + sx * g.nbands + lbnd) : -INFINITY;
-    const double Pal = (okb && bound_avg) ? __ldcg(g.pmax + c.sA * g.nbands + lbnd) : -INFINITY;
+    const double Pal = (okb && bound_avg) ? __ldcg(g.pmax + sA * g.nbands + lbnd) : -INFINITY;
     const double dPl = (okb && use_rec) ? __ldcg(g.sdp + lbnd) : 0.0;
     uint32_t occ_any = 0;
     double mc = INFINITY;
     if (lane == 0) {
       occ_any = __ldcg(g.tocc + sx * tiles + tile);
       if (op == OP_DIST || with_avg) occ_any |= __ldcg(g.tocc + sa * tiles + tile);
-      if (op == OP_STEP) occ_any |= __ldcg(g.tocc + c.sXn * tiles + tile);
-      if (with_avg) occ_any |= __ldcg(g.tocc + c.sA * tiles + tile);
+      if (op == OP_STEP) occ_any |= __ldcg(g.tocc + sXn * tiles + tile);
+      if (with_avg) occ_any |= __ldcg(g.tocc + sA * tiles + tile);
       if (bound) mc = __ldcg(g.tminc + tile);
     }
     double Q = Qc, Qa = Qac;
@@ -216,8 +222,6 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
       Q = max_nan(Q, __shfl_xor_sync(0xffffffffu, Q, msk));
       Qa = max_nan(Qa, __shfl_xor_sync(0xffffffffu, Qa, msk));
     }
-    // a non-finite step (tau) would turn 0 * inf into NaN: screen nothing
-    const bool open = op == OP_STEP && !isfinite(c.tau);
     // RN(max p + max q) <= min C, tested band by band with a vote (rounding is
     // monotone: the same decision); !(a <= b) keeps NaN bounds active
     const double mcb = __shfl_sync(0xffffffffu, mc, 0);
@@ -231,12 +235,12 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
 #endif
       if (lane == 0) {
         // the output slots' tile summaries are rebuilt by K1 from the cells it writes
-        if (op == OP_STEP) g.tocc[c.sXn * tiles + tile] = 0;
-        if (with_avg) g.tocc[c.sA * tiles + tile] = 0;
+        if (op == OP_STEP) g.tocc[sXn * tiles + tile] = 0;
+        if (with_avg) g.tocc[sA * tiles + tile] = 0;
         // metadata traffic of a per-cell screen: per (band, strip) min C and the
         // cell maxima of q (current, average), 4 occupancy words, the flag word
-        if (op == OP_STEP && c.sstat)
-          atomicAdd(&c.sstat[ST_META], (unsigned long long)g.nbt * kWarps * (kCellsPerStrip * 8 * 3 + 4 * 4 + 4));
+        if (op == OP_STEP && sstat)
+          atomicAdd(&sstat[ST_META], (unsigned long long)g.nbt * kWarps * (kCellsPerStrip * 8 * 3 + 4 * 4 + 4));
       }
       // ---- per cell: lane (bq, s) covers bands bq, bq + 4, ... of strip s
       const int s = lane & 7, bq = lane >> 3;
@@ -280,8 +284,8 @@ __global__ void __launch_bounds__(32 * kScreenWarps, kScreenCtasPerSm) screen_ke
           const int64_t ow = band * g.nstrips + strip;
           ox[u] = valid[u] ? __ldcg(g.occ + sx * sstride + ow) : 0u;
           oa[u] = (valid[u] && (op == OP_DIST || with_avg)) ? __ldcg(g.occ + sa * sstride + ow) : 0u;
-          zx[u] = (valid[u] && op == OP_STEP) ? __ldcg(g.occ + c.sXn * sstride + ow) : 0u;
-          za[u] = (valid[u] && with_avg) ? __ldcg(g.occ + c.sA * sstride + ow) : 0u;
+          zx[u] = (valid[u] && op == OP_STEP) ? __ldcg(g.occ + sXn * sstride + ow) : 0u;
+          za[u] = (valid[u] && with_avg) ? __ldcg(g.occ + sA * sstride + ow) : 0u;
 #pragma unroll
           for (int k = 0; k < kCellsPerStrip; ++k) {
             const int64_t cell = strip * kCellsPerStrip + k;
